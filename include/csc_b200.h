@@ -1,0 +1,174 @@
+/* csc_b200.h — C ABI of libcscb200.so, the B200 (sm_100a) CSC hot path.
+ *
+ * Drop-in boundary for the reference package `cscluster`
+ * (/root/reference/pkg/src/cscluster). Every entry point below replaces one
+ * reference function (cited as file:line); the Python mirror package
+ * `paper_1706_03591_b200` binds them with ctypes, and INTEGRATION.md shows the
+ * ctypes stub a cscluster maintainer would add.
+ *
+ * Conventions
+ *  - All functions return an int status: CSC_OK (0) or a CSC_ERR_* code; the
+ *    message of the last failure on the calling thread is csc_last_error().
+ *  - Pointers named *_dev / device arrays are caller-owned device buffers
+ *    (any allocator; the Python side uses torch). The library never frees
+ *    caller memory. Pointers documented "host" are plain host memory.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Work is
+ *    enqueued asynchronously unless a function is documented to synchronise
+ *    (it then says so: it returns a host-side count or scalar).
+ *  - Dense blocks (signals, features, centroids) are row-major with a leading
+ *    dimension `ld` (elements per row, ld >= d). The filter needs ld*elem_size
+ *    to be a multiple of 16 bytes; padding columns must be zero and stay zero.
+ *  - Results are deterministic: no floating-point atomics; every reduction
+ *    has a fixed order for a given device.
+ */
+#ifndef CSC_B200_H
+#define CSC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSC_OK 0
+#define CSC_ERR_ARG 1  /* invalid argument (maps to ValueError) */
+#define CSC_ERR_CUDA 2 /* CUDA runtime / launch failure */
+#define CSC_ERR_CAPACITY 3 /* caller-supplied buffer too small */
+
+#define CSC_F64 0
+#define CSC_F32 1
+
+#define CSC_LAP_NORMALIZED 0
+#define CSC_LAP_COMBINATORIAL 1
+
+typedef struct csc_chebop csc_chebop; /* opaque Chebyshev operator plan */
+
+/* ---- library ------------------------------------------------------------ */
+int csc_version(void);
+const char *csc_last_error(void);
+/* number of SMs of the current device (host int) */
+int csc_device_info(int *sm_count, int *cc_major, int *cc_minor);
+
+/* ---- graph -> Laplacian (graphs.py:29-76 Graph.degrees/adjacency,
+ *      graphs.py:339-362 laplacian) -------------------------------------- */
+/* Builds the sorted CSR of the normalized (I - D^-1/2 W D^-1/2, isolated rows
+ * empty) or combinatorial (D - W) Laplacian from canonical edges (lo < hi,
+ * sorted by lo*n+hi, no duplicates — the Graph invariant), bit-identical to
+ * the reference: deg = (sum over lo-edges) + (sum over hi-edges) in edge
+ * order, inv = 1/sqrt(deg), off-diagonal -((inv_i*w)*inv_j), diag 1.0.
+ * w == NULL means unit weights. indices/vals need capacity 2m+n.
+ * SYNCHRONISES: writes *nnz_out and *bound_out (host). deg_dev may be NULL. */
+int csc_laplacian_build(int64_t n, int64_t m, const int64_t *lo_dev, const int64_t *hi_dev,
+                        const double *w_dev, int variant, int32_t *indptr_dev,
+                        int32_t *indices_dev, double *vals_dev, int64_t capacity,
+                        double *deg_dev, int64_t *nnz_out, double *bound_out, void *stream);
+
+/* Edge-set delta on canonical codes (code = lo*n + hi, graphs.py:78-80):
+ * new = sort((prev \ del) U ins). prev/del/ins must be sorted ascending and
+ * duplicate-free; del must be a subset of prev and ins disjoint from
+ * prev \ del. new_codes needs capacity m_prev - n_del + n_ins.
+ * SYNCHRONISES: writes *m_new_out (host); fails if del is not found in prev. */
+int csc_edge_delta(int64_t n, const int64_t *prev_dev, int64_t m_prev, const int64_t *del_dev,
+                   int64_t n_del, const int64_t *ins_dev, int64_t n_ins, int64_t *new_dev,
+                   int64_t capacity, int64_t *m_new_out, void *stream);
+/* lo = code / n, hi = code % n */
+int csc_codes_split(int64_t n, const int64_t *codes_dev, int64_t m, int64_t *lo_dev,
+                    int64_t *hi_dev, void *stream);
+
+/* ---- Chebyshev filter (filters.py:155-196) ------------------------------ */
+/* Plan for x(L) = I - scale*L (filters.py:172-176, scale = 2/lambda_max):
+ * builds M = I - scale*L on device (exact zeros dropped; an isolated row of
+ * the normalized L gets M_ii = 1) in the requested dtype, plus the
+ * nnz-balanced schedule (rows longer than a threshold are split into
+ * fixed-size segments reduced in a fixed order). SYNCHRONISES once. */
+int csc_chebop_create(const int32_t *indptr_dev, const int32_t *indices_dev,
+                      const double *vals_dev, int64_t n, int64_t nnz, double scale, int dtype,
+                      void *stream, csc_chebop **op_out);
+int csc_chebop_destroy(csc_chebop *op);
+/* host outputs: rows, stored nnz of M, long rows, long-row segments */
+int csc_chebop_info(const csc_chebop *op, int64_t *n, int64_t *nnz, int64_t *n_long,
+                    int64_t *n_segments);
+
+/* out = h(L) x = sum_j coeffs[j] T_j(M) x by the three-term recurrence,
+ * running ncoeffs-1 fused SpMM sweeps (each order: gather M*T_j, write
+ * T_{j+1} = 2 M T_j - T_{j-1}, accumulate out += c_j T_{j+1}).
+ * x, out: n x ld (dtype of the plan); work: 2*n*ld elements of scratch.
+ * coeffs_host: ncoeffs >= 2 doubles (host). If sumsq_dev != NULL the last
+ * sweep also reduces ||out||_F^2 into sumsq_dev[0] (double, device) — the
+ * eigencount of filters.py:190-196 before its scale factor. */
+int csc_cheb_filter(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t d,
+                    const double *coeffs_host, int32_t ncoeffs, void *out_dev, void *work_dev,
+                    double *sumsq_dev, void *stream);
+
+/* Chebyshev moments of the block (single-pass eigencount bisection):
+ * mu_dev[q] = sum over columns of <x, T_q(M) x>, q = 0 .. 2*m, from one
+ * m-order sweep via <T_j,T_j> and <T_{j+1},T_j>. mu_dev: 2m+1 doubles.
+ * work: 2*n*ld elements. */
+int csc_cheb_moments(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t d, int32_t m,
+                     double *mu_dev, void *work_dev, void *stream);
+
+/* Measurement hook: when enabled, every main sweep launch of csc_cheb_filter /
+ * csc_cheb_moments is bracketed by CUDA events on its stream (up to 4096
+ * launches); csc_sweep_times returns their durations in ms and resets. */
+int csc_sweep_timing(int enable);
+int csc_sweep_times(float *ms_host, int max_count, int *count_out);
+
+/* sum of squares of a dense n x ld block (dtype) into out_dev[0] (double) and
+ * the count of non-finite entries into nonfinite_dev[0] (int64, nullable). */
+int csc_sumsq(const void *x_dev, int64_t count, int dtype, double *out_dev,
+              int64_t *nonfinite_dev, void *stream);
+
+/* ---- k-means (kmeans.py:54-117), fp64 ---------------------------------- */
+/* rownorm[i] = sum_c f[i,c]^2 */
+int csc_kmeans_rownorms(const double *f_dev, int64_t n, int64_t d, int64_t ld,
+                        double *rownorm_dev, void *stream);
+/* labels[i] = first argmin_j max(0, |f_i|^2 - 2 f_i.c_j + |c_j|^2) (kmeans.py:54-61, 96-97);
+ * own_d2[i] = that minimum; counts[j] = cluster sizes (int32). c: k x ldc. */
+int csc_kmeans_assign(const double *f_dev, const double *rownorm_dev, int64_t n, int64_t d,
+                      int64_t ld, const double *c_dev, int64_t ldc, const double *cnorm_dev,
+                      int64_t k, int32_t *labels_dev, double *own_d2_dev, int32_t *counts_dev,
+                      void *stream);
+/* empty-cluster repair (kmeans.py:99-108): for each empty j ascending, move the
+ * row with the largest own_d2 (first max) to j and set its own_d2 to -1.
+ * No-op when every count is positive (checked on device; no sync). */
+int csc_kmeans_repair(int32_t *labels_dev, double *own_d2_dev, int32_t *counts_dev, int64_t n,
+                      int64_t k, void *stream);
+/* means by label (kmeans.py:80-85): c = sums / max(count,1), cnorm = |c_j|^2,
+ * counts recomputed from labels; deterministic (fixed-order partials). */
+int csc_kmeans_update(const double *f_dev, const int32_t *labels_dev, int64_t n, int64_t d,
+                      int64_t ld, int64_t k, double *c_dev, int64_t ldc, double *cnorm_dev,
+                      int32_t *counts_dev, void *stream);
+/* cost2 = sum_i |f_i - c_{label_i}|^2 (kmeans.py:111) into cost2_dev[0] */
+int csc_kmeans_cost(const double *f_dev, const int32_t *labels_dev, const double *c_dev,
+                    int64_t ldc, int64_t n, int64_t d, int64_t ld, double *cost2_dev,
+                    void *stream);
+/* k-means++ (kmeans.py:64-77). Rows are split into `nchunks` contiguous
+ * chunks (use csc_kmeanspp_nchunks(n)); closest = (first ? d2 : min(closest,
+ * d2)) with d2 = |f_i - c_row|^2 (difference form), chunk_sums_dev[b] = the
+ * chunk's sum of closest, total_dev[0] (nullable) = their sum in order. */
+int csc_kmeanspp_nchunks(int64_t n);
+int csc_kmeanspp_dist(const double *f_dev, int64_t n, int64_t d, int64_t ld,
+                      const double *c_row_dev, double *closest_dev, int first,
+                      double *chunk_sums_dev, int64_t nchunks, double *total_dev,
+                      void *stream);
+/* D^2 draw for one uniform u: idx = first i with closest_i > 0 and
+ * prefix_i > u * total (Generator.choice(n, p=closest/total) ==
+ * searchsorted(cumsum(p), u, 'right')). If fixed_idx >= 0 it is used instead
+ * (the reference's rng.integers(n) paths). Copies row idx of f into
+ * c_row_dev and writes idx to idx_dev[0] (int64). */
+int csc_kmeanspp_pick(const double *f_dev, int64_t n, int64_t d, int64_t ld,
+                      const double *closest_dev, const double *chunk_sums_dev,
+                      int64_t nchunks, double u, int64_t fixed_idx, double *c_row_dev,
+                      int64_t *idx_dev, void *stream);
+
+/* ---- dense helpers ------------------------------------------------------ */
+/* dst[:, j] = src[:, cols[j]] for j < ncols (row-major, f64), the Theta
+ * assembly of dynamic.py:163-168. cols_dev: int64. */
+int csc_gather_columns(const double *src_dev, int64_t n, int64_t ld_src, const int64_t *cols_dev,
+                       int64_t ncols, double *dst_dev, int64_t ld_dst, int64_t dst_col0,
+                       void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSC_B200_H */

@@ -1,0 +1,1011 @@
+// Fused Chebyshev SpMM filter for sm_100a (the hot path of
+// cscluster.filters.apply_filter, filters.py:155-187).
+//
+// Operator. The reference applies x(L) = I - s L (s = 2/lambda_max) as
+// v - s*(L@v) (filters.py:172-176). The plan stores M = I - s L explicitly in
+// CSR (built once on device, exact zeros dropped), so one order is a pure SpMM
+// plus a row-local epilogue:
+//     T_1     = M x,                 out  = c_0 x + c_1 T_1
+//     T_{j+1} = 2 M T_j - T_{j-1},   out += c_j T_{j+1}
+// For the normalized Laplacian and s = 1 the diagonal of M is exactly zero,
+// so M is D^-1/2 W D^-1/2 (one gather fewer per row than L), and isolated
+// rows carry M_ii = 1.
+//
+// Layout. Dense blocks are row-major with a 16-byte-multiple row stride, so a
+// nonzero gathers one contiguous row of T_j with 128-bit loads. A group of G
+// lanes owns one row; lane l loads vectors l, l+G, ... of each gathered row.
+// Column indices and values of the row are loaded cooperatively (one per lane)
+// and broadcast with width-G shuffles; four gathered rows are in flight per
+// lane before their FMAs (memory-level parallelism for the HBM-bound gather).
+//
+// Skew. Rows with more than kLongThr stored entries are excluded from the
+// main sweep and split into kSeg-entry segments, one warp per segment; the
+// segment partials are summed in segment order by a finishing kernel, so the
+// result is independent of scheduling.
+//
+// Determinism. Every output element is produced by exactly one thread with a
+// fixed accumulation order; the optional ||out||^2 uses fixed per-block
+// partials reduced in block order.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kLongThr = 1024;  // rows with more entries go to the segment path
+constexpr int kSeg = 512;       // entries per segment of a long row
+
+template <typename T>
+struct V16;
+template <>
+struct V16<double> {
+  using V = double2;
+  static constexpr int E = 2;
+};
+template <>
+struct V16<float> {
+  using V = float4;
+  static constexpr int E = 4;
+};
+
+__device__ __forceinline__ double2 vzero(double2) { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ float4 vzero(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+__device__ __forceinline__ void vfma(double2 &acc, double a, const double2 &x) {
+  acc.x = fma(a, x.x, acc.x);
+  acc.y = fma(a, x.y, acc.y);
+}
+__device__ __forceinline__ void vfma(float4 &acc, float a, const float4 &x) {
+  acc.x = fmaf(a, x.x, acc.x);
+  acc.y = fmaf(a, x.y, acc.y);
+  acc.z = fmaf(a, x.z, acc.z);
+  acc.w = fmaf(a, x.w, acc.w);
+}
+__device__ __forceinline__ void vadd(double2 &acc, const double2 &x) {
+  acc.x += x.x;
+  acc.y += x.y;
+}
+__device__ __forceinline__ void vadd(float4 &acc, const float4 &x) {
+  acc.x += x.x;
+  acc.y += x.y;
+  acc.z += x.z;
+  acc.w += x.w;
+}
+__device__ __forceinline__ double vdot(const double2 &a, const double2 &b) {
+  return a.x * b.x + a.y * b.y;
+}
+__device__ __forceinline__ double vdot(const float4 &a, const float4 &b) {
+  return (double)a.x * b.x + (double)a.y * b.y + (double)a.z * b.z + (double)a.w * b.w;
+}
+
+// Row epilogue shared by all sweeps. Modes:
+//   kFirst: T_1 = acc;            out = ca*x + cb*T_1     (prev = x)
+//   kMid:   T_{j+1} = 2acc - T_{j-1}; out += ca*T_{j+1}
+//   kMoment: T_{j+1} = 2acc - T_{j-1} (or acc for the first order);
+//            m0 += <T_{j+1},T_{j+1}>, m1 += <T_{j+1}, T_j>   (no out)
+enum { kFirst = 0, kMid = 1, kMomFirst = 2, kMomMid = 3 };
+
+template <int MODE>
+__device__ __forceinline__ void epilogue(double2 acc, const double2 *prev, const double2 *own,
+                                         double2 *next, double2 *out, size_t off, double ca,
+                                         double cb, double &s0, double &s1, bool sumsq) {
+  if (MODE == kFirst) {
+    const double2 x = prev[off];
+    next[off] = acc;
+    double2 o;
+    o.x = fma(cb, acc.x, ca * x.x);
+    o.y = fma(cb, acc.y, ca * x.y);
+    out[off] = o;
+    if (sumsq) s0 += vdot(o, o);
+  } else if (MODE == kMid) {
+    const double2 p = prev[off];
+    double2 t;
+    t.x = 2.0 * acc.x - p.x;
+    t.y = 2.0 * acc.y - p.y;
+    next[off] = t;
+    double2 o = out[off];
+    o.x = fma(ca, t.x, o.x);
+    o.y = fma(ca, t.y, o.y);
+    out[off] = o;
+    if (sumsq) s0 += vdot(o, o);
+  } else {
+    double2 t = acc;
+    if (MODE == kMomMid) {
+      const double2 p = prev[off];
+      t.x = 2.0 * acc.x - p.x;
+      t.y = 2.0 * acc.y - p.y;
+    }
+    next[off] = t;
+    const double2 c = own[off];
+    s0 += vdot(t, t);
+    s1 += vdot(t, c);
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void epilogue(float4 acc, const float4 *prev, const float4 *own,
+                                         float4 *next, float4 *out, size_t off, double ca,
+                                         double cb, double &s0, double &s1, bool sumsq) {
+  const float a = (float)ca, b = (float)cb;
+  if (MODE == kFirst) {
+    const float4 x = prev[off];
+    next[off] = acc;
+    float4 o;
+    o.x = fmaf(b, acc.x, a * x.x);
+    o.y = fmaf(b, acc.y, a * x.y);
+    o.z = fmaf(b, acc.z, a * x.z);
+    o.w = fmaf(b, acc.w, a * x.w);
+    out[off] = o;
+    if (sumsq) s0 += vdot(o, o);
+  } else if (MODE == kMid) {
+    const float4 p = prev[off];
+    float4 t;
+    t.x = 2.f * acc.x - p.x;
+    t.y = 2.f * acc.y - p.y;
+    t.z = 2.f * acc.z - p.z;
+    t.w = 2.f * acc.w - p.w;
+    next[off] = t;
+    float4 o = out[off];
+    o.x = fmaf(a, t.x, o.x);
+    o.y = fmaf(a, t.y, o.y);
+    o.z = fmaf(a, t.z, o.z);
+    o.w = fmaf(a, t.w, o.w);
+    out[off] = o;
+    if (sumsq) s0 += vdot(o, o);
+  } else {
+    float4 t = acc;
+    if (MODE == kMomMid) {
+      const float4 p = prev[off];
+      t.x = 2.f * acc.x - p.x;
+      t.y = 2.f * acc.y - p.y;
+      t.z = 2.f * acc.z - p.z;
+      t.w = 2.f * acc.w - p.w;
+    }
+    next[off] = t;
+    const float4 c = own[off];
+    s0 += vdot(t, t);
+    s1 += vdot(t, c);
+  }
+}
+
+struct SweepArgs {
+  const int32_t *indptr;
+  const int32_t *indices;
+  const void *vals;
+  int64_t n;
+  int nvec;       // 16-byte vectors per row actually used (chunk width)
+  int64_t ldv;    // row stride in 16-byte vectors
+  const void *gat;   // T_j (gathered)
+  const void *prev;  // T_{j-1}, or x for the first order
+  const void *own;   // T_j own rows (moments only)
+  void *next;        // T_{j+1}
+  void *out;
+  double ca, cb;
+  double *partials;  // per-block partial sums (nullable unless sumsq/moments)
+  int sumsq;
+};
+
+// Gather-accumulate of entries [beg, end) of one row into acc[VPL] by a group
+// of G lanes (glane = lane within group, gmask = the group's lanes).
+template <typename T, int G, int VPL>
+__device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
+                                           const T *__restrict__ vals,
+                                           const typename V16<T>::V *__restrict__ gat, int beg,
+                                           int end, int glane, unsigned gmask, int nvec,
+                                           int64_t ldv, typename V16<T>::V (&acc)[VPL]) {
+  using VT = typename V16<T>::V;
+  for (int base = beg; base < end; base += G) {
+    const int nz = base + glane;
+    int my_col = 0;
+    T my_val = T(0);
+    if (nz < end) {
+      my_col = __ldg(indices + nz);
+      my_val = __ldg(vals + nz);
+    }
+    const int cnt = min(G, end - base);
+    int u = 0;
+    for (; u + 4 <= cnt; u += 4) {
+      int c[4];
+      T a[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        c[t] = __shfl_sync(gmask, my_col, u + t, G);
+        a[t] = __shfl_sync(gmask, my_val, u + t, G);
+      }
+      VT x[4][VPL];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const VT *src = gat + (int64_t)c[t] * ldv;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const int v = glane + q * G;
+          x[t][q] = (v < nvec) ? __ldg(src + v) : vzero(VT());
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) vfma(acc[q], a[t], x[t][q]);
+    }
+    for (; u < cnt; ++u) {
+      const int c0 = __shfl_sync(gmask, my_col, u, G);
+      const T a0 = __shfl_sync(gmask, my_val, u, G);
+      const VT *src = gat + (int64_t)c0 * ldv;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int v = glane + q * G;
+        if (v < nvec) vfma(acc[q], a0, __ldg(src + v));
+      }
+    }
+  }
+}
+
+// One Chebyshev order over all rows with at most kLongThr entries.
+template <typename T, int G, int VPL, int MODE>
+__global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs A) {
+  using VT = typename V16<T>::V;
+  __shared__ double red[kBlock / 32];
+  const int lane = threadIdx.x & 31;
+  const int glane = lane % G;
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((lane / G) * G));
+  const int groups_per_block = kBlock / G;
+  const int64_t ngroups = (int64_t)gridDim.x * groups_per_block;
+  const T *vals = static_cast<const T *>(A.vals);
+  const VT *gat = static_cast<const VT *>(A.gat);
+  const VT *prev = static_cast<const VT *>(A.prev);
+  const VT *own = static_cast<const VT *>(A.own);
+  VT *next = static_cast<VT *>(A.next);
+  VT *out = static_cast<VT *>(A.out);
+  double s0 = 0.0, s1 = 0.0;
+  const bool sumsq = A.sumsq != 0;
+
+  for (int64_t row = (int64_t)blockIdx.x * groups_per_block + threadIdx.x / G; row < A.n;
+       row += ngroups) {
+    const int beg = __ldg(A.indptr + row), end = __ldg(A.indptr + row + 1);
+    if (end - beg > kLongThr) continue;  // segment path
+    VT acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = vzero(VT());
+    gather_row<T, G, VPL>(A.indices, vals, gat, beg, end, glane, gmask, A.nvec, A.ldv, acc);
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int v = glane + q * G;
+      if (v < A.nvec)
+        epilogue<MODE>(acc[q], prev, own, next, out, (size_t)row * A.ldv + v, A.ca, A.cb, s0,
+                       s1, sumsq);
+    }
+  }
+  if (A.partials) {
+    const double b0 = block_sum<kBlock>(s0, red);
+    if (MODE >= kMomFirst) {
+      const double b1 = block_sum<kBlock>(s1, red);
+      if (threadIdx.x == 0) {
+        A.partials[2 * blockIdx.x] = b0;
+        A.partials[2 * blockIdx.x + 1] = b1;
+      }
+    } else if (threadIdx.x == 0) {
+      A.partials[blockIdx.x] = b0;
+    }
+  }
+}
+
+// Long rows, phase 1: one warp per kSeg-entry segment -> scratch[seg].
+template <typename T, int VPL>
+__global__ void __launch_bounds__(kBlock)
+    long_partial_kernel(SweepArgs A, const int32_t *__restrict__ long_rows,
+                        const int32_t *__restrict__ seg_off, int64_t n_long, int64_t n_seg,
+                        typename V16<T>::V *__restrict__ scratch) {
+  using VT = typename V16<T>::V;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
+  const T *vals = static_cast<const T *>(A.vals);
+  const VT *gat = static_cast<const VT *>(A.gat);
+  for (int64_t s = (int64_t)blockIdx.x * (kBlock / 32) + threadIdx.x / 32; s < n_seg;
+       s += warps) {
+    // long row owning segment s: last r with seg_off[r] <= s
+    int64_t lo = 0, hi = n_long - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (__ldg(seg_off + mid) <= s) lo = mid; else hi = mid - 1;
+    }
+    const int row = __ldg(long_rows + lo);
+    const int rbeg = __ldg(A.indptr + row), rend = __ldg(A.indptr + row + 1);
+    const int beg = rbeg + (int)(s - __ldg(seg_off + lo)) * kSeg;
+    const int end = min(beg + kSeg, rend);
+    VT acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = vzero(VT());
+    gather_row<T, 32, VPL>(A.indices, vals, gat, beg, end, lane, 0xffffffffu, A.nvec, A.ldv, acc);
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int v = lane + q * 32;
+      if (v < A.nvec) scratch[s * A.ldv + v] = acc[q];
+    }
+  }
+}
+
+// Long rows, phase 2: one warp per long row sums its segments in order and
+// applies the epilogue. Partials go after the main sweep's.
+template <typename T, int VPL, int MODE>
+__global__ void __launch_bounds__(kBlock)
+    long_finish_kernel(SweepArgs A, const int32_t *__restrict__ long_rows,
+                       const int32_t *__restrict__ seg_off, int64_t n_long,
+                       const typename V16<T>::V *__restrict__ scratch, int64_t partial_base) {
+  using VT = typename V16<T>::V;
+  __shared__ double red[kBlock / 32];
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
+  const VT *prev = static_cast<const VT *>(A.prev);
+  const VT *own = static_cast<const VT *>(A.own);
+  VT *next = static_cast<VT *>(A.next);
+  VT *out = static_cast<VT *>(A.out);
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * (kBlock / 32) + threadIdx.x / 32; r < n_long;
+       r += warps) {
+    const int row = long_rows[r];
+    VT acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = vzero(VT());
+    for (int64_t s = seg_off[r]; s < seg_off[r + 1]; ++s) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int v = lane + q * 32;
+        if (v < A.nvec) vadd(acc[q], scratch[s * A.ldv + v]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int v = lane + q * 32;
+      if (v < A.nvec)
+        epilogue<MODE>(acc[q], prev, own, next, out, (size_t)row * A.ldv + v, A.ca, A.cb, s0,
+                       s1, A.sumsq != 0);
+    }
+  }
+  if (A.partials) {
+    const double b0 = block_sum<kBlock>(s0, red);
+    if (MODE >= kMomFirst) {
+      const double b1 = block_sum<kBlock>(s1, red);
+      if (threadIdx.x == 0) {
+        A.partials[2 * (partial_base + blockIdx.x)] = b0;
+        A.partials[2 * (partial_base + blockIdx.x) + 1] = b1;
+      }
+    } else if (threadIdx.x == 0) {
+      A.partials[partial_base + blockIdx.x] = b0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Plan construction: M = I - s L, schedule of long rows
+// ---------------------------------------------------------------------------
+
+__global__ void op_count_kernel(const int32_t *__restrict__ indptr,
+                                const int32_t *__restrict__ indices,
+                                const double *__restrict__ vals, int64_t n, double s,
+                                int32_t *__restrict__ counts) {
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    int cnt = 0;
+    double lii = 0.0;
+    for (int jj = indptr[row]; jj < indptr[row + 1]; ++jj) {
+      if (indices[jj] == row) {
+        lii = vals[jj];
+      } else if (-s * vals[jj] != 0.0) {
+        ++cnt;
+      }
+    }
+    if (1.0 - s * lii != 0.0) ++cnt;
+    counts[row] = cnt;
+  }
+}
+
+template <typename T>
+__global__ void op_fill_kernel(const int32_t *__restrict__ indptr,
+                               const int32_t *__restrict__ indices,
+                               const double *__restrict__ vals, int64_t n, double s,
+                               const int32_t *__restrict__ mptr, int32_t *__restrict__ mcol,
+                               T *__restrict__ mval) {
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    double lii = 0.0;
+    for (int jj = indptr[row]; jj < indptr[row + 1]; ++jj)
+      if (indices[jj] == row) lii = vals[jj];
+    const double dii = 1.0 - s * lii;
+    int pos = mptr[row];
+    bool placed = (dii == 0.0);
+    for (int jj = indptr[row]; jj < indptr[row + 1]; ++jj) {
+      const int c = indices[jj];
+      if (c == row) continue;
+      if (!placed && c > row) {
+        mcol[pos] = (int32_t)row;
+        mval[pos] = (T)dii;
+        ++pos;
+        placed = true;
+      }
+      const double v = -s * vals[jj];
+      if (v != 0.0) {
+        mcol[pos] = c;
+        mval[pos] = (T)v;
+        ++pos;
+      }
+    }
+    if (!placed) {
+      mcol[pos] = (int32_t)row;
+      mval[pos] = (T)dii;
+    }
+  }
+}
+
+struct IsLong {
+  const int32_t *counts;
+  __device__ bool operator()(int32_t row) const { return counts[row] > kLongThr; }
+};
+
+__global__ void seg_count_kernel(const int32_t *__restrict__ long_rows,
+                                 const int32_t *__restrict__ counts, int64_t n_long,
+                                 int32_t *__restrict__ seg_cnt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_long;
+       r += (int64_t)gridDim.x * blockDim.x)
+    seg_cnt[r] = (counts[long_rows[r]] + kSeg - 1) / kSeg;
+}
+
+__global__ void sumsq_kernel(const double2 *__restrict__ x2, int64_t nvec2,
+                             const double *__restrict__ tail, int64_t ntail,
+                             double *__restrict__ partials, unsigned long long *nonfinite) {
+  __shared__ double red[kBlock / 32];
+  double s = 0.0;
+  unsigned long long bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < nvec2;
+       i += (int64_t)gridDim.x * kBlock) {
+    const double2 v = __ldg(x2 + i);
+    s += v.x * v.x + v.y * v.y;
+    bad += !isfinite(v.x) + !isfinite(v.y);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ntail) {
+    const double v = tail[threadIdx.x];
+    s += v * v;
+    bad += !isfinite(v);
+  }
+  const double b = block_sum<kBlock>(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+  if (nonfinite && bad) atomicAdd(nonfinite, bad);
+}
+
+__global__ void sumsq_f32_kernel(const float4 *__restrict__ x4, int64_t nvec4,
+                                 const float *__restrict__ tail, int64_t ntail,
+                                 double *__restrict__ partials, unsigned long long *nonfinite) {
+  __shared__ double red[kBlock / 32];
+  double s = 0.0;
+  unsigned long long bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < nvec4;
+       i += (int64_t)gridDim.x * kBlock) {
+    const float4 v = __ldg(x4 + i);
+    s += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+    bad += !isfinite(v.x) + !isfinite(v.y) + !isfinite(v.z) + !isfinite(v.w);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ntail) {
+    const float v = tail[threadIdx.x];
+    s += (double)v * v;
+    bad += !isfinite(v);
+  }
+  const double b = block_sum<kBlock>(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+  if (nonfinite && bad) atomicAdd(nonfinite, bad);
+}
+
+// mu from the per-order moment sums (see csc_cheb_moments):
+//   mu_{2j}   = 2 <T_j,T_j>     - mu_0
+//   mu_{2j+1} = 2 <T_{j+1},T_j> - mu_1
+__global__ void moments_finish_kernel(const double *__restrict__ sums /* [m+1][2] */, int m,
+                                      double mu0, double *__restrict__ mu) {
+  // sums[2*j]   = <T_j, T_j>      (j = 1..m), sums[0] = <x,x>
+  // sums[2*j+1] = <T_j, T_{j-1}>  (j = 1..m)
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double m0 = sums[0];
+  mu[0] = m0;
+  const double m1 = sums[3];  // <T_1, T_0>
+  mu[1] = m1;
+  for (int j = 1; j <= m; ++j) mu[2 * j] = 2.0 * sums[2 * j] - m0;
+  for (int j = 1; j < m; ++j) mu[2 * j + 1] = 2.0 * sums[2 * (j + 1) + 1] - m1;
+  (void)mu0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Plan object
+// ---------------------------------------------------------------------------
+
+// Optional per-sweep CUDA-event timing (bench.py reads the durations of the
+// dominant kernel inside its timed region). Off unless enabled.
+namespace sweeptime {
+constexpr int kCap = 4096;
+static bool enabled = false;
+static cudaEvent_t ev[2 * kCap];
+static int count = 0;
+static bool created = false;
+}  // namespace sweeptime
+
+struct csc_chebop {
+  int64_t n = 0, nnz = 0;
+  int dtype = CSC_F64;
+  double scale = 1.0;
+  int32_t *indptr = nullptr;
+  int32_t *indices = nullptr;
+  void *vals = nullptr;
+  int32_t *long_rows = nullptr;
+  int32_t *seg_off = nullptr;
+  int64_t n_long = 0, n_seg = 0;
+  cudaStream_t stream = nullptr;  // last stream used (for stream-ordered free)
+};
+
+namespace {
+
+template <typename T, int G, int VPL, int MODE>
+int launch_sweep(const SweepArgs &A, int grid, cudaStream_t st) {
+  const bool timed = sweeptime::enabled && sweeptime::count < sweeptime::kCap;
+  if (timed) cudaEventRecord(sweeptime::ev[2 * sweeptime::count], st);
+  sweep_kernel<T, G, VPL, MODE><<<grid, kBlock, 0, st>>>(A);
+  CSC_CHECK_LAUNCH();
+  if (timed) {
+    cudaEventRecord(sweeptime::ev[2 * sweeptime::count + 1], st);
+    ++sweeptime::count;
+  }
+  return CSC_OK;
+}
+
+template <typename T, int G, int VPL>
+int sweep_grid() {
+  static int occ = 0;
+  if (occ == 0) {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, sweep_kernel<T, G, VPL, kMid>, kBlock, 0);
+    occ = o > 0 ? o : 1;
+  }
+  return occ * csc::device_info().sm_count;
+}
+
+template <typename T, int G, int VPL>
+int run_order_gv(const csc_chebop &op, SweepArgs A, int mode, double *partials,
+                 int64_t &nparts, cudaStream_t st, void *seg_scratch) {
+  using VT = typename V16<T>::V;
+  const int64_t groups_per_block = kBlock / G;
+  int grid = (int)std::min<int64_t>(sweep_grid<T, G, VPL>(),
+                                    std::max<int64_t>(1, csc::ceil_div(op.n, groups_per_block)));
+  A.partials = partials;
+  int rc = CSC_OK;
+  switch (mode) {
+    case kFirst: rc = launch_sweep<T, G, VPL, kFirst>(A, grid, st); break;
+    case kMid: rc = launch_sweep<T, G, VPL, kMid>(A, grid, st); break;
+    case kMomFirst: rc = launch_sweep<T, G, VPL, kMomFirst>(A, grid, st); break;
+    default: rc = launch_sweep<T, G, VPL, kMomMid>(A, grid, st); break;
+  }
+  if (rc != CSC_OK) return rc;
+  nparts = grid;
+  if (op.n_long > 0) {
+    constexpr int LV = (VPL * G + 31) / 32;  // vectors per lane at G = 32
+    const int pgrid = (int)std::min<int64_t>(csc::device_info().sm_count * 8,
+                                             csc::ceil_div(op.n_seg, kBlock / 32));
+    long_partial_kernel<T, LV><<<pgrid, kBlock, 0, st>>>(A, op.long_rows, op.seg_off, op.n_long,
+                                                         op.n_seg, static_cast<VT *>(seg_scratch));
+    CSC_CHECK_LAUNCH();
+    const int fgrid = (int)std::min<int64_t>(csc::device_info().sm_count * 4,
+                                             csc::ceil_div(op.n_long, kBlock / 32));
+    const VT *sc = static_cast<const VT *>(seg_scratch);
+    switch (mode) {
+      case kFirst:
+        long_finish_kernel<T, LV, kFirst><<<fgrid, kBlock, 0, st>>>(A, op.long_rows, op.seg_off,
+                                                                    op.n_long, sc, grid);
+        break;
+      case kMid:
+        long_finish_kernel<T, LV, kMid><<<fgrid, kBlock, 0, st>>>(A, op.long_rows, op.seg_off,
+                                                                  op.n_long, sc, grid);
+        break;
+      case kMomFirst:
+        long_finish_kernel<T, LV, kMomFirst><<<fgrid, kBlock, 0, st>>>(
+            A, op.long_rows, op.seg_off, op.n_long, sc, grid);
+        break;
+      default:
+        long_finish_kernel<T, LV, kMomMid><<<fgrid, kBlock, 0, st>>>(A, op.long_rows, op.seg_off,
+                                                                     op.n_long, sc, grid);
+        break;
+    }
+    CSC_CHECK_LAUNCH();
+    nparts += fgrid;
+  }
+  return CSC_OK;
+}
+
+// upper bound of partial slots one order can use
+int64_t max_partials(const csc_chebop &op) {
+  const int64_t sms = csc::device_info().sm_count;
+  return sms * 32 + sms * 4 + 8;
+}
+
+template <typename T>
+int run_order(const csc_chebop &op, const SweepArgs &A, int mode, double *partials,
+              int64_t &nparts, cudaStream_t st, void *seg_scratch) {
+  const int nvec = A.nvec;
+  if (nvec <= 4) return run_order_gv<T, 4, 1>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (nvec <= 8) return run_order_gv<T, 8, 1>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (nvec <= 16) return run_order_gv<T, 16, 1>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (nvec <= 32) return run_order_gv<T, 32, 1>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (nvec <= 64) return run_order_gv<T, 32, 2>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (nvec <= 128) return run_order_gv<T, 32, 4>(op, A, mode, partials, nparts, st, seg_scratch);
+  return run_order_gv<T, 32, 8>(op, A, mode, partials, nparts, st, seg_scratch);
+}
+
+constexpr int kMaxVecChunk = 256;  // widest row chunk one sweep handles
+
+template <typename T>
+int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *coeffs,
+                  int ncoeffs, T *out, T *work, double *sumsq_dev, cudaStream_t st) {
+  using VT = typename V16<T>::V;
+  constexpr int E = V16<T>::E;
+  const int64_t ldv = ld / E;
+  const int64_t n = op.n;
+  csc::Scratch parts, segs;
+  const int64_t maxp = max_partials(op);
+  CSC_TRY_CUDA(parts.alloc(sizeof(double) * maxp, st));
+  if (op.n_long > 0)
+    CSC_TRY_CUDA(segs.alloc(sizeof(VT) * (size_t)op.n_seg * ldv, st));
+  const int64_t nchunks = csc::ceil_div(ldv, kMaxVecChunk);
+  const bool fused_sumsq = sumsq_dev && nchunks == 1;
+  for (int64_t ch = 0; ch < nchunks; ++ch) {
+    const int64_t v0 = ch * kMaxVecChunk;
+    const int nvec = (int)std::min<int64_t>(kMaxVecChunk, ldv - v0);
+    const VT *xv = reinterpret_cast<const VT *>(x) + v0;
+    VT *ta = reinterpret_cast<VT *>(work) + v0;
+    VT *tb = reinterpret_cast<VT *>(work + n * ld) + v0;
+    VT *ov = reinterpret_cast<VT *>(out) + v0;
+    SweepArgs A{};
+    A.indptr = op.indptr;
+    A.indices = op.indices;
+    A.vals = op.vals;
+    A.n = n;
+    A.nvec = nvec;
+    A.ldv = ldv;
+    A.out = ov;
+    // order 1
+    A.gat = xv;
+    A.prev = xv;
+    A.next = ta;
+    A.ca = coeffs[0];
+    A.cb = coeffs[1];
+    A.sumsq = (fused_sumsq && ncoeffs == 2) ? 1 : 0;
+    int64_t np = 0;
+    int rc = run_order<T>(op, A, kFirst, A.sumsq ? parts.as<double>() : nullptr, np, st,
+                          segs.ptr);
+    if (rc != CSC_OK) return rc;
+    const VT *t_prev = xv;
+    VT *t_cur = ta, *t_next = tb;
+    for (int j = 2; j < ncoeffs; ++j) {
+      A.gat = t_cur;
+      A.prev = t_prev;
+      A.next = t_next;
+      A.ca = coeffs[j];
+      A.cb = 0.0;
+      A.sumsq = (fused_sumsq && j == ncoeffs - 1) ? 1 : 0;
+      rc = run_order<T>(op, A, kMid, A.sumsq ? parts.as<double>() : nullptr, np, st, segs.ptr);
+      if (rc != CSC_OK) return rc;
+      t_prev = t_cur;
+      t_cur = t_next;
+      t_next = const_cast<VT *>(t_prev);  // T_{j+1} overwrites T_{j-1} row-locally
+    }
+    if (fused_sumsq) {
+      reduce_partials_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), np, sumsq_dev);
+      CSC_CHECK_LAUNCH();
+    }
+  }
+  if (sumsq_dev && !fused_sumsq) return csc_sumsq(out, n * ld, op.dtype, sumsq_dev, nullptr, st);
+  return CSC_OK;
+}
+
+
+// fixed-order reduction of interleaved (s0, s1) block partials into out[0..1]
+__global__ void reduce_pairs_kernel(const double *__restrict__ partials, int64_t count,
+                                    double *__restrict__ out) {
+  __shared__ double smem[32];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
+    a += partials[2 * i];
+    b += partials[2 * i + 1];
+  }
+  a = block_sum<1024>(a, smem);
+  b = block_sum<1024>(b, smem);
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+template <typename T>
+int cheb_moments_t(const csc_chebop &op, const T *x, int64_t ld, int m, double *mu, T *work,
+                   cudaStream_t st) {
+  using VT = typename V16<T>::V;
+  constexpr int E = V16<T>::E;
+  const int64_t ldv = ld / E;
+  const int64_t n = op.n;
+  CSC_REQUIRE(ldv <= kMaxVecChunk, "csc_cheb_moments: rows wider than %d vectors unsupported",
+              kMaxVecChunk);
+  csc::Scratch parts, segs, sums;
+  const int64_t maxp = max_partials(op);
+  CSC_TRY_CUDA(parts.alloc(sizeof(double) * 2 * maxp, st));
+  CSC_TRY_CUDA(sums.alloc(sizeof(double) * 2 * (m + 1), st));
+  if (op.n_long > 0) CSC_TRY_CUDA(segs.alloc(sizeof(VT) * (size_t)op.n_seg * ldv, st));
+  double *S = sums.as<double>();
+  // S[0] = <x, x>; S[2j] = <T_j,T_j>, S[2j+1] = <T_j,T_{j-1}> for j = 1..m
+  int rc = csc_sumsq(x, n * ld, op.dtype, S, nullptr, st);
+  if (rc != CSC_OK) return rc;
+  const VT *xv = reinterpret_cast<const VT *>(x);
+  VT *ta = reinterpret_cast<VT *>(work);
+  VT *tb = reinterpret_cast<VT *>(work + n * ld);
+  SweepArgs A{};
+  A.indptr = op.indptr;
+  A.indices = op.indices;
+  A.vals = op.vals;
+  A.n = n;
+  A.nvec = (int)ldv;
+  A.ldv = ldv;
+  const VT *t_prev = nullptr;
+  const VT *t_cur = xv;
+  VT *t_next = ta;
+  for (int j = 0; j < m; ++j) {  // produces T_{j+1}
+    A.gat = t_cur;
+    A.own = t_cur;
+    A.prev = t_prev;
+    A.next = t_next;
+    int64_t np = 0;
+    rc = run_order<T>(op, A, j == 0 ? kMomFirst : kMomMid, parts.as<double>(), np, st, segs.ptr);
+    if (rc != CSC_OK) return rc;
+    reduce_pairs_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), np, S + 2 * (j + 1));
+    CSC_CHECK_LAUNCH();
+    t_prev = t_cur;
+    t_cur = t_next;
+    t_next = (j == 0) ? tb : const_cast<VT *>(t_prev);
+  }
+  moments_finish_kernel<<<1, 32, 0, st>>>(S, m, 0.0, mu);
+  CSC_CHECK_LAUNCH();
+  return CSC_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const double *vals,
+                      int64_t n, int64_t nnz, double scale, int dtype, void *stream,
+                      csc_chebop **op_out) {
+  csc::clear_error();
+  CSC_REQUIRE(op_out != nullptr, "csc_chebop_create: op_out is NULL");
+  CSC_REQUIRE(n >= 0 && nnz >= 0, "csc_chebop_create: negative size");
+  CSC_REQUIRE(n + nnz < (int64_t)INT32_MAX, "csc_chebop_create: n + nnz exceeds int32 indexing");
+  CSC_REQUIRE(dtype == CSC_F64 || dtype == CSC_F32, "csc_chebop_create: bad dtype %d", dtype);
+  CSC_REQUIRE(scale > 0.0 && isfinite(scale), "csc_chebop_create: scale must be positive");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  csc::device_info();
+  csc_chebop *op = new csc_chebop();
+  op->n = n;
+  op->dtype = dtype;
+  op->scale = scale;
+  op->stream = st;
+  auto fail = [&](int rc) {
+    csc_chebop_destroy(op);
+    return rc;
+  };
+  const size_t esz = dtype == CSC_F64 ? 8 : 4;
+  const int threads = 256;
+  const int grid = (int)std::min<int64_t>(csc::device_info().sm_count * 16,
+                                          std::max<int64_t>(1, csc::ceil_div(n, threads)));
+  // row counts of M
+  csc::Scratch counts, scan_tmp;
+  if (cudaMallocAsync((void **)&op->indptr, sizeof(int32_t) * (n + 1), st) != cudaSuccess) {
+    csc::set_error("csc_chebop_create: allocation failed");
+    return fail(CSC_ERR_CUDA);
+  }
+  if (counts.alloc(sizeof(int32_t) * (n + 1), st) != cudaSuccess) return fail(CSC_ERR_CUDA);
+  cudaMemsetAsync(counts.ptr, 0, sizeof(int32_t) * (n + 1), st);
+  if (n > 0) op_count_kernel<<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale,
+                                                        counts.as<int32_t>());
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts.as<int32_t>(), op->indptr, n + 1, st);
+  if (scan_tmp.alloc(tmp_bytes, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
+  cub::DeviceScan::ExclusiveSum(scan_tmp.ptr, tmp_bytes, counts.as<int32_t>(), op->indptr, n + 1,
+                                st);
+  int32_t mnnz = 0;
+  if (cudaMemcpyAsync(&mnnz, op->indptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    csc::set_error("csc_chebop_create: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(CSC_ERR_CUDA);
+  }
+  op->nnz = mnnz;
+  if (cudaMallocAsync((void **)&op->indices, sizeof(int32_t) * std::max<int64_t>(mnnz, 1), st) !=
+          cudaSuccess ||
+      cudaMallocAsync(&op->vals, esz * std::max<int64_t>(mnnz, 1), st) != cudaSuccess) {
+    csc::set_error("csc_chebop_create: allocation failed");
+    return fail(CSC_ERR_CUDA);
+  }
+  if (n > 0) {
+    if (dtype == CSC_F64)
+      op_fill_kernel<double><<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale, op->indptr,
+                                                       op->indices,
+                                                       static_cast<double *>(op->vals));
+    else
+      op_fill_kernel<float><<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale, op->indptr,
+                                                      op->indices, static_cast<float *>(op->vals));
+  }
+  // long-row schedule
+  csc::Scratch nsel, sel_tmp, segcnt;
+  if (nsel.alloc(sizeof(int32_t) * 2, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
+  if (cudaMallocAsync((void **)&op->long_rows, sizeof(int32_t) * std::max<int64_t>(n, 1), st) !=
+      cudaSuccess)
+    return fail(CSC_ERR_CUDA);
+  thrust::counting_iterator<int32_t> rows_it(0);
+  IsLong pred{counts.as<int32_t>()};
+  size_t sel_bytes = 0;
+  cub::DeviceSelect::If(nullptr, sel_bytes, rows_it, op->long_rows, nsel.as<int32_t>(), n, pred, st);
+  if (sel_tmp.alloc(sel_bytes, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
+  cub::DeviceSelect::If(sel_tmp.ptr, sel_bytes, rows_it, op->long_rows, nsel.as<int32_t>(), n,
+                        pred, st);
+  int32_t n_long = 0;
+  if (cudaMemcpyAsync(&n_long, nsel.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    csc::set_error("csc_chebop_create: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(CSC_ERR_CUDA);
+  }
+  op->n_long = n_long;
+  if (n_long > 0) {
+    if (segcnt.alloc(sizeof(int32_t) * (n_long + 1), st) != cudaSuccess ||
+        cudaMallocAsync((void **)&op->seg_off, sizeof(int32_t) * (n_long + 1), st) != cudaSuccess)
+      return fail(CSC_ERR_CUDA);
+    cudaMemsetAsync(segcnt.ptr, 0, sizeof(int32_t) * (n_long + 1), st);
+    seg_count_kernel<<<(int)std::min<int64_t>(1024, csc::ceil_div(n_long, 256)), 256, 0, st>>>(
+        op->long_rows, counts.as<int32_t>(), n_long, segcnt.as<int32_t>());
+    size_t b2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, segcnt.as<int32_t>(), op->seg_off, n_long + 1, st);
+    csc::Scratch t2;
+    if (t2.alloc(b2, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
+    cub::DeviceScan::ExclusiveSum(t2.ptr, b2, segcnt.as<int32_t>(), op->seg_off, n_long + 1, st);
+    int32_t nseg = 0;
+    if (cudaMemcpyAsync(&nseg, op->seg_off + n_long, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                        st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return fail(CSC_ERR_CUDA);
+    op->n_seg = nseg;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    csc::set_error("csc_chebop_create: %s", cudaGetErrorString(e));
+    return fail(CSC_ERR_CUDA);
+  }
+  *op_out = op;
+  return CSC_OK;
+}
+
+int csc_chebop_destroy(csc_chebop *op) {
+  if (!op) return CSC_OK;
+  cudaStream_t st = op->stream;
+  if (op->indptr) cudaFreeAsync(op->indptr, st);
+  if (op->indices) cudaFreeAsync(op->indices, st);
+  if (op->vals) cudaFreeAsync(op->vals, st);
+  if (op->long_rows) cudaFreeAsync(op->long_rows, st);
+  if (op->seg_off) cudaFreeAsync(op->seg_off, st);
+  delete op;
+  return CSC_OK;
+}
+
+int csc_chebop_info(const csc_chebop *op, int64_t *n, int64_t *nnz, int64_t *n_long,
+                    int64_t *n_segments) {
+  CSC_REQUIRE(op != nullptr, "csc_chebop_info: NULL plan");
+  if (n) *n = op->n;
+  if (nnz) *nnz = op->nnz;
+  if (n_long) *n_long = op->n_long;
+  if (n_segments) *n_segments = op->n_seg;
+  return CSC_OK;
+}
+
+int csc_cheb_filter(const csc_chebop *op, const void *x, int64_t ld, int64_t d,
+                    const double *coeffs, int32_t ncoeffs, void *out, void *work,
+                    double *sumsq_dev, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(op != nullptr, "csc_cheb_filter: NULL plan");
+  CSC_REQUIRE(ncoeffs >= 2, "csc_cheb_filter: need at least 2 coefficients, got %d", ncoeffs);
+  CSC_REQUIRE(d >= 1 && ld >= d, "csc_cheb_filter: need 1 <= d <= ld");
+  const int64_t esz = op->dtype == CSC_F64 ? 8 : 4;
+  CSC_REQUIRE((ld * esz) % 16 == 0, "csc_cheb_filter: row stride must be a multiple of 16 bytes");
+  CSC_REQUIRE(aligned16(x) && aligned16(out) && aligned16(work),
+              "csc_cheb_filter: buffers must be 16-byte aligned");
+  CSC_REQUIRE(coeffs != nullptr, "csc_cheb_filter: NULL coefficients");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const_cast<csc_chebop *>(op)->stream = st;
+  if (op->n == 0) return CSC_OK;
+  if (op->dtype == CSC_F64)
+    return cheb_filter_t<double>(*op, static_cast<const double *>(x), ld, coeffs, ncoeffs,
+                                 static_cast<double *>(out), static_cast<double *>(work),
+                                 sumsq_dev, st);
+  return cheb_filter_t<float>(*op, static_cast<const float *>(x), ld, coeffs, ncoeffs,
+                              static_cast<float *>(out), static_cast<float *>(work), sumsq_dev,
+                              st);
+}
+
+int csc_cheb_moments(const csc_chebop *op, const void *x, int64_t ld, int64_t d, int32_t m,
+                     double *mu_dev, void *work, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(op != nullptr, "csc_cheb_moments: NULL plan");
+  CSC_REQUIRE(m >= 1, "csc_cheb_moments: need m >= 1");
+  CSC_REQUIRE(d >= 1 && ld >= d, "csc_cheb_moments: need 1 <= d <= ld");
+  const int64_t esz = op->dtype == CSC_F64 ? 8 : 4;
+  CSC_REQUIRE((ld * esz) % 16 == 0, "csc_cheb_moments: row stride must be a multiple of 16 bytes");
+  CSC_REQUIRE(aligned16(x) && aligned16(work), "csc_cheb_moments: buffers must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const_cast<csc_chebop *>(op)->stream = st;
+  if (op->n == 0) {
+    CSC_TRY_CUDA(cudaMemsetAsync(mu_dev, 0, sizeof(double) * (2 * m + 1), st));
+    return CSC_OK;
+  }
+  if (op->dtype == CSC_F64)
+    return cheb_moments_t<double>(*op, static_cast<const double *>(x), ld, m, mu_dev,
+                                  static_cast<double *>(work), st);
+  return cheb_moments_t<float>(*op, static_cast<const float *>(x), ld, m, mu_dev,
+                               static_cast<float *>(work), st);
+}
+
+int csc_sweep_timing(int enable) {
+  if (enable && !sweeptime::created) {
+    for (int i = 0; i < 2 * sweeptime::kCap; ++i) CSC_TRY_CUDA(cudaEventCreate(&sweeptime::ev[i]));
+    sweeptime::created = true;
+  }
+  sweeptime::enabled = enable != 0;
+  sweeptime::count = 0;
+  return CSC_OK;
+}
+
+int csc_sweep_times(float *ms_out, int max_count, int *count_out) {
+  CSC_REQUIRE(count_out != nullptr, "csc_sweep_times: NULL count_out");
+  const int c = std::min(sweeptime::count, max_count);
+  for (int i = 0; i < c; ++i) {
+    CSC_TRY_CUDA(cudaEventSynchronize(sweeptime::ev[2 * i + 1]));
+    CSC_TRY_CUDA(cudaEventElapsedTime(ms_out + i, sweeptime::ev[2 * i], sweeptime::ev[2 * i + 1]));
+  }
+  *count_out = c;
+  sweeptime::count = 0;
+  return CSC_OK;
+}
+
+int csc_sumsq(const void *x, int64_t count, int dtype, double *out_dev, int64_t *nonfinite_dev,
+              void *stream) {
+  CSC_REQUIRE(count >= 0, "csc_sumsq: negative count");
+  CSC_REQUIRE(dtype == CSC_F64 || dtype == CSC_F32, "csc_sumsq: bad dtype");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t E = dtype == CSC_F64 ? 2 : 4;
+  CSC_REQUIRE(aligned16(x) || count == 0, "csc_sumsq: buffer must be 16-byte aligned");
+  const int64_t nv = count / E, ntail = count % E;
+  const int grid = (int)std::min<int64_t>(csc::device_info().sm_count * 8,
+                                          std::max<int64_t>(1, csc::ceil_div(nv, kBlock)));
+  csc::Scratch parts;
+  CSC_TRY_CUDA(parts.alloc(sizeof(double) * grid, st));
+  if (nonfinite_dev) CSC_TRY_CUDA(cudaMemsetAsync(nonfinite_dev, 0, sizeof(int64_t), st));
+  auto *nf = reinterpret_cast<unsigned long long *>(nonfinite_dev);
+  if (dtype == CSC_F64) {
+    const double *xd = static_cast<const double *>(x);
+    sumsq_kernel<<<grid, kBlock, 0, st>>>(reinterpret_cast<const double2 *>(xd), nv,
+                                          xd + nv * E, ntail, parts.as<double>(), nf);
+  } else {
+    const float *xf = static_cast<const float *>(x);
+    sumsq_f32_kernel<<<grid, kBlock, 0, st>>>(reinterpret_cast<const float4 *>(xf), nv,
+                                              xf + nv * E, ntail, parts.as<double>(), nf);
+  }
+  CSC_CHECK_LAUNCH();
+  reduce_partials_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), grid, out_dev);
+  CSC_CHECK_LAUNCH();
+  return CSC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// Library-level entry points and shared helpers.
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace csc {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+void clear_error() { g_last_error.clear(); }
+
+const DeviceInfo &device_info() {
+  static std::mutex mu;
+  static std::vector<DeviceInfo> cache;
+  static std::vector<bool> pool_ready;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if ((int)cache.size() <= dev) {
+    cache.resize(dev + 1);
+    pool_ready.resize(dev + 1, false);
+  }
+  DeviceInfo &info = cache[dev];
+  if (info.sm_count == 0) {
+    cudaDeviceGetAttribute(&info.sm_count, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&info.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&info.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cudaDeviceGetAttribute(&info.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (info.sm_count <= 0) info.sm_count = 148;
+  }
+  if (!pool_ready[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    pool_ready[dev] = true;
+  }
+  return info;
+}
+
+cudaError_t Scratch::alloc(size_t bytes, cudaStream_t s) {
+  stream = s;
+  if (bytes == 0) bytes = 16;
+  return cudaMallocAsync(&ptr, bytes, s);
+}
+
+Scratch::~Scratch() {
+  if (ptr) cudaFreeAsync(ptr, stream);
+}
+
+}  // namespace csc
+
+__global__ void reduce_partials_kernel(const double *__restrict__ partials, int64_t count,
+                                       double *__restrict__ out) {
+  __shared__ double smem[32];
+  double v = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) v += partials[i];
+  v = block_sum<1024>(v, smem);
+  if (threadIdx.x == 0) out[0] = v;
+}
+
+extern "C" {
+
+int csc_version(void) { return 1; }
+
+const char *csc_last_error(void) { return csc::g_last_error.c_str(); }
+
+int csc_device_info(int *sm_count, int *cc_major, int *cc_minor) {
+  int ndev = 0;
+  CSC_TRY_CUDA(cudaGetDeviceCount(&ndev));
+  CSC_REQUIRE(ndev > 0, "no CUDA device visible");
+  const csc::DeviceInfo &info = csc::device_info();
+  if (sm_count) *sm_count = info.sm_count;
+  if (cc_major) *cc_major = info.cc_major;
+  if (cc_minor) *cc_minor = info.cc_minor;
+  return CSC_OK;
+}
+
+}  // extern "C"

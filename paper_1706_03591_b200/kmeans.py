@@ -1,0 +1,202 @@
+"""Lloyd k-means with k-means++ seeding on the GPU (mirror of cscluster.kmeans).
+
+Reference: /root/reference/pkg/src/cscluster/kmeans.py
+  KmeansConfig  kmeans.py:17-28     Assignment   kmeans.py:31-51
+  _kmeanspp_init kmeans.py:64-77    _lloyd       kmeans.py:88-117
+  kmeans        kmeans.py:120-144   kmeans_cost  kmeans.py:147-157
+
+The RNG stream is consumed on the host exactly as the reference does
+(``integers(n)`` for the first centroid and the zero-mass fallback, one
+``random()`` per D^2 draw, which is what ``Generator.choice(n, p=...)``
+consumes), so the same seed picks the same centroid rows; distances, the
+draw, assignment, repair, means and cost run in libcscb200. One 8-byte
+device->host read per k-means++ draw and per Lloyd iteration carries the
+values the reference branches on.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import as_device_block, ptr, require_cuda, row_stride, stream
+from .signals import FeatureMatrix, as_seed_sequence, block_nonfinite
+
+
+@dataclass(frozen=True)
+class KmeansConfig:
+    restarts: int = 10
+    max_iters: int = 100
+    tol: float = 1e-6
+    init: str = "kmeanspp"
+
+    def __post_init__(self):
+        if self.restarts < 1:
+            raise ValueError("need at least one restart")
+        if self.init != "kmeanspp":
+            raise ValueError(f"unknown init {self.init!r}")
+
+
+@dataclass(frozen=True, eq=False)
+class Assignment:
+    """Cluster labels plus sizes and the cost on the features it was solved on."""
+
+    labels: np.ndarray
+    cluster_sizes: np.ndarray
+    feature_cost: float
+
+    @property
+    def n(self) -> int:
+        return int(self.labels.size)
+
+    @property
+    def k(self) -> int:
+        return int(self.cluster_sizes.size)
+
+    def indicator(self) -> np.ndarray:
+        """Dense n x k indicator X with entries 1/sqrt(s_j); X^T X = I."""
+        x = np.zeros((self.n, self.k))
+        x[np.arange(self.n), self.labels] = 1.0 / np.sqrt(self.cluster_sizes[self.labels])
+        return x
+
+
+class _Workspace:
+    """Device buffers for one (features, k) problem, reused across restarts."""
+
+    def __init__(self, blk: torch.Tensor, d: int, k: int):
+        dev = blk.device
+        self.blk, self.n, self.d, self.k = blk, blk.shape[0], d, k
+        self.ld = blk.shape[1]
+        self.ldc = row_stride(d)
+        f64, i32 = torch.float64, torch.int32
+        self.fnorm = torch.empty(self.n, dtype=f64, device=dev)
+        self.cent = torch.zeros((k, self.ldc), dtype=f64, device=dev)
+        self.cnorm = torch.empty(k, dtype=f64, device=dev)
+        self.labels = torch.zeros(self.n, dtype=i32, device=dev)
+        self.own = torch.empty(self.n, dtype=f64, device=dev)
+        self.counts = torch.zeros(k, dtype=i32, device=dev)
+        self.closest = torch.empty(self.n, dtype=f64, device=dev)
+        self.nchunks = int(_native.lib().csc_kmeanspp_nchunks(self.n))
+        self.chunk_sums = torch.empty(self.nchunks, dtype=f64, device=dev)
+        self.scalars = torch.empty(2, dtype=f64, device=dev)
+        self.idx = torch.empty(1, dtype=torch.int64, device=dev)
+        _native.call("csc_kmeans_rownorms", ptr(blk), self.n, d, self.ld, ptr(self.fnorm), stream())
+
+    # -- k-means++ (kmeans.py:64-77) ------------------------------------------
+    def _pick(self, j: int, u: float = 0.0, fixed: int = -1):
+        crow = self.cent[j]
+        _native.call("csc_kmeanspp_pick", ptr(self.blk), self.n, self.d, self.ld, ptr(self.closest),
+                     ptr(self.chunk_sums), self.nchunks, float(u), int(fixed), ptr(crow), ptr(self.idx),
+                     stream())
+
+    def _dist(self, j: int, first: bool):
+        _native.call("csc_kmeanspp_dist", ptr(self.blk), self.n, self.d, self.ld, ptr(self.cent[j]),
+                     ptr(self.closest), int(first), ptr(self.chunk_sums), self.nchunks, ptr(self.scalars),
+                     stream())
+
+    def kmeanspp(self, rng: np.random.Generator, record: list | None = None):
+        n, k = self.n, self.k
+        self._pick(0, fixed=int(rng.integers(n)))
+        if record is not None:
+            record.append(int(self.idx.item()))
+        self._dist(0, True)
+        for j in range(1, k):
+            total = float(self.scalars[0].item())
+            if total <= 0.0:
+                self._pick(j, fixed=int(rng.integers(n)))
+            else:
+                self._pick(j, u=rng.random())
+            if record is not None:
+                record.append(int(self.idx.item()))
+            if j < k - 1:
+                self._dist(j, False)
+
+    # -- Lloyd (kmeans.py:88-117) -------------------------------------------------
+    def lloyd(self, max_iters: int, tol: float, history: list | None = None):
+        s = stream()
+        n, d, k = self.n, self.d, self.k
+        _native.call("csc_kmeans_rownorms", ptr(self.cent), k, d, self.ldc, ptr(self.cnorm), s)
+        self.labels.zero_()
+        prev = np.inf
+        for _ in range(max_iters):
+            _native.call("csc_kmeans_assign", ptr(self.blk), ptr(self.fnorm), n, d, self.ld, ptr(self.cent),
+                         self.ldc, ptr(self.cnorm), k, ptr(self.labels), ptr(self.own), ptr(self.counts), s)
+            _native.call("csc_kmeans_repair", ptr(self.labels), ptr(self.own), ptr(self.counts), n, k, s)
+            _native.call("csc_kmeans_update", ptr(self.blk), ptr(self.labels), n, d, self.ld, k, ptr(self.cent),
+                         self.ldc, ptr(self.cnorm), ptr(self.counts), s)
+            _native.call("csc_kmeans_cost", ptr(self.blk), ptr(self.labels), ptr(self.cent), self.ldc, n, d,
+                         self.ld, ptr(self.scalars[1:]), s)
+            cost2 = float(self.scalars[1].item())
+            if history is not None:
+                history.append(np.sqrt(cost2))
+            if np.isfinite(prev) and prev - cost2 <= tol * prev:
+                prev = cost2
+                break
+            prev = cost2
+        return prev
+
+
+def _features_block(f):
+    """Accept numpy / torch / FeatureMatrix features; validate like kmeans.py:127-134."""
+    if isinstance(f, FeatureMatrix):
+        return f.device_block(), f.d
+    if isinstance(f, tuple):  # (padded block, d) from the internal pipeline
+        return f
+    if isinstance(f, torch.Tensor):
+        if f.ndim != 2:
+            raise ValueError("features must be a 2-d matrix")
+        blk, d, _ = as_device_block(f)
+        return blk, d
+    f = np.asarray(f, dtype=np.float64)
+    if f.ndim != 2:
+        raise ValueError("features must be a 2-d matrix")
+    if not np.all(np.isfinite(f)):
+        raise ValueError("features must be finite")
+    blk, d, _ = as_device_block(f)
+    return blk, d
+
+
+def kmeans(f, k: int, cfg: KmeansConfig | None = None, seed=0) -> Assignment:
+    """Best of cfg.restarts Lloyd runs (k-means++ seeded); deterministic given seed.
+
+    Each restart draws from its own spawned RNG stream; ties in cost keep the
+    earliest restart (kmeans.py:136-144).
+    """
+    cfg = cfg or KmeansConfig()
+    host = not isinstance(f, (FeatureMatrix, tuple, torch.Tensor))
+    blk, d = _features_block(f)
+    require_cuda()
+    if not host and block_nonfinite(blk) != 0:
+        raise ValueError("features must be finite")
+    n = blk.shape[0]
+    if not 1 <= k <= n:
+        raise ValueError(f"need 1 <= k <= n, got k={k}, n={n}")
+    ws = _Workspace(blk, d, k)
+    best = None
+    for child in as_seed_sequence(seed).spawn(cfg.restarts):
+        ws.kmeanspp(np.random.default_rng(child))
+        cost2 = ws.lloyd(cfg.max_iters, cfg.tol)
+        if best is None or cost2 < best[0]:
+            best = (cost2, ws.labels.clone())
+    cost2, labels = best
+    labels = labels.cpu().numpy().astype(np.int64)
+    sizes = np.bincount(labels, minlength=k)
+    return Assignment(labels, sizes, float(np.sqrt(max(cost2, 0.0))))
+
+
+def kmeans_cost(f, assignment: Assignment) -> float:
+    """Cost ||F - X X^T F||_F of an existing assignment, in centroid form."""
+    blk, d = _features_block(f)
+    if blk.shape[0] != assignment.n:
+        raise ValueError("feature rows and assignment length differ")
+    ws = _Workspace(blk, d, assignment.k)
+    ws.labels.copy_(torch.from_numpy(np.asarray(assignment.labels, dtype=np.int32)))
+    s = stream()
+    _native.call("csc_kmeans_update", ptr(blk), ptr(ws.labels), ws.n, d, ws.ld, ws.k, ptr(ws.cent), ws.ldc,
+                 ptr(ws.cnorm), ptr(ws.counts), s)
+    _native.call("csc_kmeans_cost", ptr(blk), ptr(ws.labels), ptr(ws.cent), ws.ldc, ws.n, d, ws.ld,
+                 ptr(ws.scalars[1:]), s)
+    return float(np.sqrt(ws.scalars[1].item()))

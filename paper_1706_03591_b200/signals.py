@@ -1,0 +1,146 @@
+"""Random probe signals and device-resident feature blocks (mirror of cscluster.signals).
+
+Reference: /root/reference/pkg/src/cscluster/signals.py
+  as_seed_sequence  signals.py:9-13
+  random_signals    signals.py:16-37  (same numpy PCG64/SeedSequence streams,
+                                        bit-identical values)
+  FeatureMatrix     signals.py:40-87  (same fields and checks; the values live
+                                        on the GPU as a padded row-major block
+                                        and are copied to the host on access)
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import download_block, ptr, require_cuda, row_stride, stream, upload_block
+
+
+def as_seed_sequence(seed) -> np.random.SeedSequence:
+    """Coerce an integer seed (or pass through a SeedSequence) for stream spawning."""
+    if isinstance(seed, np.random.SeedSequence):
+        return seed
+    return np.random.SeedSequence(seed)
+
+
+def random_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> np.ndarray:
+    """n x d i.i.d. N(0, 1/scale_dim); column c from SeedSequence(seed).spawn(d)[c]."""
+    if d < 1:
+        raise ValueError("need at least one signal column")
+    if n < 1:
+        raise ValueError("need at least one node")
+    dim = d if scale_dim is None else int(scale_dim)
+    if dim < 1:
+        raise ValueError("scale_dim must be positive")
+    sigma = 1.0 / np.sqrt(dim)
+    children = as_seed_sequence(seed).spawn(d)
+    out = np.empty((n, d))
+    for c, child in enumerate(children):
+        out[:, c] = np.random.default_rng(child).normal(0.0, sigma, size=n)
+    return out
+
+
+def block_nonfinite(blk: torch.Tensor) -> int:
+    """Count of non-finite entries of a device block (one sync)."""
+    s = torch.empty(1, dtype=torch.float64, device=blk.device)
+    bad = torch.zeros(1, dtype=torch.int64, device=blk.device)
+    code = _native.CSC_F64 if blk.dtype == torch.float64 else _native.CSC_F32
+    _native.call("csc_sumsq", ptr(blk), blk.numel(), code, ptr(s), ptr(bad), stream())
+    return int(bad.item())
+
+
+def gather_columns(src: torch.Tensor, cols, dst: torch.Tensor, col0: int = 0) -> None:
+    """dst[:, col0 + j] = src[:, cols[j]] (float64 blocks) on the GPU."""
+    cols_t = torch.as_tensor(np.asarray(cols, dtype=np.int64)).to(src.device)
+    if cols_t.numel() == 0:
+        return
+    _native.call("csc_gather_columns", ptr(src), src.shape[0], src.shape[1], ptr(cols_t), cols_t.numel(),
+                 ptr(dst), dst.shape[1], col0, stream())
+
+
+class FeatureMatrix:
+    """Block of filtered signals with per-column provenance tags.
+
+    ``step_tags[c]`` records the time step whose graph filtered column c and
+    ``stream_tags[c]`` the RNG stream index within that step's draw. Values are
+    float64 and must be finite (ValueError otherwise), as in signals.py:53-62.
+    """
+
+    def __init__(self, values, step_tags, stream_tags):
+        if isinstance(values, torch.Tensor):
+            if values.ndim != 2:
+                raise ValueError("feature values must be a 2-d matrix")
+            n, d = values.shape
+            blk = torch.zeros((n, row_stride(d)), dtype=torch.float64, device=require_cuda())
+            blk[:, :d].copy_(values)
+            self._set(blk, d, None, step_tags, stream_tags, check=True)
+        else:
+            host = np.asarray(values, dtype=np.float64)
+            if host.ndim != 2:
+                raise ValueError("feature values must be a 2-d matrix")
+            self._set(None, host.shape[1], host, step_tags, stream_tags, check=True)
+
+    @classmethod
+    def _from_block(cls, blk: torch.Tensor, d: int, step_tags, stream_tags, check: bool = True):
+        fm = cls.__new__(cls)
+        fm._set(blk, d, None, step_tags, stream_tags, check)
+        return fm
+
+    def _set(self, blk, d, host, step_tags, stream_tags, check):
+        steps = np.asarray(step_tags, dtype=np.int64)
+        streams = np.asarray(stream_tags, dtype=np.int64)
+        if steps.shape != (d,) or streams.shape != (d,):
+            raise ValueError("provenance tags must have one entry per column")
+        if check:
+            finite = np.all(np.isfinite(host)) if host is not None else block_nonfinite(blk) == 0
+            if not finite:
+                raise ValueError("feature values must be finite")
+        self._blk, self._d, self._host = blk, int(d), host
+        self.step_tags, self.stream_tags = steps, streams
+
+    @classmethod
+    def tagged(cls, values, step: int) -> "FeatureMatrix":
+        """Wrap a freshly filtered block: all columns from `step`, streams 0..d-1."""
+        d = values.shape[1]
+        return cls(values, np.full(d, step, dtype=np.int64), np.arange(d, dtype=np.int64))
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._host is None:
+            self._host = download_block(self._blk, self._d)
+        return self._host
+
+    def device_block(self) -> torch.Tensor:
+        """Padded (n, ld) float64 block on the GPU (uploaded on first use)."""
+        if self._blk is None:
+            self._blk = upload_block(self._host)
+        return self._blk
+
+    @property
+    def n(self) -> int:
+        return self._blk.shape[0] if self._blk is not None else self._host.shape[0]
+
+    @property
+    def d(self) -> int:
+        return self._d
+
+    def take(self, cols) -> "FeatureMatrix":
+        """Column subset, tags carried along."""
+        cols = np.asarray(cols, dtype=np.int64)
+        if cols.size and (cols.min() < -self._d or cols.max() >= self._d):
+            raise IndexError("column index out of range")
+        cols = np.where(cols < 0, cols + self._d, cols)
+        src = self.device_block()
+        out = torch.zeros((self.n, row_stride(cols.size)), dtype=torch.float64, device=src.device)
+        gather_columns(src, cols, out)
+        return FeatureMatrix._from_block(out, cols.size, self.step_tags[cols], self.stream_tags[cols],
+                                         check=False)
+
+    def with_step(self, step: int) -> "FeatureMatrix":
+        fm = FeatureMatrix.__new__(FeatureMatrix)
+        fm._set(self._blk, self._d, self._host, np.full(self._d, step, dtype=np.int64), self.stream_tags,
+                check=False)
+        return fm

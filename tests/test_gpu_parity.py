@@ -1,0 +1,398 @@
+"""GPU parity: libcscb200 through the drop-in API vs the pinned CPU oracle.
+
+Tolerances (north_star): Laplacian / CSR updates bit-exact; fp64 features
+relative Frobenius <= 1e-10; lambda_k in the same bisection interval (here:
+identical probe sequence); k-means from the reference's initial centroids
+ARI >= 0.999 and cost within 1e-9 relative. fp32 is reported separately
+(<= 1e-4 here, measured values in DESIGN.md).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import csc_oracle as O
+from oracle import native as ON
+
+pytestmark = pytest.mark.gpu
+
+FEAT_TOL = 1e-10
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def P(cuda_ok):
+    import paper_1706_03591_b200 as P
+    return P
+
+
+def graph_from(g, name, P):
+    return P.Graph(int(g[f"{name}_n"]), g[f"{name}_i"], g[f"{name}_j"], g[f"{name}_w"])
+
+
+# ---------------------------------------------------------------------------
+# Laplacian: bit-exact (graphs.py:339-362)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["path3", "path10", "triangle", "isolated", "single", "empty",
+                                  "sbm60", "weighted"])
+@pytest.mark.parametrize("variant", ["normalized", "combinatorial"])
+def test_laplacian_bitwise_small(P, name, variant):
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, name, P), variant)
+    m = lap.matrix
+    p = f"{name}_{variant}"
+    assert np.array_equal(m.indptr, g[f"{p}_indptr"])
+    assert np.array_equal(m.indices, g[f"{p}_indices"])
+    assert np.array_equal(m.data, g[f"{p}_data"])
+    assert lap.lambda_max_bound == float(g[f"{p}_bound"])
+
+
+def test_laplacian_bitwise_cfg1(P):
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    m = lap.matrix
+    assert np.array_equal(m.indptr, g["L_indptr"])
+    assert np.array_equal(m.indices, g["L_indices"])
+    assert np.array_equal(m.data, g["L_data"])
+
+
+def test_laplacian_random_weighted_bitwise(P):
+    rng = np.random.default_rng(3)
+    n = 3000
+    m = 40000
+    i = rng.integers(0, n, m)
+    j = rng.integers(0, n, m)
+    ok = i != j
+    code = np.unique(np.minimum(i, j)[ok] * n + np.maximum(i, j)[ok])
+    lo, hi = code // n, code % n
+    w = rng.uniform(0.01, 5.0, code.size)
+    perm = rng.permutation(code.size)
+    g = P.Graph(n, hi[perm], lo[perm], w[perm])
+    for variant in ("normalized", "combinatorial"):
+        lap = P.laplacian(g, variant)
+        ip, ix, dv, bound = O.laplacian_csr(n, g.edge_i, g.edge_j, g.edge_w, variant)
+        assert np.array_equal(lap.matrix.indptr, ip)
+        assert np.array_equal(lap.matrix.indices, ix)
+        assert np.array_equal(lap.matrix.data, dv)
+        assert lap.lambda_max_bound == bound
+
+
+# ---------------------------------------------------------------------------
+# Filter (filters.py:155-187)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("tag", ["m37", "m40none", "sig60", "ident", "lin", "allpass"])
+def test_filter_small_golden(P, tag):
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, "sbm60", P))
+    poly = P.FilterPoly(len(g[f"f60_{tag}_coeffs"]) - 1, g[f"f60_{tag}_coeffs"], 1.0,
+                        float(g[f"f60_{tag}_lmax"]), "none")
+    counter = P.MatvecCounter()
+    out = P.apply_filter(lap, poly, g["f60_x"], counter)
+    assert rel(out, g[f"f60_{tag}_out"]) <= FEAT_TOL
+    assert counter.count == (len(poly.coeffs) - 1) * 6
+
+
+def test_filter_identity_and_linear_kats(P):
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, "sbm60", P))
+    x = np.random.default_rng(0).normal(size=(lap.n, 4))
+    ident = P.FilterPoly(5, np.array([1.0, 0, 0, 0, 0, 0]), 1.0, 2.0, "none")
+    assert np.allclose(P.apply_filter(lap, ident, x), x, atol=1e-14)
+    lmax = lap.lambda_max_bound
+    lin = P.FilterPoly(1, np.array([lmax / 2, -lmax / 2]), 1.0, lmax, "none")
+    x3 = np.random.default_rng(1).normal(size=(lap.n, 3))
+    assert np.allclose(P.apply_filter(lap, lin, x3), lap.matrix @ x3, atol=1e-10)
+
+
+def test_filter_cfg1_golden_and_fp32(P):
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    poly = P.cheb_coeffs(0.5, 2.0, 50)
+    assert np.array_equal(poly.coeffs, g["coeffs_05"])
+    out = P.apply_filter(lap, poly, g["R"])
+    assert rel(out, g["filt_05"]) <= FEAT_TOL
+    out32 = P.apply_filter(lap, poly, g["R"], precision="fp32")
+    e32 = rel(out32, g["filt_05"])
+    print(f"cfg1 fp32 rel Frobenius error {e32:.3e}")
+    assert e32 <= 1e-4
+
+
+def test_filter_combinatorial_weighted(P):
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, "weighted", P), "combinatorial")
+    poly = P.FilterPoly(30, g["fw_coeffs"], 1.0, float(g["fw_lmax"]), "jackson")
+    out = P.apply_filter(lap, poly, g["fw_x"])
+    assert rel(out, g["fw_out"]) <= FEAT_TOL
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 8, 17, 40, 64, 100, 128, 200, 600])
+def test_filter_widths(P, d):
+    """Every row-group/vector template and the >256-vector column chunking."""
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    x = np.random.default_rng(d).normal(size=(lap.n, d))
+    poly = P.cheb_coeffs(0.7, 2.0, 12)
+    out = P.apply_filter(lap, poly, x)
+    ref = ON.cheb_filter(g["L_indptr"], g["L_indices"], g["L_data"], 2.0, poly.coeffs, x)
+    assert rel(out, ref) <= FEAT_TOL
+
+
+def test_filter_long_rows_segment_path(P):
+    """Hub rows above the long-row threshold go through the segment kernels."""
+    rng = np.random.default_rng(7)
+    n = 6000
+    hubs = [0, 17, 4000]
+    ii, jj = [], []
+    for h, deg in zip(hubs, [5000, 2500, 1100]):
+        nb = rng.choice(np.setdiff1d(np.arange(n), [h]), size=deg, replace=False)
+        ii.append(np.full(deg, h))
+        jj.append(nb)
+    base_i = rng.integers(0, n, 30000)
+    base_j = rng.integers(0, n, 30000)
+    ii.append(base_i)
+    jj.append(base_j)
+    i = np.concatenate(ii)
+    j = np.concatenate(jj)
+    ok = i != j
+    code = np.unique(np.minimum(i, j)[ok] * n + np.maximum(i, j)[ok])
+    g = P.Graph(n, code // n, code % n, np.ones(code.size))
+    lap = P.laplacian(g)
+    plan = lap.plan(1.0)
+    assert plan.n_long >= 3 and plan.n_seg > plan.n_long
+    for d in (3, 40, 128):
+        x = rng.normal(size=(n, d))
+        poly = P.cheb_coeffs(0.4, 2.0, 20)
+        out = P.apply_filter(lap, poly, x)
+        m = lap.matrix
+        ref = ON.cheb_filter(m.indptr, m.indices, m.data, 2.0, poly.coeffs, x)
+        assert rel(out, ref) <= FEAT_TOL
+        est, _ = P.eigencount(lap, 0.4, d, m=20, seed=1)
+        r = O.random_signals(n, d, 1)
+        ref_e = float((ON.cheb_filter(m.indptr, m.indices, m.data, 2.0, poly.coeffs, r) ** 2).sum())
+        assert abs(est - ref_e) <= 1e-10 * ref_e
+
+
+def test_filter_deterministic(P):
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    poly = P.cheb_coeffs(0.5, 2.0, 50)
+    a = P.apply_filter(lap, poly, g["R"])
+    b = P.apply_filter(lap, poly, g["R"])
+    assert np.array_equal(a, b)
+
+
+def test_filter_errors(P):
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, "sbm60", P))
+    poly = P.cheb_coeffs(0.5, 2.0, 5)
+    with pytest.raises(ValueError):
+        P.apply_filter(lap, poly, np.zeros(lap.n))
+    with pytest.raises(ValueError):
+        P.apply_filter(lap, poly, np.zeros((lap.n + 1, 2)))
+
+
+def test_filter_from_scipy_laplacian(P):
+    """A user-built LaplacianMatrix (SciPy CSR) is uploaded on first use."""
+    import scipy.sparse as sp
+    g = golden("cfg1")
+    mat = sp.csr_matrix((g["L_data"], g["L_indices"], g["L_indptr"]), shape=(1000, 1000))
+    lap = P.LaplacianMatrix(mat, "normalized", 2.0)
+    out = P.apply_filter(lap, P.FilterPoly(50, g["coeffs_05"], 0.5, 2.0, "jackson"), g["R"])
+    assert rel(out, g["filt_05"]) <= FEAT_TOL
+
+
+# ---------------------------------------------------------------------------
+# Eigencount bisection (filters.py:199-277)
+# ---------------------------------------------------------------------------
+
+def test_bisection_cfg1_same_probes(P):
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    from paper_1706_03591_b200.filters import _search_cutoff
+    counter = P.MatvecCounter()
+    cfg = P.FilterConfig(order=50, max_iters=8)
+    cut, filt, poly, iters, est = _search_cutoff(lap, 10, g["R"], (0.0, 2.0), cfg, counter, 1.0)
+    assert cut == float(g["cutoff"]) and iters == int(g["iters"])
+    assert abs(est - float(g["est"])) <= 1e-10 * float(g["est"])
+    assert rel(filt, g["features"]) <= FEAT_TOL
+    assert counter.count == iters * 50 * 40
+
+
+def test_find_lambda_k_small_trace(P):
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, "sbm60", P))
+    counter = P.MatvecCounter()
+    lam, feats, iters = P.find_lambda_k(lap, 3, d=12, m=40, seed=5, counter=counter)
+    assert lam == float(g["flk_lambda"]) and iters == int(g["flk_iters"])
+    assert rel(feats.values, g["flk_features"]) <= FEAT_TOL
+    assert counter.count == iters * 40 * 12
+
+
+def test_search_errors(P):
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, "sbm60", P))
+    with pytest.raises(ValueError):
+        P.find_lambda_k(lap, 3, d=10, interval=(1.0, 0.5))
+    with pytest.raises(ValueError):
+        P.find_lambda_k(lap, lap.n, d=10)
+    # non-convergence carries the reference's error fields
+    cl = P.Graph(10, *np.triu_indices(5, 1), np.ones(10))
+    lap2 = P.laplacian(cl)
+    with pytest.raises(P.EigencountSearchError) as err:
+        P.find_lambda_k(lap2, 2, d=100, m=60, seed=6, interval=(1.9, 2.0), tol=0.0, max_iters=2)
+    assert err.value.iterations == 2
+    assert 1.9 < err.value.last_cutoff < 2.0
+
+
+# ---------------------------------------------------------------------------
+# k-means (kmeans.py)
+# ---------------------------------------------------------------------------
+
+def test_kmeanspp_same_picks_and_lloyd_from_reference_init(P):
+    g = golden("cfg1")
+    f = g["features"]
+    from paper_1706_03591_b200.kmeans import _Workspace
+    from paper_1706_03591_b200._device import upload_block
+    import torch
+    blk = upload_block(f)
+    ws = _Workspace(blk, 40, 10)
+    child = np.random.SeedSequence(0).spawn(2)[1].spawn(1)[0]
+    picks = []
+    ws.kmeanspp(np.random.default_rng(child), record=picks)
+    _, ref_picks = O.kmeanspp(f, 10, np.random.default_rng(child))
+    assert picks == ref_picks
+    cent = ws.cent[:, :40].cpu().numpy()
+    assert np.array_equal(cent, g["km_init"])
+    hist = []
+    cost2 = ws.lloyd(20, 1e-6, hist)
+    labels = ws.labels.cpu().numpy()
+    assert O.adjusted_rand(labels, g["km_labels"]) >= 0.999
+    assert abs(cost2 - float(g["km_cost2"])) <= 1e-9 * float(g["km_cost2"])
+    np.testing.assert_allclose(hist, g["km_hist"], rtol=1e-9)
+    torch.cuda.synchronize()
+
+
+def test_kmeans_goldens(P):
+    g = golden("kmeans")
+    a = P.kmeans(g["a_f"], 3, seed=123)
+    assert O.adjusted_rand(a.labels, g["a_labels"]) >= 0.999
+    assert abs(a.feature_cost - float(g["a_cost"])) <= 1e-9 * float(g["a_cost"])
+    for s in range(6):
+        b = P.kmeans(np.array([[0.0], [0.0], [5.0]]), 3, P.KmeansConfig(restarts=1), seed=s)
+        assert np.array_equal(b.labels, g[f"dup{s}_labels"])
+        assert b.cluster_sizes.min() >= 1
+    r = P.kmeans(np.array([[0.0, 0.0], [2.0, 0.0], [0.0, 0.1], [2.0, 0.1]]), 2,
+                 P.KmeansConfig(restarts=10), seed=0)
+    assert np.isclose(r.feature_cost, float(g["rect_cost"]), rtol=1e-9)
+    kb = P.kmeans(g["b_f"], 12, P.KmeansConfig(restarts=3, max_iters=50), seed=77)
+    assert O.adjusted_rand(kb.labels, g["b_labels"]) >= 0.999
+    assert abs(kb.feature_cost - float(g["b_cost"])) <= 1e-9 * float(g["b_cost"])
+
+
+def test_kmeans_validation_and_cost(P):
+    with pytest.raises(ValueError):
+        P.kmeans(np.zeros((4, 2)), 5)
+    with pytest.raises(ValueError):
+        P.kmeans(np.zeros((4, 2)), 0)
+    with pytest.raises(ValueError):
+        P.kmeans(np.array([[np.nan, 0.0]]), 1)
+    rng = np.random.default_rng(3)
+    f = rng.normal(size=(30, 4))
+    labels = rng.integers(0, 3, size=30)
+    labels[:3] = [0, 1, 2]
+    a = P.Assignment(labels, np.bincount(labels, minlength=3), 0.0)
+    x = a.indicator()
+    assert np.isclose(P.kmeans_cost(f, a), np.linalg.norm(f - x @ (x.T @ f)), atol=1e-10)
+    six = P.kmeans(rng.normal(size=(6, 2)), 6, P.KmeansConfig(restarts=5), seed=1)
+    assert six.cluster_sizes.tolist() == [1] * 6 and six.feature_cost <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# CSC + dynamic CSC end to end
+# ---------------------------------------------------------------------------
+
+def test_csc_assign_cfg1(P):
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    counter = P.MatvecCounter()
+    a, diag = P.csc_assign(lap, 10, 40, filter_cfg=P.FilterConfig(order=50, max_iters=8),
+                           kmeans_cfg=P.KmeansConfig(restarts=1, max_iters=20), seed=0, counter=counter)
+    assert diag.lambda_k == float(g["csc_lambda"]) and diag.search_iters == int(g["csc_iters"])
+    assert diag.matvecs == int(g["csc_matvecs"]) == counter.count
+    assert O.adjusted_rand(a.labels, g["csc_labels"]) >= 0.999
+    assert abs(a.feature_cost - float(g["csc_cost"])) <= 1e-9 * float(g["csc_cost"])
+
+
+def test_dynamic_sequence_small_golden(P):
+    g = golden("dynamic_small")
+    graphs = [graph_from(g, f"g{t}", P) for t in range(4)]
+    cfg = P.DynamicConfig(k=4, d=40, p=0.5, filter=P.FilterConfig(order=60),
+                          kmeans=P.KmeansConfig(restarts=6))
+    a, state, diag = P.dynamic_init(graphs[0], cfg, seed=10)
+    steps = [(a, state, diag)]
+    for gt in graphs[1:]:
+        a, state, diag = P.dynamic_step(state, gt, cfg)
+        steps.append((a, state, diag))
+    for t, (a, st, dg) in enumerate(steps):
+        assert dg.lambda_k == float(g[f"s{t}_lambda"])
+        assert dg.refined == bool(g[f"s{t}_refined"]) and dg.search_iters == int(g[f"s{t}_iters"])
+        assert dg.reused == int(g[f"s{t}_reused"])
+        assert dg.matvecs_total == int(g[f"s{t}_mv_total"]) and dg.matvecs_fresh == int(g[f"s{t}_mv_fresh"])
+        assert np.array_equal(st.features.step_tags, g[f"s{t}_step_tags"])
+        assert np.array_equal(st.features.stream_tags, g[f"s{t}_stream_tags"])
+        assert rel(st.features.values, g[f"s{t}_features"]) <= FEAT_TOL
+        assert O.adjusted_rand(a.labels, g[f"s{t}_labels"]) >= 0.999
+        assert abs(a.feature_cost - float(g[f"s{t}_cost"])) <= 1e-9 * float(g[f"s{t}_cost"])
+
+
+def test_dynamic_bitwise_reuse_and_refilter(P):
+    g = golden("dynamic_small")
+    g0, g1 = graph_from(g, "g0", P), graph_from(g, "g1", P)
+    cfg = P.DynamicConfig(k=4, d=20, p=0.35, filter=P.FilterConfig(order=60),
+                          kmeans=P.KmeansConfig(restarts=2))
+    _, state, _ = P.dynamic_init(g0, cfg, seed=4)
+    prev = state.features.values.copy()
+    _, state2, diag = P.dynamic_step(state, g1, cfg)
+    theta = state2.features
+    assert diag.reused == 7
+    for col in range(7):
+        assert np.array_equal(theta.values[:, col], prev[:, int(theta.stream_tags[col])])
+    # refined/fresh columns equal a direct apply_filter of the same raw draw
+    ss = np.random.SeedSequence(4)
+    ss.spawn(2)
+    _, sig_ss, _ = ss.spawn(3)
+    raw = P.random_signals(g1.n, 13, sig_ss, scale_dim=20)
+    expected = P.apply_filter(P.laplacian(g1), state2.filter, raw)
+    assert np.array_equal(theta.values[:, 7:], expected)
+
+
+def test_edge_delta_matches_reference_sequence(P):
+    """apply_delta on the GPU reproduces the reference's next graph and its Laplacian bit-exactly."""
+    g = golden("dynamic_small")
+    g0 = graph_from(g, "g0", P)
+    for t in range(1, 4):
+        nxt = graph_from(g, f"g{t}", P)
+        prev_codes, next_codes = g0.edge_codes(), nxt.edge_codes()
+        dl = np.setdiff1d(prev_codes, next_codes)
+        il = np.setdiff1d(next_codes, prev_codes)
+        gd = g0.apply_delta(dl, il)
+        assert gd.m == nxt.m
+        assert np.array_equal(gd.edge_codes(), next_codes)
+        lap = P.laplacian(gd)
+        ip, ix, dv, _ = O.laplacian_csr(nxt.n, nxt.edge_i, nxt.edge_j, nxt.edge_w)
+        assert np.array_equal(lap.matrix.indptr, ip)
+        assert np.array_equal(lap.matrix.indices, ix)
+        assert np.array_equal(lap.matrix.data, dv)
+        g0 = gd
+    codes = g0.edge_codes()
+    absent = next(c for c in range(1, g0.n) if c not in set(codes.tolist()))
+    with pytest.raises(ValueError):
+        g0.apply_delta([absent], [])       # deleting a non-edge
+    with pytest.raises(ValueError):
+        g0.apply_delta([], [codes[0]])     # inserting an existing edge

@@ -1,0 +1,125 @@
+"""CPU-only tests: C-ABI library loads and exports the header, host-side logic
+mirrors the reference (validation, coefficients, RNG, tags), and the compute
+path refuses to run without a GPU (no CPU fallback)."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from oracle import csc_oracle as O
+
+
+def test_library_loads_and_exports_header_symbols():
+    from paper_1706_03591_b200 import _native
+    lib = _native.load()
+    declared = _native.header_symbols()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(_native.SIGNATURES) == declared
+    assert lib.csc_version() >= 1
+
+
+def test_status_mapping():
+    from paper_1706_03591_b200 import _native
+    _native.check(0, "ok")
+    with pytest.raises(ValueError):
+        _native.check(_native.CSC_ERR_ARG, "bad")
+    with pytest.raises(_native.NativeError):
+        _native.check(_native.CSC_ERR_CUDA, "cuda")
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback():
+    import paper_1706_03591_b200 as P
+    g = P.Graph(3, [0, 1], [1, 2], [1.0, 1.0])
+    with pytest.raises(RuntimeError, match="CUDA"):
+        P.laplacian(g)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        P.kmeans(np.ones((4, 2)), 2)
+
+
+def test_graph_validation_and_canonical_order():
+    import paper_1706_03591_b200 as P
+    g = P.Graph(4, [2, 0, 3], [0, 1, 1], [1.0, 2.0, 3.0])
+    assert g.edge_i.tolist() == [0, 0, 1] and g.edge_j.tolist() == [1, 2, 3]
+    assert g.edge_w.tolist() == [2.0, 1.0, 3.0]
+    assert g.m == 3 and np.array_equal(g.edge_codes(), [1, 2, 7])
+    assert np.array_equal(g.degrees, [3.0, 5.0, 1.0, 3.0])
+    for bad in [(4, [0], [0], [1.0]), (4, [0], [5], [1.0]), (4, [0], [1], [0.0]),
+                (4, [0, 1], [1, 0], [1.0, 1.0]), (4, [0, 1], [1], [1.0]), (-1, [], [], [])]:
+        with pytest.raises(ValueError):
+            P.Graph(*bad)
+    with pytest.raises(AttributeError):
+        g.n = 5
+    assert P.graphs_equal(g, P.Graph(4, [0, 2, 1], [1, 0, 3], [2.0, 1.0, 3.0]))
+
+
+def test_coefficients_match_oracle_bitwise():
+    import paper_1706_03591_b200 as P
+    g = golden("small")
+    assert np.array_equal(P.cheb_coeffs(1.0, 2.0, 8, damping="none").coeffs, g["c_mid_none"])
+    assert np.array_equal(P.cheb_coeffs(0.3, 2.0, 12).coeffs, g["c_03_j"])
+    assert np.array_equal(P.cheb_coeffs(5.0, 12.0, 12, damping="none").coeffs, g["c_5_12"])
+    assert np.array_equal(P.cheb_coeffs(0.8, 2.0, 30, response="sigmoid", sigmoid_sharpness=20.0).coeffs,
+                          g["c_sig"])
+    assert np.array_equal(P.jackson_damping(40), g["jackson40"])
+    for kw in [dict(lambda_c=0.0, lambda_max=2.0, m=10), dict(lambda_c=-0.5, lambda_max=2.0, m=10),
+               dict(lambda_c=1.0, lambda_max=0.0, m=10), dict(lambda_c=1.0, lambda_max=2.0, m=0),
+               dict(lambda_c=1.0, lambda_max=2.0, m=10, damping="gauss")]:
+        with pytest.raises(ValueError):
+            P.cheb_coeffs(**kw)
+    poly = P.cheb_coeffs(2.5, 2.0, m=50, damping="none")
+    assert np.allclose(poly.evaluate(np.linspace(0, 2, 100)), 1.0, atol=1e-9)
+
+
+def test_random_signals_bitwise_and_validation():
+    import paper_1706_03591_b200 as P
+    g = golden("small")
+    assert np.array_equal(P.random_signals(7, 3, seed=5), g["rs_7_3_5"])
+    assert np.array_equal(P.random_signals(40, 3, seed=9, scale_dim=5), g["rs_40_3_9_sd5"])
+    assert P.random_signals(7, 3, seed=5).flags["C_CONTIGUOUS"]
+    with pytest.raises(ValueError):
+        P.random_signals(5, 0)
+    with pytest.raises(ValueError):
+        P.random_signals(0, 5)
+
+
+def test_feature_matrix_host_semantics():
+    import paper_1706_03591_b200 as P
+    fm = P.FeatureMatrix.tagged(np.zeros((4, 3)), step=2)
+    assert fm.step_tags.tolist() == [2, 2, 2] and fm.stream_tags.tolist() == [0, 1, 2]
+    assert fm.n == 4 and fm.d == 3
+    with pytest.raises(ValueError):
+        P.FeatureMatrix(np.array([[np.inf]]), np.array([0]), np.array([0]))
+    with pytest.raises(ValueError):
+        P.FeatureMatrix(np.zeros((4, 3)), np.array([0, 1]), np.array([0, 1]))
+    assert fm.with_step(5).step_tags.tolist() == [5, 5, 5]
+
+
+def test_configs_and_helpers():
+    import paper_1706_03591_b200 as P
+    assert P.warm_interval(0.5, 2.0) == (0.25, 1.0)
+    assert P.warm_interval(1.5, 2.0) == (0.75, 2.0)
+    c = P.MatvecCounter()
+    c.add(3)
+    c.add(4)
+    assert c.count == 7
+    with pytest.raises(ValueError):
+        P.DynamicConfig(k=2, d=10, p=0.6)
+    with pytest.raises(ValueError):
+        P.DynamicConfig(k=0, d=10)
+    assert P.DynamicConfig(k=2, d=207, p=0.5).reuse_count == 103
+    assert P.DynamicConfig(k=2, d=10, p=0.33).reuse_count == 3
+    with pytest.raises(ValueError):
+        P.FilterConfig(order=0)
+    with pytest.raises(ValueError):
+        P.FilterConfig(precision="fp16")
+    with pytest.raises(ValueError):
+        P.KmeansConfig(restarts=0)
+
+
+def test_laplacian_rejects_unknown_variant():
+    import paper_1706_03591_b200 as P
+    with pytest.raises(ValueError):
+        P.laplacian(P.Graph(3, [0], [1], [1.0]), "random-walk")
