@@ -89,6 +89,11 @@ int csc_chebop_destroy(csc_chebop *op);
 int csc_chebop_info(const csc_chebop *op, int64_t *n, int64_t *nnz, int64_t *n_long,
                     int64_t *n_segments);
 
+/* copy the plan's M (CSR) and long-row schedule into caller buffers
+ * (sizes from csc_chebop_info; any pointer may be NULL) — for tests/tools */
+int csc_chebop_export(const csc_chebop *op, int32_t *indptr_dev, int32_t *indices_dev,
+                      void *vals_dev, int32_t *long_rows_dev, int32_t *seg_off_dev, void *stream);
+
 /* out = h(L) x = sum_j coeffs[j] T_j(M) x by the three-term recurrence,
  * running ncoeffs-1 fused SpMM sweeps (each order: gather M*T_j, write
  * T_{j+1} = 2 M T_j - T_{j-1}, accumulate out += c_j T_{j+1}).

@@ -79,7 +79,12 @@ def download_block(t: torch.Tensor, d: int) -> np.ndarray:
     v = t[:, :d]
     if v.dtype != torch.float64:
         v = v.to(torch.float64)
-    return v.contiguous().cpu().numpy()
+    if not v.is_contiguous():
+        v = v.contiguous()
+    host = torch.empty(v.shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(v, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return host.numpy()
 
 
 def as_device_block(x, dtype: torch.dtype = torch.float64):

@@ -382,6 +382,14 @@ __global__ void __launch_bounds__(kBlock)
 // Plan construction: M = I - s L, schedule of long rows
 // ---------------------------------------------------------------------------
 
+// Entries of M = I - s L, computed exactly like numpy's I - s*L (s*L rounded,
+// then subtracted; no FMA contraction), shared by the count and fill passes
+// so both always agree on which entries are zero.
+__device__ __forceinline__ double m_offdiag(double s, double lij) { return -__dmul_rn(s, lij); }
+__device__ __forceinline__ double m_diag(double s, double lii) {
+  return __dsub_rn(1.0, __dmul_rn(s, lii));
+}
+
 __global__ void op_count_kernel(const int32_t *__restrict__ indptr,
                                 const int32_t *__restrict__ indices,
                                 const double *__restrict__ vals, int64_t n, double s,
@@ -393,11 +401,11 @@ __global__ void op_count_kernel(const int32_t *__restrict__ indptr,
     for (int jj = indptr[row]; jj < indptr[row + 1]; ++jj) {
       if (indices[jj] == row) {
         lii = vals[jj];
-      } else if (-s * vals[jj] != 0.0) {
+      } else if (m_offdiag(s, vals[jj]) != 0.0) {
         ++cnt;
       }
     }
-    if (1.0 - s * lii != 0.0) ++cnt;
+    if (m_diag(s, lii) != 0.0) ++cnt;
     counts[row] = cnt;
   }
 }
@@ -413,7 +421,7 @@ __global__ void op_fill_kernel(const int32_t *__restrict__ indptr,
     double lii = 0.0;
     for (int jj = indptr[row]; jj < indptr[row + 1]; ++jj)
       if (indices[jj] == row) lii = vals[jj];
-    const double dii = 1.0 - s * lii;
+    const double dii = m_diag(s, lii);
     int pos = mptr[row];
     bool placed = (dii == 0.0);
     for (int jj = indptr[row]; jj < indptr[row + 1]; ++jj) {
@@ -425,7 +433,7 @@ __global__ void op_fill_kernel(const int32_t *__restrict__ indptr,
         ++pos;
         placed = true;
       }
-      const double v = -s * vals[jj];
+      const double v = m_offdiag(s, vals[jj]);
       if (v != 0.0) {
         mcol[pos] = c;
         mval[pos] = (T)v;
@@ -901,6 +909,28 @@ int csc_chebop_destroy(csc_chebop *op) {
   return CSC_OK;
 }
 
+int csc_chebop_export(const csc_chebop *op, int32_t *indptr_dev, int32_t *indices_dev,
+                      void *vals_dev, int32_t *long_rows_dev, int32_t *seg_off_dev, void *stream) {
+  CSC_REQUIRE(op != nullptr, "csc_chebop_export: NULL plan");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t esz = op->dtype == CSC_F64 ? 8 : 4;
+  if (indptr_dev)
+    CSC_TRY_CUDA(cudaMemcpyAsync(indptr_dev, op->indptr, sizeof(int32_t) * (op->n + 1),
+                                 cudaMemcpyDeviceToDevice, st));
+  if (indices_dev && op->nnz)
+    CSC_TRY_CUDA(cudaMemcpyAsync(indices_dev, op->indices, sizeof(int32_t) * op->nnz,
+                                 cudaMemcpyDeviceToDevice, st));
+  if (vals_dev && op->nnz)
+    CSC_TRY_CUDA(cudaMemcpyAsync(vals_dev, op->vals, esz * op->nnz, cudaMemcpyDeviceToDevice, st));
+  if (long_rows_dev && op->n_long)
+    CSC_TRY_CUDA(cudaMemcpyAsync(long_rows_dev, op->long_rows, sizeof(int32_t) * op->n_long,
+                                 cudaMemcpyDeviceToDevice, st));
+  if (seg_off_dev && op->n_long)
+    CSC_TRY_CUDA(cudaMemcpyAsync(seg_off_dev, op->seg_off, sizeof(int32_t) * (op->n_long + 1),
+                                 cudaMemcpyDeviceToDevice, st));
+  return CSC_OK;
+}
+
 int csc_chebop_info(const csc_chebop *op, int64_t *n, int64_t *nnz, int64_t *n_long,
                     int64_t *n_segments) {
   CSC_REQUIRE(op != nullptr, "csc_chebop_info: NULL plan");
@@ -962,8 +992,8 @@ int csc_sweep_timing(int enable) {
     for (int i = 0; i < 2 * sweeptime::kCap; ++i) CSC_TRY_CUDA(cudaEventCreate(&sweeptime::ev[i]));
     sweeptime::created = true;
   }
+  if (enable) sweeptime::count = 0;  // disabling keeps the recorded launches for csc_sweep_times
   sweeptime::enabled = enable != 0;
-  sweeptime::count = 0;
   return CSC_OK;
 }
 

@@ -213,6 +213,19 @@ class _ChebPlan:
             self.handle = None
 
 
+def export_plan(plan: _ChebPlan):
+    """(indptr, indices, vals, long_rows, seg_off) of a plan as numpy arrays."""
+    dev = require_cuda()
+    ip = torch.empty(plan.n + 1, dtype=torch.int32, device=dev)
+    ix = torch.empty(max(plan.nnz, 1), dtype=torch.int32, device=dev)
+    vv = torch.empty(max(plan.nnz, 1), dtype=plan.dtype, device=dev)
+    lr = torch.empty(max(plan.n_long, 1), dtype=torch.int32, device=dev)
+    so = torch.empty(plan.n_long + 1, dtype=torch.int32, device=dev)
+    _native.call("csc_chebop_export", plan.handle, ptr(ip), ptr(ix), ptr(vv), ptr(lr), ptr(so), stream())
+    return (ip.cpu().numpy(), ix[:plan.nnz].cpu().numpy(), vv[:plan.nnz].cpu().numpy(),
+            lr[:plan.n_long].cpu().numpy(), so.cpu().numpy() if plan.n_long else np.zeros(1, np.int32))
+
+
 class LaplacianMatrix:
     """Sparse symmetric Laplacian plus an upper bound on its top eigenvalue.
 

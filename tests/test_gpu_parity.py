@@ -396,3 +396,36 @@ def test_edge_delta_matches_reference_sequence(P):
         g0.apply_delta([absent], [])       # deleting a non-edge
     with pytest.raises(ValueError):
         g0.apply_delta([], [codes[0]])     # inserting an existing edge
+
+
+def _expected_M(m, s):
+    """M = I - s L restated on the CPU: exact zeros dropped, isolated rows M_ii = 1."""
+    import scipy.sparse as sp
+    n = m.shape[0]
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        cs = m.indices[m.indptr[i]:m.indptr[i + 1]]
+        vs = m.data[m.indptr[i]:m.indptr[i + 1]]
+        lii = vs[cs == i][0] if np.any(cs == i) else 0.0
+        ent = {int(c): -s * v for c, v in zip(cs, vs) if c != i}
+        ent[i] = 1.0 - s * lii
+        for c in sorted(ent):
+            if ent[c] != 0.0:
+                rows.append(i)
+                cols.append(c)
+                vals.append(ent[c])
+    return sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+
+
+@pytest.mark.parametrize("name,variant", [("sbm60", "normalized"), ("weighted", "combinatorial"),
+                                          ("weighted", "normalized"), ("isolated", "combinatorial")])
+def test_operator_plan_bitwise(P, name, variant):
+    from paper_1706_03591_b200.graphs import export_plan
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, name, P), variant)
+    s = 2.0 / lap.lambda_max_bound if lap.lambda_max_bound > 0 else 1.0
+    ip, ix, vv, _, _ = export_plan(lap.plan(s))
+    exp = _expected_M(lap.matrix, s)
+    assert np.array_equal(ip, exp.indptr)
+    assert np.array_equal(ix, exp.indices)
+    assert np.array_equal(vv, exp.data)
