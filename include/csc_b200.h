@@ -112,6 +112,13 @@ int csc_cheb_filter(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t
 int csc_cheb_moments(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t d, int32_t m,
                      double *mu_dev, void *work_dev, void *stream);
 
+/* Tuning knobs (process-wide; defaults are the measured best):
+ *   "chunk_bytes"  row-chunk width per sweep series (default 4096)
+ *   "near_window"  >0: gathers within +-window rows of the output row use
+ *                  L2 evict_last, others evict_first (default 0 = off)
+ *   "stream_hint"  1: row-local streams use L2 evict_first (default 1) */
+int csc_set_tuning(const char *key, int64_t value);
+
 /* Measurement hook: when enabled, every main sweep launch of csc_cheb_filter /
  * csc_cheb_moments is bracketed by CUDA events on its stream (up to 4096
  * launches); csc_sweep_times returns their durations in ms and resets. */

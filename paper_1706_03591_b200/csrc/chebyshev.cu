@@ -29,6 +29,9 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 
 namespace {
@@ -80,6 +83,73 @@ __device__ __forceinline__ double vdot(const float4 &a, const float4 &b) {
   return (double)a.x * b.x + (double)a.y * b.y + (double)a.z * b.z + (double)a.w * b.w;
 }
 
+// L2 cache policies. The row-local streams of a sweep (T_{j-1}, out, T_{j+1},
+// CSR) are touched once per order; marking them evict_first keeps the L2 for
+// the randomly gathered rows of T_j. (CSC_STREAM_HINT=0 disables, for A/B.)
+__device__ __forceinline__ uint64_t make_policy(int hint) {
+  uint64_t p;
+  if (hint)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t make_gather_policy(int last) {
+  uint64_t p;
+  if (last)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_g(const double2 *a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ld_g(const float4 *a, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld_s(const double2 *a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ld_s(const float4 *a, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_s(double2 *a, const double2 &v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
+               :: "l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_s(float4 *a, const float4 &v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+               :: "l"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ int ld_s(const int32_t *a, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_s(const double *a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_s(const float *a, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 // Row epilogue shared by all sweeps. Modes:
 //   kFirst: T_1 = acc;            out = ca*x + cb*T_1     (prev = x)
 //   kMid:   T_{j+1} = 2acc - T_{j-1}; out += ca*T_{j+1}
@@ -90,35 +160,36 @@ enum { kFirst = 0, kMid = 1, kMomFirst = 2, kMomMid = 3 };
 template <int MODE>
 __device__ __forceinline__ void epilogue(double2 acc, const double2 *prev, const double2 *own,
                                          double2 *next, double2 *out, size_t off, double ca,
-                                         double cb, double &s0, double &s1, bool sumsq) {
+                                         double cb, double &s0, double &s1, bool sumsq,
+                                         uint64_t pol) {
   if (MODE == kFirst) {
-    const double2 x = prev[off];
-    next[off] = acc;
+    const double2 x = ld_s(prev + off, pol);
+    st_s(next + off, acc, pol);
     double2 o;
     o.x = fma(cb, acc.x, ca * x.x);
     o.y = fma(cb, acc.y, ca * x.y);
-    out[off] = o;
+    st_s(out + off, o, pol);
     if (sumsq) s0 += vdot(o, o);
   } else if (MODE == kMid) {
-    const double2 p = prev[off];
+    const double2 p = ld_s(prev + off, pol);
     double2 t;
     t.x = 2.0 * acc.x - p.x;
     t.y = 2.0 * acc.y - p.y;
-    next[off] = t;
-    double2 o = out[off];
+    st_s(next + off, t, pol);
+    double2 o = ld_s(out + off, pol);
     o.x = fma(ca, t.x, o.x);
     o.y = fma(ca, t.y, o.y);
-    out[off] = o;
+    st_s(out + off, o, pol);
     if (sumsq) s0 += vdot(o, o);
   } else {
     double2 t = acc;
     if (MODE == kMomMid) {
-      const double2 p = prev[off];
+      const double2 p = ld_s(prev + off, pol);
       t.x = 2.0 * acc.x - p.x;
       t.y = 2.0 * acc.y - p.y;
     }
-    next[off] = t;
-    const double2 c = own[off];
+    st_s(next + off, t, pol);
+    const double2 c = ld_s(own + off, pol);
     s0 += vdot(t, t);
     s1 += vdot(t, c);
   }
@@ -127,44 +198,45 @@ __device__ __forceinline__ void epilogue(double2 acc, const double2 *prev, const
 template <int MODE>
 __device__ __forceinline__ void epilogue(float4 acc, const float4 *prev, const float4 *own,
                                          float4 *next, float4 *out, size_t off, double ca,
-                                         double cb, double &s0, double &s1, bool sumsq) {
+                                         double cb, double &s0, double &s1, bool sumsq,
+                                         uint64_t pol) {
   const float a = (float)ca, b = (float)cb;
   if (MODE == kFirst) {
-    const float4 x = prev[off];
-    next[off] = acc;
+    const float4 x = ld_s(prev + off, pol);
+    st_s(next + off, acc, pol);
     float4 o;
     o.x = fmaf(b, acc.x, a * x.x);
     o.y = fmaf(b, acc.y, a * x.y);
     o.z = fmaf(b, acc.z, a * x.z);
     o.w = fmaf(b, acc.w, a * x.w);
-    out[off] = o;
+    st_s(out + off, o, pol);
     if (sumsq) s0 += vdot(o, o);
   } else if (MODE == kMid) {
-    const float4 p = prev[off];
+    const float4 p = ld_s(prev + off, pol);
     float4 t;
     t.x = 2.f * acc.x - p.x;
     t.y = 2.f * acc.y - p.y;
     t.z = 2.f * acc.z - p.z;
     t.w = 2.f * acc.w - p.w;
-    next[off] = t;
-    float4 o = out[off];
+    st_s(next + off, t, pol);
+    float4 o = ld_s(out + off, pol);
     o.x = fmaf(a, t.x, o.x);
     o.y = fmaf(a, t.y, o.y);
     o.z = fmaf(a, t.z, o.z);
     o.w = fmaf(a, t.w, o.w);
-    out[off] = o;
+    st_s(out + off, o, pol);
     if (sumsq) s0 += vdot(o, o);
   } else {
     float4 t = acc;
     if (MODE == kMomMid) {
-      const float4 p = prev[off];
+      const float4 p = ld_s(prev + off, pol);
       t.x = 2.f * acc.x - p.x;
       t.y = 2.f * acc.y - p.y;
       t.z = 2.f * acc.z - p.z;
       t.w = 2.f * acc.w - p.w;
     }
-    next[off] = t;
-    const float4 c = own[off];
+    st_s(next + off, t, pol);
+    const float4 c = ld_s(own + off, pol);
     s0 += vdot(t, t);
     s1 += vdot(t, c);
   }
@@ -185,6 +257,8 @@ struct SweepArgs {
   double ca, cb;
   double *partials;  // per-block partial sums (nullable unless sumsq/moments)
   int sumsq;
+  int hint;          // 1: evict_first policy on the row-local streams
+  int near;          // >0: gathers of rows within +-near of the output row use evict_last
 };
 
 // Gather-accumulate of entries [beg, end) of one row into acc[VPL] by a group
@@ -194,15 +268,17 @@ __device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
                                            const T *__restrict__ vals,
                                            const typename V16<T>::V *__restrict__ gat, int beg,
                                            int end, int glane, unsigned gmask, int nvec,
-                                           int64_t ldv, typename V16<T>::V (&acc)[VPL]) {
+                                           int64_t ldv, typename V16<T>::V (&acc)[VPL],
+                                           uint64_t pol, int64_t row, int near, uint64_t pnear,
+                                           uint64_t pfar) {
   using VT = typename V16<T>::V;
   for (int base = beg; base < end; base += G) {
     const int nz = base + glane;
     int my_col = 0;
     T my_val = T(0);
     if (nz < end) {
-      my_col = __ldg(indices + nz);
-      my_val = __ldg(vals + nz);
+      my_col = ld_s(indices + nz, pol);
+      my_val = ld_s(vals + nz, pol);
     }
     const int cnt = min(G, end - base);
     int u = 0;
@@ -215,13 +291,27 @@ __device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
         a[t] = __shfl_sync(gmask, my_val, u + t, G);
       }
       VT x[4][VPL];
+      if (near > 0) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const VT *src = gat + (int64_t)c[t] * ldv;
+        for (int t = 0; t < 4; ++t) {
+          const VT *src = gat + (int64_t)c[t] * ldv;
+          const int64_t dist = (int64_t)c[t] - row;
+          const uint64_t pg = (dist < near && dist > -near) ? pnear : pfar;
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          const int v = glane + q * G;
-          x[t][q] = (v < nvec) ? __ldg(src + v) : vzero(VT());
+          for (int q = 0; q < VPL; ++q) {
+            const int v = glane + q * G;
+            x[t][q] = (v < nvec) ? ld_g(src + v, pg) : vzero(VT());
+          }
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const VT *src = gat + (int64_t)c[t] * ldv;
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            const int v = glane + q * G;
+            x[t][q] = (v < nvec) ? __ldg(src + v) : vzero(VT());
+          }
         }
       }
 #pragma unroll
@@ -261,6 +351,8 @@ __global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs A) {
   VT *out = static_cast<VT *>(A.out);
   double s0 = 0.0, s1 = 0.0;
   const bool sumsq = A.sumsq != 0;
+  const uint64_t pol = make_policy(A.hint);
+  const uint64_t pnear = make_gather_policy(1), pfar = make_gather_policy(0);
 
   for (int64_t row = (int64_t)blockIdx.x * groups_per_block + threadIdx.x / G; row < A.n;
        row += ngroups) {
@@ -269,13 +361,14 @@ __global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs A) {
     VT acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = vzero(VT());
-    gather_row<T, G, VPL>(A.indices, vals, gat, beg, end, glane, gmask, A.nvec, A.ldv, acc);
+    gather_row<T, G, VPL>(A.indices, vals, gat, beg, end, glane, gmask, A.nvec, A.ldv, acc, pol, row,
+                          A.near, pnear, pfar);
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
       const int v = glane + q * G;
       if (v < A.nvec)
         epilogue<MODE>(acc[q], prev, own, next, out, (size_t)row * A.ldv + v, A.ca, A.cb, s0,
-                       s1, sumsq);
+                       s1, sumsq, pol);
     }
   }
   if (A.partials) {
@@ -303,6 +396,8 @@ __global__ void __launch_bounds__(kBlock)
   const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
   const T *vals = static_cast<const T *>(A.vals);
   const VT *gat = static_cast<const VT *>(A.gat);
+  const uint64_t pol = make_policy(A.hint);
+  const uint64_t pnear = make_gather_policy(1), pfar = make_gather_policy(0);
   for (int64_t s = (int64_t)blockIdx.x * (kBlock / 32) + threadIdx.x / 32; s < n_seg;
        s += warps) {
     // long row owning segment s: last r with seg_off[r] <= s
@@ -318,11 +413,12 @@ __global__ void __launch_bounds__(kBlock)
     VT acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = vzero(VT());
-    gather_row<T, 32, VPL>(A.indices, vals, gat, beg, end, lane, 0xffffffffu, A.nvec, A.ldv, acc);
+    gather_row<T, 32, VPL>(A.indices, vals, gat, beg, end, lane, 0xffffffffu, A.nvec, A.ldv, acc, pol,
+                           row, A.near, pnear, pfar);
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
       const int v = lane + q * 32;
-      if (v < A.nvec) scratch[s * A.ldv + v] = acc[q];
+      if (v < A.nvec) scratch[s * A.nvec + v] = acc[q];
     }
   }
 }
@@ -343,6 +439,7 @@ __global__ void __launch_bounds__(kBlock)
   VT *next = static_cast<VT *>(A.next);
   VT *out = static_cast<VT *>(A.out);
   double s0 = 0.0, s1 = 0.0;
+  const uint64_t pol = make_policy(A.hint);
   for (int64_t r = (int64_t)blockIdx.x * (kBlock / 32) + threadIdx.x / 32; r < n_long;
        r += warps) {
     const int row = long_rows[r];
@@ -353,7 +450,7 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         const int v = lane + q * 32;
-        if (v < A.nvec) vadd(acc[q], scratch[s * A.ldv + v]);
+        if (v < A.nvec) vadd(acc[q], scratch[s * A.nvec + v]);
       }
     }
 #pragma unroll
@@ -361,7 +458,7 @@ __global__ void __launch_bounds__(kBlock)
       const int v = lane + q * 32;
       if (v < A.nvec)
         epilogue<MODE>(acc[q], prev, own, next, out, (size_t)row * A.ldv + v, A.ca, A.cb, s0,
-                       s1, A.sumsq != 0);
+                       s1, A.sumsq != 0, pol);
     }
   }
   if (A.partials) {
@@ -648,6 +745,38 @@ int run_order(const csc_chebop &op, const SweepArgs &A, int mode, double *partia
 
 constexpr int kMaxVecChunk = 256;  // widest row chunk one sweep handles
 
+int g_near = -1, g_hint = -1;
+int64_t g_chunk_vectors = -1;
+
+int near_window() {
+  if (g_near < 0) {
+    const char *e = getenv("CSC_NEAR_WINDOW");
+    g_near = e ? atoi(e) : 0;
+  }
+  return g_near;
+}
+
+// Row chunk width (bytes) per sweep series: narrower chunks shrink the gathered
+// working set (more L2 reuse) at the price of re-reading the CSR per chunk.
+// Interleaved A/B on B200 (tools/ab_sweep.py, cfg3 fp64 d=128): 1024 B 4.59,
+// 512 B 5.18, 256 B 5.67 ms/order -> default: no chunking up to 4 KB rows.
+int64_t chunk_vectors() {
+  if (g_chunk_vectors < 0) {
+    const char *e = getenv("CSC_CHUNK_BYTES");
+    const int64_t bytes = e ? atoll(e) : 16 * kMaxVecChunk;
+    g_chunk_vectors = std::max<int64_t>(1, std::min<int64_t>(bytes / 16, kMaxVecChunk));
+  }
+  return g_chunk_vectors;
+}
+
+int stream_hint() {
+  if (g_hint < 0) {
+    const char *e = getenv("CSC_STREAM_HINT");
+    g_hint = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_hint;
+}
+
 template <typename T>
 int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *coeffs,
                   int ncoeffs, T *out, T *work, double *sumsq_dev, cudaStream_t st) {
@@ -657,19 +786,28 @@ int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *co
   const int64_t n = op.n;
   csc::Scratch parts, segs;
   const int64_t maxp = max_partials(op);
-  CSC_TRY_CUDA(parts.alloc(sizeof(double) * maxp, st));
+  // balanced chunks of at most chunk_vectors() 16-byte vectors
+  const int64_t nchunks = csc::ceil_div(ldv, chunk_vectors());
+  const int64_t per = csc::ceil_div(ldv, nchunks);
+  const bool fused_sumsq = sumsq_dev != nullptr;
+  if (fused_sumsq) {
+    // one slot range per chunk, zero-filled: the final fixed-order reduction
+    // over all slots is independent of how many each chunk used
+    CSC_TRY_CUDA(parts.alloc(sizeof(double) * maxp * nchunks, st));
+    CSC_TRY_CUDA(cudaMemsetAsync(parts.ptr, 0, sizeof(double) * maxp * nchunks, st));
+  }
   if (op.n_long > 0)
-    CSC_TRY_CUDA(segs.alloc(sizeof(VT) * (size_t)op.n_seg * ldv, st));
-  const int64_t nchunks = csc::ceil_div(ldv, kMaxVecChunk);
-  const bool fused_sumsq = sumsq_dev && nchunks == 1;
+    CSC_TRY_CUDA(segs.alloc(sizeof(VT) * (size_t)op.n_seg * per, st));
   for (int64_t ch = 0; ch < nchunks; ++ch) {
-    const int64_t v0 = ch * kMaxVecChunk;
-    const int nvec = (int)std::min<int64_t>(kMaxVecChunk, ldv - v0);
+    const int64_t v0 = ch * per;
+    const int nvec = (int)std::min<int64_t>(per, ldv - v0);
     const VT *xv = reinterpret_cast<const VT *>(x) + v0;
     VT *ta = reinterpret_cast<VT *>(work) + v0;
     VT *tb = reinterpret_cast<VT *>(work + n * ld) + v0;
     VT *ov = reinterpret_cast<VT *>(out) + v0;
     SweepArgs A{};
+    A.hint = stream_hint();
+    A.near = near_window();
     A.indptr = op.indptr;
     A.indices = op.indices;
     A.vals = op.vals;
@@ -685,8 +823,8 @@ int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *co
     A.cb = coeffs[1];
     A.sumsq = (fused_sumsq && ncoeffs == 2) ? 1 : 0;
     int64_t np = 0;
-    int rc = run_order<T>(op, A, kFirst, A.sumsq ? parts.as<double>() : nullptr, np, st,
-                          segs.ptr);
+    double *cparts = fused_sumsq ? parts.as<double>() + ch * maxp : nullptr;
+    int rc = run_order<T>(op, A, kFirst, A.sumsq ? cparts : nullptr, np, st, segs.ptr);
     if (rc != CSC_OK) return rc;
     const VT *t_prev = xv;
     VT *t_cur = ta, *t_next = tb;
@@ -697,18 +835,17 @@ int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *co
       A.ca = coeffs[j];
       A.cb = 0.0;
       A.sumsq = (fused_sumsq && j == ncoeffs - 1) ? 1 : 0;
-      rc = run_order<T>(op, A, kMid, A.sumsq ? parts.as<double>() : nullptr, np, st, segs.ptr);
+      rc = run_order<T>(op, A, kMid, A.sumsq ? cparts : nullptr, np, st, segs.ptr);
       if (rc != CSC_OK) return rc;
       t_prev = t_cur;
       t_cur = t_next;
       t_next = const_cast<VT *>(t_prev);  // T_{j+1} overwrites T_{j-1} row-locally
     }
-    if (fused_sumsq) {
-      reduce_partials_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), np, sumsq_dev);
-      CSC_CHECK_LAUNCH();
-    }
   }
-  if (sumsq_dev && !fused_sumsq) return csc_sumsq(out, n * ld, op.dtype, sumsq_dev, nullptr, st);
+  if (fused_sumsq) {
+    reduce_partials_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), maxp * nchunks, sumsq_dev);
+    CSC_CHECK_LAUNCH();
+  }
   return CSC_OK;
 }
 
@@ -752,6 +889,8 @@ int cheb_moments_t(const csc_chebop &op, const T *x, int64_t ld, int m, double *
   VT *ta = reinterpret_cast<VT *>(work);
   VT *tb = reinterpret_cast<VT *>(work + n * ld);
   SweepArgs A{};
+  A.hint = stream_hint();
+  A.near = near_window();
   A.indptr = op.indptr;
   A.indices = op.indices;
   A.vals = op.vals;
@@ -985,6 +1124,25 @@ int csc_cheb_moments(const csc_chebop *op, const void *x, int64_t ld, int64_t d,
                                   static_cast<double *>(work), st);
   return cheb_moments_t<float>(*op, static_cast<const float *>(x), ld, m, mu_dev,
                                static_cast<float *>(work), st);
+}
+
+int csc_set_tuning(const char *key, int64_t value) {
+  CSC_REQUIRE(key != nullptr, "csc_set_tuning: NULL key");
+  const std::string k(key);
+  if (k == "chunk_bytes") {
+    chunk_vectors();
+    g_chunk_vectors = std::max<int64_t>(1, std::min<int64_t>(value / 16, kMaxVecChunk));
+  } else if (k == "near_window") {
+    near_window();
+    g_near = (int)value;
+  } else if (k == "stream_hint") {
+    stream_hint();
+    g_hint = value ? 1 : 0;
+  } else {
+    csc::set_error("csc_set_tuning: unknown key '%s'", key);
+    return CSC_ERR_ARG;
+  }
+  return CSC_OK;
 }
 
 int csc_sweep_timing(int enable) {
