@@ -867,6 +867,16 @@ __global__ void reduce_pairs_kernel(const double *__restrict__ partials, int64_t
   }
 }
 
+// per-chunk order sums S_ch[q] (q >= 2) added in chunk order; S[0] = <x,x>
+__global__ void combine_sums_kernel(const double *__restrict__ per_chunk, int64_t nchunks,
+                                    int64_t len, double *__restrict__ S) {
+  for (int64_t q = 2 + threadIdx.x; q < len; q += blockDim.x) {
+    double v = 0.0;
+    for (int64_t c = 0; c < nchunks; ++c) v += per_chunk[c * len + q];
+    S[q] = v;
+  }
+}
+
 template <typename T>
 int cheb_moments_t(const csc_chebop &op, const T *x, int64_t ld, int m, double *mu, T *work,
                    cudaStream_t st) {
@@ -874,46 +884,56 @@ int cheb_moments_t(const csc_chebop &op, const T *x, int64_t ld, int m, double *
   constexpr int E = V16<T>::E;
   const int64_t ldv = ld / E;
   const int64_t n = op.n;
-  CSC_REQUIRE(ldv <= kMaxVecChunk, "csc_cheb_moments: rows wider than %d vectors unsupported",
-              kMaxVecChunk);
-  csc::Scratch parts, segs, sums;
+  const int64_t nchunks = csc::ceil_div(ldv, kMaxVecChunk);
+  const int64_t per = csc::ceil_div(ldv, nchunks);
+  const int64_t len = 2 * (m + 1);
+  csc::Scratch parts, segs, sums, chunk_sums;
   const int64_t maxp = max_partials(op);
   CSC_TRY_CUDA(parts.alloc(sizeof(double) * 2 * maxp, st));
-  CSC_TRY_CUDA(sums.alloc(sizeof(double) * 2 * (m + 1), st));
-  if (op.n_long > 0) CSC_TRY_CUDA(segs.alloc(sizeof(VT) * (size_t)op.n_seg * ldv, st));
+  CSC_TRY_CUDA(sums.alloc(sizeof(double) * len, st));
+  CSC_TRY_CUDA(chunk_sums.alloc(sizeof(double) * len * nchunks, st));
+  CSC_TRY_CUDA(cudaMemsetAsync(chunk_sums.ptr, 0, sizeof(double) * len * nchunks, st));
+  if (op.n_long > 0) CSC_TRY_CUDA(segs.alloc(sizeof(VT) * (size_t)op.n_seg * per, st));
   double *S = sums.as<double>();
-  // S[0] = <x, x>; S[2j] = <T_j,T_j>, S[2j+1] = <T_j,T_{j-1}> for j = 1..m
+  // S[0] = <x, x> over the whole block; S[2j] = <T_j,T_j>, S[2j+1] = <T_j,T_{j-1}>
   int rc = csc_sumsq(x, n * ld, op.dtype, S, nullptr, st);
   if (rc != CSC_OK) return rc;
-  const VT *xv = reinterpret_cast<const VT *>(x);
-  VT *ta = reinterpret_cast<VT *>(work);
-  VT *tb = reinterpret_cast<VT *>(work + n * ld);
-  SweepArgs A{};
-  A.hint = stream_hint();
-  A.near = near_window();
-  A.indptr = op.indptr;
-  A.indices = op.indices;
-  A.vals = op.vals;
-  A.n = n;
-  A.nvec = (int)ldv;
-  A.ldv = ldv;
-  const VT *t_prev = nullptr;
-  const VT *t_cur = xv;
-  VT *t_next = ta;
-  for (int j = 0; j < m; ++j) {  // produces T_{j+1}
-    A.gat = t_cur;
-    A.own = t_cur;
-    A.prev = t_prev;
-    A.next = t_next;
-    int64_t np = 0;
-    rc = run_order<T>(op, A, j == 0 ? kMomFirst : kMomMid, parts.as<double>(), np, st, segs.ptr);
-    if (rc != CSC_OK) return rc;
-    reduce_pairs_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), np, S + 2 * (j + 1));
-    CSC_CHECK_LAUNCH();
-    t_prev = t_cur;
-    t_cur = t_next;
-    t_next = (j == 0) ? tb : const_cast<VT *>(t_prev);
+  for (int64_t ch = 0; ch < nchunks; ++ch) {
+    const int64_t v0 = ch * per;
+    const VT *xv = reinterpret_cast<const VT *>(x) + v0;
+    VT *ta = reinterpret_cast<VT *>(work) + v0;
+    VT *tb = reinterpret_cast<VT *>(work + n * ld) + v0;
+    double *Sc = chunk_sums.as<double>() + ch * len;
+    SweepArgs A{};
+    A.hint = stream_hint();
+    A.near = near_window();
+    A.indptr = op.indptr;
+    A.indices = op.indices;
+    A.vals = op.vals;
+    A.n = n;
+    A.nvec = (int)std::min<int64_t>(per, ldv - v0);
+    A.ldv = ldv;
+    const VT *t_prev = nullptr;
+    const VT *t_cur = xv;
+    VT *t_next = ta;
+    for (int j = 0; j < m; ++j) {  // produces T_{j+1}
+      A.gat = t_cur;
+      A.own = t_cur;
+      A.prev = t_prev;
+      A.next = t_next;
+      int64_t np = 0;
+      rc = run_order<T>(op, A, j == 0 ? kMomFirst : kMomMid, parts.as<double>(), np, st,
+                        segs.ptr);
+      if (rc != CSC_OK) return rc;
+      reduce_pairs_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), np, Sc + 2 * (j + 1));
+      CSC_CHECK_LAUNCH();
+      t_prev = t_cur;
+      t_cur = t_next;
+      t_next = (j == 0) ? tb : const_cast<VT *>(t_prev);
+    }
   }
+  combine_sums_kernel<<<1, 256, 0, st>>>(chunk_sums.as<double>(), nchunks, len, S);
+  CSC_CHECK_LAUNCH();
   moments_finish_kernel<<<1, 32, 0, st>>>(S, m, 0.0, mu);
   CSC_CHECK_LAUNCH();
   return CSC_OK;

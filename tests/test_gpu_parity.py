@@ -429,3 +429,87 @@ def test_operator_plan_bitwise(P, name, variant):
     assert np.array_equal(ip, exp.indptr)
     assert np.array_equal(ix, exp.indices)
     assert np.array_equal(vv, exp.data)
+
+
+# ---------------------------------------------------------------------------
+# Chebyshev moments and the single-pass bisection
+# ---------------------------------------------------------------------------
+
+def _oracle_moments(m_csr, s, x, m):
+    """mu_q = <x, T_q(M) x> (summed over columns) by the CPU recurrence."""
+    import scipy.sparse as sp
+    n = m_csr.shape[0]
+    M = sp.identity(n) - s * m_csr
+    t_prev, t_cur = x, M @ x
+    mu = [float((x * x).sum()), float((x * t_cur).sum())]
+    for _ in range(2, 2 * m + 1):
+        t_prev, t_cur = t_cur, 2.0 * (M @ t_cur) - t_prev
+        mu.append(float((x * t_cur).sum()))
+    return np.array(mu)
+
+
+@pytest.mark.parametrize("d", [5, 40, 600])
+def test_moments_match_oracle(P, d):
+    from paper_1706_03591_b200.filters import block_moments
+    from paper_1706_03591_b200._device import upload_block
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    x = np.random.default_rng(d).normal(size=(lap.n, d)) / np.sqrt(d)
+    mu = block_moments(lap, upload_block(x), d, 30, 2.0)
+    ref = _oracle_moments(lap.matrix, 1.0, x, 30)
+    scale = np.abs(ref).max()
+    assert np.abs(mu - ref).max() <= 1e-12 * scale
+
+
+def test_moment_energy_equals_block_energy(P):
+    from paper_1706_03591_b200.filters import block_moments, moment_energy
+    from paper_1706_03591_b200._device import upload_block
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    mu = block_moments(lap, upload_block(g["R"]), 40, 50, 2.0)
+    for cut in (0.1, 0.3, 0.5, 1.0, 1.9):
+        poly = P.cheb_coeffs(cut, 2.0, 50)
+        ref = O.count_from_block(ON.cheb_filter(g["L_indptr"], g["L_indices"], g["L_data"], 2.0,
+                                                poly.coeffs, g["R"]), 1.0)
+        assert abs(moment_energy(mu, poly.coeffs) - ref) <= 1e-11 * max(ref, 1.0)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "small"])
+def test_moment_search_equals_probe_search(P, case):
+    from paper_1706_03591_b200.filters import _search_cutoff
+    if case == "cfg1":
+        g = golden("cfg1")
+        lap = P.laplacian(graph_from(g, "g", P))
+        r, k, order, iters_max = g["R"], 10, 50, 8
+    else:
+        g = golden("small")
+        lap = P.laplacian(graph_from(g, "sbm60", P))
+        r, k, order, iters_max = O.random_signals(60, 12, 5), 3, 40, 20
+    res = {}
+    for mode in ("moments", "probe"):
+        cnt = P.MatvecCounter()
+        cfg = P.FilterConfig(order=order, max_iters=iters_max, search=mode)
+        res[mode] = (_search_cutoff(lap, k, r, (0.0, 2.0), cfg, cnt, 1.0), cnt)
+    (cm, fm, pm, im, em), cntm = res["moments"]
+    (cp, fp, pp, ip_, ep), cntp = res["probe"]
+    assert cm == cp and im == ip_
+    assert np.array_equal(fm, fp)
+    assert abs(em - ep) <= 1e-12 * abs(ep)
+    assert cntm.count == cntp.count == im * order * r.shape[1]
+    assert cntm.physical <= 2 * order * r.shape[1] + cntp.physical  # moment pass + final features
+    assert cntm.physical == 2 * order * r.shape[1] or im == 1
+
+
+def test_reference_counter_accepted(P):
+    """A counter without the physical ledger (like cscluster.MatvecCounter) works."""
+    class RefCounter:
+        def __init__(self):
+            self.count = 0
+
+        def add(self, k):
+            self.count += int(k)
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, "sbm60", P))
+    c = RefCounter()
+    lam, feats, iters = P.find_lambda_k(lap, 3, d=12, m=40, seed=5, counter=c)
+    assert c.count == iters * 40 * 12
