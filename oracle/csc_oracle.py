@@ -279,3 +279,21 @@ def adjusted_rand(a, b) -> float:
     if mx == exp:
         return 1.0
     return float((s - exp) / (mx - exp))
+
+
+def moments(indptr, indices, data, lambda_max: float, x, m: int) -> np.ndarray:
+    """mu_q = sum over columns of <x, T_q(M) x>, q = 0..2m, M = I - (2/lambda_max) L.
+
+    Checker for the moment bisection (not a reference function; the
+    reference recomputes the filtered block per probe, filters.py:237-242).
+    """
+    n = len(indptr) - 1
+    a = sp.csr_matrix((np.asarray(data, np.float64), np.asarray(indices), np.asarray(indptr)), shape=(n, n))
+    s = 2.0 / lambda_max
+    x = np.asarray(x, dtype=np.float64)
+    t_prev, t_cur = x, x - s * (a @ x)
+    mu = [float((x * x).sum()), float((x * t_cur).sum())]
+    for _ in range(2, 2 * m + 1):
+        t_prev, t_cur = t_cur, 2.0 * (t_cur - s * (a @ t_cur)) - t_prev
+        mu.append(float((x * t_cur).sum()))
+    return np.array(mu)
