@@ -140,6 +140,8 @@ int csc_kmeans_assign(const double *f_dev, const double *rownorm_dev, int64_t n,
                       int64_t ld, const double *c_dev, int64_t ldc, const double *cnorm_dev,
                       int64_t k, int32_t *labels_dev, double *own_d2_dev, int32_t *counts_dev,
                       void *stream);
+/* k-means tuning knob: "assign_tn" = 4 (default) or 8 centroids per thread */
+int csc_kmeans_tuning(const char *key, int64_t value);
 /* empty-cluster repair (kmeans.py:99-108): for each empty j ascending, move the
  * row with the largest own_d2 (first max) to j and set its own_d2 to -1.
  * No-op when every count is positive (checked on device; no sync). */
@@ -172,6 +174,16 @@ int csc_kmeanspp_pick(const double *f_dev, int64_t n, int64_t d, int64_t ld,
                       const double *closest_dev, const double *chunk_sums_dev,
                       int64_t nchunks, double u, int64_t fixed_idx, double *c_row_dev,
                       int64_t *idx_dev, void *stream);
+
+/* Batched k-means++ for R <= 16 restarts in one pass per centroid index.
+ * first_idx_host[r] = the restart's integers(n) draw; uniforms_host[r*(k-1)+j-1]
+ * = its j-th random() draw (host arrays). Writes cent[r*k*ldc + j*ldc + c]
+ * (device, R x k x ldc). flags_dev[r] (int32, device) = first j whose D^2
+ * mass was 0 (the reference then draws integers(n): the caller must replay
+ * that restart on the sequential path), else -1. */
+int csc_kmeanspp_batch(const double *f_dev, int64_t n, int64_t d, int64_t ld, int64_t R, int64_t k,
+                       const int64_t *first_idx_host, const double *uniforms_host, double *cent_dev,
+                       int64_t ldc, int32_t *flags_dev, void *stream);
 
 /* ---- dense helpers ------------------------------------------------------ */
 /* dst[:, j] = src[:, cols[j]] for j < ncols (row-major, f64), the Theta

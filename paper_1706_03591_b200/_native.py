@@ -43,12 +43,14 @@ SIGNATURES = {
     "csc_sweep_times": ([ctypes.POINTER(ctypes.c_float), _INT, ctypes.POINTER(_INT)], _INT),
     "csc_kmeans_rownorms": ([_P, _I64, _I64, _I64, _P, _P], _INT),
     "csc_kmeans_assign": ([_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P], _INT),
+    "csc_kmeans_tuning": ([ctypes.c_char_p, _I64], _INT),
     "csc_kmeans_repair": ([_P, _P, _P, _I64, _I64, _P], _INT),
     "csc_kmeans_update": ([_P, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P], _INT),
     "csc_kmeans_cost": ([_P, _P, _P, _I64, _I64, _I64, _I64, _P, _P], _INT),
     "csc_kmeanspp_nchunks": ([_I64], _INT),
     "csc_kmeanspp_dist": ([_P, _I64, _I64, _I64, _P, _P, _INT, _P, _I64, _P, _P], _INT),
     "csc_kmeanspp_pick": ([_P, _I64, _I64, _I64, _P, _P, _I64, _D, _I64, _P, _P, _P], _INT),
+    "csc_kmeanspp_batch": ([_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _P, _P], _INT),
     "csc_gather_columns": ([_P, _I64, _I64, _P, _I64, _P, _I64, _I64, _P], _INT),
 }
 

@@ -17,6 +17,7 @@
 //           single-block D^2 draw for one host-supplied uniform
 //           (Generator.choice(n, p) == searchsorted(cumsum(p), u, 'right')).
 #include <cub/cub.cuh>
+#include <string>
 
 #include "common.cuh"
 
@@ -145,6 +146,161 @@ __global__ void __launch_bounds__(kAssignThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// assign v2: 128 rows x 64 centroids per 128-thread block, 8x8 FP64 register
+// tile per thread (rows ty+16i, centroids tx+8j), the centroid tile resident
+// in shared memory transposed [d][64], F streamed in 16-wide d stages with
+// cp.async double buffering (zero-fill outside the matrix). FP64-FMA bound.
+// ---------------------------------------------------------------------------
+constexpr int kAM = 128, kAN = 64, kAK = 16, kAKP = kAK + 2, kANP = kAN + 1;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  const int src_size = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(src_size));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// 128 rows x 64 centroids per block; each thread owns 8 rows (ty + 16 i) and
+// TN centroids (tx + (64/TN) j). TN = 8: 128 threads; TN = 4: 256 threads.
+template <int TN>
+__global__ void __launch_bounds__(16 * (kAN / TN), (TN == 8 ? 2 : 2))
+    assign2_kernel(const double *__restrict__ f, const double *__restrict__ fnorm, int64_t n,
+                   int64_t d, int64_t ld, const double *__restrict__ cent, int64_t ldc,
+                   const double *__restrict__ cnorm, int64_t k, int32_t *__restrict__ labels,
+                   double *__restrict__ own, int32_t *__restrict__ counts) {
+  constexpr int CT = kAN / TN;        // centroid-threads per row group
+  constexpr int NT = 16 * CT;         // threads per block
+  extern __shared__ __align__(16) double smem[];
+  const int64_t dpad = (d + kAK - 1) / kAK * kAK;
+  double *Cs = smem;                    // [dpad][kANP]
+  double *Fs = smem + dpad * kANP;      // [2][kAM][kAKP]
+  const int tid = threadIdx.x;
+  const int tx = tid % CT, ty = tid / CT;
+  const int64_t r0 = (int64_t)blockIdx.x * kAM;
+  const int nst = (int)(dpad / kAK);
+  double fn[8], best_v[8];
+  int best_i[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = r0 + ty + 16 * i;
+    fn[i] = r < n ? fnorm[r] : 0.0;
+    best_v[i] = INFINITY;
+    best_i[i] = 0;
+  }
+  auto load_stage = [&](int st, int buf) {
+    const int64_t k0 = (int64_t)st * kAK;
+#pragma unroll
+    for (int q = 0; q < 1024 / NT; ++q) {  // 128 rows x 8 vectors of 2 doubles
+      const int v = tid + NT * q;
+      const int row = v >> 3, vc = v & 7;
+      const int64_t gr = r0 + row, gc = k0 + 2 * vc;
+      const bool ok = gr < n && gc < ld;  // ld is even: the pair is inside the row
+      const double *src = ok ? f + gr * ld + gc : f;
+      cp_async16(Fs + ((size_t)buf * kAM + row) * kAKP + 2 * vc, src, ok);
+    }
+  };
+  for (int64_t c0 = 0; c0 < k; c0 += kAN) {
+    __syncthreads();  // previous tile's readers of Cs / Fs are done
+    for (int64_t e = tid; e < dpad * kAN; e += NT) {
+      const int64_t cc = e / dpad, dd = e - cc * dpad;  // coalesced along a centroid row
+      Cs[dd * kANP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
+    }
+    double acc[8][TN];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+    load_stage(0, 0);
+    cp_async_commit();
+    for (int st = 0; st < nst; ++st) {
+      if (st + 1 < nst) load_stage(st + 1, (st + 1) & 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      const double *Fb = Fs + (size_t)(st & 1) * kAM * kAKP;
+      const double *Cb = Cs + (size_t)st * kAK * kANP;
+#pragma unroll
+      for (int kk = 0; kk < kAK; ++kk) {
+        double a[8], b[TN];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = Fb[(ty + 16 * i) * kAKP + kk];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) b[j] = Cb[kk * kANP + tx + CT * j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double v = INFINITY;
+      int vi = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t c = c0 + tx + CT * j;
+        if (c < k) {
+          const double t = __dsub_rn(fn[i], __dmul_rn(2.0, acc[i][j]));
+          double d2 = __dadd_rn(t, cnorm[c]);
+          d2 = d2 > 0.0 ? d2 : 0.0;
+          if (d2 < v) {
+            v = d2;
+            vi = (int)c;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < CT; o <<= 1) {  // the CT lanes of a row group are adjacent
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+        if (ov < v || (ov == v && oi < vi)) {
+          v = ov;
+          vi = oi;
+        }
+      }
+      if (v < best_v[i] || (v == best_v[i] && vi < best_i[i])) {
+        best_v[i] = v;
+        best_i[i] = vi;
+      }
+    }
+  }
+  if (tx == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t r = r0 + ty + 16 * i;
+      if (r < n) {
+        labels[r] = best_i[i];
+        own[r] = best_v[i];
+        if (counts) atomicAdd(counts + best_i[i], 1);
+      }
+    }
+  }
+}
+
+int g_assign_tn = 8;
+
+template <int TN>
+int launch_assign2(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
+                   const double *c, int64_t ldc, const double *cnorm, int64_t k, int32_t *labels,
+                   double *own, int32_t *counts, size_t smem, cudaStream_t st) {
+  static size_t configured = 0;
+  if (smem > configured) {
+    CSC_TRY_CUDA(cudaFuncSetAttribute(assign2_kernel<TN>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  assign2_kernel<TN><<<(unsigned)csc::ceil_div(n, kAM), 16 * (kAN / TN), smem, st>>>(
+      f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts);
+  return CSC_OK;
+}
+
 // argmax with first-index ties over a[0..n) by one block (result in thread 0)
 __device__ void block_argmax(const double *a, int64_t n, double &bv, int64_t &bi) {
   __shared__ double sv[32];
@@ -220,10 +376,21 @@ __global__ void update_partial_kernel(const double *__restrict__ f,
   const int c = threadIdx.x;
   const bool active = c < cw && col0 + c < d;
   if (active) {
-    for (int64_t r = rbeg; r < rend; ++r) {
-      const int32_t l = labels[r];
-      sm[(size_t)l * cw + c] += f[r * ld + col0 + c];
+    const double *fc = f + col0 + c;
+    int64_t r = rbeg;
+    // 8 rows in flight per thread: loads first, then the (ordered) smem adds
+    for (; r + 8 <= rend; r += 8) {
+      int32_t l[8];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        l[u] = __ldg(labels + r + u);
+        v[u] = __ldg(fc + (r + u) * ld);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sm[(size_t)l[u] * cw + c] += v[u];
     }
+    for (; r < rend; ++r) sm[(size_t)labels[r] * cw + c] += fc[r * ld];
   }
   if (blockIdx.y == 0)
     for (int64_t r = rbeg + threadIdx.x; r < rend; r += blockDim.x) atomicAdd(scnt + labels[r], 1);
@@ -238,31 +405,52 @@ __global__ void update_partial_kernel(const double *__restrict__ f,
   (void)nb;
 }
 
+// one warp per (centroid j, column c): lanes add the block partials b = lane,
+// lane+32, ... in order, then a fixed shuffle tree; means = sum / max(count,1)
 __global__ void update_finish_kernel(const double *__restrict__ psum,
                                      const int32_t *__restrict__ pcnt, int64_t nb, int64_t d,
                                      int64_t k, double *__restrict__ cent, int64_t ldc,
-                                     double *__restrict__ cnorm, int32_t *__restrict__ counts) {
-  __shared__ double red[32];
-  __shared__ int32_t s_cnt;
-  const int64_t j = blockIdx.x;
-  if (threadIdx.x == 0) {
+                                     double *__restrict__ cent_t, int32_t *__restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (w >= k * (d + 1)) return;
+  const int64_t j = w / (d + 1), c = w - j * (d + 1);
+  if (c == d) {  // the count
     int32_t cnt = 0;
-    for (int64_t b = 0; b < nb; ++b) cnt += pcnt[b * k + j];
-    s_cnt = cnt;
-    counts[j] = cnt;
+    for (int64_t b = lane; b < nb; b += 32) cnt += pcnt[b * k + j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) counts[j] = cnt;
+    return;
   }
-  __syncthreads();
-  const double denom = (double)(s_cnt > 1 ? s_cnt : 1);
-  double nrm = 0.0;
-  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
-    double s = 0.0;
-    for (int64_t b = 0; b < nb; ++b) s += psum[(b * k + j) * d + c];
-    const double mean = __ddiv_rn(s, denom);
+  double s = 0.0;
+  int32_t cnt = 0;
+  for (int64_t b = lane; b < nb; b += 32) {
+    s += psum[(b * k + j) * d + c];
+    cnt += pcnt[b * k + j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if (lane == 0) {
+    const double mean = __ddiv_rn(s, (double)(cnt > 1 ? cnt : 1));
     cent[j * ldc + c] = mean;
-    nrm = fma(mean, mean, nrm);
+    if (cent_t) cent_t[c * k + j] = mean;
   }
-  nrm = block_sum<128>(nrm, red);
-  if (threadIdx.x == 0) cnorm[j] = nrm;
+}
+
+__global__ void centroid_norms_kernel(const double *__restrict__ cent, int64_t ldc, int64_t d,
+                                      int64_t k, double *__restrict__ cnorm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (j >= k) return;
+  double s = 0.0;
+  for (int64_t c = lane; c < d; c += 32) s = fma(cent[j * ldc + c], cent[j * ldc + c], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) cnorm[j] = s;
 }
 
 __global__ void cost_kernel(const double *__restrict__ f, const int32_t *__restrict__ labels,
@@ -378,6 +566,148 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 0) idx_out[0] = idx;
 }
 
+// ---------------------------------------------------------------------------
+// Batched k-means++ over R restarts (independent RNG streams, uniforms drawn
+// on the host in each stream's order). One pass over F per centroid index
+// serves all restarts; draws need no host round trip. A restart whose D^2
+// mass ever reaches 0 is flagged (the reference then draws integers(n)
+// instead of random(), changing its stream), and the host replays it.
+// ---------------------------------------------------------------------------
+
+// closest[r][i] = (first ? d2 : min(closest, d2)), d2 = |f_i - crow_r|^2, for r < R;
+// chunk_sums[r][b] = sum of closest[r] over contiguous chunk b (block b).
+__global__ void kppb_dist_kernel(const double *__restrict__ f, int64_t n, int64_t d, int64_t ld,
+                                 const double *__restrict__ crows, int64_t crow_stride, int R,
+                                 double *__restrict__ closest, int first, int64_t chunk,
+                                 double *__restrict__ chunk_sums, int64_t nchunks) {
+  extern __shared__ double sh[];  // R x d centroid rows, then 8 x R block partials
+  double *cs = sh;
+  double *wsum = sh + (size_t)R * d;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t e = threadIdx.x; e < (int64_t)R * d; e += blockDim.x) {
+    const int64_t r = e / d, c = e - r * d;
+    cs[e] = crows[r * crow_stride + c];
+  }
+  __syncthreads();
+  const int64_t rbeg = blockIdx.x * chunk, rend = min(n, rbeg + chunk);
+  double part[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) part[r] = 0.0;
+  for (int64_t i = rbeg + wid; i < rend; i += blockDim.x / 32) {
+    const double *row = f + i * ld;
+    double acc[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+    for (int64_t c = lane; c < d; c += 32) {
+      const double x = row[c];
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (r < R) {
+          const double t = x - cs[r * d + c];
+          acc[r] = fma(t, t, acc[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r < R) {
+        double v = acc[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == r) {
+          double* slot = closest + (int64_t)r * n + i;
+          const double cl = first ? v : fmin(*slot, v);
+          *slot = cl;
+          part[r] += cl;
+        }
+      }
+    }
+  }
+  // per-warp partial of restart r lives in lane r; fixed-order block sum
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    if (r < R && lane == r) wsum[wid * R + r] = part[r];
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += wsum[w * R + threadIdx.x];
+    chunk_sums[(int64_t)threadIdx.x * nchunks + blockIdx.x] = t;
+  }
+}
+
+// Block r draws centroid j of restart r from its chunk sums and uniform.
+__global__ void __launch_bounds__(1024)
+    kppb_pick_kernel(const double *__restrict__ f, int64_t n, int64_t d, int64_t ld,
+                     const double *__restrict__ closest, const double *__restrict__ chunk_sums,
+                     int64_t nchunks, int64_t chunk, const double *__restrict__ uniforms,
+                     int64_t kminus1, int j, double *__restrict__ cent, int64_t cent_stride,
+                     int64_t ldc, int32_t *__restrict__ flags) {
+  typedef cub::BlockScan<double, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long s_idx;
+  __shared__ double s_total, s_target, s_base;
+  __shared__ int64_t s_chunk;
+  const int r = blockIdx.x;
+  const double *cl = closest + (int64_t)r * n;
+  const double *cs = chunk_sums + (int64_t)r * nchunks;
+  // chunk-level inclusive scan (nchunks <= 1024)
+  const double v = threadIdx.x < nchunks ? cs[threadIdx.x] : 0.0;
+  double incl, total;
+  Scan(tmp).InclusiveSum(v, incl, total);
+  if (threadIdx.x == 0) {
+    s_total = total;
+    s_idx = ~0ull;
+    s_chunk = nchunks - 1;
+  }
+  __syncthreads();
+  if (!(s_total > 0.0)) {
+    if (threadIdx.x == 0) {
+      if (flags[r] < 0) flags[r] = j;
+      s_idx = 0;
+    }
+    __syncthreads();
+  } else {
+    const double target = uniforms[(int64_t)r * kminus1 + (j - 1)] * s_total;
+    if (threadIdx.x < nchunks && incl > target) atomicMin((unsigned long long *)&s_chunk, (unsigned long long)threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == (int)s_chunk) s_base = incl - v;
+    if (threadIdx.x == 0) s_target = target;
+    __syncthreads();
+    double running = s_base;
+    bool found = false;
+    for (int64_t t0 = s_chunk * chunk; t0 < n && !found; t0 += 1024) {
+      const int64_t i = t0 + threadIdx.x;
+      const double x = i < n ? cl[i] : 0.0;
+      double inc2, agg;
+      __syncthreads();
+      Scan(tmp).InclusiveSum(x, inc2, agg);
+      const bool hit = i < n && x > 0.0 && running + inc2 > s_target;
+      if (__syncthreads_or(hit)) {
+        if (hit) atomicMin(&s_idx, (unsigned long long)i);
+        __syncthreads();
+        found = true;
+      }
+      running += agg;
+    }
+    if (!found && threadIdx.x == 0) {
+      int64_t last = n - 1;
+      while (last > 0 && !(cl[last] > 0.0)) --last;
+      s_idx = (unsigned long long)last;
+    }
+    __syncthreads();
+  }
+  const int64_t idx = (int64_t)s_idx;
+  double *crow = cent + (int64_t)r * cent_stride + (int64_t)j * ldc;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) crow[c] = f[idx * ld + c];
+}
+
+__global__ void kppb_first_kernel(const double *__restrict__ f, int64_t d, int64_t ld,
+                                  const int64_t *__restrict__ first_idx, double *__restrict__ cent,
+                                  int64_t cent_stride) {
+  const int r = blockIdx.x;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x)
+    cent[(int64_t)r * cent_stride + c] = f[first_idx[r] * ld + c];
+}
+
 __global__ void gather_cols_kernel(const double *__restrict__ src, int64_t n, int64_t lds,
                                    const int64_t *__restrict__ cols, int64_t ncols,
                                    double *__restrict__ dst, int64_t ldd, int64_t col0) {
@@ -415,10 +745,33 @@ int csc_kmeans_assign(const double *f, const double *fnorm, int64_t n, int64_t d
   CSC_REQUIRE(k < INT32_MAX, "csc_kmeans_assign: k too large");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (counts) CSC_TRY_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * k, st));
-  assign_kernel<<<(unsigned)csc::ceil_div(n, kBM), kAssignThreads, 0, st>>>(
-      f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts);
+  const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
+  const size_t smem = sizeof(double) * (dpad * kANP + 2 * kAM * kAKP);
+  const bool aligned = (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(f) & 15u) == 0);
+  if (aligned && (int64_t)smem <= (int64_t)csc::device_info().max_smem_optin) {
+    const int rc = g_assign_tn == 8
+                       ? launch_assign2<8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts,
+                                           smem, st)
+                       : launch_assign2<4>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts,
+                                           smem, st);
+    if (rc != CSC_OK) return rc;
+  } else {
+    assign_kernel<<<(unsigned)csc::ceil_div(n, kBM), kAssignThreads, 0, st>>>(
+        f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts);
+  }
   CSC_CHECK_LAUNCH();
   return CSC_OK;
+}
+
+int csc_kmeans_tuning(const char *key, int64_t value) {
+  CSC_REQUIRE(key != nullptr, "csc_kmeans_tuning: NULL key");
+  if (std::string(key) == "assign_tn") {
+    CSC_REQUIRE(value == 4 || value == 8, "assign_tn must be 4 or 8");
+    g_assign_tn = (int)value;
+    return CSC_OK;
+  }
+  csc::set_error("csc_kmeans_tuning: unknown key '%s'", key);
+  return CSC_ERR_ARG;
 }
 
 int csc_kmeans_repair(int32_t *labels, double *own, int32_t *counts, int64_t n, int64_t k,
@@ -444,9 +797,9 @@ int csc_kmeans_update(const double *f, const int32_t *labels, int64_t n, int64_t
               (long long)k);
   cw = std::min<int64_t>(std::min<int64_t>(cw, 256), d);
   const int64_t ny = csc::ceil_div(d, cw);
-  // rows per block: enough blocks to fill the GPU, at least 32 rows each
+  // rows per block: ~8 resident blocks per SM, at least 64 rows each
   const int64_t nb = std::max<int64_t>(
-      1, std::min<int64_t>((int64_t)info.sm_count * 2, csc::ceil_div(n, 32)));
+      1, std::min<int64_t>((int64_t)info.sm_count * 8, csc::ceil_div(n, 64)));
   const int64_t chunk = csc::ceil_div(n, nb);
   const size_t smem = sizeof(double) * k * cw + cnt_bytes;
   CSC_TRY_CUDA(cudaFuncSetAttribute(update_partial_kernel,
@@ -458,8 +811,11 @@ int csc_kmeans_update(const double *f, const int32_t *labels, int64_t n, int64_t
   update_partial_kernel<<<dim3((unsigned)nb, (unsigned)ny), threads, smem, st>>>(
       f, labels, n, d, ld, k, chunk, (int)cw, psum.as<double>(), pcnt.as<int32_t>());
   CSC_CHECK_LAUNCH();
-  update_finish_kernel<<<(unsigned)k, 128, 0, st>>>(psum.as<double>(), pcnt.as<int32_t>(), nb, d,
-                                                    k, c, ldc, cnorm, counts);
+  const int64_t warps = k * (d + 1);
+  update_finish_kernel<<<(unsigned)csc::ceil_div(warps, 8), 256, 0, st>>>(
+      psum.as<double>(), pcnt.as<int32_t>(), nb, d, k, c, ldc, nullptr, counts);
+  CSC_CHECK_LAUNCH();
+  centroid_norms_kernel<<<(unsigned)csc::ceil_div(k, 8), 256, 0, st>>>(c, ldc, d, k, cnorm);
   CSC_CHECK_LAUNCH();
   return CSC_OK;
 }
@@ -509,6 +865,48 @@ int csc_kmeanspp_pick(const double *f, int64_t n, int64_t d, int64_t ld, const d
   kpp_pick_kernel<<<1, 1024, 0, st>>>(f, n, d, ld, closest, chunk_sums, nchunks, chunk, u,
                                       fixed_idx, crow, idx_dev);
   CSC_CHECK_LAUNCH();
+  return CSC_OK;
+}
+
+int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_t R, int64_t k,
+                       const int64_t *first_idx_host, const double *uniforms_host, double *cent,
+                       int64_t ldc, int32_t *flags_dev, void *stream) {
+  CSC_REQUIRE(n >= 1 && d >= 1 && ld >= d && ldc >= d && k >= 1, "csc_kmeanspp_batch: bad shape");
+  CSC_REQUIRE(R >= 1 && R <= 16, "csc_kmeanspp_batch: 1 <= R <= 16 restarts per batch");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nchunks = std::min<int64_t>(1024, csc_kmeanspp_nchunks(n));
+  const int64_t chunk = csc::ceil_div(n, nchunks);
+  const int64_t cent_stride = k * ldc;
+  csc::Scratch closest, sums, fidx, unif;
+  CSC_TRY_CUDA(closest.alloc(sizeof(double) * R * n, st));
+  CSC_TRY_CUDA(sums.alloc(sizeof(double) * R * nchunks, st));
+  CSC_TRY_CUDA(fidx.alloc(sizeof(int64_t) * R, st));
+  CSC_TRY_CUDA(unif.alloc(sizeof(double) * std::max<int64_t>(1, R * (k - 1)), st));
+  CSC_TRY_CUDA(cudaMemcpyAsync(fidx.ptr, first_idx_host, sizeof(int64_t) * R,
+                               cudaMemcpyHostToDevice, st));
+  if (k > 1)
+    CSC_TRY_CUDA(cudaMemcpyAsync(unif.ptr, uniforms_host, sizeof(double) * R * (k - 1),
+                                 cudaMemcpyHostToDevice, st));
+  CSC_TRY_CUDA(cudaMemsetAsync(flags_dev, 0xff, sizeof(int32_t) * R, st));
+  kppb_first_kernel<<<(unsigned)R, 128, 0, st>>>(f, d, ld, fidx.as<int64_t>(), cent, cent_stride);
+  CSC_CHECK_LAUNCH();
+  const size_t smem = sizeof(double) * (R * d + 8 * R);
+  CSC_REQUIRE(smem <= 48 * 1024, "csc_kmeanspp_batch: R*d too large");
+  for (int64_t j = 0; j < k; ++j) {
+    if (j > 0) {
+      kppb_pick_kernel<<<(unsigned)R, 1024, 0, st>>>(f, n, d, ld, closest.as<double>(),
+                                                     sums.as<double>(), nchunks, chunk,
+                                                     unif.as<double>(), k - 1, (int)j, cent,
+                                                     cent_stride, ldc, flags_dev);
+      CSC_CHECK_LAUNCH();
+    }
+    if (j < k - 1) {
+      kppb_dist_kernel<<<(unsigned)nchunks, 256, smem, st>>>(
+          f, n, d, ld, cent + j * ldc, cent_stride, (int)R, closest.as<double>(), j == 0 ? 1 : 0,
+          chunk, sums.as<double>(), nchunks);
+      CSC_CHECK_LAUNCH();
+    }
+  }
   return CSC_OK;
 }
 

@@ -139,6 +139,36 @@ class _Workspace:
         return prev
 
 
+KPP_BATCH = 16  # restarts per batched k-means++ launch series (libcscb200 limit)
+
+
+def batched_kmeanspp(ws: _Workspace, children) -> torch.Tensor:
+    """k-means++ seeds of every restart: (restarts, k, ldc) on the GPU.
+
+    Each restart's stream is drawn on the host in the reference's order
+    (integers(n), then k-1 random(); kmeans.py:67-74) and the draws run in
+    one batched device pass per centroid index. A restart that hits a zero
+    D^2 mass (the reference then switches to integers(n)) is flagged by the
+    device and replayed on the sequential path with a fresh generator.
+    """
+    n, k, R = ws.n, ws.k, len(children)
+    seeds = torch.zeros((R, k, ws.ldc), dtype=torch.float64, device=ws.blk.device)
+    flags = torch.empty(KPP_BATCH, dtype=torch.int32, device=ws.blk.device)
+    for g0 in range(0, R, KPP_BATCH):
+        grp = list(range(g0, min(R, g0 + KPP_BATCH)))
+        rngs = [np.random.default_rng(children[r]) for r in grp]
+        first = np.array([int(rng.integers(n)) for rng in rngs], dtype=np.int64)
+        unif = np.ascontiguousarray(np.stack([rng.random(k - 1) for rng in rngs]) if k > 1
+                                    else np.zeros((len(grp), 1)))
+        _native.call("csc_kmeanspp_batch", ptr(ws.blk), n, ws.d, ws.ld, len(grp), k,
+                     first.ctypes.data, unif.ctypes.data, ptr(seeds[g0]), ws.ldc, ptr(flags), stream())
+        bad = flags[: len(grp)].cpu().numpy()
+        for gi in np.flatnonzero(bad >= 0):
+            ws.kmeanspp(np.random.default_rng(children[grp[gi]]))
+            seeds[grp[gi]].copy_(ws.cent)
+    return seeds
+
+
 def _features_block(f):
     """Accept numpy / torch / FeatureMatrix features; validate like kmeans.py:127-134."""
     if isinstance(f, FeatureMatrix):
@@ -175,9 +205,11 @@ def kmeans(f, k: int, cfg: KmeansConfig | None = None, seed=0) -> Assignment:
     if not 1 <= k <= n:
         raise ValueError(f"need 1 <= k <= n, got k={k}, n={n}")
     ws = _Workspace(blk, d, k)
+    children = as_seed_sequence(seed).spawn(cfg.restarts)
+    seeds = batched_kmeanspp(ws, children)
     best = None
-    for child in as_seed_sequence(seed).spawn(cfg.restarts):
-        ws.kmeanspp(np.random.default_rng(child))
+    for r in range(cfg.restarts):
+        ws.cent.copy_(seeds[r])
         cost2 = ws.lloyd(cfg.max_iters, cfg.tol)
         if best is None or cost2 < best[0]:
             best = (cost2, ws.labels.clone())

@@ -10,7 +10,8 @@ Reference: /root/reference/pkg/src/cscluster/signals.py
 """
 from __future__ import annotations
 
-import ctypes
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import torch
@@ -26,8 +27,25 @@ def as_seed_sequence(seed) -> np.random.SeedSequence:
     return np.random.SeedSequence(seed)
 
 
-def random_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> np.ndarray:
-    """n x d i.i.d. N(0, 1/scale_dim); column c from SeedSequence(seed).spawn(d)[c]."""
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(max_workers=max(1, min(32, os.cpu_count() or 1)),
+                                   thread_name_prefix="csc-rng")
+    return _POOL
+
+
+def signal_columns(n: int, d: int, seed=0, scale_dim: int | None = None) -> np.ndarray:
+    """The random block column-major: (d, n), row c = column c of random_signals.
+
+    Column c is sigma * standard_normal(n) from default_rng(SeedSequence(seed)
+    .spawn(d)[c]) -- the same draws as the reference's normal(0.0, sigma, n)
+    and the same bits (0.0 + sigma*z, signals.py:34-37). Columns are
+    independent streams, generated in a thread pool (numpy releases the GIL).
+    """
     if d < 1:
         raise ValueError("need at least one signal column")
     if n < 1:
@@ -37,10 +55,34 @@ def random_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> np.n
         raise ValueError("scale_dim must be positive")
     sigma = 1.0 / np.sqrt(dim)
     children = as_seed_sequence(seed).spawn(d)
-    out = np.empty((n, d))
-    for c, child in enumerate(children):
-        out[:, c] = np.random.default_rng(child).normal(0.0, sigma, size=n)
-    return out
+    cols = np.empty((d, n))
+
+    def fill(c):
+        row = cols[c]
+        np.random.default_rng(children[c]).standard_normal(size=n, out=row)
+        row *= sigma
+        row += 0.0
+
+    if n * d >= 1 << 20 and d > 1:
+        list(_pool().map(fill, range(d)))
+    else:
+        for c in range(d):
+            fill(c)
+    return cols
+
+
+def random_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> np.ndarray:
+    """n x d i.i.d. N(0, 1/scale_dim); column c from SeedSequence(seed).spawn(d)[c]."""
+    return np.ascontiguousarray(signal_columns(n, d, seed, scale_dim).T)
+
+
+def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> torch.Tensor:
+    """random_signals as a padded (n, ld) float64 device block (transposed on the GPU)."""
+    cols = torch.from_numpy(signal_columns(n, d, seed, scale_dim))
+    dev = require_cuda()
+    blk = torch.zeros((n, row_stride(d)), dtype=torch.float64, device=dev)
+    blk[:, :d].copy_(cols.to(dev).t())
+    return blk
 
 
 def block_nonfinite(blk: torch.Tensor) -> int:

@@ -513,3 +513,55 @@ def test_reference_counter_accepted(P):
     c = RefCounter()
     lam, feats, iters = P.find_lambda_k(lap, 3, d=12, m=40, seed=5, counter=c)
     assert c.count == iters * 40 * 12
+
+
+def test_refine_ledger_odd_width(P):
+    """Stale cutoff -> refinement; ledger = order * n_fresh * (1 + iters) (test_dynamic.py:105-127)."""
+    g = golden("dynamic_small")
+    g0, g1 = graph_from(g, "g0", P), graph_from(g, "g1", P)
+    cfg = P.DynamicConfig(k=4, d=26, p=0.5, filter=P.FilterConfig(order=60),
+                          kmeans=P.KmeansConfig(restarts=2))
+    _, state, _ = P.dynamic_init(g0, cfg, seed=6)
+    state.lambda_k = 0.3
+    state.filter = P.cheb_coeffs(0.15, 2.0, 60)
+    _, state2, diag = P.dynamic_step(state, g1, cfg)
+    assert diag.refined and diag.search_iters >= 1
+    assert diag.matvecs_total == 60 * 13 * (1 + diag.search_iters)
+    ss = np.random.SeedSequence(6)
+    ss.spawn(2)
+    _, sig_ss, _ = ss.spawn(3)
+    raw = P.random_signals(g1.n, 13, sig_ss, scale_dim=26)
+    poly = P.cheb_coeffs(state2.lambda_k, 2.0, 60)
+    assert np.array_equal(state2.features.values[:, 13:], P.apply_filter(P.laplacian(g1), poly, raw))
+
+
+def test_csc_features_small_d_ledger(P):
+    g = golden("small")
+    lap = P.laplacian(graph_from(g, "sbm60", P))
+    c = P.MatvecCounter()
+    with pytest.warns(UserWarning, match="rank-deficient"):
+        feats, cut, poly = P.csc_features(lap, 3, 2, P.FilterConfig(order=30), seed=0, counter=c)
+    assert feats.d == 2 and feats.values.shape == (60, 2)
+    assert c.count % (30 * 2) == 0
+
+
+def test_batched_kmeanspp_matches_sequential(P):
+    """Batched seeding == per-restart sequential seeding == the reference picks."""
+    from paper_1706_03591_b200.kmeans import _Workspace, batched_kmeanspp
+    from paper_1706_03591_b200._device import upload_block
+    g = golden("cfg1")
+    f = g["features"]
+    ws = _Workspace(upload_block(f), 40, 10)
+    kids = np.random.SeedSequence(0).spawn(2)[1].spawn(5)
+    seeds = batched_kmeanspp(ws, kids)
+    for r, child in enumerate(kids):
+        ref, _ = O.kmeanspp(f, 10, np.random.default_rng(child))
+        assert np.array_equal(seeds[r, :, :40].cpu().numpy(), ref)
+    # zero D^2 mass -> replay path (duplicate points; kmeans.py:70-72)
+    dup = np.array([[0.0], [0.0], [5.0]])
+    ws2 = _Workspace(upload_block(dup), 1, 3)
+    kids2 = np.random.SeedSequence(3).spawn(4)
+    seeds2 = batched_kmeanspp(ws2, kids2)
+    for r, child in enumerate(kids2):
+        ref, _ = O.kmeanspp(dup, 3, np.random.default_rng(child))
+        assert np.array_equal(seeds2[r, :, :1].cpu().numpy(), ref)

@@ -1,0 +1,87 @@
+"""Time the end-to-end CSC pipeline at scale (phase split, host clock + syncs).
+
+    python tools/time_pipeline.py --what cfg3       # static csc_assign, n=1M, k=100, d=128, m=100
+    python tools/time_pipeline.py --what cfg5 --churn 0.01 --p 0.5 --steps 3
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1706_03591_b200 as P  # noqa: E402
+from paper_1706_03591_b200 import generators as G  # noqa: E402
+from paper_1706_03591_b200.signals import device_signals  # noqa: E402
+from paper_1706_03591_b200.filters import FilteredBlock, _search_cutoff  # noqa: E402
+
+
+def tic():
+    torch.cuda.synchronize()
+    return time.perf_counter()
+
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--what", default="cfg3")
+ap.add_argument("--churn", type=float, default=0.01)
+ap.add_argument("--p", type=float, default=0.5)
+ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--restarts", type=int, default=10)
+ap.add_argument("--search", default="moments")
+a = ap.parse_args()
+out = {"what": a.what}
+if a.what == "cfg3":
+    n, k, d, m = 1_000_000, 100, 128, 100
+    t = tic()
+    q1, q2 = G.sbm_probabilities(n, k, 32.0, 0.02)
+    g = G.graph_from_codes(n, G.planted_partition_codes(n, k, q1, q2, 3))
+    out["gen_s"] = time.perf_counter() - t
+    t = tic(); lap = P.laplacian(g); out["laplacian_ms"] = (tic() - t) * 1e3
+    t = tic(); blk = device_signals(n, d, 0); out["signals_ms"] = (tic() - t) * 1e3
+    cnt = P.MatvecCounter()
+    t = tic()
+    cut, filt, poly, iters, est = _search_cutoff(lap, k, FilteredBlock(blk, d), (0.0, 2.0),
+                                                 P.FilterConfig(order=m, search=a.search), cnt, 1.0)
+    out["search_ms"] = (tic() - t) * 1e3
+    out.update(cutoff=cut, iters=iters, est=est, logical_matvecs=cnt.count, physical_matvecs=cnt.physical)
+    feats = P.FeatureMatrix._from_block(filt.blk, d, np.zeros(d, np.int64), np.arange(d))
+    t = tic()
+    asg = P.kmeans(feats, k, P.KmeansConfig(restarts=a.restarts), seed=1)
+    out["kmeans_ms"] = (tic() - t) * 1e3
+    out["kmeans_cost"] = asg.feature_cost
+    out["cluster_sizes_minmax"] = [int(asg.cluster_sizes.min()), int(asg.cluster_sizes.max())]
+    planted = np.repeat(np.arange(k), G.block_sizes(n, k))
+    from oracle import csc_oracle as O
+    out["ari_vs_planted"] = O.adjusted_rand(asg.labels, planted)
+else:
+    n, k, d, m = 2_000_000, 64, 96, 80
+    t = tic()
+    q1, q2 = G.sbm_probabilities(n, k, 20.0, 0.05)
+    codes = G.planted_partition_codes(n, k, q1, q2, 5)
+    labels = np.repeat(np.arange(k), G.block_sizes(n, k))
+    graphs = [G.graph_from_codes(n, codes)]
+    cur = codes
+    for s in range(a.steps):
+        dl, il = G.edge_churn(cur, n, labels, q1, q2, a.churn, seed=50 + s)
+        graphs.append(graphs[-1].apply_delta(dl, il))
+        cur = np.union1d(np.setdiff1d(cur, dl, assume_unique=True), il)
+    out["gen_s"] = time.perf_counter() - t
+    cfg = P.DynamicConfig(k=k, d=d, p=a.p, filter=P.FilterConfig(order=m, search=a.search),
+                          kmeans=P.KmeansConfig(restarts=a.restarts))
+    t = tic()
+    _, state, diag = P.dynamic_init(graphs[0], cfg, seed=0)
+    out["init_ms"] = (tic() - t) * 1e3
+    out["init_iters"] = diag.search_iters
+    steps = []
+    for gt in graphs[1:]:
+        ph = {}
+        t = tic()
+        asg, state, diag = P.dynamic_step(state, gt, cfg, timings=ph)
+        ms = (tic() - t) * 1e3
+        steps.append({"ms": ms, "refined": diag.refined, "iters": diag.search_iters,
+                      "phases": {kk: round(v, 1) for kk, v in ph.items()}})
+    out["steps"] = steps
+print(json.dumps(out))
