@@ -140,6 +140,20 @@ int csc_kmeans_assign(const double *f_dev, const double *rownorm_dev, int64_t n,
                       int64_t ld, const double *c_dev, int64_t ldc, const double *cnorm_dev,
                       int64_t k, int32_t *labels_dev, double *own_d2_dev, int32_t *counts_dev,
                       void *stream);
+/* Lloyd plan: scratch for bounds-pruned iterations (n, d, ld, k fixed). */
+typedef struct csc_kmeans_plan csc_kmeans_plan;
+int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *stream,
+                           csc_kmeans_plan **out);
+int csc_kmeans_plan_destroy(csc_kmeans_plan *plan);
+/* One Lloyd iteration (kmeans.py:96-111) on device: assignment (all rows if
+ * full != 0, else only rows whose Hamerly bounds cannot exclude a change,
+ * recomputed in the reference's GEMM form), empty-cluster repair (exact: a
+ * full reassignment precedes it), means by label, counts, and cost2 into
+ * cost2_dev[0] via the centroid identity (Q_j - 2 m_j.S_j + n_j |m_j|^2).
+ * The first iteration of a run must pass full = 1. cent is updated in place. */
+int csc_kmeans_iterate(csc_kmeans_plan *plan, const double *f_dev, const double *rownorm_dev,
+                       double *c_dev, int64_t ldc, double *cnorm_dev, int32_t *labels_dev,
+                       int32_t *counts_dev, int full, double *cost2_dev, void *stream);
 /* k-means tuning knob: "assign_tn" = 4 (default) or 8 centroids per thread */
 int csc_kmeans_tuning(const char *key, int64_t value);
 /* empty-cluster repair (kmeans.py:99-108): for each empty j ascending, move the

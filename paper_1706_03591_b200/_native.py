@@ -43,6 +43,9 @@ SIGNATURES = {
     "csc_sweep_times": ([ctypes.POINTER(ctypes.c_float), _INT, ctypes.POINTER(_INT)], _INT),
     "csc_kmeans_rownorms": ([_P, _I64, _I64, _I64, _P, _P], _INT),
     "csc_kmeans_assign": ([_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P], _INT),
+    "csc_kmeans_plan_create": ([_I64, _I64, _I64, _I64, _P, ctypes.POINTER(_P)], _INT),
+    "csc_kmeans_plan_destroy": ([_P], _INT),
+    "csc_kmeans_iterate": ([_P, _P, _P, _P, _I64, _P, _P, _P, _INT, _P, _P], _INT),
     "csc_kmeans_tuning": ([ctypes.c_char_p, _I64], _INT),
     "csc_kmeans_repair": ([_P, _P, _P, _I64, _I64, _P], _INT),
     "csc_kmeans_update": ([_P, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P], _INT),

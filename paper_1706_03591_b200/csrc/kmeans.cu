@@ -173,24 +173,32 @@ __global__ void __launch_bounds__(16 * (kAN / TN), (TN == 8 ? 2 : 2))
     assign2_kernel(const double *__restrict__ f, const double *__restrict__ fnorm, int64_t n,
                    int64_t d, int64_t ld, const double *__restrict__ cent, int64_t ldc,
                    const double *__restrict__ cnorm, int64_t k, int32_t *__restrict__ labels,
-                   double *__restrict__ own, int32_t *__restrict__ counts) {
+                   double *__restrict__ own, int32_t *__restrict__ counts,
+                   const int32_t *__restrict__ rows, const int32_t *__restrict__ nrows_dev,
+                   double *__restrict__ ub, double *__restrict__ lb,
+                   const int32_t *__restrict__ gate) {
   constexpr int CT = kAN / TN;        // centroid-threads per row group
   constexpr int NT = 16 * CT;         // threads per block
   extern __shared__ __align__(16) double smem[];
   const int64_t dpad = (d + kAK - 1) / kAK * kAK;
   double *Cs = smem;                    // [dpad][kANP]
   double *Fs = smem + dpad * kANP;      // [2][kAM][kAKP]
+  if (gate && *gate == 0) return;
+  const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;  // rows to process (list length)
   const int tid = threadIdx.x;
   const int tx = tid % CT, ty = tid / CT;
   const int64_t r0 = (int64_t)blockIdx.x * kAM;
+  if (r0 >= nr) return;
   const int nst = (int)(dpad / kAK);
-  double fn[8], best_v[8];
+  double fn[8], best_v[8], second_v[8];
   int best_i[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t r = r0 + ty + 16 * i;
-    fn[i] = r < n ? fnorm[r] : 0.0;
+    const int64_t g = r < nr ? (rows ? (int64_t)rows[r] : r) : -1;
+    fn[i] = g >= 0 ? fnorm[g] : 0.0;
     best_v[i] = INFINITY;
+    second_v[i] = INFINITY;
     best_i[i] = 0;
   }
   auto load_stage = [&](int st, int buf) {
@@ -199,7 +207,9 @@ __global__ void __launch_bounds__(16 * (kAN / TN), (TN == 8 ? 2 : 2))
     for (int q = 0; q < 1024 / NT; ++q) {  // 128 rows x 8 vectors of 2 doubles
       const int v = tid + NT * q;
       const int row = v >> 3, vc = v & 7;
-      const int64_t gr = r0 + row, gc = k0 + 2 * vc;
+      const int64_t lr = r0 + row;
+      const int64_t gr = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : n;
+      const int64_t gc = k0 + 2 * vc;
       const bool ok = gr < n && gc < ld;  // ld is even: the pair is inside the row
       const double *src = ok ? f + gr * ld + gc : f;
       cp_async16(Fs + ((size_t)buf * kAM + row) * kAKP + 2 * vc, src, ok);
@@ -241,7 +251,8 @@ __global__ void __launch_bounds__(16 * (kAN / TN), (TN == 8 ? 2 : 2))
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      double v = INFINITY;
+      // (min, argmin, second min) over this thread's centroids, first index wins ties
+      double v = INFINITY, v2 = INFINITY;
       int vi = 0x7fffffff;
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
@@ -251,33 +262,48 @@ __global__ void __launch_bounds__(16 * (kAN / TN), (TN == 8 ? 2 : 2))
           double d2 = __dadd_rn(t, cnorm[c]);
           d2 = d2 > 0.0 ? d2 : 0.0;
           if (d2 < v) {
+            v2 = v;
             v = d2;
             vi = (int)c;
+          } else if (d2 < v2) {
+            v2 = d2;
           }
         }
       }
 #pragma unroll
       for (int o = 1; o < CT; o <<= 1) {  // the CT lanes of a row group are adjacent
         const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
         const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
         if (ov < v || (ov == v && oi < vi)) {
+          v2 = fmin(ov2, v);
           v = ov;
           vi = oi;
+        } else {
+          v2 = fmin(v2, ov);
         }
       }
       if (v < best_v[i] || (v == best_v[i] && vi < best_i[i])) {
+        second_v[i] = fmin(v2, best_v[i]);
         best_v[i] = v;
         best_i[i] = vi;
+      } else {
+        second_v[i] = fmin(second_v[i], v);
       }
     }
   }
   if (tx == 0) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int64_t r = r0 + ty + 16 * i;
-      if (r < n) {
+      const int64_t lr = r0 + ty + 16 * i;
+      const int64_t r = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : -1;
+      if (r >= 0) {
         labels[r] = best_i[i];
         own[r] = best_v[i];
+        if (ub) {
+          ub[r] = sqrt(best_v[i]);
+          lb[r] = sqrt(second_v[i]);
+        }
         if (counts) atomicAdd(counts + best_i[i], 1);
       }
     }
@@ -289,7 +315,9 @@ int g_assign_tn = 8;
 template <int TN>
 int launch_assign2(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
                    const double *c, int64_t ldc, const double *cnorm, int64_t k, int32_t *labels,
-                   double *own, int32_t *counts, size_t smem, cudaStream_t st) {
+                   double *own, int32_t *counts, size_t smem, cudaStream_t st,
+                   const int32_t *rows = nullptr, const int32_t *nrows_dev = nullptr,
+                   double *ub = nullptr, double *lb = nullptr, const int32_t *gate = nullptr) {
   static size_t configured = 0;
   if (smem > configured) {
     CSC_TRY_CUDA(cudaFuncSetAttribute(assign2_kernel<TN>,
@@ -297,7 +325,7 @@ int launch_assign2(const double *f, const double *fnorm, int64_t n, int64_t d, i
     configured = smem;
   }
   assign2_kernel<TN><<<(unsigned)csc::ceil_div(n, kAM), 16 * (kAN / TN), smem, st>>>(
-      f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts);
+      f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts, rows, nrows_dev, ub, lb, gate);
   return CSC_OK;
 }
 
@@ -364,13 +392,18 @@ __global__ void repair_kernel(int32_t *__restrict__ labels, double *__restrict__
 __global__ void update_partial_kernel(const double *__restrict__ f,
                                       const int32_t *__restrict__ labels, int64_t n, int64_t d,
                                       int64_t ld, int64_t k, int64_t chunk, int cw,
-                                      double *__restrict__ psum, int32_t *__restrict__ pcnt) {
+                                      double *__restrict__ psum, int32_t *__restrict__ pcnt,
+                                      const double *__restrict__ fnorm, double *__restrict__ pq) {
   extern __shared__ double sm[];
-  int32_t *scnt = reinterpret_cast<int32_t *>(sm + (size_t)k * cw);
+  double *sq = sm + (size_t)k * cw;  // per-cluster sum of |f_i|^2 (y == 0 blocks)
+  int32_t *scnt = reinterpret_cast<int32_t *>(sq + k);
   const int64_t b = blockIdx.x;
   const int64_t col0 = (int64_t)blockIdx.y * cw;
   for (int64_t i = threadIdx.x; i < k * cw; i += blockDim.x) sm[i] = 0.0;
-  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) scnt[i] = 0;
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+    scnt[i] = 0;
+    sq[i] = 0.0;
+  }
   __syncthreads();
   const int64_t rbeg = b * chunk, rend = min(n, rbeg + chunk);
   const int c = threadIdx.x;
@@ -392,8 +425,11 @@ __global__ void update_partial_kernel(const double *__restrict__ f,
     }
     for (; r < rend; ++r) sm[(size_t)labels[r] * cw + c] += fc[r * ld];
   }
-  if (blockIdx.y == 0)
+  if (blockIdx.y == 0) {
     for (int64_t r = rbeg + threadIdx.x; r < rend; r += blockDim.x) atomicAdd(scnt + labels[r], 1);
+    if (pq && threadIdx.x == blockDim.x - 1)  // ordered per-cluster |f|^2 sums (extra warp)
+      for (int64_t r = rbeg; r < rend; ++r) sq[labels[r]] += fnorm[r];
+  }
   __syncthreads();
   const int64_t nb = gridDim.x;
   for (int64_t i = threadIdx.x; i < k * cw; i += blockDim.x) {
@@ -401,7 +437,10 @@ __global__ void update_partial_kernel(const double *__restrict__ f,
     if (col0 + cc < d) psum[(b * k + j) * d + col0 + cc] = sm[i];
   }
   if (blockIdx.y == 0)
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) pcnt[b * k + j] = scnt[j];
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+      pcnt[b * k + j] = scnt[j];
+      if (pq) pq[b * k + j] = sq[j];
+    }
   (void)nb;
 }
 
@@ -719,12 +758,230 @@ __global__ void gather_cols_kernel(const double *__restrict__ src, int64_t n, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Lloyd plan: bounds-pruned iterations (Hamerly)
+// ---------------------------------------------------------------------------
+// ub[i] >= |f_i - c_{a(i)}|, lb[i] <= min_{j != a(i)} |f_i - c_j| (distances,
+// not squares). After the centroids move by delta_j, ub += delta_a and
+// lb -= max_{j != a} delta_j. If ub + eta <= max(lb, s_a) with
+// s_a = min_{j != a} |c_a - c_j| / 2, no centroid can beat a(i) and the row
+// keeps its label without any distance computation; every other row is
+// recomputed in the reference's GEMM form. eta covers the rounding of the
+// GEMM-form distances (|d| error <= ~3e-8 (|f| + |c|)), so a skipped row is
+// one whose reference argmin cannot change; near-ties are always recomputed.
+// Labels, means and counts therefore follow kmeans.py:96-110.
+
+__global__ void bound_kernel(int64_t n, const int32_t *__restrict__ labels,
+                             double *__restrict__ ub, double *__restrict__ lb,
+                             const double *__restrict__ delta, const double *__restrict__ scal,
+                             const double *__restrict__ shalf, const double *__restrict__ fnorm,
+                             int32_t *__restrict__ cand, int32_t *__restrict__ flags) {
+  const bool force = flags[2] != 0;
+  const double d1 = scal[1], d2 = scal[2], cmax = scal[4];
+  const int j1 = (int)scal[3];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    bool keep = false;
+    if (!force) {
+      const int a = labels[r];
+      const double u = ub[r] + delta[a];
+      const double l = lb[r] - (a == j1 ? d2 : d1);
+      const double eta = 1e-7 * (sqrt(fnorm[r]) + cmax);
+      keep = u + eta <= fmax(l, shalf[a]);
+      ub[r] = u;
+      lb[r] = l;
+    }
+    if (!keep) cand[atomicAdd(flags, 1)] = (int32_t)r;
+  }
+}
+
+__global__ void label_hist_kernel(int64_t n, int64_t k, const int32_t *__restrict__ labels,
+                                  int32_t *__restrict__ counts) {
+  extern __shared__ int32_t h[];
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) h[j] = 0;
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(h + labels[r], 1);
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x)
+    if (h[j]) atomicAdd(counts + j, h[j]);
+}
+
+// flags[1] = some cluster is empty (full reassignment needed for the repair,
+// and again next iteration); counts are then cleared for the full recount.
+__global__ void check_empty_kernel(int64_t k, int32_t *__restrict__ counts,
+                                   int32_t *__restrict__ flags) {
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x)
+    if (counts[j] == 0) any = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    flags[1] = any;
+    flags[2] = any;
+  }
+  if (any)
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) counts[j] = 0;
+}
+
+__global__ void gated_repair_kernel(int32_t *__restrict__ labels, double *__restrict__ own,
+                                    const int32_t *__restrict__ counts, int64_t n, int64_t k,
+                                    const int32_t *__restrict__ flags) {
+  if (flags[1] == 0) return;
+  for (int64_t j = 0; j < k; ++j) {
+    if (counts[j] != 0) continue;
+    double bv;
+    int64_t bi = 0;
+    block_argmax(own, n, bv, bi);
+    if (threadIdx.x == 0) {
+      labels[bi] = (int32_t)j;
+      own[bi] = -1.0;
+    }
+    __syncthreads();
+  }
+}
+
+// warp per (centroid j, column c): S[j][c] = sum of the block partials in
+// order; the extra warp per j adds the counts and the |f|^2 partials.
+__global__ void sums_finish_kernel(const double *__restrict__ psum,
+                                   const int32_t *__restrict__ pcnt,
+                                   const double *__restrict__ pq, int64_t nb, int64_t d,
+                                   int64_t k, double *__restrict__ S, int32_t *__restrict__ counts,
+                                   double *__restrict__ Q) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (w >= k * (d + 1)) return;
+  const int64_t j = w / (d + 1), c = w - j * (d + 1);
+  if (c == d) {
+    int32_t cnt = 0;
+    double q = 0.0;
+    for (int64_t b = lane; b < nb; b += 32) {
+      cnt += pcnt[b * k + j];
+      q += pq[b * k + j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      q += __shfl_xor_sync(0xffffffffu, q, o);
+    }
+    if (lane == 0) {
+      counts[j] = cnt;
+      Q[j] = q;
+    }
+    return;
+  }
+  double sacc = 0.0;
+  for (int64_t b = lane; b < nb; b += 32) sacc += psum[(b * k + j) * d + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+  if (lane == 0) S[j * d + c] = sacc;
+}
+
+// block per centroid: mean = S / max(count, 1) (kmeans.py:84), movement
+// delta_j, |c_j|^2, and the cluster's cost term via the centroid identity
+// sum_i |f_i - m|^2 = Q - 2 m.S + count |m|^2 (with the rounded mean m).
+__global__ void centroid_finish_kernel(const double *__restrict__ S,
+                                       const int32_t *__restrict__ counts,
+                                       const double *__restrict__ Q, int64_t d, int64_t k,
+                                       double *__restrict__ cent, int64_t ldc,
+                                       double *__restrict__ cnorm, double *__restrict__ delta,
+                                       double *__restrict__ cterm) {
+  __shared__ double red[32];
+  const int64_t j = blockIdx.x;
+  const int32_t cnt = counts[j];
+  const double denom = (double)(cnt > 1 ? cnt : 1);
+  double mv = 0.0, nrm = 0.0, dot = 0.0;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    const double sjc = S[j * d + c];
+    const double mean = __ddiv_rn(sjc, denom);
+    const double old = cent[j * ldc + c];
+    cent[j * ldc + c] = mean;
+    mv = fma(mean - old, mean - old, mv);
+    nrm = fma(mean, mean, nrm);
+    dot = fma(mean, sjc, dot);
+  }
+  mv = block_sum<128>(mv, red);
+  nrm = block_sum<128>(nrm, red);
+  dot = block_sum<128>(dot, red);
+  if (threadIdx.x == 0) {
+    delta[j] = sqrt(mv);
+    cnorm[j] = nrm;
+    cterm[j] = cnt > 0 ? (Q[j] - 2.0 * dot) + (double)cnt * nrm : 0.0;
+  }
+}
+
+// scal[0] = cost2 (sum of cluster terms, fixed order), scal[1..3] = largest
+// movement, second largest, its centroid; scal[4] = max_j |c_j|.
+__global__ void iter_finish_kernel(int64_t k, const double *__restrict__ cterm,
+                                   const double *__restrict__ delta,
+                                   const double *__restrict__ cnorm, double *__restrict__ scal) {
+  if (threadIdx.x != 0) return;
+  double cost = 0.0, d1 = 0.0, d2 = 0.0, cm = 0.0;
+  int64_t j1 = 0;
+  for (int64_t j = 0; j < k; ++j) {
+    cost += cterm[j];
+    const double dj = delta[j];
+    if (dj > d1) {
+      d2 = d1;
+      d1 = dj;
+      j1 = j;
+    } else if (dj > d2) {
+      d2 = dj;
+    }
+    cm = fmax(cm, cnorm[j]);
+  }
+  scal[0] = cost > 0.0 ? cost : 0.0;
+  scal[1] = d1;
+  scal[2] = d2;
+  scal[3] = (double)j1;
+  scal[4] = sqrt(cm);
+}
+
+// shalf[j] = min_{j' != j} |c_j - c_j'| / 2 (difference form), +inf for k = 1
+__global__ void shalf_kernel(const double *__restrict__ cent, int64_t ldc, int64_t d, int64_t k,
+                             double *__restrict__ shalf) {
+  __shared__ double red[32];
+  const int64_t j = blockIdx.x;
+  double best = INFINITY;
+  for (int64_t o = threadIdx.x; o < k; o += blockDim.x) {
+    if (o == j) continue;
+    double s = 0.0;
+    for (int64_t c = 0; c < d; ++c) {
+      const double t = cent[j * ldc + c] - cent[o * ldc + c];
+      s = fma(t, t, s);
+    }
+    best = fmin(best, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) b = fmin(b, red[w]);
+    shalf[j] = 0.5 * sqrt(b);
+  }
+}
+
 int grid_cap(int64_t want, int per_sm = 8) {
   return (int)std::min<int64_t>((int64_t)csc::device_info().sm_count * per_sm,
                                 std::max<int64_t>(1, want));
 }
 
 }  // namespace
+
+struct csc_kmeans_plan {
+  int64_t n = 0, d = 0, ld = 0, k = 0;
+  int64_t nb = 0, chunk = 0, cw = 0, ny = 0;
+  void *base = nullptr;
+  double *ub, *lb, *own, *psum, *pq, *S, *Q, *cterm, *delta, *shalf, *scal;
+  int32_t *cand, *flags, *pcnt;
+  size_t smem = 0;
+  cudaStream_t stream = nullptr;
+};
 
 extern "C" {
 
@@ -792,7 +1049,7 @@ int csc_kmeans_update(const double *f, const int32_t *labels, int64_t n, int64_t
   // columns per block so that k*cw doubles (+ k counts) fit in shared memory
   const int64_t budget = std::max<int64_t>(48 * 1024, (int64_t)info.max_smem_optin) - 1024;
   const int64_t cnt_bytes = sizeof(int32_t) * k;
-  int64_t cw = (budget - cnt_bytes) / (int64_t)(sizeof(double) * k);
+  int64_t cw = (budget - cnt_bytes) / (int64_t)(sizeof(double) * k) - 1;
   CSC_REQUIRE(cw >= 1, "csc_kmeans_update: k=%lld too large for shared-memory partials",
               (long long)k);
   cw = std::min<int64_t>(std::min<int64_t>(cw, 256), d);
@@ -801,7 +1058,7 @@ int csc_kmeans_update(const double *f, const int32_t *labels, int64_t n, int64_t
   const int64_t nb = std::max<int64_t>(
       1, std::min<int64_t>((int64_t)info.sm_count * 8, csc::ceil_div(n, 64)));
   const int64_t chunk = csc::ceil_div(n, nb);
-  const size_t smem = sizeof(double) * k * cw + cnt_bytes;
+  const size_t smem = sizeof(double) * k * (cw + 1) + cnt_bytes;
   CSC_TRY_CUDA(cudaFuncSetAttribute(update_partial_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   csc::Scratch psum, pcnt;
@@ -809,7 +1066,8 @@ int csc_kmeans_update(const double *f, const int32_t *labels, int64_t n, int64_t
   CSC_TRY_CUDA(pcnt.alloc(sizeof(int32_t) * nb * k, st));
   const int threads = (int)std::max<int64_t>(32, csc::ceil_div(cw, 32) * 32);
   update_partial_kernel<<<dim3((unsigned)nb, (unsigned)ny), threads, smem, st>>>(
-      f, labels, n, d, ld, k, chunk, (int)cw, psum.as<double>(), pcnt.as<int32_t>());
+      f, labels, n, d, ld, k, chunk, (int)cw, psum.as<double>(), pcnt.as<int32_t>(), nullptr,
+      nullptr);
   CSC_CHECK_LAUNCH();
   const int64_t warps = k * (d + 1);
   update_finish_kernel<<<(unsigned)csc::ceil_div(warps, 8), 256, 0, st>>>(
@@ -817,6 +1075,134 @@ int csc_kmeans_update(const double *f, const int32_t *labels, int64_t n, int64_t
   CSC_CHECK_LAUNCH();
   centroid_norms_kernel<<<(unsigned)csc::ceil_div(k, 8), 256, 0, st>>>(c, ldc, d, k, cnorm);
   CSC_CHECK_LAUNCH();
+  return CSC_OK;
+}
+
+int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *stream,
+                           csc_kmeans_plan **out) {
+  csc::clear_error();
+  CSC_REQUIRE(out != nullptr, "csc_kmeans_plan_create: NULL out");
+  CSC_REQUIRE(n >= 1 && d >= 1 && ld >= d && k >= 1 && n < INT32_MAX && k < INT32_MAX,
+              "csc_kmeans_plan_create: bad shape");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const csc::DeviceInfo &info = csc::device_info();
+  csc_kmeans_plan *p = new csc_kmeans_plan();
+  p->n = n;
+  p->d = d;
+  p->ld = ld;
+  p->k = k;
+  p->stream = st;
+  const int64_t budget = std::max<int64_t>(48 * 1024, (int64_t)info.max_smem_optin) - 1024;
+  int64_t cw = (budget - (int64_t)sizeof(int32_t) * k) / (int64_t)(sizeof(double) * k) - 1;
+  if (cw < 1) {
+    delete p;
+    csc::set_error("csc_kmeans_plan_create: k=%lld too large", (long long)k);
+    return CSC_ERR_ARG;
+  }
+  p->cw = std::min<int64_t>(std::min<int64_t>(cw, 256), d);
+  p->ny = csc::ceil_div(d, p->cw);
+  p->nb = std::max<int64_t>(1, std::min<int64_t>((int64_t)info.sm_count * 8, csc::ceil_div(n, 64)));
+  p->chunk = csc::ceil_div(n, p->nb);
+  p->smem = sizeof(double) * k * (p->cw + 1) + sizeof(int32_t) * k;
+  const size_t nd = (size_t)n, kk = (size_t)k;
+  const size_t doubles = 3 * nd + (size_t)p->nb * kk * d + (size_t)p->nb * kk + kk * d + 4 * kk + 8;
+  const size_t ints = nd + 4 + (size_t)p->nb * kk;
+  if (cudaMallocAsync(&p->base, doubles * 8 + ints * 4 + 64, st) != cudaSuccess) {
+    delete p;
+    csc::set_error("csc_kmeans_plan_create: allocation failed");
+    return CSC_ERR_CUDA;
+  }
+  double *dp = static_cast<double *>(p->base);
+  p->ub = dp; dp += nd;
+  p->lb = dp; dp += nd;
+  p->own = dp; dp += nd;
+  p->psum = dp; dp += (size_t)p->nb * kk * d;
+  p->pq = dp; dp += (size_t)p->nb * kk;
+  p->S = dp; dp += kk * d;
+  p->Q = dp; dp += kk;
+  p->cterm = dp; dp += kk;
+  p->delta = dp; dp += kk;
+  p->shalf = dp; dp += kk;
+  p->scal = dp; dp += 8;
+  int32_t *ip = reinterpret_cast<int32_t *>(dp);
+  p->cand = ip; ip += nd;
+  p->flags = ip; ip += 4;
+  p->pcnt = ip;
+  CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t) * 4, st));
+  CSC_TRY_CUDA(cudaFuncSetAttribute(update_partial_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
+  *out = p;
+  return CSC_OK;
+}
+
+int csc_kmeans_plan_destroy(csc_kmeans_plan *p) {
+  if (!p) return CSC_OK;
+  if (p->base) cudaFreeAsync(p->base, p->stream);
+  delete p;
+  return CSC_OK;
+}
+
+int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm, double *cent,
+                       int64_t ldc, double *cnorm, int32_t *labels, int32_t *counts, int full,
+                       double *cost2_dev, void *stream) {
+  CSC_REQUIRE(p != nullptr, "csc_kmeans_iterate: NULL plan");
+  CSC_REQUIRE(ldc >= p->d, "csc_kmeans_iterate: ldc < d");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  p->stream = st;
+  const int64_t n = p->n, d = p->d, ld = p->ld, k = p->k;
+  const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
+  const size_t asmem = sizeof(double) * (dpad * kANP + 2 * kAM * kAKP);
+  CSC_REQUIRE((ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(f) & 15u) == 0) &&
+                  (int64_t)asmem <= (int64_t)csc::device_info().max_smem_optin,
+              "csc_kmeans_iterate: features must be 16-byte aligned with an even row stride");
+  auto assign = [&](const int32_t *rows, const int32_t *nrows, int32_t *cnts, const int32_t *gate) {
+    return g_assign_tn == 8
+               ? launch_assign2<8>(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own, cnts,
+                                   asmem, st, rows, nrows, p->ub, p->lb, gate)
+               : launch_assign2<4>(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own, cnts,
+                                   asmem, st, rows, nrows, p->ub, p->lb, gate);
+  };
+  int rc;
+  CSC_TRY_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * k, st));
+  if (full) {
+    CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t) * 4, st));
+    if ((rc = assign(nullptr, nullptr, counts, nullptr)) != CSC_OK) return rc;
+  } else {
+    CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t), st));  // candidate count
+    bound_kernel<<<grid_cap(csc::ceil_div(n, 256)), 256, 0, st>>>(
+        n, labels, p->ub, p->lb, p->delta, p->scal, p->shalf, fnorm, p->cand, p->flags);
+    CSC_CHECK_LAUNCH();
+    if ((rc = assign(p->cand, p->flags, nullptr, nullptr)) != CSC_OK) return rc;
+    label_hist_kernel<<<grid_cap(csc::ceil_div(n, 256), 4), 256, sizeof(int32_t) * k, st>>>(
+        n, k, labels, counts);
+    CSC_CHECK_LAUNCH();
+  }
+  CSC_CHECK_LAUNCH();
+  // empty cluster: full GEMM-form reassignment (own distances for every row), then the repair
+  check_empty_kernel<<<1, 1024, 0, st>>>(k, counts, p->flags);
+  CSC_CHECK_LAUNCH();
+  if ((rc = assign(nullptr, nullptr, counts, p->flags + 1)) != CSC_OK) return rc;
+  CSC_CHECK_LAUNCH();
+  gated_repair_kernel<<<1, 1024, 0, st>>>(labels, p->own, counts, n, k, p->flags);
+  CSC_CHECK_LAUNCH();
+  // means, counts, movement, cost terms
+  const int threads = (int)(csc::ceil_div(p->cw, 32) * 32 + 32);
+  update_partial_kernel<<<dim3((unsigned)p->nb, (unsigned)p->ny), threads, p->smem, st>>>(
+      f, labels, n, d, ld, k, p->chunk, (int)p->cw, p->psum, p->pcnt, fnorm, p->pq);
+  CSC_CHECK_LAUNCH();
+  const int64_t warps = k * (d + 1);
+  sums_finish_kernel<<<(unsigned)csc::ceil_div(warps, 8), 256, 0, st>>>(
+      p->psum, p->pcnt, p->pq, p->nb, d, k, p->S, counts, p->Q);
+  CSC_CHECK_LAUNCH();
+  centroid_finish_kernel<<<(unsigned)k, 128, 0, st>>>(p->S, counts, p->Q, d, k, cent, ldc, cnorm,
+                                                      p->delta, p->cterm);
+  CSC_CHECK_LAUNCH();
+  iter_finish_kernel<<<1, 32, 0, st>>>(k, p->cterm, p->delta, cnorm, p->scal);
+  CSC_CHECK_LAUNCH();
+  shalf_kernel<<<(unsigned)k, 128, 0, st>>>(cent, ldc, d, k, p->shalf);
+  CSC_CHECK_LAUNCH();
+  if (cost2_dev)
+    CSC_TRY_CUDA(cudaMemcpyAsync(cost2_dev, p->scal, sizeof(double), cudaMemcpyDeviceToDevice, st));
   return CSC_OK;
 }
 

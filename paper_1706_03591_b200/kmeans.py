@@ -115,7 +115,31 @@ class _Workspace:
                 self._dist(j, False)
 
     # -- Lloyd (kmeans.py:88-117) -------------------------------------------------
-    def lloyd(self, max_iters: int, tol: float, history: list | None = None):
+    def _plan(self):
+        if getattr(self, "plan", None) is None:
+            h = ctypes.c_void_p()
+            _native.call("csc_kmeans_plan_create", self.n, self.d, self.ld, self.k, stream(), ctypes.byref(h))
+            self.plan = h
+        return self.plan
+
+    def __del__(self):
+        h = getattr(self, "plan", None)
+        if h:
+            try:
+                _native.lib().csc_kmeans_plan_destroy(h)
+            except Exception:
+                pass
+            self.plan = None
+
+    def lloyd(self, max_iters: int, tol: float, history: list | None = None, pruned: bool = True):
+        """Lloyd iterations from the seeds in self.cent; returns cost2 of the last one.
+
+        pruned=True: bounds-pruned device iterations (csc_kmeans_iterate), cost
+        by the centroid identity for the stop test and the exact difference
+        form (kmeans.py:111) for the returned value.
+        """
+        if pruned:
+            return self._lloyd_pruned(max_iters, tol, history)
         s = stream()
         n, d, k = self.n, self.d, self.k
         _native.call("csc_kmeans_rownorms", ptr(self.cent), k, d, self.ldc, ptr(self.cnorm), s)
@@ -136,6 +160,32 @@ class _Workspace:
                 prev = cost2
                 break
             prev = cost2
+        return prev
+
+    def _lloyd_pruned(self, max_iters: int, tol: float, history: list | None):
+        s = stream()
+        n, d, k = self.n, self.d, self.k
+        plan = self._plan()
+        _native.call("csc_kmeans_rownorms", ptr(self.cent), k, d, self.ldc, ptr(self.cnorm), s)
+        self.labels.zero_()
+        prev = np.inf
+        ran = False
+        for it in range(max_iters):
+            _native.call("csc_kmeans_iterate", plan, ptr(self.blk), ptr(self.fnorm), ptr(self.cent), self.ldc,
+                         ptr(self.cnorm), ptr(self.labels), ptr(self.counts), int(it == 0), ptr(self.scalars[1:]),
+                         s)
+            ran = True
+            cost2 = float(self.scalars[1].item())
+            if history is not None:
+                history.append(np.sqrt(cost2))
+            if np.isfinite(prev) and prev - cost2 <= tol * prev:
+                prev = cost2
+                break
+            prev = cost2
+        if ran:  # returned cost in the reference's difference form
+            _native.call("csc_kmeans_cost", ptr(self.blk), ptr(self.labels), ptr(self.cent), self.ldc, n, d,
+                         self.ld, ptr(self.scalars[1:]), s)
+            prev = float(self.scalars[1].item())
         return prev
 
 

@@ -23,6 +23,7 @@ ap.add_argument("--k", type=int, default=64)
 ap.add_argument("--restarts", type=int, default=2)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--tn", type=int, default=0)
+ap.add_argument("--unpruned", action="store_true")
 a = ap.parse_args()
 if a.tn:
     from paper_1706_03591_b200 import _native
@@ -41,7 +42,8 @@ for r in range(a.restarts):
     torch.cuda.synchronize(); res.setdefault("kmeanspp_ms", []).append((time.perf_counter() - t) * 1e3)
     hist = []
     t = time.perf_counter()
-    ws.lloyd(a.iters, 0.0, hist)
+    ws.lloyd(a.iters, 0.0, hist, pruned=not a.unpruned)
     torch.cuda.synchronize(); dt = (time.perf_counter() - t) * 1e3
     res.setdefault("lloyd_ms_per_iter", []).append(dt / len(hist))
+    res.setdefault("final_cost", []).append(float(hist[-1]))
 print(json.dumps({"n": a.n, "d": a.d, "k": a.k, **res}))
