@@ -145,6 +145,9 @@ typedef struct csc_kmeans_plan csc_kmeans_plan;
 int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *stream,
                            csc_kmeans_plan **out);
 int csc_kmeans_plan_destroy(csc_kmeans_plan *plan);
+/* rows re-assigned by the last pruned iteration; whether it needed the
+ * empty-cluster full pass (host outputs; synchronises) */
+int csc_kmeans_plan_stats(const csc_kmeans_plan *plan, int64_t *candidates, int32_t *gated);
 /* One Lloyd iteration (kmeans.py:96-111) on device: assignment (all rows if
  * full != 0, else only rows whose Hamerly bounds cannot exclude a change,
  * recomputed in the reference's GEMM form), empty-cluster repair (exact: a

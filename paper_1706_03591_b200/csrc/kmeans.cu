@@ -310,7 +310,215 @@ __global__ void __launch_bounds__(16 * (kAN / TN), (TN == 8 ? 2 : 2))
   }
 }
 
+// ---------------------------------------------------------------------------
+// assign v3: persistent (2 blocks per SM), 128 x 64 tile, 8x8 per thread,
+// centroid tile loaded once per block per pass, 3-stage cp.async ring that
+// runs across the block's row tiles. k > 64: one pass per 64-centroid tile;
+// pass p > 0 merges with the (min, argmin, second) kept in own/labels/lb.
+// ---------------------------------------------------------------------------
+// (min, argmin, second min) of TN distances by a fixed pairwise tree; the
+// left operand always holds the smaller centroid indices, so the first index
+// wins exact ties like numpy's argmin.
+struct Min3 {
+  double v, v2;
+  int i;
+};
+__device__ __forceinline__ Min3 min3_merge(const Min3 &a, const Min3 &b) {
+  Min3 r;
+  if (b.v < a.v) {
+    r.v = b.v;
+    r.i = b.i;
+    r.v2 = fmin(b.v2, a.v);
+  } else {
+    r.v = a.v;
+    r.i = a.i;
+    r.v2 = fmin(a.v2, b.v);
+  }
+  return r;
+}
+
+template <int kStages>
+__global__ void __launch_bounds__(128, 2)
+    assign3_kernel(const double *__restrict__ f, const double *__restrict__ fnorm, int64_t n,
+                   int64_t d, int64_t ld, const double *__restrict__ cent, int64_t ldc,
+                   const double *__restrict__ cnorm, int64_t k, int64_t c0, int last_pass,
+                   int32_t *__restrict__ labels, double *__restrict__ own,
+                   int32_t *__restrict__ counts, const int32_t *__restrict__ rows,
+                   const int32_t *__restrict__ nrows_dev, double *__restrict__ ub,
+                   double *__restrict__ lb, const int32_t *__restrict__ gate) {
+  constexpr int TN = 8, CT = 8, NT = 128;
+  if (gate && *gate == 0) return;
+  extern __shared__ __align__(16) double smem[];
+  const int64_t dpad = (d + kAK - 1) / kAK * kAK;
+  double *Cs = smem;                  // [dpad][kANP]
+  double *Fs = smem + dpad * kANP;    // [kStages][kAM][kAKP]
+  const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;
+  const int64_t ntiles = (nr + kAM - 1) / kAM;
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int tid = threadIdx.x;
+  const int tx = tid % CT, ty = tid / CT;
+  const int nst = (int)(dpad / kAK);
+  const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t total = my_tiles * nst;
+  for (int64_t e = tid; e < dpad * kAN; e += NT) {
+    const int64_t cc = e / dpad, dd = e - cc * dpad;
+    Cs[dd * kANP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
+  }
+  auto tile_row = [&](int64_t g) -> int64_t {  // first local row of stage g's tile
+    return (blockIdx.x + (g / nst) * (int64_t)gridDim.x) * kAM;
+  };
+  auto load_stage = [&](int64_t g) {
+    const int64_t r0 = tile_row(g);
+    const int64_t k0 = (int64_t)(g % nst) * kAK;
+    double *buf = Fs + (size_t)(g % kStages) * kAM * kAKP;
+#pragma unroll
+    for (int q = 0; q < 1024 / NT; ++q) {
+      const int v = tid + NT * q;
+      const int row = v >> 3, vc = v & 7;
+      const int64_t lr = r0 + row;
+      const int64_t gr = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : n;
+      const int64_t gc = k0 + 2 * vc;
+      const bool ok = gr < n && gc < ld;
+      cp_async16(buf + row * kAKP + 2 * vc, ok ? f + gr * ld + gc : f, ok);
+    }
+  };
+#pragma unroll
+  for (int g = 0; g < kStages - 1; ++g) {
+    if (g < total) load_stage(g);
+    cp_async_commit();
+  }
+  double acc[8][TN];
+  for (int64_t g = 0; g < total; ++g) {
+    if (g + kStages - 1 < total) load_stage(g + kStages - 1);
+    cp_async_commit();
+    cp_async_wait<kStages - 1>();
+    __syncthreads();
+    const int st = (int)(g % nst);
+    if (st == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+    }
+    const double *Fb = Fs + (size_t)(g % kStages) * kAM * kAKP;
+    const double *Cb = Cs + (size_t)st * kAK * kANP;
+#pragma unroll
+    for (int kk = 0; kk < kAK; ++kk) {
+      double a[8], b[TN];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = Fb[(ty + 16 * i) * kAKP + kk];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Cb[kk * kANP + tx + CT * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+    if (st == nst - 1) {  // epilogue of this row tile
+      const int64_t r0 = tile_row(g);
+      double cn[TN];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t c = c0 + tx + CT * j;
+        cn[j] = c < k ? cnorm[c] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t lr = r0 + ty + 16 * i;
+        const int64_t r = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : -1;
+        const double fni = r >= 0 ? fnorm[r] : 0.0;
+        Min3 m[TN];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {  // independent: (|f|^2 - 2 f.c) + |c|^2, clamped
+          const double t = __dsub_rn(fni, __dmul_rn(2.0, acc[i][j]));
+          const double d2 = fmax(__dadd_rn(t, cn[j]), 0.0);
+          m[j].v = (c0 + tx + CT * j < k) ? d2 : INFINITY;
+          m[j].i = (int)(c0 + tx + CT * j);
+          m[j].v2 = INFINITY;
+        }
+#pragma unroll
+        for (int w = 1; w < TN; w <<= 1)
+#pragma unroll
+          for (int j = 0; j + w < TN; j += 2 * w) m[j] = min3_merge(m[j], m[j + w]);
+        double v = m[0].v, v2 = m[0].v2;
+        int vi = m[0].i;
+#pragma unroll
+        for (int o = 1; o < CT; o <<= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+          if (ov < v || (ov == v && oi < vi)) {
+            v2 = fmin(ov2, v);
+            v = ov;
+            vi = oi;
+          } else {
+            v2 = fmin(v2, ov);
+          }
+        }
+        if (tx == 0 && r >= 0) {
+          if (c0 > 0) {  // merge with earlier centroid tiles (smaller indices win ties)
+            const double pv = own[r], pv2 = lb[r];
+            const int pi = labels[r];
+            if (pv <= v) {
+              v2 = fmin(pv2, v);
+              v = pv;
+              vi = pi;
+            } else {
+              v2 = fmin(v2, pv);
+            }
+          }
+          labels[r] = vi;
+          own[r] = v;
+          if (last_pass) {
+            if (ub) {
+              ub[r] = sqrt(v);
+              lb[r] = sqrt(v2);
+            }
+            if (counts) atomicAdd(counts + vi, 1);
+          } else {
+            lb[r] = v2;  // carried (squared) second minimum for the next pass
+          }
+        }
+      }
+    }
+  }
+}
+
 int g_assign_tn = 8;
+int g_assign_ver = 3;
+
+int launch_assign3(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
+                   const double *c, int64_t ldc, const double *cnorm, int64_t k, int32_t *labels,
+                   double *own, int32_t *counts, cudaStream_t st, const int32_t *rows,
+                   const int32_t *nrows_dev, double *ub, double *lb, const int32_t *gate) {
+  const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
+  const size_t cbytes = sizeof(double) * dpad * kANP, sbytes = sizeof(double) * kAM * kAKP;
+  // three stages when two blocks still fit in one SM's shared memory, else two
+  const bool three = 2 * (cbytes + 3 * sbytes + 1024) <= 228 * 1024;
+  const size_t smem = cbytes + (three ? 3 : 2) * sbytes;
+  static size_t configured2 = 0, configured3 = 0;
+  size_t &configured = three ? configured3 : configured2;
+  if (smem > configured) {
+    CSC_TRY_CUDA(cudaFuncSetAttribute(three ? assign3_kernel<3> : assign3_kernel<2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  const int grid = std::max(1, csc::device_info().sm_count * 2);
+  for (int64_t c0 = 0; c0 < k; c0 += kAN) {
+    const int last = c0 + kAN >= k;
+    if (three)
+      assign3_kernel<3><<<grid, 128, smem, st>>>(f, fnorm, n, d, ld, c, ldc, cnorm, k, c0, last,
+                                                  labels, own, last ? counts : nullptr, rows,
+                                                  nrows_dev, ub, lb, gate);
+    else
+      assign3_kernel<2><<<grid, 128, smem, st>>>(f, fnorm, n, d, ld, c, ldc, cnorm, k, c0, last,
+                                                  labels, own, last ? counts : nullptr, rows,
+                                                  nrows_dev, ub, lb, gate);
+    CSC_CHECK_LAUNCH();
+  }
+  return CSC_OK;
+}
 
 template <int TN>
 int launch_assign2(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
@@ -1005,7 +1213,13 @@ int csc_kmeans_assign(const double *f, const double *fnorm, int64_t n, int64_t d
   const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
   const size_t smem = sizeof(double) * (dpad * kANP + 2 * kAM * kAKP);
   const bool aligned = (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(f) & 15u) == 0);
-  if (aligned && (int64_t)smem <= (int64_t)csc::device_info().max_smem_optin) {
+  if (aligned && g_assign_ver == 3) {
+    csc::Scratch lbs;
+    if (k > kAN) CSC_TRY_CUDA(lbs.alloc(sizeof(double) * n, st));
+    const int rc = launch_assign3(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts, st,
+                                  nullptr, nullptr, nullptr, lbs.as<double>(), nullptr);
+    if (rc != CSC_OK) return rc;
+  } else if (aligned && (int64_t)smem <= (int64_t)csc::device_info().max_smem_optin) {
     const int rc = g_assign_tn == 8
                        ? launch_assign2<8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts,
                                            smem, st)
@@ -1022,6 +1236,11 @@ int csc_kmeans_assign(const double *f, const double *fnorm, int64_t n, int64_t d
 
 int csc_kmeans_tuning(const char *key, int64_t value) {
   CSC_REQUIRE(key != nullptr, "csc_kmeans_tuning: NULL key");
+  if (std::string(key) == "assign_ver") {
+    CSC_REQUIRE(value == 2 || value == 3, "assign_ver must be 2 or 3");
+    g_assign_ver = (int)value;
+    return CSC_OK;
+  }
   if (std::string(key) == "assign_tn") {
     CSC_REQUIRE(value == 4 || value == 8, "assign_tn must be 4 or 8");
     g_assign_tn = (int)value;
@@ -1135,6 +1354,16 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   return CSC_OK;
 }
 
+int csc_kmeans_plan_stats(const csc_kmeans_plan *p, int64_t *candidates, int32_t *gated) {
+  CSC_REQUIRE(p != nullptr, "csc_kmeans_plan_stats: NULL plan");
+  int32_t h[4] = {0, 0, 0, 0};
+  CSC_TRY_CUDA(cudaMemcpyAsync(h, p->flags, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+  CSC_TRY_CUDA(cudaStreamSynchronize(p->stream));
+  if (candidates) *candidates = h[0];
+  if (gated) *gated = h[1];
+  return CSC_OK;
+}
+
 int csc_kmeans_plan_destroy(csc_kmeans_plan *p) {
   if (!p) return CSC_OK;
   if (p->base) cudaFreeAsync(p->base, p->stream);
@@ -1156,6 +1385,9 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
                   (int64_t)asmem <= (int64_t)csc::device_info().max_smem_optin,
               "csc_kmeans_iterate: features must be 16-byte aligned with an even row stride");
   auto assign = [&](const int32_t *rows, const int32_t *nrows, int32_t *cnts, const int32_t *gate) {
+    if (g_assign_ver == 3)
+      return launch_assign3(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own, cnts, st,
+                            rows, nrows, p->ub, p->lb, gate);
     return g_assign_tn == 8
                ? launch_assign2<8>(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own, cnts,
                                    asmem, st, rows, nrows, p->ub, p->lb, gate)

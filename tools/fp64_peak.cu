@@ -1,6 +1,7 @@
 // FP64 FMA peak probe: independent FMA chains per thread, all SMs.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/fp64_peak tools/fp64_peak.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void fma_kernel(double *out, int iters, double a, double b) {
@@ -17,12 +18,14 @@ __global__ void fma_kernel(double *out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
-int main() {
+int main(int argc, char **argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double *out;
   cudaMalloc(&out, 8);
-  const int threads = 512, blocks = sms * 4, iters = 20000;
+  const int threads = argc > 1 ? atoi(argv[1]) : 512;
+  const int per_sm = argc > 2 ? atoi(argv[2]) : 4;
+  const int blocks = sms * per_sm, iters = 20000;
   fma_kernel<<<blocks, threads>>>(out, 100, 0.999999, 1e-7);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -38,6 +41,7 @@ int main() {
     if (ms < best) best = ms;
   }
   const double flops = 2.0 * 16.0 * iters * (double)threads * blocks;
-  printf("{\"fp64_fma_tflops\": %.3f, \"ms\": %.3f, \"sms\": %d}\n", flops / best / 1e9, best, sms);
+  printf("{\"fp64_fma_tflops\": %.3f, \"ms\": %.3f, \"sms\": %d, \"warps_per_sm\": %d}\n",
+         flops / best / 1e9, best, sms, threads / 32 * per_sm);
   return 0;
 }

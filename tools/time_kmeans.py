@@ -24,10 +24,14 @@ ap.add_argument("--restarts", type=int, default=2)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--tn", type=int, default=0)
 ap.add_argument("--unpruned", action="store_true")
+ap.add_argument("--ver", type=int, default=0)
 a = ap.parse_args()
 if a.tn:
     from paper_1706_03591_b200 import _native
     _native.check(_native.lib().csc_kmeans_tuning(b"assign_tn", a.tn), "tuning")
+if a.ver:
+    from paper_1706_03591_b200 import _native
+    _native.check(_native.lib().csc_kmeans_tuning(b"assign_ver", a.ver), "tuning")
 g = torch.Generator(device="cuda").manual_seed(0)
 centers = torch.randn((a.k, a.d), dtype=torch.float64, device="cuda", generator=g) * 0.05
 lab = torch.randint(0, a.k, (a.n,), device="cuda", generator=g)
