@@ -116,7 +116,10 @@ int csc_cheb_moments(const csc_chebop *op, const void *x_dev, int64_t ld, int64_
  *   "chunk_bytes"  row-chunk width per sweep series (default 4096)
  *   "near_window"  >0: gathers within +-window rows of the output row use
  *                  L2 evict_last, others evict_first (default 0 = off)
- *   "stream_hint"  1: row-local streams use L2 evict_first (default 1) */
+ *   "stream_hint"  1: row-local streams use L2 evict_first (default 1)
+ *   "vpl"          preferred 16-byte vectors per lane (1, 2, 4): narrower row
+ *                  groups, more gathers in flight per lane (default 0 = 2 for rows
+ *                  up to 512 B, else 1) */
 int csc_set_tuning(const char *key, int64_t value);
 
 /* Measurement hook: when enabled, every main sweep launch of csc_cheb_filter /

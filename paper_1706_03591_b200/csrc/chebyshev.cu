@@ -259,6 +259,12 @@ struct SweepArgs {
   int sumsq;
   int hint;          // 1: evict_first policy on the row-local streams
   int near;          // >0: gathers of rows within +-near of the output row use evict_last
+  // long-row segments handled by the first seg_blocks blocks of the same launch
+  int seg_blocks;
+  const int32_t *long_rows;
+  const int32_t *seg_off;
+  int64_t n_long, n_seg;
+  void *seg_scratch;
 };
 
 // Gather-accumulate of entries [beg, end) of one row into acc[VPL] by a group
@@ -333,16 +339,28 @@ __device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
 }
 
 // One Chebyshev order over all rows with at most kLongThr entries.
+template <typename T, int LV>
+__device__ __forceinline__ void segment_body(const SweepArgs &A, int64_t first_warp,
+                                             int64_t nwarps);
+
 template <typename T, int G, int VPL, int MODE>
 __global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs A) {
   using VT = typename V16<T>::V;
   __shared__ double red[kBlock / 32];
+  if ((int)blockIdx.x < A.seg_blocks) {  // long-row segments, overlapped with the rows
+    constexpr int LV = (VPL * G + 31) / 32;
+    segment_body<T, LV>(A, (int64_t)blockIdx.x * (kBlock / 32) + threadIdx.x / 32,
+                        (int64_t)A.seg_blocks * (kBlock / 32));
+    return;
+  }
+  const int64_t bid = (int64_t)blockIdx.x - A.seg_blocks;
+  const int64_t nblocks = (int64_t)gridDim.x - A.seg_blocks;
   const int lane = threadIdx.x & 31;
   const int glane = lane % G;
   const unsigned gmask =
       (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((lane / G) * G));
   const int groups_per_block = kBlock / G;
-  const int64_t ngroups = (int64_t)gridDim.x * groups_per_block;
+  const int64_t ngroups = nblocks * groups_per_block;
   const T *vals = static_cast<const T *>(A.vals);
   const VT *gat = static_cast<const VT *>(A.gat);
   const VT *prev = static_cast<const VT *>(A.prev);
@@ -354,8 +372,7 @@ __global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs A) {
   const uint64_t pol = make_policy(A.hint);
   const uint64_t pnear = make_gather_policy(1), pfar = make_gather_policy(0);
 
-  for (int64_t row = (int64_t)blockIdx.x * groups_per_block + threadIdx.x / G; row < A.n;
-       row += ngroups) {
+  for (int64_t row = bid * groups_per_block + threadIdx.x / G; row < A.n; row += ngroups) {
     const int beg = __ldg(A.indptr + row), end = __ldg(A.indptr + row + 1);
     if (end - beg > kLongThr) continue;  // segment path
     VT acc[VPL];
@@ -376,30 +393,29 @@ __global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs A) {
     if (MODE >= kMomFirst) {
       const double b1 = block_sum<kBlock>(s1, red);
       if (threadIdx.x == 0) {
-        A.partials[2 * blockIdx.x] = b0;
-        A.partials[2 * blockIdx.x + 1] = b1;
+        A.partials[2 * bid] = b0;
+        A.partials[2 * bid + 1] = b1;
       }
     } else if (threadIdx.x == 0) {
-      A.partials[blockIdx.x] = b0;
+      A.partials[bid] = b0;
     }
   }
 }
 
 // Long rows, phase 1: one warp per kSeg-entry segment -> scratch[seg].
 template <typename T, int VPL>
-__global__ void __launch_bounds__(kBlock)
-    long_partial_kernel(SweepArgs A, const int32_t *__restrict__ long_rows,
-                        const int32_t *__restrict__ seg_off, int64_t n_long, int64_t n_seg,
-                        typename V16<T>::V *__restrict__ scratch) {
+__device__ __forceinline__ void segment_body(const SweepArgs &A, int64_t first_warp,
+                                             int64_t warps) {
   using VT = typename V16<T>::V;
   const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
   const T *vals = static_cast<const T *>(A.vals);
   const VT *gat = static_cast<const VT *>(A.gat);
+  VT *scratch = static_cast<VT *>(A.seg_scratch);
+  const int32_t *long_rows = A.long_rows, *seg_off = A.seg_off;
+  const int64_t n_long = A.n_long, n_seg = A.n_seg;
   const uint64_t pol = make_policy(A.hint);
   const uint64_t pnear = make_gather_policy(1), pfar = make_gather_policy(0);
-  for (int64_t s = (int64_t)blockIdx.x * (kBlock / 32) + threadIdx.x / 32; s < n_seg;
-       s += warps) {
+  for (int64_t s = first_warp; s < n_seg; s += warps) {
     // long row owning segment s: last r with seg_off[r] <= s
     int64_t lo = 0, hi = n_long - 1;
     while (lo < hi) {
@@ -681,6 +697,18 @@ int run_order_gv(const csc_chebop &op, SweepArgs A, int mode, double *partials,
   int grid = (int)std::min<int64_t>(sweep_grid<T, G, VPL>(),
                                     std::max<int64_t>(1, csc::ceil_div(op.n, groups_per_block)));
   A.partials = partials;
+  A.seg_blocks = 0;
+  if (op.n_long > 0) {
+    A.seg_blocks = (int)std::min<int64_t>(csc::device_info().sm_count * 4,
+                                          csc::ceil_div(op.n_seg, kBlock / 32));
+    A.long_rows = op.long_rows;
+    A.seg_off = op.seg_off;
+    A.n_long = op.n_long;
+    A.n_seg = op.n_seg;
+    A.seg_scratch = seg_scratch;
+  }
+  const int main_grid = grid;
+  grid += A.seg_blocks;
   int rc = CSC_OK;
   switch (mode) {
     case kFirst: rc = launch_sweep<T, G, VPL, kFirst>(A, grid, st); break;
@@ -689,14 +717,10 @@ int run_order_gv(const csc_chebop &op, SweepArgs A, int mode, double *partials,
     default: rc = launch_sweep<T, G, VPL, kMomMid>(A, grid, st); break;
   }
   if (rc != CSC_OK) return rc;
+  grid = main_grid;
   nparts = grid;
   if (op.n_long > 0) {
     constexpr int LV = (VPL * G + 31) / 32;  // vectors per lane at G = 32
-    const int pgrid = (int)std::min<int64_t>(csc::device_info().sm_count * 8,
-                                             csc::ceil_div(op.n_seg, kBlock / 32));
-    long_partial_kernel<T, LV><<<pgrid, kBlock, 0, st>>>(A, op.long_rows, op.seg_off, op.n_long,
-                                                         op.n_seg, static_cast<VT *>(seg_scratch));
-    CSC_CHECK_LAUNCH();
     const int fgrid = (int)std::min<int64_t>(csc::device_info().sm_count * 4,
                                              csc::ceil_div(op.n_long, kBlock / 32));
     const VT *sc = static_cast<const VT *>(seg_scratch);
@@ -730,17 +754,40 @@ int64_t max_partials(const csc_chebop &op) {
   return sms * 32 + sms * 4 + 8;
 }
 
+int g_vpl_pref = -1;  // preferred 16-byte vectors per lane for short rows (tuning knob)
+
+int vpl_pref() {
+  if (g_vpl_pref < 0) {
+    const char *e = getenv("CSC_VPL");
+    g_vpl_pref = e ? atoi(e) : 0;
+    if (g_vpl_pref != 1 && g_vpl_pref != 2 && g_vpl_pref != 4) g_vpl_pref = 0;
+  }
+  return g_vpl_pref;
+}
+
+template <typename T, int G>
+int run_order_g(const csc_chebop &op, const SweepArgs &A, int mode, double *partials,
+                int64_t &nparts, cudaStream_t st, void *seg_scratch) {
+  const int need = (A.nvec + G - 1) / G;  // vectors per lane at this group width
+  if (need <= 1) return run_order_gv<T, G, 1>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (need <= 2) return run_order_gv<T, G, 2>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (need <= 4) return run_order_gv<T, G, 4>(op, A, mode, partials, nparts, st, seg_scratch);
+  return run_order_gv<T, G, 8>(op, A, mode, partials, nparts, st, seg_scratch);
+}
+
+// Row-group width G: the smallest power of two >= nvec / preferred-VPL
+// (4..32); each lane then holds ceil(nvec/G) <= 8 vectors of every gathered row.
 template <typename T>
 int run_order(const csc_chebop &op, const SweepArgs &A, int mode, double *partials,
               int64_t &nparts, cudaStream_t st, void *seg_scratch) {
-  const int nvec = A.nvec;
-  if (nvec <= 4) return run_order_gv<T, 4, 1>(op, A, mode, partials, nparts, st, seg_scratch);
-  if (nvec <= 8) return run_order_gv<T, 8, 1>(op, A, mode, partials, nparts, st, seg_scratch);
-  if (nvec <= 16) return run_order_gv<T, 16, 1>(op, A, mode, partials, nparts, st, seg_scratch);
-  if (nvec <= 32) return run_order_gv<T, 32, 1>(op, A, mode, partials, nparts, st, seg_scratch);
-  if (nvec <= 64) return run_order_gv<T, 32, 2>(op, A, mode, partials, nparts, st, seg_scratch);
-  if (nvec <= 128) return run_order_gv<T, 32, 4>(op, A, mode, partials, nparts, st, seg_scratch);
-  return run_order_gv<T, 32, 8>(op, A, mode, partials, nparts, st, seg_scratch);
+  // default (0): 2 vectors per lane for rows up to 512 B, else full-warp groups
+  // (A/B on B200: cfg4 fp32 d=64 4.59 vs 4.76 ms/order, cfg5 d=48 3.33 vs 3.40)
+  const int pref = vpl_pref() ? vpl_pref() : (A.nvec <= 32 ? 2 : 1);
+  const int want = (A.nvec + pref - 1) / pref;
+  if (want <= 4) return run_order_g<T, 4>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (want <= 8) return run_order_g<T, 8>(op, A, mode, partials, nparts, st, seg_scratch);
+  if (want <= 16) return run_order_g<T, 16>(op, A, mode, partials, nparts, st, seg_scratch);
+  return run_order_g<T, 32>(op, A, mode, partials, nparts, st, seg_scratch);
 }
 
 constexpr int kMaxVecChunk = 256;  // widest row chunk one sweep handles
@@ -1155,6 +1202,10 @@ int csc_set_tuning(const char *key, int64_t value) {
   } else if (k == "near_window") {
     near_window();
     g_near = (int)value;
+  } else if (k == "vpl") {
+    vpl_pref();
+    CSC_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4, "vpl must be 0, 1, 2 or 4");
+    g_vpl_pref = (int)value;
   } else if (k == "stream_hint") {
     stream_hint();
     g_hint = value ? 1 : 0;
