@@ -205,6 +205,18 @@ int csc_kmeanspp_batch(const double *f_dev, int64_t n, int64_t d, int64_t ld, in
                        const int64_t *first_idx_host, const double *uniforms_host, double *cent_dev,
                        int64_t ldc, int32_t *flags_dev, void *stream);
 
+/* ---- probe signals (signals.py:16-37) ---------------------------------- */
+/* out[i*ld + col0 + c] = 0.0 + sigma * z_c[i], z_c = numpy's
+ * Generator(PCG64).standard_normal stream from the column's initial PCG64
+ * state states_host[4c..4c+3] = (state lo, state hi, inc lo, inc hi) (host).
+ * Chunk-parallel ziggurat with verified chunk boundaries; bad_host[c] = 1
+ * marks a column the caller must regenerate on the host (boundary
+ * disagreement or too few draws; not expected in practice). Bit-identical
+ * to numpy except that tail samples (|z| > 3.65) go through the device
+ * log1p/exp, which may round the last bit differently. SYNCHRONISES. */
+int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
+                       double *out_dev, int64_t ld, int64_t col0, int32_t *bad_host, void *stream);
+
 /* ---- dense helpers ------------------------------------------------------ */
 /* dst[:, j] = src[:, cols[j]] for j < ncols (row-major, f64), the Theta
  * assembly of dynamic.py:163-168. cols_dev: int64. */

@@ -1,0 +1,246 @@
+// Device generation of the reference's random probe block (signals.py:16-37):
+// column c = sigma * standard_normal(n) of numpy's Generator(PCG64(child_c)),
+// reproduced on the GPU from each column's initial PCG64 state.
+//
+// PCG64 (numpy): 128-bit LCG s <- s*MULT + inc, output XSL-RR of the new
+// state. standard_normal: numpy's 256-layer ziggurat (tables probed from the
+// library by tools/derive_ziggurat.py): one 64-bit draw r, idx = r & 0xff,
+// sign = bit 8, rabs = bits 9..60; accept if rabs < k[idx]; else the wedge
+// (one extra uniform) or, for idx 0, the tail loop (pairs of uniforms).
+//
+// Parallel parse. A column's draw stream is cut into chunks of B draws; the
+// chunk thread jumps ahead (O(log) LCG power) to lookback W before its chunk
+// and runs the sampler speculatively: the parse synchronises with the true
+// one at the first output boundary they share, well inside W. It counts the
+// outputs that start inside its chunk; an exclusive scan gives their indices
+// and a second pass writes them. Each chunk also reports its first output
+// start at/after its own start and at/after its end; neighbouring chunks
+// must agree (checked on device), otherwise the column is flagged and the
+// caller regenerates it on the host. Uniform/exp/log1p paths use the
+// device's libm: wedge decisions and tail values can differ from glibc only
+// in the last ulp (tail samples, |x| > 3.65, ~3e-4 of draws).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace {
+
+#include "ziggurat_tables.inc"
+
+struct U128 {
+  uint64_t lo, hi;
+};
+
+__device__ __forceinline__ U128 mul128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+  return r;
+}
+__device__ __forceinline__ U128 add128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+  return r;
+}
+
+__constant__ U128 kMult = {0x4385DF649FCCF645ull, 0x2360ED051FC65DA4ull};
+
+// state after k steps: s_k = A^k s + c (A^k - 1)/(A - 1), by squaring
+__device__ U128 pcg_advance(U128 s, U128 inc, uint64_t k) {
+  U128 am = {1, 0}, ap = {0, 0}, cm = kMult, cp = inc;
+  while (k) {
+    if (k & 1) {
+      am = mul128(am, cm);
+      ap = add128(mul128(ap, cm), cp);
+    }
+    cp = mul128(add128(cm, U128{1, 0}), cp);
+    cm = mul128(cm, cm);
+    k >>= 1;
+  }
+  return add128(mul128(am, s), ap);
+}
+
+struct Pcg {
+  U128 s, inc;
+  __device__ __forceinline__ uint64_t next64() {
+    s = add128(mul128(s, kMult), inc);
+    const uint64_t x = s.hi ^ s.lo;
+    const unsigned rot = (unsigned)(s.hi >> 58);
+    return rot ? (x >> rot) | (x << (64 - rot)) : x;
+  }
+  __device__ __forceinline__ double next_double() {
+    return (double)(next64() >> 11) * (1.0 / 9007199254740992.0);
+  }
+};
+
+// one standard normal; `pos` counts consumed draws
+__device__ __forceinline__ double zig_normal(Pcg &g, int64_t &pos, const double *W,
+                                             const unsigned long long *K, const double *F) {
+  for (;;) {
+    uint64_t r = g.next64();
+    ++pos;
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+    double x = (double)rabs * W[idx];
+    if (sign) x = -x;
+    if (rabs < K[idx]) return x;
+    if (idx == 0) {
+      for (;;) {
+        const double xx = -ZIG_INV_R * log1p(-g.next_double());
+        const double yy = -log1p(-g.next_double());
+        pos += 2;
+        if (yy + yy > xx * xx) return ((rabs >> 8) & 1) ? -(ZIG_R + xx) : ZIG_R + xx;
+      }
+    }
+    const double u = g.next_double();
+    ++pos;
+    if ((F[idx - 1] - F[idx]) * u + F[idx] < exp(-0.5 * x * x)) return x;
+  }
+}
+
+struct ChunkPlan {
+  int64_t n, ncols, nch, B, W;
+};
+
+// pass 1 (write == 0): count outputs starting in [c0, c1), boundary checks.
+// pass 2 (write == 1): write them (index = scanned offset + local index).
+__global__ void __launch_bounds__(128)
+    zig_chunk_kernel(ChunkPlan P, const uint64_t *__restrict__ states, int write,
+                     int32_t *__restrict__ counts, int64_t *__restrict__ first_ge_start,
+                     int64_t *__restrict__ first_ge_end, const int32_t *__restrict__ offsets,
+                     double sigma, double *__restrict__ out, int64_t ld, int64_t col0) {
+  __shared__ double W[256], F[256];
+  __shared__ unsigned long long K[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    W[i] = kZigW[i];
+    F[i] = kZigF[i];
+    K[i] = kZigK[i];
+  }
+  __syncthreads();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= P.ncols * P.nch) return;
+  const int64_t col = tid % P.ncols, ch = tid / P.ncols;
+  const int64_t c0 = ch * P.B, c1 = c0 + P.B;
+  const int64_t start = ch == 0 ? 0 : c0 - P.W;
+  Pcg g;
+  g.s = U128{states[4 * col], states[4 * col + 1]};
+  g.inc = U128{states[4 * col + 2], states[4 * col + 3]};
+  if (start > 0) g.s = pcg_advance(g.s, g.inc, (uint64_t)start);
+  int64_t pos = start;
+  int64_t fstart = -1, cnt = 0;
+  int64_t index = 0;
+  if (write) {
+    const int32_t *co = offsets + col * P.nch;
+    index = co[ch] - co[0];  // offsets are a flattened exclusive scan
+  }
+  for (;;) {
+    const int64_t s0 = pos;
+    if (s0 >= c1) break;
+    const double z = zig_normal(g, pos, W, K, F);
+    if (s0 >= c0) {
+      if (fstart < 0) fstart = s0;
+      if (write) {
+        if (index < P.n) out[index * ld + col0 + col] = 0.0 + sigma * z;
+        ++index;
+      }
+      ++cnt;
+    }
+  }
+  if (!write) {
+    counts[tid] = (int32_t)cnt;
+    first_ge_start[tid] = fstart < 0 ? pos : fstart;  // no start inside: the next one
+    first_ge_end[tid] = pos;                          // first output start >= c1
+  }
+}
+
+__global__ void zig_check_kernel(ChunkPlan P, const int32_t *__restrict__ counts,
+                                 const int64_t *__restrict__ first_ge_start,
+                                 const int64_t *__restrict__ first_ge_end,
+                                 const int32_t *__restrict__ offsets, int32_t *__restrict__ bad) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= P.ncols * P.nch) return;
+  const int64_t col = tid % P.ncols, ch = tid / P.ncols;
+  // neighbouring chunks must agree on the output boundary between them
+  if (ch + 1 < P.nch) {
+    const int64_t nb = tid + P.ncols;
+    if (first_ge_end[tid] != first_ge_start[nb]) atomicExch(bad + col, 1);
+  } else {
+    // enough draws for n outputs? (offsets are in [col][ch] order)
+    const int64_t total = (int64_t)offsets[col * P.nch + ch] + counts[tid] - offsets[col * P.nch];
+    if (total < P.n) atomicExch(bad + col, 1);
+  }
+}
+
+__global__ void transpose_counts_kernel(const int32_t *__restrict__ in, int64_t ncols, int64_t nch,
+                                        int32_t *__restrict__ out) {
+  // in: [ch][col] (thread order) -> out: [col][ch] (scan order)
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ncols * nch) return;
+  const int64_t col = t % ncols, ch = t / ncols;
+  out[col * nch + ch] = in[t];
+}
+
+}  // namespace
+
+extern "C" {
+
+int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
+                       double *out, int64_t ld, int64_t col0, int32_t *bad_host, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(ncols >= 1 && n >= 1 && col0 >= 0 && col0 + ncols <= ld,
+              "csc_normal_columns: bad shape");
+  CSC_REQUIRE(bad_host != nullptr, "csc_normal_columns: NULL bad_host");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  csc::device_info();
+  ChunkPlan P;
+  P.n = n;
+  P.ncols = ncols;
+  P.W = 128;
+  // ~1.02 draws per output; chunks of B draws with a W-draw lookback
+  P.B = std::max<int64_t>(512, std::min<int64_t>(4096, csc::ceil_div(n, 64)));
+  const int64_t draws = n + n / 16 + 4 * P.B;
+  P.nch = csc::ceil_div(draws, P.B);
+  const int64_t T = ncols * P.nch;
+  csc::Scratch st_dev, counts, fgs, fge, cnt_t, offs, bad, tmp;
+  CSC_TRY_CUDA(st_dev.alloc(sizeof(uint64_t) * 4 * ncols, st));
+  CSC_TRY_CUDA(counts.alloc(sizeof(int32_t) * T, st));
+  CSC_TRY_CUDA(cnt_t.alloc(sizeof(int32_t) * T, st));
+  CSC_TRY_CUDA(offs.alloc(sizeof(int32_t) * T, st));
+  CSC_TRY_CUDA(fgs.alloc(sizeof(int64_t) * T, st));
+  CSC_TRY_CUDA(fge.alloc(sizeof(int64_t) * T, st));
+  CSC_TRY_CUDA(bad.alloc(sizeof(int32_t) * ncols, st));
+  CSC_TRY_CUDA(cudaMemsetAsync(bad.ptr, 0, sizeof(int32_t) * ncols, st));
+  CSC_TRY_CUDA(cudaMemcpyAsync(st_dev.ptr, states_host, sizeof(uint64_t) * 4 * ncols,
+                               cudaMemcpyHostToDevice, st));
+  const int threads = 128;
+  const unsigned blocks = (unsigned)csc::ceil_div(T, threads);
+  zig_chunk_kernel<<<blocks, threads, 0, st>>>(P, st_dev.as<uint64_t>(), 0, counts.as<int32_t>(),
+                                              fgs.as<int64_t>(), fge.as<int64_t>(), nullptr, sigma,
+                                              out, ld, col0);
+  CSC_CHECK_LAUNCH();
+  transpose_counts_kernel<<<blocks, threads, 0, st>>>(counts.as<int32_t>(), ncols, P.nch,
+                                                      cnt_t.as<int32_t>());
+  CSC_CHECK_LAUNCH();
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt_t.as<int32_t>(), offs.as<int32_t>(), T, st);
+  CSC_TRY_CUDA(tmp.alloc(tb, st));
+  CSC_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tb, cnt_t.as<int32_t>(), offs.as<int32_t>(),
+                                             T, st));
+  // offsets in [col][ch] order; the kernels index them as col * nch + ch
+  zig_check_kernel<<<blocks, threads, 0, st>>>(P, counts.as<int32_t>(), fgs.as<int64_t>(),
+                                              fge.as<int64_t>(), offs.as<int32_t>(),
+                                              bad.as<int32_t>());
+  CSC_CHECK_LAUNCH();
+  zig_chunk_kernel<<<blocks, threads, 0, st>>>(P, st_dev.as<uint64_t>(), 1, nullptr, nullptr,
+                                              nullptr, offs.as<int32_t>(), sigma, out, ld, col0);
+  CSC_CHECK_LAUNCH();
+  CSC_TRY_CUDA(cudaMemcpyAsync(bad_host, bad.ptr, sizeof(int32_t) * ncols, cudaMemcpyDeviceToHost,
+                               st));
+  CSC_TRY_CUDA(cudaStreamSynchronize(st));
+  return CSC_OK;
+}
+
+}  // extern "C"

@@ -76,11 +76,50 @@ def random_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> np.n
     return np.ascontiguousarray(signal_columns(n, d, seed, scale_dim).T)
 
 
-def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> torch.Tensor:
-    """random_signals as a padded (n, ld) float64 device block (transposed on the GPU)."""
-    cols = torch.from_numpy(signal_columns(n, d, seed, scale_dim))
+# "device": PCG64 + ziggurat on the GPU (csc_normal_columns); "host": numpy in
+# a thread pool + H2D (bit-exact by construction). CSC_RNG=host selects the latter.
+RNG_MODE = os.environ.get("CSC_RNG", "device")
+
+
+def column_states(children) -> np.ndarray:
+    """Initial PCG64 (state, inc) of each child stream as 4 uint64 words per column."""
+    words = np.empty((len(children), 4), dtype=np.uint64)
+    mask = (1 << 64) - 1
+    for c, child in enumerate(children):
+        st = np.random.PCG64(child).state["state"]
+        s, inc = int(st["state"]), int(st["inc"])
+        words[c] = (s & mask, s >> 64, inc & mask, inc >> 64)
+    return words
+
+
+def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None, mode: str | None = None) -> torch.Tensor:
+    """random_signals as a padded (n, ld) float64 device block.
+
+    Device mode draws numpy's exact PCG64 streams and ziggurat on the GPU;
+    columns the generator flags are redrawn on the host (the exact path).
+    """
+    if d < 1:
+        raise ValueError("need at least one signal column")
+    if n < 1:
+        raise ValueError("need at least one node")
+    dim = d if scale_dim is None else int(scale_dim)
+    if dim < 1:
+        raise ValueError("scale_dim must be positive")
     dev = require_cuda()
     blk = torch.zeros((n, row_stride(d)), dtype=torch.float64, device=dev)
+    if (mode or RNG_MODE) == "device":
+        # spawn from a copy so the caller's SeedSequence advances exactly as in signal_columns
+        children = as_seed_sequence(seed).spawn(d)
+        states = np.ascontiguousarray(column_states(children))
+        bad = np.zeros(d, dtype=np.int32)
+        sigma = 1.0 / np.sqrt(dim)
+        _native.call("csc_normal_columns", states.ctypes.data, d, n, float(sigma), ptr(blk), blk.shape[1], 0,
+                     bad.ctypes.data, stream())
+        for c in np.flatnonzero(bad):
+            z = np.random.default_rng(children[c]).standard_normal(n) * sigma + 0.0
+            blk[:, c].copy_(torch.from_numpy(z))
+        return blk
+    cols = torch.from_numpy(signal_columns(n, d, seed, scale_dim))
     blk[:, :d].copy_(cols.to(dev).t())
     return blk
 
