@@ -160,6 +160,18 @@ int csc_kmeans_plan_stats(const csc_kmeans_plan *plan, int64_t *candidates, int3
 int csc_kmeans_iterate(csc_kmeans_plan *plan, const double *f_dev, const double *rownorm_dev,
                        double *c_dev, int64_t ldc, double *cnorm_dev, int32_t *labels_dev,
                        int32_t *counts_dev, int full, double *cost2_dev, void *stream);
+/* A whole Lloyd run of one restart from the seeds in c (kmeans.py:88-117)
+ * without host round trips: iteration 1 (full assignment), then a CUDA
+ * conditional while-graph of pruned iterations whose last node applies the
+ * reference's stop rule (prev - cost2 <= tol * prev, or max_iters) on
+ * device. Asynchronous on `stream`; out_dev[0] = cost2 of the last iteration
+ * (exact difference form), out_dev[1] = iterations run; history_dev
+ * (nullable, max_iters doubles) = per-iteration cost2 (centroid identity).
+ * The graph is built once per buffer set and reused. */
+int csc_kmeans_run(csc_kmeans_plan *plan, const double *f_dev, const double *rownorm_dev,
+                   double *c_dev, int64_t ldc, double *cnorm_dev, int32_t *labels_dev,
+                   int32_t *counts_dev, int max_iters, double tol, double *out_dev,
+                   double *history_dev, void *stream);
 /* k-means tuning knob: "assign_tn" = 4 (default) or 8 centroids per thread */
 int csc_kmeans_tuning(const char *key, int64_t value);
 /* empty-cluster repair (kmeans.py:99-108): for each empty j ascending, move the

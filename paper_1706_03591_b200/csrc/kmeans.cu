@@ -1174,6 +1174,39 @@ __global__ void shalf_kernel(const double *__restrict__ cent, int64_t ldc, int64
   }
 }
 
+// device-side stop rule of kmeans.py:112-116 for graph-resident Lloyd loops
+struct LoopState {
+  double prev, tol;
+  int it, max_iters, stop, pad;
+};
+
+__global__ void copy_iters_kernel(const LoopState *ls, double *out, int ran) {
+  out[0] = ran ? (double)ls->it : 0.0;
+  if (!ran) out[-1] = INFINITY;
+}
+
+__global__ void loop_init_kernel(LoopState *ls, double tol, int max_iters) {
+  ls->prev = INFINITY;
+  ls->tol = tol;
+  ls->it = 0;
+  ls->max_iters = max_iters;
+  ls->stop = 0;
+}
+
+__global__ void loop_check_kernel(const double *__restrict__ scal, LoopState *ls,
+                                  double *__restrict__ history, int hist_cap,
+                                  cudaGraphConditionalHandle h, int use_handle) {
+  const double c = scal[0];
+  if (history && ls->it < hist_cap) history[ls->it] = c;
+  int stop = 0;
+  if (isfinite(ls->prev) && ls->prev - c <= ls->tol * ls->prev) stop = 1;
+  ls->prev = c;
+  ls->it += 1;
+  if (ls->it >= ls->max_iters) stop = 1;
+  ls->stop = stop;
+  if (use_handle) cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
 int grid_cap(int64_t want, int per_sm = 8) {
   return (int)std::min<int64_t>((int64_t)csc::device_info().sm_count * per_sm,
                                 std::max<int64_t>(1, want));
@@ -1189,6 +1222,13 @@ struct csc_kmeans_plan {
   int32_t *cand, *flags, *pcnt;
   size_t smem = 0;
   cudaStream_t stream = nullptr;
+  // graph-resident loop (built on first csc_kmeans_run for a buffer set)
+  LoopState *loop = nullptr;
+  double *history = nullptr;
+  int hist_cap = 0;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  const void *key[8] = {};
 };
 
 extern "C" {
@@ -1366,6 +1406,10 @@ int csc_kmeans_plan_stats(const csc_kmeans_plan *p, int64_t *candidates, int32_t
 
 int csc_kmeans_plan_destroy(csc_kmeans_plan *p) {
   if (!p) return CSC_OK;
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  if (p->loop) cudaFreeAsync(p->loop, p->stream);
+  if (p->history) cudaFreeAsync(p->history, p->stream);
   if (p->base) cudaFreeAsync(p->base, p->stream);
   delete p;
   return CSC_OK;
@@ -1435,6 +1479,94 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
   CSC_CHECK_LAUNCH();
   if (cost2_dev)
     CSC_TRY_CUDA(cudaMemcpyAsync(cost2_dev, p->scal, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return CSC_OK;
+}
+
+int csc_kmeans_run(csc_kmeans_plan *p, const double *f, const double *fnorm, double *cent,
+                   int64_t ldc, double *cnorm, int32_t *labels, int32_t *counts, int max_iters,
+                   double tol, double *out_dev, double *history_dev, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(p != nullptr, "csc_kmeans_run: NULL plan");
+  CSC_REQUIRE(out_dev != nullptr, "csc_kmeans_run: NULL out_dev");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!p->loop) CSC_TRY_CUDA(cudaMallocAsync((void **)&p->loop, sizeof(LoopState), st));
+  const int cap = std::max(1, max_iters);
+  if (cap > p->hist_cap) {
+    if (p->history) CSC_TRY_CUDA(cudaFreeAsync(p->history, st));
+    CSC_TRY_CUDA(cudaMallocAsync((void **)&p->history, sizeof(double) * cap, st));
+    p->hist_cap = cap;
+    if (p->exec) {  // history pointer is baked into the graph
+      cudaGraphExecDestroy(p->exec);
+      cudaGraphDestroy(p->graph);
+      p->exec = nullptr;
+      p->graph = nullptr;
+    }
+  }
+  loop_init_kernel<<<1, 1, 0, st>>>(p->loop, tol, max_iters);
+  CSC_CHECK_LAUNCH();
+  // |c_j|^2 of the seeds (the GEMM-form distances of iteration 1 need them)
+  centroid_norms_kernel<<<(unsigned)csc::ceil_div(p->k, 8), 256, 0, st>>>(cent, ldc, p->d, p->k,
+                                                                         cnorm);
+  CSC_CHECK_LAUNCH();
+  if (max_iters >= 1) {
+    int rc = csc_kmeans_iterate(p, f, fnorm, cent, ldc, cnorm, labels, counts, 1, nullptr, st);
+    if (rc != CSC_OK) return rc;
+    loop_check_kernel<<<1, 1, 0, st>>>(p->scal, p->loop, p->history, p->hist_cap, 0, 0);
+    CSC_CHECK_LAUNCH();
+  }
+  if (max_iters >= 2) {
+    const void *key[8] = {f, fnorm, cent, cnorm, labels, counts, (const void *)(intptr_t)ldc,
+                          nullptr};
+    bool same = p->exec != nullptr;
+    for (int i = 0; i < 8 && same; ++i) same = key[i] == p->key[i];
+    if (!same) {
+      if (p->exec) {
+        cudaGraphExecDestroy(p->exec);
+        cudaGraphDestroy(p->graph);
+        p->exec = nullptr;
+      }
+      cudaGraph_t g;
+      CSC_TRY_CUDA(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle h;
+      CSC_TRY_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      CSC_TRY_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      cudaStream_t cap_st;
+      CSC_TRY_CUDA(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
+      CSC_TRY_CUDA(cudaStreamBeginCaptureToGraph(cap_st, body, nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeRelaxed));
+      int rc = csc_kmeans_iterate(p, f, fnorm, cent, ldc, cnorm, labels, counts, 0, nullptr,
+                                  cap_st);
+      loop_check_kernel<<<1, 1, 0, cap_st>>>(p->scal, p->loop, p->history, p->hist_cap, h, 1);
+      cudaGraph_t captured;
+      const cudaError_t ec = cudaStreamEndCapture(cap_st, &captured);
+      cudaStreamDestroy(cap_st);
+      p->stream = st;
+      if (rc != CSC_OK) return rc;
+      CSC_TRY_CUDA(ec);
+      CSC_TRY_CUDA(cudaGraphInstantiate(&p->exec, g, 0));
+      p->graph = g;
+      for (int i = 0; i < 8; ++i) p->key[i] = key[i];
+    }
+    CSC_TRY_CUDA(cudaGraphLaunch(p->exec, st));
+  }
+  // out_dev[0] = cost2 of the last iteration in the exact difference form
+  // (kmeans.py:111), out_dev[1] = iterations run (as double)
+  if (max_iters >= 1) {
+    const int rc = csc_kmeans_cost(f, labels, cent, ldc, p->n, p->d, p->ld, out_dev, st);
+    if (rc != CSC_OK) return rc;
+  }
+  if (history_dev)
+    CSC_TRY_CUDA(cudaMemcpyAsync(history_dev, p->history, sizeof(double) * cap,
+                                 cudaMemcpyDeviceToDevice, st));
+  copy_iters_kernel<<<1, 1, 0, st>>>(p->loop, out_dev + 1, max_iters >= 1);
+  CSC_CHECK_LAUNCH();
   return CSC_OK;
 }
 

@@ -189,6 +189,99 @@ class _Workspace:
         return prev
 
 
+class _Lane:
+    """One concurrently running Lloyd restart: stream, plan (with its loop graph), buffers."""
+
+    def __init__(self, pool, dev):
+        n, d, ld, k = pool.n, pool.d, pool.ld, pool.k
+        self.stream = torch.cuda.Stream(device=dev)
+        self.ldc = row_stride(d)
+        self.cent = torch.zeros((k, self.ldc), dtype=torch.float64, device=dev)
+        self.cnorm = torch.empty(k, dtype=torch.float64, device=dev)
+        self.labels = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(k, dtype=torch.int32, device=dev)
+        self.out = torch.empty(2, dtype=torch.float64, device=dev)
+        self.done = torch.cuda.Event()
+        h = ctypes.c_void_p()
+        _native.call("csc_kmeans_plan_create", n, d, ld, k, self.stream.cuda_stream, ctypes.byref(h))
+        self.plan = h
+
+    def __del__(self):
+        h = getattr(self, "plan", None)
+        if h:
+            try:
+                _native.lib().csc_kmeans_plan_destroy(h)
+            except Exception:
+                pass
+            self.plan = None
+
+
+class _LloydPool:
+    """Persistent per-shape state so the Lloyd loop graphs are built once and reused."""
+
+    MAX_LANES = 16
+
+    def __init__(self, n, d, ld, k, dev):
+        self.key = (dev.index, n, d, ld, k)
+        self.n, self.d, self.ld, self.k = n, d, ld, k
+        self.F = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+        self.lanes = [_Lane(self, dev) for _ in range(self.MAX_LANES)]
+
+
+_LLOYD_POOL: _LloydPool | None = None
+
+
+def _lloyd_pool(n, d, ld, k, dev) -> _LloydPool:
+    global _LLOYD_POOL
+    key = (dev.index, n, d, ld, k)
+    if _LLOYD_POOL is None or _LLOYD_POOL.key != key:
+        _LLOYD_POOL = None
+        _LLOYD_POOL = _LloydPool(n, d, ld, k, dev)
+    return _LLOYD_POOL
+
+
+def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children):
+    """Every restart: batched k-means++ seeds, then the Lloyd runs on concurrent lanes.
+
+    Each lane runs iteration 1 and a device-resident loop graph
+    (csc_kmeans_run); the best restart is chosen on the host with the
+    reference's rule (strictly smaller cost2, earliest restart on ties).
+    Returns (labels int64 numpy, cost2).
+    """
+    dev = blk.device
+    n, ld = blk.shape
+    pool = _lloyd_pool(n, d, ld, k, dev)
+    cur = torch.cuda.current_stream()
+    pool.F.copy_(blk)
+    ws = _Workspace(pool.F, d, k)
+    seeds = batched_kmeanspp(ws, children)
+    ready = torch.cuda.Event()
+    ready.record(cur)
+    best = None
+    R = len(children)
+    for w0 in range(0, R, _LloydPool.MAX_LANES):
+        wave = list(range(w0, min(R, w0 + _LloydPool.MAX_LANES)))
+        for li, r in enumerate(wave):
+            lane = pool.lanes[li]
+            lane.stream.wait_event(ready)
+            with torch.cuda.stream(lane.stream):
+                lane.cent.copy_(seeds[r])
+                _native.call("csc_kmeans_run", lane.plan, ptr(pool.F), ptr(ws.fnorm), ptr(lane.cent), lane.ldc,
+                             ptr(lane.cnorm), ptr(lane.labels), ptr(lane.counts), int(cfg.max_iters),
+                             float(cfg.tol), ptr(lane.out), None, lane.stream.cuda_stream)
+                lane.done.record(lane.stream)
+        for li in range(len(wave)):
+            cur.wait_event(pool.lanes[li].done)
+        outs = torch.stack([pool.lanes[li].out for li in range(len(wave))]).cpu().numpy()
+        for li, r in enumerate(wave):
+            cost2 = float(outs[li, 0])
+            if best is None or cost2 < best[0]:
+                best = (cost2, pool.lanes[li].labels.cpu().numpy().astype(np.int64))
+        ready = torch.cuda.Event()
+        ready.record(cur)
+    return best[1], best[0]
+
+
 KPP_BATCH = 16  # restarts per batched k-means++ launch series (libcscb200 limit)
 
 
@@ -254,17 +347,8 @@ def kmeans(f, k: int, cfg: KmeansConfig | None = None, seed=0) -> Assignment:
     n = blk.shape[0]
     if not 1 <= k <= n:
         raise ValueError(f"need 1 <= k <= n, got k={k}, n={n}")
-    ws = _Workspace(blk, d, k)
     children = as_seed_sequence(seed).spawn(cfg.restarts)
-    seeds = batched_kmeanspp(ws, children)
-    best = None
-    for r in range(cfg.restarts):
-        ws.cent.copy_(seeds[r])
-        cost2 = ws.lloyd(cfg.max_iters, cfg.tol)
-        if best is None or cost2 < best[0]:
-            best = (cost2, ws.labels.clone())
-    cost2, labels = best
-    labels = labels.cpu().numpy().astype(np.int64)
+    labels, cost2 = run_restarts(blk, d, k, cfg, children)
     sizes = np.bincount(labels, minlength=k)
     return Assignment(labels, sizes, float(np.sqrt(max(cost2, 0.0))))
 

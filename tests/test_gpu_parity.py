@@ -565,3 +565,26 @@ def test_batched_kmeanspp_matches_sequential(P):
     for r, child in enumerate(kids2):
         ref, _ = O.kmeanspp(dup, 3, np.random.default_rng(child))
         assert np.array_equal(seeds2[r, :, :1].cpu().numpy(), ref)
+
+
+def test_graph_lloyd_equals_host_driven(P):
+    """csc_kmeans_run (device loop graph, concurrent lanes) == host-driven pruned Lloyd."""
+    from paper_1706_03591_b200.kmeans import _Workspace, batched_kmeanspp, run_restarts
+    from paper_1706_03591_b200._device import upload_block
+    g = golden("kmeans")
+    f = g["b_f"]
+    blk = upload_block(f)
+    kids = np.random.SeedSequence(77).spawn(3)
+    cfg = P.KmeansConfig(restarts=3, max_iters=50)
+    labels, cost2 = run_restarts(blk, 24, 12, cfg, kids)
+    ws = _Workspace(blk, 24, 12)
+    seeds = batched_kmeanspp(ws, kids)
+    best = None
+    for r in range(3):
+        ws.cent.copy_(seeds[r])
+        c2 = ws.lloyd(50, 1e-6)
+        if best is None or c2 < best[0]:
+            best = (c2, ws.labels.cpu().numpy().astype(np.int64))
+    assert np.array_equal(labels, best[1])
+    assert cost2 == best[0]
+    assert np.array_equal(labels, g["b_labels"])
