@@ -337,8 +337,8 @@ __device__ __forceinline__ Min3 min3_merge(const Min3 &a, const Min3 &b) {
   return r;
 }
 
-template <int kStages>
-__global__ void __launch_bounds__(128, 2)
+template <int kStages, int TM, int TN, int RT, int CT>
+__global__ void __launch_bounds__(RT * CT, 2)
     assign3_kernel(const double *__restrict__ f, const double *__restrict__ fnorm, int64_t n,
                    int64_t d, int64_t ld, const double *__restrict__ cent, int64_t ldc,
                    const double *__restrict__ cnorm, int64_t k, int64_t c0, int last_pass,
@@ -346,34 +346,38 @@ __global__ void __launch_bounds__(128, 2)
                    int32_t *__restrict__ counts, const int32_t *__restrict__ rows,
                    const int32_t *__restrict__ nrows_dev, double *__restrict__ ub,
                    double *__restrict__ lb, const int32_t *__restrict__ gate) {
-  constexpr int TN = 8, CT = 8, NT = 128;
+  constexpr int NT = RT * CT;       // threads
+  constexpr int BM = RT * TM;       // rows per tile
+  constexpr int BN = CT * TN;       // centroids per pass
+  constexpr int BNP = BN + 1;       // padded Cs row
   if (gate && *gate == 0) return;
   extern __shared__ __align__(16) double smem[];
   const int64_t dpad = (d + kAK - 1) / kAK * kAK;
-  double *Cs = smem;                  // [dpad][kANP]
-  double *Fs = smem + dpad * kANP;    // [kStages][kAM][kAKP]
+  double *Cs = smem;                  // [dpad][BNP]
+  double *Fs = smem + dpad * BNP;     // [kStages][BM][kAKP]
   const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;
-  const int64_t ntiles = (nr + kAM - 1) / kAM;
+  const int64_t ntiles = (nr + BM - 1) / BM;
   if ((int64_t)blockIdx.x >= ntiles) return;
   const int tid = threadIdx.x;
   const int tx = tid % CT, ty = tid / CT;
   const int nst = (int)(dpad / kAK);
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int64_t total = my_tiles * nst;
-  for (int64_t e = tid; e < dpad * kAN; e += NT) {
+  for (int64_t e = tid; e < dpad * BN; e += NT) {
     const int64_t cc = e / dpad, dd = e - cc * dpad;
-    Cs[dd * kANP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
+    Cs[dd * BNP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
   }
   auto tile_row = [&](int64_t g) -> int64_t {  // first local row of stage g's tile
-    return (blockIdx.x + (g / nst) * (int64_t)gridDim.x) * kAM;
+    return (blockIdx.x + (g / nst) * (int64_t)gridDim.x) * BM;
   };
   auto load_stage = [&](int64_t g) {
     const int64_t r0 = tile_row(g);
     const int64_t k0 = (int64_t)(g % nst) * kAK;
-    double *buf = Fs + (size_t)(g % kStages) * kAM * kAKP;
+    double *buf = Fs + (size_t)(g % kStages) * BM * kAKP;
 #pragma unroll
-    for (int q = 0; q < 1024 / NT; ++q) {
+    for (int q = 0; q < (BM * 8 + NT - 1) / NT; ++q) {
       const int v = tid + NT * q;
+      if (v >= BM * 8) break;
       const int row = v >> 3, vc = v & 7;
       const int64_t lr = r0 + row;
       const int64_t gr = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : n;
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(128, 2)
     if (g < total) load_stage(g);
     cp_async_commit();
   }
-  double acc[8][TN];
+  double acc[TM][TN];
   for (int64_t g = 0; g < total; ++g) {
     if (g + kStages - 1 < total) load_stage(g + kStages - 1);
     cp_async_commit();
@@ -396,21 +400,21 @@ __global__ void __launch_bounds__(128, 2)
     const int st = (int)(g % nst);
     if (st == 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
     }
-    const double *Fb = Fs + (size_t)(g % kStages) * kAM * kAKP;
-    const double *Cb = Cs + (size_t)st * kAK * kANP;
+    const double *Fb = Fs + (size_t)(g % kStages) * BM * kAKP;
+    const double *Cb = Cs + (size_t)st * kAK * BNP;
 #pragma unroll
     for (int kk = 0; kk < kAK; ++kk) {
-      double a[8], b[TN];
+      double a[TM], b[TN];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = Fb[(ty + 16 * i) * kAKP + kk];
+      for (int i = 0; i < TM; ++i) a[i] = Fb[(ty + RT * i) * kAKP + kk];
 #pragma unroll
-      for (int j = 0; j < TN; ++j) b[j] = Cb[kk * kANP + tx + CT * j];
+      for (int j = 0; j < TN; ++j) b[j] = Cb[kk * BNP + tx + CT * j];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
@@ -424,8 +428,8 @@ __global__ void __launch_bounds__(128, 2)
         cn[j] = c < k ? cnorm[c] : 0.0;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int64_t lr = r0 + ty + 16 * i;
+      for (int i = 0; i < TM; ++i) {
+        const int64_t lr = r0 + ty + RT * i;
         const int64_t r = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : -1;
         const double fni = r >= 0 ? fnorm[r] : 0.0;
         Min3 m[TN];
@@ -488,36 +492,67 @@ __global__ void __launch_bounds__(128, 2)
 int g_assign_tn = 8;
 int g_assign_ver = 3;
 
-int launch_assign3(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
-                   const double *c, int64_t ldc, const double *cnorm, int64_t k, int32_t *labels,
-                   double *own, int32_t *counts, cudaStream_t st, const int32_t *rows,
-                   const int32_t *nrows_dev, double *ub, double *lb, const int32_t *gate) {
+// 88: 8x8 per thread, 16x8 threads (default: fastest at cfg3/cfg5 scale in
+// tools/ab_assign.py); 48/44/42: 4x8, 4x4 (16x16 threads), 4x4 (32x8 threads)
+int g_assign_tile = 88;
+
+template <int TM, int TN, int RT, int CT>
+int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
+                     const double *c, int64_t ldc, const double *cnorm, int64_t k,
+                     int32_t *labels, double *own, int32_t *counts, cudaStream_t st,
+                     const int32_t *rows, const int32_t *nrows_dev, double *ub, double *lb,
+                     const int32_t *gate) {
+  constexpr int BM = RT * TM, BN = CT * TN, NT = RT * CT;
   const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
-  const size_t cbytes = sizeof(double) * dpad * kANP, sbytes = sizeof(double) * kAM * kAKP;
+  const size_t cbytes = sizeof(double) * dpad * (BN + 1), sbytes = sizeof(double) * BM * kAKP;
   // three stages when two blocks still fit in one SM's shared memory, else two
   const bool three = 2 * (cbytes + 3 * sbytes + 1024) <= 228 * 1024;
   const size_t smem = cbytes + (three ? 3 : 2) * sbytes;
   static size_t configured2 = 0, configured3 = 0;
   size_t &configured = three ? configured3 : configured2;
   if (smem > configured) {
-    CSC_TRY_CUDA(cudaFuncSetAttribute(three ? assign3_kernel<3> : assign3_kernel<2>,
+    CSC_TRY_CUDA(cudaFuncSetAttribute(three ? assign3_kernel<3, TM, TN, RT, CT>
+                                            : assign3_kernel<2, TM, TN, RT, CT>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
   const int grid = std::max(1, csc::device_info().sm_count * 2);
-  for (int64_t c0 = 0; c0 < k; c0 += kAN) {
-    const int last = c0 + kAN >= k;
+  for (int64_t c0 = 0; c0 < k; c0 += BN) {
+    const int last = c0 + BN >= k;
     if (three)
-      assign3_kernel<3><<<grid, 128, smem, st>>>(f, fnorm, n, d, ld, c, ldc, cnorm, k, c0, last,
-                                                  labels, own, last ? counts : nullptr, rows,
-                                                  nrows_dev, ub, lb, gate);
+      assign3_kernel<3, TM, TN, RT, CT><<<grid, NT, smem, st>>>(
+          f, fnorm, n, d, ld, c, ldc, cnorm, k, c0, last, labels, own, last ? counts : nullptr,
+          rows, nrows_dev, ub, lb, gate);
     else
-      assign3_kernel<2><<<grid, 128, smem, st>>>(f, fnorm, n, d, ld, c, ldc, cnorm, k, c0, last,
-                                                  labels, own, last ? counts : nullptr, rows,
-                                                  nrows_dev, ub, lb, gate);
+      assign3_kernel<2, TM, TN, RT, CT><<<grid, NT, smem, st>>>(
+          f, fnorm, n, d, ld, c, ldc, cnorm, k, c0, last, labels, own, last ? counts : nullptr,
+          rows, nrows_dev, ub, lb, gate);
     CSC_CHECK_LAUNCH();
   }
   return CSC_OK;
+}
+
+int launch_assign3(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
+                   const double *c, int64_t ldc, const double *cnorm, int64_t k, int32_t *labels,
+                   double *own, int32_t *counts, cudaStream_t st, const int32_t *rows,
+                   const int32_t *nrows_dev, double *ub, double *lb, const int32_t *gate) {
+  switch (g_assign_tile) {
+    case 88:
+      return launch_assign3_t<8, 8, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                           counts, st, rows, nrows_dev, ub, lb, gate);
+    case 48:
+      return launch_assign3_t<4, 8, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                           counts, st, rows, nrows_dev, ub, lb, gate);
+    case 42:
+      return launch_assign3_t<4, 4, 32, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                           counts, st, rows, nrows_dev, ub, lb, gate);
+    case 44:
+      return launch_assign3_t<4, 4, 16, 16>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                            counts, st, rows, nrows_dev, ub, lb, gate);
+    default:
+      return launch_assign3_t<8, 8, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                           counts, st, rows, nrows_dev, ub, lb, gate);
+  }
 }
 
 template <int TN>
@@ -1254,8 +1289,8 @@ int csc_kmeans_assign(const double *f, const double *fnorm, int64_t n, int64_t d
   const size_t smem = sizeof(double) * (dpad * kANP + 2 * kAM * kAKP);
   const bool aligned = (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(f) & 15u) == 0);
   if (aligned && g_assign_ver == 3) {
-    csc::Scratch lbs;
-    if (k > kAN) CSC_TRY_CUDA(lbs.alloc(sizeof(double) * n, st));
+    csc::Scratch lbs;  // carried second minimum between centroid passes
+    CSC_TRY_CUDA(lbs.alloc(sizeof(double) * n, st));
     const int rc = launch_assign3(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts, st,
                                   nullptr, nullptr, nullptr, lbs.as<double>(), nullptr);
     if (rc != CSC_OK) return rc;
@@ -1276,6 +1311,11 @@ int csc_kmeans_assign(const double *f, const double *fnorm, int64_t n, int64_t d
 
 int csc_kmeans_tuning(const char *key, int64_t value) {
   CSC_REQUIRE(key != nullptr, "csc_kmeans_tuning: NULL key");
+  if (std::string(key) == "assign_tile") {
+    CSC_REQUIRE(value == 44 || value == 88 || value == 48 || value == 42, "assign_tile: 44, 88, 48 or 42");
+    g_assign_tile = (int)value;
+    return CSC_OK;
+  }
   if (std::string(key) == "assign_ver") {
     CSC_REQUIRE(value == 2 || value == 3, "assign_ver must be 2 or 3");
     g_assign_ver = (int)value;

@@ -25,13 +25,18 @@ c = torch.zeros((a.k, ld), dtype=torch.float64, device="cuda")
 c[:, :a.d] = torch.randn((a.k, a.d), dtype=torch.float64, device="cuda", generator=g)
 fn = (f * f).sum(1)
 cn = (c * c).sum(1)
-labels = {v: torch.empty(a.n, dtype=torch.int32, device="cuda") for v in (2, 3)}
+VARIANTS = [("v2", "assign_ver", 2), ("v3-88", "assign_tile", 88), ("v3-48", "assign_tile", 48),
+            ("v3-44", "assign_tile", 44), ("v3-42", "assign_tile", 42)]
+labels = {v[0]: torch.empty(a.n, dtype=torch.int32, device="cuda") for v in VARIANTS}
 own = torch.empty(a.n, dtype=torch.float64, device="cuda")
 counts = torch.empty(a.k, dtype=torch.int32, device="cuda")
-times = {2: [], 3: []}
+times = {v[0]: [] for v in VARIANTS}
 for r in range(a.rounds):
-    for v in (2, 3):
-        _native.check(lib.csc_kmeans_tuning(b"assign_ver", v), "tuning")
+    for name, key, val in VARIANTS:
+        v = name
+        _native.check(lib.csc_kmeans_tuning(b"assign_ver", 2 if name == "v2" else 3), "tuning")
+        if key == "assign_tile":
+            _native.check(lib.csc_kmeans_tuning(b"assign_tile", val), "tuning")
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         _native.call("csc_kmeans_assign", ptr(f), ptr(fn), a.n, a.d, ld, ptr(c), ld, ptr(cn), a.k,
@@ -41,8 +46,8 @@ for r in range(a.rounds):
         if r:
             times[v].append(e0.elapsed_time(e1))
 flop = 2.0 * a.n * a.k * a.d
-for v in (2, 3):
+for v, _, _ in VARIANTS:
     m = statistics.median(times[v])
-    print(f"assign v{v}: n={a.n} d={a.d} k={a.k} median {m:.3f} ms ({flop / m / 1e9:.1f} TFLOP/s) "
+    print(f"assign {v}: n={a.n} d={a.d} k={a.k} median {m:.3f} ms ({flop / m / 1e9:.1f} TFLOP/s) "
           f"min {min(times[v]):.3f} max {max(times[v]):.3f}")
-print("labels equal:", bool(torch.equal(labels[2], labels[3])))
+print("labels equal:", all(bool(torch.equal(labels["v2"], labels[v[0]])) for v in VARIANTS))
