@@ -71,6 +71,14 @@ int csc_laplacian_build(int64_t n, int64_t m, const int64_t *lo_dev, const int64
 int csc_edge_delta(int64_t n, const int64_t *prev_dev, int64_t m_prev, const int64_t *del_dev,
                    int64_t n_del, const int64_t *ins_dev, int64_t n_ins, int64_t *new_dev,
                    int64_t capacity, int64_t *m_new_out, void *stream);
+/* Graph canonicalisation (graphs.py:29-54) on device: codes_out = stable
+ * ascending sort of min(i,j)*n + max(i,j) (numpy argsort kind="stable"),
+ * w_out = weights in that order. flags_host[0..3] = endpoint out of range,
+ * self-loop, weight <= 0, duplicate (the sort is skipped if any of the first
+ * three is set; the caller raises in that order). SYNCHRONISES. */
+int csc_graph_canonicalize(int64_t n, int64_t m, const int64_t *ei_dev, const int64_t *ej_dev,
+                           const double *w_dev, int64_t *codes_out_dev, double *w_out_dev,
+                           int32_t *flags_host, void *stream);
 /* lo = code / n, hi = code % n */
 int csc_codes_split(int64_t n, const int64_t *codes_dev, int64_t m, int64_t *lo_dev,
                     int64_t *hi_dev, void *stream);

@@ -30,6 +30,7 @@ SIGNATURES = {
     "csc_device_info": ([ctypes.POINTER(_INT)] * 3, _INT),
     "csc_laplacian_build": ([_I64, _I64, _P, _P, _P, _INT, _P, _P, _P, _I64, _P, _PI64, _PD, _P], _INT),
     "csc_edge_delta": ([_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _PI64, _P], _INT),
+    "csc_graph_canonicalize": ([_I64, _I64, _P, _P, _P, _P, _P, _P, _P], _INT),
     "csc_codes_split": ([_I64, _P, _I64, _P, _P, _P], _INT),
     "csc_chebop_create": ([_P, _P, _P, _I64, _I64, _D, _INT, _P, ctypes.POINTER(_P)], _INT),
     "csc_chebop_destroy": ([_P], _INT),

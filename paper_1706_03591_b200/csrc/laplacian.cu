@@ -158,6 +158,40 @@ __global__ void iota_kernel(int32_t *__restrict__ a, int64_t m) {
     a[e] = (int32_t)e;
 }
 
+// --- Graph canonicalisation (graphs.py:29-54) -------------------------------
+// flags: [0] endpoint out of range, [1] self-loop, [2] weight <= 0, [3] duplicate
+__global__ void canon_codes_kernel(int64_t n, int64_t m, const int64_t *__restrict__ ei,
+                                   const int64_t *__restrict__ ej, const double *__restrict__ w,
+                                   int64_t *__restrict__ codes, int64_t *__restrict__ iota,
+                                   unsigned int *__restrict__ flags) {
+  unsigned int f0 = 0, f1 = 0, f2 = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = ei[e], b = ej[e];
+    f0 |= (a < 0 || b < 0 || a >= n || b >= n);
+    f1 |= (a == b);
+    f2 |= !(w[e] > 0.0);
+    const int64_t lo = a < b ? a : b, hi = a < b ? b : a;
+    codes[e] = lo * n + hi;
+    iota[e] = e;
+  }
+  if (f0) atomicOr(flags + 0, 1u);
+  if (f1) atomicOr(flags + 1, 1u);
+  if (f2) atomicOr(flags + 2, 1u);
+}
+
+__global__ void canon_finish_kernel(int64_t m, const int64_t *__restrict__ sorted,
+                                    const int64_t *__restrict__ perm, const double *__restrict__ w,
+                                    double *__restrict__ w_out, unsigned int *__restrict__ flags) {
+  unsigned int dup = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e > 0 && sorted[e] == sorted[e - 1]) dup = 1;
+    w_out[e] = w[perm[e]];
+  }
+  if (dup) atomicOr(flags + 3, 1u);
+}
+
 int grid_for(int64_t work, int threads = 256) {
   return (int)std::min<int64_t>(csc::device_info().sm_count * 16,
                                 std::max<int64_t>(1, csc::ceil_div(work, threads)));
@@ -323,6 +357,52 @@ int csc_edge_delta(int64_t n, const int64_t *prev, int64_t m_prev, const int64_t
     return CSC_ERR_ARG;
   }
   *m_new_out = m_new;
+  return CSC_OK;
+}
+
+int csc_graph_canonicalize(int64_t n, int64_t m, const int64_t *ei, const int64_t *ej,
+                           const double *w, int64_t *codes_out, double *w_out, int32_t *flags_host,
+                           void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(n >= 0 && m >= 0 && flags_host != nullptr, "csc_graph_canonicalize: bad arguments");
+  CSC_REQUIRE(n < (int64_t)3037000499, "csc_graph_canonicalize: n*n overflows int64 codes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  csc::device_info();
+  for (int i = 0; i < 4; ++i) flags_host[i] = 0;
+  if (m == 0) return CSC_OK;
+  csc::Scratch codes, iota, perm, flags, tmp;
+  CSC_TRY_CUDA(codes.alloc(sizeof(int64_t) * m, st));
+  CSC_TRY_CUDA(iota.alloc(sizeof(int64_t) * m, st));
+  CSC_TRY_CUDA(perm.alloc(sizeof(int64_t) * m, st));
+  CSC_TRY_CUDA(flags.alloc(sizeof(unsigned int) * 4, st));
+  CSC_TRY_CUDA(cudaMemsetAsync(flags.ptr, 0, sizeof(unsigned int) * 4, st));
+  canon_codes_kernel<<<grid_for(m), 256, 0, st>>>(n, m, ei, ej, w, codes.as<int64_t>(),
+                                                  iota.as<int64_t>(), flags.as<unsigned int>());
+  CSC_CHECK_LAUNCH();
+  unsigned int h[4];
+  CSC_TRY_CUDA(cudaMemcpyAsync(h, flags.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CSC_TRY_CUDA(cudaStreamSynchronize(st));
+  flags_host[0] = h[0];
+  flags_host[1] = h[1];
+  flags_host[2] = h[2];
+  if (h[0] || h[1] || h[2]) return CSC_OK;  // caller raises in the reference's order
+  // stable LSD radix sort of the codes (numpy argsort kind="stable")
+  int bits = 1;
+  const unsigned long long maxcode = (unsigned long long)n * (unsigned long long)n;
+  while (bits < 63 && (1ull << bits) < maxcode) ++bits;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, codes.as<int64_t>(), codes_out, iota.as<int64_t>(),
+                                  perm.as<int64_t>(), m, 0, bits, st);
+  CSC_TRY_CUDA(tmp.alloc(tb, st));
+  CSC_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, codes.as<int64_t>(), codes_out,
+                                               iota.as<int64_t>(), perm.as<int64_t>(), m, 0, bits,
+                                               st));
+  canon_finish_kernel<<<grid_for(m), 256, 0, st>>>(m, codes_out, perm.as<int64_t>(), w, w_out,
+                                                   flags.as<unsigned int>());
+  CSC_CHECK_LAUNCH();
+  CSC_TRY_CUDA(cudaMemcpyAsync(h, flags.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CSC_TRY_CUDA(cudaStreamSynchronize(st));
+  flags_host[3] = h[3];
   return CSC_OK;
 }
 

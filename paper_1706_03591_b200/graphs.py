@@ -25,6 +25,8 @@ from . import _native
 from ._device import dtype_code, ptr, require_cuda, stream
 
 LAPLACIAN_VARIANTS = ("combinatorial", "normalized")
+# graphs at least this large are canonicalised on the GPU when one is present
+DEVICE_CANON_MIN_EDGES = 1 << 16
 
 
 class Graph:
@@ -44,6 +46,9 @@ class Graph:
         w = np.asarray(edge_w, dtype=np.float64).ravel()
         if not (i.shape == j.shape == w.shape):
             raise ValueError("edge arrays must have equal length")
+        if i.size >= DEVICE_CANON_MIN_EDGES and torch.cuda.is_available():
+            self._canonicalize_on_device(int(n), i, j, w)
+            return
         if i.size:
             if i.min() < 0 or j.min() < 0 or max(i.max(), j.max()) >= n:
                 raise ValueError("edge endpoint out of range [0, n)")
@@ -60,6 +65,26 @@ class Graph:
                 raise ValueError("duplicate edges (after canonicalizing endpoint order)")
             i, j, w = lo[order], hi[order], w[order]
         self._init(int(n), i, j, w, None, int(i.size))
+
+    def _canonicalize_on_device(self, n, i, j, w):
+        """K9 on the GPU: validation flags, stable radix sort of the codes, duplicate check."""
+        dev = require_cuda()
+        m = i.size
+        ti, tj, tw = (torch.from_numpy(a).to(dev) for a in (i, j, w))
+        codes = torch.empty(m, dtype=torch.int64, device=dev)
+        w_sorted = torch.empty(m, dtype=torch.float64, device=dev)
+        flags = np.zeros(4, dtype=np.int32)
+        _native.call("csc_graph_canonicalize", n, m, ptr(ti), ptr(tj), ptr(tw), ptr(codes), ptr(w_sorted),
+                     flags.ctypes.data, stream())
+        for flag, msg in zip(flags, ("edge endpoint out of range [0, n)", "self-loops are not allowed",
+                                     "edge weights must be positive",
+                                     "duplicate edges (after canonicalizing endpoint order)")):
+            if flag:
+                raise ValueError(msg)
+        self._init(n, None, None, None, codes, m)
+        unit = bool(np.all(w == 1.0))
+        object.__setattr__(self, "_unit", unit)
+        object.__setattr__(self, "_w_dev", None if unit else w_sorted)
 
     def _init(self, n, i, j, w, codes_dev, m):
         object.__setattr__(self, "n", n)
@@ -81,7 +106,8 @@ class Graph:
             codes = self._codes_dev.cpu().numpy()
             object.__setattr__(self, "_i", codes // self.n)
             object.__setattr__(self, "_j", codes % self.n)
-            object.__setattr__(self, "_w", np.ones(codes.size))
+            wd = getattr(self, "_w_dev", None)
+            object.__setattr__(self, "_w", wd.cpu().numpy() if wd is not None else np.ones(codes.size))
         return self._i, self._j, self._w
 
     @property
@@ -156,7 +182,13 @@ class Graph:
                 lo = torch.empty_like(codes)
                 hi = torch.empty_like(codes)
                 _native.call("csc_codes_split", self.n, ptr(codes), self.m, ptr(lo), ptr(hi), stream())
-            w = None if self.unit_weights() else torch.from_numpy(self._w).to(dev)
+            wd = getattr(self, "_w_dev", None)
+            if self.unit_weights():
+                w = None
+            elif wd is not None:
+                w = wd
+            else:
+                w = torch.from_numpy(self._host()[2]).to(dev)
             object.__setattr__(self, "_dev_edges", (lo, hi, w))
         return self._dev_edges
 

@@ -588,3 +588,40 @@ def test_graph_lloyd_equals_host_driven(P):
     assert np.array_equal(labels, best[1])
     assert cost2 == best[0]
     assert np.array_equal(labels, g["b_labels"])
+
+
+def test_graph_device_canonicalisation(P):
+    """K9 on device (graphs.py:29-54): same canonical order, weights and errors as the reference."""
+    from paper_1706_03591_b200.graphs import DEVICE_CANON_MIN_EDGES
+    rng = np.random.default_rng(11)
+    n = 50000
+    m = DEVICE_CANON_MIN_EDGES * 3
+    a = rng.integers(0, n, m)
+    b = rng.integers(0, n, m)
+    ok = a != b
+    code = np.unique(np.minimum(a, b)[ok] * n + np.maximum(a, b)[ok])
+    lo, hi = code // n, code % n
+    flip = rng.random(code.size) < 0.5
+    ii, jj = np.where(flip, hi, lo), np.where(flip, lo, hi)
+    perm = rng.permutation(code.size)
+    ii, jj = ii[perm], jj[perm]
+    w = rng.uniform(0.1, 2.0, code.size)
+    g = P.Graph(n, ii, jj, w)
+    assert g._i is None  # built on the device
+    clo, chi, cw = O.canonical_edges(n, ii, jj, w)
+    assert g.m == code.size
+    assert np.array_equal(g.edge_i, clo) and np.array_equal(g.edge_j, chi) and np.array_equal(g.edge_w, cw)
+    lap = P.laplacian(g)
+    ip, ix, dv, _ = O.laplacian_csr(n, clo, chi, cw)
+    assert np.array_equal(lap.matrix.indptr, ip) and np.array_equal(lap.matrix.data, dv)
+    unit = P.Graph(n, ii, jj, np.ones(code.size))
+    assert unit.unit_weights() and np.array_equal(unit.edge_codes(), code)
+    bad_cases = [
+        (np.r_[ii, n], np.r_[jj, 0], np.r_[w, 1.0], "out of range"),
+        (np.r_[ii, 5], np.r_[jj, 5], np.r_[w, 1.0], "self-loops"),
+        (ii, jj, np.r_[w[:-1], 0.0], "positive"),
+        (np.r_[ii, jj[0]], np.r_[jj, ii[0]], np.r_[w, 1.0], "duplicate"),
+    ]
+    for bi, bj, bw, msg in bad_cases:
+        with pytest.raises(ValueError, match=msg):
+            P.Graph(n, bi, bj, bw)
