@@ -503,12 +503,15 @@ __device__ __forceinline__ double m_diag(double s, double lii) {
   return __dsub_rn(1.0, __dmul_rn(s, lii));
 }
 
+constexpr int kWarpRow = 32;  // rows with more stored entries are built by a warp
+
 __global__ void op_count_kernel(const int32_t *__restrict__ indptr,
                                 const int32_t *__restrict__ indices,
                                 const double *__restrict__ vals, int64_t n, double s,
                                 int32_t *__restrict__ counts) {
   for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < n;
        row += (int64_t)gridDim.x * blockDim.x) {
+    if (indptr[row + 1] - indptr[row] > kWarpRow) continue;
     int cnt = 0;
     double lii = 0.0;
     for (int jj = indptr[row]; jj < indptr[row + 1]; ++jj) {
@@ -531,6 +534,7 @@ __global__ void op_fill_kernel(const int32_t *__restrict__ indptr,
                                T *__restrict__ mval) {
   for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < n;
        row += (int64_t)gridDim.x * blockDim.x) {
+    if (indptr[row + 1] - indptr[row] > kWarpRow) continue;
     double lii = 0.0;
     for (int jj = indptr[row]; jj < indptr[row + 1]; ++jj)
       if (indices[jj] == row) lii = vals[jj];
@@ -554,6 +558,102 @@ __global__ void op_fill_kernel(const int32_t *__restrict__ indptr,
       }
     }
     if (!placed) {
+      mcol[pos] = (int32_t)row;
+      mval[pos] = (T)dii;
+    }
+  }
+}
+
+// Warp-per-row count/fill for rows with more than kWarpRow entries: the same
+// entries as the thread kernels (exact zeros dropped, the diagonal placed
+// before the first column > row), compacted with ballots in column order.
+__device__ __forceinline__ double warp_row_diag(const int32_t *indices, const double *vals,
+                                                int beg, int end, int64_t row, int lane) {
+  double lii = 0.0;
+  for (int jj = beg + lane; jj < end; jj += 32)
+    if (indices[jj] == row) lii = vals[jj];
+  // at most one lane holds it; the others contribute 0
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double other = __shfl_xor_sync(0xffffffffu, lii, o);
+    if (other != 0.0) lii = other;
+  }
+  return lii;
+}
+
+__global__ void op_count_warp_kernel(const int32_t *__restrict__ indptr,
+                                     const int32_t *__restrict__ indices,
+                                     const double *__restrict__ vals, int64_t n, double s,
+                                     int32_t *__restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; row < n;
+       row += warps) {
+    const int beg = indptr[row], end = indptr[row + 1];
+    if (end - beg <= kWarpRow) continue;
+    const double lii = warp_row_diag(indices, vals, beg, end, row, lane);
+    int cnt = 0;
+    for (int base = beg; base < end; base += 32) {
+      const int jj = base + lane;
+      const bool keep = jj < end && indices[jj] != row && m_offdiag(s, vals[jj]) != 0.0;
+      cnt += __popc(__ballot_sync(0xffffffffu, keep));
+    }
+    if (lane == 0) counts[row] = cnt + (m_diag(s, lii) != 0.0 ? 1 : 0);
+  }
+}
+
+template <typename T>
+__global__ void op_fill_warp_kernel(const int32_t *__restrict__ indptr,
+                                    const int32_t *__restrict__ indices,
+                                    const double *__restrict__ vals, int64_t n, double s,
+                                    const int32_t *__restrict__ mptr, int32_t *__restrict__ mcol,
+                                    T *__restrict__ mval) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; row < n;
+       row += warps) {
+    const int beg = indptr[row], end = indptr[row + 1];
+    if (end - beg <= kWarpRow) continue;
+    const double dii = m_diag(s, warp_row_diag(indices, vals, beg, end, row, lane));
+    int pos = mptr[row];
+    bool placed = (dii == 0.0);
+    for (int base = beg; base < end; base += 32) {
+      const int jj = base + lane;
+      const bool valid = jj < end;
+      const int c = valid ? indices[jj] : INT32_MAX;
+      const double v = valid ? m_offdiag(s, vals[jj]) : 0.0;
+      const bool keep = valid && c != row && v != 0.0;
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      int shift = 0;
+      if (!placed) {
+        const unsigned after = __ballot_sync(0xffffffffu, valid && c > row);
+        if (after) {
+          const int ins = __ffs(after) - 1;  // first lane with column > row
+          if (lane == 0) {
+            const int p = pos + __popc(km & ((1u << ins) - 1u));
+            mcol[p] = (int32_t)row;
+            mval[p] = (T)dii;
+          }
+          shift = lane >= ins ? 1 : 0;
+          placed = true;
+          if (keep) {
+            const int p = pos + __popc(km & lt) + shift;
+            mcol[p] = c;
+            mval[p] = (T)v;
+          }
+          pos += __popc(km) + 1;
+          continue;
+        }
+      }
+      if (keep) {
+        const int p = pos + __popc(km & lt);
+        mcol[p] = c;
+        mval[p] = (T)v;
+      }
+      pos += __popc(km);
+    }
+    if (!placed && lane == 0) {
       mcol[pos] = (int32_t)row;
       mval[pos] = (T)dii;
     }
@@ -1024,8 +1124,12 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
   }
   if (counts.alloc(sizeof(int32_t) * (n + 1), st) != cudaSuccess) return fail(CSC_ERR_CUDA);
   cudaMemsetAsync(counts.ptr, 0, sizeof(int32_t) * (n + 1), st);
-  if (n > 0) op_count_kernel<<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale,
-                                                        counts.as<int32_t>());
+  if (n > 0) {
+    op_count_kernel<<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale,
+                                              counts.as<int32_t>());
+    op_count_warp_kernel<<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale,
+                                                   counts.as<int32_t>());
+  }
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts.as<int32_t>(), op->indptr, n + 1, st);
   if (scan_tmp.alloc(tmp_bytes, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
@@ -1046,13 +1150,18 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
     return fail(CSC_ERR_CUDA);
   }
   if (n > 0) {
-    if (dtype == CSC_F64)
+    if (dtype == CSC_F64) {
       op_fill_kernel<double><<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale, op->indptr,
                                                        op->indices,
                                                        static_cast<double *>(op->vals));
-    else
+      op_fill_warp_kernel<double><<<grid, threads, 0, st>>>(
+          indptr, indices, vals, n, scale, op->indptr, op->indices, static_cast<double *>(op->vals));
+    } else {
       op_fill_kernel<float><<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale, op->indptr,
                                                       op->indices, static_cast<float *>(op->vals));
+      op_fill_warp_kernel<float><<<grid, threads, 0, st>>>(
+          indptr, indices, vals, n, scale, op->indptr, op->indices, static_cast<float *>(op->vals));
+    }
   }
   // long-row schedule
   csc::Scratch nsel, sel_tmp, segcnt;

@@ -68,35 +68,55 @@ __device__ __forceinline__ double off_value(int variant, double inv_i, double w,
   return -w;
 }
 
-__global__ void fill_kernel(int64_t n, const int64_t *__restrict__ lo,
-                            const int64_t *__restrict__ hi, const double *__restrict__ w,
-                            const int32_t *__restrict__ lo_ptr, const int32_t *__restrict__ hi_ptr,
-                            const int32_t *__restrict__ perm, const double *__restrict__ deg,
-                            const double *__restrict__ inv, int variant,
-                            const int32_t *__restrict__ indptr, int32_t *__restrict__ indices,
-                            double *__restrict__ vals) {
+// Entry-parallel fill (same values and positions as fill_kernel): the row of
+// an entry and its slot are known without walking the row, so hub rows of
+// skewed graphs do not serialise.
+__global__ void fill_upper_kernel(int64_t m, const int64_t *__restrict__ lo,
+                                  const int64_t *__restrict__ hi, const double *__restrict__ w,
+                                  const int32_t *__restrict__ lo_ptr,
+                                  const int32_t *__restrict__ hi_ptr,
+                                  const double *__restrict__ deg, const double *__restrict__ inv,
+                                  int variant, const int32_t *__restrict__ indptr,
+                                  int32_t *__restrict__ indices, double *__restrict__ vals) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = lo[e], j = hi[e];
+    const double dg = deg[i];
+    const int diag = (variant == CSC_LAP_NORMALIZED ? dg > 0.0 : dg != 0.0) ? 1 : 0;
+    const int64_t pos = indptr[i] + (hi_ptr[i + 1] - hi_ptr[i]) + diag + (e - lo_ptr[i]);
+    indices[pos] = (int32_t)j;
+    vals[pos] = off_value(variant, inv[i], w ? w[e] : 1.0, inv[j]);
+  }
+}
+
+__global__ void fill_lower_kernel(int64_t m, const int64_t *__restrict__ lo,
+                                  const int64_t *__restrict__ hi, const double *__restrict__ w,
+                                  const int32_t *__restrict__ hi_ptr,
+                                  const int32_t *__restrict__ perm,
+                                  const double *__restrict__ inv, int variant,
+                                  const int32_t *__restrict__ indptr,
+                                  int32_t *__restrict__ indices, double *__restrict__ vals) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t e = perm[t];
+    const int64_t i = hi[e], j = lo[e];
+    const int64_t pos = indptr[i] + (t - hi_ptr[i]);
+    indices[pos] = (int32_t)j;
+    vals[pos] = off_value(variant, inv[i], w ? w[e] : 1.0, inv[j]);
+  }
+}
+
+__global__ void fill_diag_kernel(int64_t n, const int32_t *__restrict__ hi_ptr,
+                                 const double *__restrict__ deg, int variant,
+                                 const int32_t *__restrict__ indptr, int32_t *__restrict__ indices,
+                                 double *__restrict__ vals) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t pos = indptr[i];
-    const double inv_i = inv[i];
-    for (int32_t t = hi_ptr[i]; t < hi_ptr[i + 1]; ++t) {  // lower neighbours, ascending
-      const int32_t e = perm[t];
-      const int64_t j = lo[e];
-      indices[pos] = (int32_t)j;
-      vals[pos] = off_value(variant, inv_i, w ? w[e] : 1.0, inv[j]);
-      ++pos;
-    }
     const double dg = deg[i];
     if (variant == CSC_LAP_NORMALIZED ? dg > 0.0 : dg != 0.0) {
+      const int64_t pos = indptr[i] + (hi_ptr[i + 1] - hi_ptr[i]);
       indices[pos] = (int32_t)i;
       vals[pos] = variant == CSC_LAP_NORMALIZED ? 1.0 : dg;
-      ++pos;
-    }
-    for (int32_t e = lo_ptr[i]; e < lo_ptr[i + 1]; ++e) {  // upper neighbours, ascending
-      const int64_t j = hi[e];
-      indices[pos] = (int32_t)j;
-      vals[pos] = off_value(variant, inv_i, w ? w[e] : 1.0, inv[j]);
-      ++pos;
     }
   }
 }
@@ -275,10 +295,19 @@ int csc_laplacian_build(int64_t n, int64_t m, const int64_t *lo, const int64_t *
   tb = tbytes;
   CSC_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tb, rowcnt.as<int32_t>(), indptr, n1, st));
   if (n > 0) {
-    fill_kernel<<<grid_for(n), 256, 0, st>>>(n, lo, hi, w, lo_ptr.as<int32_t>(),
-                                             hi_ptr.as<int32_t>(), perm.as<int32_t>(),
-                                             deg.as<double>(), inv.as<double>(), variant, indptr,
-                                             indices, vals);
+    if (m > 0) {
+      fill_upper_kernel<<<grid_for(m), 256, 0, st>>>(m, lo, hi, w, lo_ptr.as<int32_t>(),
+                                                     hi_ptr.as<int32_t>(), deg.as<double>(),
+                                                     inv.as<double>(), variant, indptr, indices,
+                                                     vals);
+      CSC_CHECK_LAUNCH();
+      fill_lower_kernel<<<grid_for(m), 256, 0, st>>>(m, lo, hi, w, hi_ptr.as<int32_t>(),
+                                                     perm.as<int32_t>(), inv.as<double>(),
+                                                     variant, indptr, indices, vals);
+      CSC_CHECK_LAUNCH();
+    }
+    fill_diag_kernel<<<grid_for(n), 256, 0, st>>>(n, hi_ptr.as<int32_t>(), deg.as<double>(),
+                                                  variant, indptr, indices, vals);
     CSC_CHECK_LAUNCH();
     tb = tbytes;
     CSC_TRY_CUDA(cub::DeviceReduce::Max(tmp.ptr, tb, deg.as<double>(), dmax.as<double>(), n, st));

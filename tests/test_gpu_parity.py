@@ -625,3 +625,31 @@ def test_graph_device_canonicalisation(P):
     for bi, bj, bw, msg in bad_cases:
         with pytest.raises(ValueError, match=msg):
             P.Graph(n, bi, bj, bw)
+
+
+@pytest.mark.parametrize("variant", ["normalized", "combinatorial"])
+def test_operator_plan_long_rows_bitwise(P, variant):
+    """Warp-built rows of M (> 32 entries) == the CPU restatement, bit for bit."""
+    from paper_1706_03591_b200.graphs import export_plan
+    rng = np.random.default_rng(21)
+    n = 3000
+    i = np.r_[np.zeros(2000, np.int64), np.full(700, 1500), rng.integers(0, n, 6000)]
+    j = np.r_[rng.permutation(np.arange(1, n))[:2000], rng.permutation(np.arange(n))[:700],
+              rng.integers(0, n, 6000)]
+    ok = i != j
+    code = np.unique(np.minimum(i, j)[ok] * n + np.maximum(i, j)[ok])
+    w = rng.uniform(0.5, 2.0, code.size)
+    g = P.Graph(n, code // n, code % n, w)
+    lap = P.laplacian(g, variant)
+    s = 2.0 / lap.lambda_max_bound
+    ip, ix, vv, _, _ = export_plan(lap.plan(s))
+    exp = _expected_M(lap.matrix, s)
+    assert np.diff(lap.matrix.indptr).max() > 600
+    assert np.array_equal(ip, exp.indptr)
+    assert np.array_equal(ix, exp.indices)
+    assert np.array_equal(vv, exp.data)
+    x = rng.normal(size=(n, 6))
+    poly = P.cheb_coeffs(0.3 * lap.lambda_max_bound, lap.lambda_max_bound, 15)
+    m = lap.matrix
+    ref = ON.cheb_filter(m.indptr, m.indices, m.data, lap.lambda_max_bound, poly.coeffs, x)
+    assert rel(P.apply_filter(lap, poly, x), ref) <= FEAT_TOL
