@@ -223,6 +223,7 @@ def main():
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dynamic", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.workload]
@@ -330,6 +331,34 @@ def main():
                "d2h_bytes_per_step": int(res.nbytes), "ms_per_step": e2e_s * 1e3,
                "api": "paper_1706_03591_b200.apply_filter(L, poly, numpy pinned) -> numpy"}
 
+    # fp32 variant of the same workload (reported separately; error in DESIGN.md)
+    variants = {}
+    if dtype == torch.float64 and not args.no_variants:
+        blk32 = blk.to(torch.float32)
+        ld32 = row_stride(d, torch.float32)
+        if ld32 != blk32.shape[1]:
+            b2 = torch.zeros((n, ld32), dtype=torch.float32, device=dev)
+            b2[:, :d] = blk32[:, :d]
+            blk32 = b2
+        out32 = torch.empty_like(blk32)
+        work32 = torch.empty((2 * n, blk32.shape[1]), dtype=torch.float32, device=dev)
+        lap.plan(1.0, torch.float32)
+        filter_block(lap, poly, blk32, d, out=out32, work=work32)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(2):
+            filter_block(lap, poly, blk32, d, out=out32, work=work32)
+        e1.record()
+        torch.cuda.synchronize()
+        ms32 = e0.elapsed_time(e1) / 2
+        b32 = 4 * (n + 1) + nnz_L * 8 + nnz_L * d * 4 + n * d * 4
+        variants["fp32"] = {"value": units * world / (ms32 / 1e3), "ms_per_step": ms32,
+                            "roofline_frac": b32 / (ms32 / order / 1e3) / 1e9 / hbm,
+                            "rel_frobenius_vs_fp64": float((out[:, :d] - out32[:, :d].double()).norm()
+                                                           / out[:, :d].norm())}
+        del blk32, out32, work32
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         m = lap.matrix
@@ -356,6 +385,8 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps), "clocks": clk.summary(),
         }
+        if variants:
+            line["variants"] = variants
         if dyn is not None:
             line["dynamic"] = dyn
         print(json.dumps(line), flush=True)
