@@ -653,3 +653,36 @@ def test_operator_plan_long_rows_bitwise(P, variant):
     m = lap.matrix
     ref = ON.cheb_filter(m.indptr, m.indices, m.data, lap.lambda_max_bound, poly.coeffs, x)
     assert rel(P.apply_filter(lap, poly, x), ref) <= FEAT_TOL
+
+
+def test_dynamic_cfg2_golden(P):
+    """BASELINE configs[1] (n=20k, k=20, d=80, p=0.5, m=60): init + 2 steps vs the live reference.
+
+    The graph sequence is rebuilt with on-device edge deltas (the reference's
+    perturbed_sequence, stored as delete/insert code lists).
+    """
+    g = golden("cfg2")
+    g0 = graph_from(g, "g0", P)
+    graphs = [g0]
+    for t in (1, 2):
+        graphs.append(graphs[-1].apply_delta(g[f"del{t}"], g[f"ins{t}"]))
+    cfg = P.DynamicConfig(k=20, d=80, p=0.5, filter=P.FilterConfig(order=60))
+    a, state, diag = P.dynamic_init(graphs[0], cfg, seed=0)
+    results = [(a, state, diag)]
+    for gt in graphs[1:]:
+        a, state, diag = P.dynamic_step(state, gt, cfg)
+        results.append((a, state, diag))
+    rows = g["rows"]
+    for t, (a, st, dg) in enumerate(results):
+        assert dg.lambda_k == float(g[f"s{t}_lambda"])
+        assert dg.search_iters == int(g[f"s{t}_iters"]) and dg.refined == bool(g[f"s{t}_refined"])
+        assert dg.matvecs_total == int(g[f"s{t}_mv_total"])
+        assert np.array_equal(st.features.step_tags, g[f"s{t}_step_tags"])
+        assert np.array_equal(st.features.stream_tags, g[f"s{t}_stream_tags"])
+        v = st.features.values
+        assert rel((v ** 2).sum(axis=0), g[f"s{t}_colnorm2"]) <= FEAT_TOL
+        assert rel(v[rows], g[f"s{t}_rowsample"]) <= FEAT_TOL
+        ari = O.adjusted_rand(a.labels, g[f"s{t}_labels"].astype(np.int64))
+        print(f"cfg2 step {t}: ARI {ari:.6f} cost {a.feature_cost:.12f} ref {float(g[f's{t}_cost']):.12f}")
+        assert ari >= 0.999
+        assert abs(a.feature_cost - float(g[f"s{t}_cost"])) <= 1e-9 * float(g[f"s{t}_cost"])
