@@ -516,7 +516,11 @@ int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  const int grid = std::max(1, csc::device_info().sm_count * 2);
+  // persistent grid sized to the work (>= 4 row tiles per block), so that small
+  // problems leave SMs free for the concurrently running restarts
+  const int64_t tiles = csc::ceil_div(n, (int64_t)BM);
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(csc::device_info().sm_count * 2, csc::ceil_div(tiles, 4)));
   for (int64_t c0 = 0; c0 < k; c0 += BN) {
     const int last = c0 + BN >= k;
     if (three)
@@ -858,11 +862,13 @@ __global__ void __launch_bounds__(1024)
 
 // closest[r][i] = (first ? d2 : min(closest, d2)), d2 = |f_i - crow_r|^2, for r < R;
 // chunk_sums[r][b] = sum of closest[r] over contiguous chunk b (block b).
-__global__ void kppb_dist_kernel(const double *__restrict__ f, int64_t n, int64_t d, int64_t ld,
-                                 const double *__restrict__ crows, int64_t crow_stride, int R,
-                                 double *__restrict__ closest, int first, int64_t chunk,
-                                 double *__restrict__ chunk_sums, int64_t nchunks) {
-  extern __shared__ double sh[];  // R x d centroid rows, then 8 x R block partials
+__global__ void __launch_bounds__(128)
+    kppb_dist_kernel(const double *__restrict__ f, int64_t n, int64_t d, int64_t ld,
+                     const double *__restrict__ crows, int64_t crow_stride, int R,
+                     double *__restrict__ closest, int first, int64_t chunk,
+                     double *__restrict__ chunk_sums, int64_t nchunks) {
+  // thread per row: one pass over the row serves all R restarts (no shuffles)
+  extern __shared__ double sh[];  // R x d centroid rows, then 4 warps x R partials
   double *cs = sh;
   double *wsum = sh + (size_t)R * d;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -875,13 +881,13 @@ __global__ void kppb_dist_kernel(const double *__restrict__ f, int64_t n, int64_
   double part[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) part[r] = 0.0;
-  for (int64_t i = rbeg + wid; i < rend; i += blockDim.x / 32) {
+  for (int64_t i = rbeg + threadIdx.x; i < rend; i += blockDim.x) {
     const double *row = f + i * ld;
     double acc[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) acc[r] = 0.0;
-    for (int64_t c = lane; c < d; c += 32) {
-      const double x = row[c];
+    for (int64_t c = 0; c < d; ++c) {
+      const double x = __ldg(row + c);
 #pragma unroll
       for (int r = 0; r < 16; ++r)
         if (r < R) {
@@ -890,24 +896,24 @@ __global__ void kppb_dist_kernel(const double *__restrict__ f, int64_t n, int64_
         }
     }
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
+    for (int r = 0; r < 16; ++r)
       if (r < R) {
-        double v = acc[r];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == r) {
-          double* slot = closest + (int64_t)r * n + i;
-          const double cl = first ? v : fmin(*slot, v);
-          *slot = cl;
-          part[r] += cl;
-        }
+        double *slot = closest + (int64_t)r * n + i;
+        const double cl = first ? acc[r] : fmin(*slot, acc[r]);
+        *slot = cl;
+        part[r] += cl;
       }
+  }
+  // fixed-order block sums per restart: warp shuffle tree, then warps in order
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    if (r < R) {
+      double v = part[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) wsum[wid * R + r] = v;
     }
   }
-  // per-warp partial of restart r lives in lane r; fixed-order block sum
-#pragma unroll
-  for (int r = 0; r < 16; ++r)
-    if (r < R && lane == r) wsum[wid * R + r] = part[r];
   __syncthreads();
   if (threadIdx.x < R) {
     double t = 0.0;
@@ -1018,7 +1024,10 @@ __global__ void bound_kernel(int64_t n, const int32_t *__restrict__ labels,
                              double *__restrict__ ub, double *__restrict__ lb,
                              const double *__restrict__ delta, const double *__restrict__ scal,
                              const double *__restrict__ shalf, const double *__restrict__ fnorm,
-                             int32_t *__restrict__ cand, int32_t *__restrict__ flags) {
+                             int32_t *__restrict__ cand, int32_t *__restrict__ flags,
+                             int32_t *__restrict__ counts, int64_t k) {
+  if (blockIdx.x == 0)  // cleared here (stream-ordered before label_hist_kernel)
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) counts[j] = 0;
   const bool force = flags[2] != 0;
   const double d1 = scal[1], d2 = scal[2], cmax = scal[4];
   const int j1 = (int)scal[3];
@@ -1155,12 +1164,93 @@ __global__ void centroid_finish_kernel(const double *__restrict__ S,
   }
 }
 
+// Single-block tail of an iteration for small k: the means, movements,
+// cost terms, scalars and half-separations of centroid_finish + iter_finish +
+// shalf in one graph node (after the multi-block sums_finish_kernel). Also
+// clears the candidate counter for the next pruned iteration.
+__global__ void __launch_bounds__(1024)
+    finish_small_kernel(int64_t d, int64_t k, const double *__restrict__ S,
+                        const int32_t *__restrict__ counts, const double *__restrict__ Q,
+                        double *__restrict__ cent, int64_t ldc, double *__restrict__ cnorm,
+                        double *__restrict__ delta, double *__restrict__ cterm,
+                        double *__restrict__ scal, double *__restrict__ shalf,
+                        int32_t *__restrict__ flags) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // B: warp per centroid: means, movement, |c|^2, cost term
+  for (int64_t j = wid; j < k; j += nw) {
+    const int32_t cnt = counts[j];
+    const double denom = (double)(cnt > 1 ? cnt : 1);
+    double mv = 0.0, nrm = 0.0, dot = 0.0;
+    for (int64_t c = lane; c < d; c += 32) {
+      const double sjc = S[j * d + c];
+      const double mean = __ddiv_rn(sjc, denom);
+      const double old = cent[j * ldc + c];
+      cent[j * ldc + c] = mean;
+      mv = fma(mean - old, mean - old, mv);
+      nrm = fma(mean, mean, nrm);
+      dot = fma(mean, sjc, dot);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mv += __shfl_xor_sync(0xffffffffu, mv, o);
+      nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+      dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    }
+    if (lane == 0) {
+      delta[j] = sqrt(mv);
+      cnorm[j] = nrm;
+      cterm[j] = cnt > 0 ? (Q[j] - 2.0 * dot) + (double)cnt * nrm : 0.0;
+    }
+  }
+  __syncthreads();
+  // C: scalars (thread 0), D: half-separations (warp per centroid)
+  if (threadIdx.x == 0) {
+    double cost = 0.0, d1 = 0.0, d2 = 0.0, cm = 0.0;
+    int64_t j1 = 0;
+    for (int64_t j = 0; j < k; ++j) {
+      cost += cterm[j];
+      const double dj = delta[j];
+      if (dj > d1) {
+        d2 = d1;
+        d1 = dj;
+        j1 = j;
+      } else if (dj > d2) {
+        d2 = dj;
+      }
+      cm = fmax(cm, cnorm[j]);
+    }
+    scal[0] = cost > 0.0 ? cost : 0.0;
+    scal[1] = d1;
+    scal[2] = d2;
+    scal[3] = (double)j1;
+    scal[4] = sqrt(cm);
+    flags[0] = 0;  // candidate counter of the next pruned iteration
+  }
+  for (int64_t j = wid; j < k; j += nw) {
+    double best = INFINITY;
+    for (int64_t o = lane; o < k; o += 32) {
+      if (o == j) continue;
+      double sacc = 0.0;
+      for (int64_t c = 0; c < d; ++c) {
+        const double t = cent[j * ldc + c] - cent[o * ldc + c];
+        sacc = fma(t, t, sacc);
+      }
+      best = fmin(best, sacc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) shalf[j] = 0.5 * sqrt(best);
+  }
+}
+
 // scal[0] = cost2 (sum of cluster terms, fixed order), scal[1..3] = largest
 // movement, second largest, its centroid; scal[4] = max_j |c_j|.
 __global__ void iter_finish_kernel(int64_t k, const double *__restrict__ cterm,
                                    const double *__restrict__ delta,
-                                   const double *__restrict__ cnorm, double *__restrict__ scal) {
+                                   const double *__restrict__ cnorm, double *__restrict__ scal,
+                                   int32_t *__restrict__ flags) {
   if (threadIdx.x != 0) return;
+  flags[0] = 0;  // candidate counter of the next pruned iteration
   double cost = 0.0, d1 = 0.0, d2 = 0.0, cm = 0.0;
   int64_t j1 = 0;
   for (int64_t j = 0; j < k; ++j) {
@@ -1259,6 +1349,7 @@ struct csc_kmeans_plan {
   cudaStream_t stream = nullptr;
   // graph-resident loop (built on first csc_kmeans_run for a buffer set)
   LoopState *loop = nullptr;
+  double *cost_parts = nullptr;  // plan-owned: no cross-stream pool reuse between lanes
   double *history = nullptr;
   int hist_cap = 0;
   cudaGraphExec_t exec = nullptr;
@@ -1449,6 +1540,7 @@ int csc_kmeans_plan_destroy(csc_kmeans_plan *p) {
   if (p->exec) cudaGraphExecDestroy(p->exec);
   if (p->graph) cudaGraphDestroy(p->graph);
   if (p->loop) cudaFreeAsync(p->loop, p->stream);
+  if (p->cost_parts) cudaFreeAsync(p->cost_parts, p->stream);
   if (p->history) cudaFreeAsync(p->history, p->stream);
   if (p->base) cudaFreeAsync(p->base, p->stream);
   delete p;
@@ -1479,14 +1571,14 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
                                    asmem, st, rows, nrows, p->ub, p->lb, gate);
   };
   int rc;
-  CSC_TRY_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * k, st));
   if (full) {
+    CSC_TRY_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * k, st));
     CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t) * 4, st));
     if ((rc = assign(nullptr, nullptr, counts, nullptr)) != CSC_OK) return rc;
   } else {
-    CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t), st));  // candidate count
+    // flags[0] (candidate count) was cleared by the previous iteration's finish
     bound_kernel<<<grid_cap(csc::ceil_div(n, 256)), 256, 0, st>>>(
-        n, labels, p->ub, p->lb, p->delta, p->scal, p->shalf, fnorm, p->cand, p->flags);
+        n, labels, p->ub, p->lb, p->delta, p->scal, p->shalf, fnorm, p->cand, p->flags, counts, k);
     CSC_CHECK_LAUNCH();
     if ((rc = assign(p->cand, p->flags, nullptr, nullptr)) != CSC_OK) return rc;
     label_hist_kernel<<<grid_cap(csc::ceil_div(n, 256), 4), 256, sizeof(int32_t) * k, st>>>(
@@ -1510,13 +1602,20 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
   sums_finish_kernel<<<(unsigned)csc::ceil_div(warps, 8), 256, 0, st>>>(
       p->psum, p->pcnt, p->pq, p->nb, d, k, p->S, counts, p->Q);
   CSC_CHECK_LAUNCH();
-  centroid_finish_kernel<<<(unsigned)k, 128, 0, st>>>(p->S, counts, p->Q, d, k, cent, ldc, cnorm,
-                                                      p->delta, p->cterm);
-  CSC_CHECK_LAUNCH();
-  iter_finish_kernel<<<1, 32, 0, st>>>(k, p->cterm, p->delta, cnorm, p->scal);
-  CSC_CHECK_LAUNCH();
-  shalf_kernel<<<(unsigned)k, 128, 0, st>>>(cent, ldc, d, k, p->shalf);
-  CSC_CHECK_LAUNCH();
+  if (k * k * d <= (int64_t(1) << 20)) {
+    // small k: one single-block node finishes the iteration
+    finish_small_kernel<<<1, 1024, 0, st>>>(d, k, p->S, counts, p->Q, cent, ldc, cnorm,
+                                            p->delta, p->cterm, p->scal, p->shalf, p->flags);
+    CSC_CHECK_LAUNCH();
+  } else {
+    centroid_finish_kernel<<<(unsigned)k, 128, 0, st>>>(p->S, counts, p->Q, d, k, cent, ldc,
+                                                        cnorm, p->delta, p->cterm);
+    CSC_CHECK_LAUNCH();
+    iter_finish_kernel<<<1, 32, 0, st>>>(k, p->cterm, p->delta, cnorm, p->scal, p->flags);
+    CSC_CHECK_LAUNCH();
+    shalf_kernel<<<(unsigned)k, 128, 0, st>>>(cent, ldc, d, k, p->shalf);
+    CSC_CHECK_LAUNCH();
+  }
   if (cost2_dev)
     CSC_TRY_CUDA(cudaMemcpyAsync(cost2_dev, p->scal, sizeof(double), cudaMemcpyDeviceToDevice, st));
   return CSC_OK;
@@ -1530,6 +1629,9 @@ int csc_kmeans_run(csc_kmeans_plan *p, const double *f, const double *fnorm, dou
   CSC_REQUIRE(out_dev != nullptr, "csc_kmeans_run: NULL out_dev");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!p->loop) CSC_TRY_CUDA(cudaMallocAsync((void **)&p->loop, sizeof(LoopState), st));
+  const int cost_grid = grid_cap(csc::ceil_div(p->n, 8));
+  if (!p->cost_parts)
+    CSC_TRY_CUDA(cudaMallocAsync((void **)&p->cost_parts, sizeof(double) * cost_grid, st));
   const int cap = std::max(1, max_iters);
   if (cap > p->hist_cap) {
     if (p->history) CSC_TRY_CUDA(cudaFreeAsync(p->history, st));
@@ -1599,8 +1701,10 @@ int csc_kmeans_run(csc_kmeans_plan *p, const double *f, const double *fnorm, dou
   // out_dev[0] = cost2 of the last iteration in the exact difference form
   // (kmeans.py:111), out_dev[1] = iterations run (as double)
   if (max_iters >= 1) {
-    const int rc = csc_kmeans_cost(f, labels, cent, ldc, p->n, p->d, p->ld, out_dev, st);
-    if (rc != CSC_OK) return rc;
+    cost_kernel<<<cost_grid, 256, 0, st>>>(f, labels, cent, ldc, p->n, p->d, p->ld, p->cost_parts);
+    CSC_CHECK_LAUNCH();
+    reduce_partials_kernel<<<1, 1024, 0, st>>>(p->cost_parts, cost_grid, out_dev);
+    CSC_CHECK_LAUNCH();
   }
   if (history_dev)
     CSC_TRY_CUDA(cudaMemcpyAsync(history_dev, p->history, sizeof(double) * cap,
@@ -1664,7 +1768,8 @@ int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_
   CSC_REQUIRE(n >= 1 && d >= 1 && ld >= d && ldc >= d && k >= 1, "csc_kmeanspp_batch: bad shape");
   CSC_REQUIRE(R >= 1 && R <= 16, "csc_kmeanspp_batch: 1 <= R <= 16 restarts per batch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t nchunks = std::min<int64_t>(1024, csc_kmeanspp_nchunks(n));
+  // contiguous row chunks (<= 1024: the draw scans them in one block), ~>= 32 rows each
+  const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(1024, csc::ceil_div(n, 32)));
   const int64_t chunk = csc::ceil_div(n, nchunks);
   const int64_t cent_stride = k * ldc;
   csc::Scratch closest, sums, fidx, unif;
@@ -1680,7 +1785,7 @@ int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_
   CSC_TRY_CUDA(cudaMemsetAsync(flags_dev, 0xff, sizeof(int32_t) * R, st));
   kppb_first_kernel<<<(unsigned)R, 128, 0, st>>>(f, d, ld, fidx.as<int64_t>(), cent, cent_stride);
   CSC_CHECK_LAUNCH();
-  const size_t smem = sizeof(double) * (R * d + 8 * R);
+  const size_t smem = sizeof(double) * (R * d + 4 * R);
   CSC_REQUIRE(smem <= 48 * 1024, "csc_kmeanspp_batch: R*d too large");
   for (int64_t j = 0; j < k; ++j) {
     if (j > 0) {
@@ -1691,7 +1796,7 @@ int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_
       CSC_CHECK_LAUNCH();
     }
     if (j < k - 1) {
-      kppb_dist_kernel<<<(unsigned)nchunks, 256, smem, st>>>(
+      kppb_dist_kernel<<<(unsigned)nchunks, 128, smem, st>>>(
           f, n, d, ld, cent + j * ldc, cent_stride, (int)R, closest.as<double>(), j == 0 ? 1 : 0,
           chunk, sums.as<double>(), nchunks);
       CSC_CHECK_LAUNCH();

@@ -225,6 +225,7 @@ class _LloydPool:
         self.key = (dev.index, n, d, ld, k)
         self.n, self.d, self.ld, self.k = n, d, ld, k
         self.F = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+        self.ws = _Workspace(self.F, d, k)  # persistent row norms etc.: stable graph keys
         self.lanes = [_Lane(self, dev) for _ in range(self.MAX_LANES)]
 
 
@@ -253,7 +254,8 @@ def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children)
     pool = _lloyd_pool(n, d, ld, k, dev)
     cur = torch.cuda.current_stream()
     pool.F.copy_(blk)
-    ws = _Workspace(pool.F, d, k)
+    ws = pool.ws
+    _native.call("csc_kmeans_rownorms", ptr(pool.F), n, d, ld, ptr(ws.fnorm), stream())
     seeds = batched_kmeanspp(ws, children)
     ready = torch.cuda.Event()
     ready.record(cur)
