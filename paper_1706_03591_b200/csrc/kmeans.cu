@@ -350,11 +350,16 @@ __global__ void __launch_bounds__(RT * CT, 2)
   constexpr int BM = RT * TM;       // rows per tile
   constexpr int BN = CT * TN;       // centroids per pass
   constexpr int BNP = BN + 1;       // padded Cs row
+  constexpr int NB = kStages + 2;   // tile-table ring (see tile_prep)
+  static_assert(NT >= BM, "one thread per tile row in tile_prep");
   if (gate && *gate == 0) return;
   extern __shared__ __align__(16) double smem[];
   const int64_t dpad = (d + kAK - 1) / kAK * kAK;
-  double *Cs = smem;                  // [dpad][BNP]
-  double *Fs = smem + dpad * BNP;     // [kStages][BM][kAKP]
+  double *Cs = smem;                          // [dpad][BNP]
+  double *Fs = Cs + dpad * BNP;               // [kStages][BM][kAKP]
+  double *Fn = Fs + kStages * BM * kAKP;      // [NB][BM] |f|^2 of the tile's rows
+  double *Cn = Fn + NB * BM;                  // [BN] |c|^2 (+inf past k)
+  int32_t *Rid = reinterpret_cast<int32_t *>(Cn + BN);  // [NB][BM] row ids (-1: padding)
   const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;
   const int64_t ntiles = (nr + BM - 1) / BM;
   if ((int64_t)blockIdx.x >= ntiles) return;
@@ -367,45 +372,83 @@ __global__ void __launch_bounds__(RT * CT, 2)
     const int64_t cc = e / dpad, dd = e - cc * dpad;
     Cs[dd * BNP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
   }
-  auto tile_row = [&](int64_t g) -> int64_t {  // first local row of stage g's tile
-    return (blockIdx.x + (g / nst) * (int64_t)gridDim.x) * BM;
-  };
-  auto load_stage = [&](int64_t g) {
-    const int64_t r0 = tile_row(g);
-    const int64_t k0 = (int64_t)(g % nst) * kAK;
-    double *buf = Fs + (size_t)(g % kStages) * BM * kAKP;
-#pragma unroll
-    for (int q = 0; q < (BM * 8 + NT - 1) / NT; ++q) {
-      const int v = tid + NT * q;
-      if (v >= BM * 8) break;
-      const int row = v >> 3, vc = v & 7;
-      const int64_t lr = r0 + row;
-      const int64_t gr = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : n;
-      const int64_t gc = k0 + 2 * vc;
-      const bool ok = gr < n && gc < ld;
-      cp_async16(buf + row * kAKP + 2 * vc, ok ? f + gr * ld + gc : f, ok);
+  // padding columns get |c|^2 = +inf, so their distance is +inf without a select
+  for (int cc = tid; cc < BN; cc += NT) Cn[cc] = c0 + cc < k ? cnorm[c0 + cc] : INFINITY;
+  // tile table of block-local tile t (ring slot b): row ids, and |f|^2 by
+  // cp.async (joins the current commit group, landing with the stage loads)
+  auto tile_prep = [&](int t, int b) {
+    if (tid < BM) {
+      const int64_t lr = (blockIdx.x + (int64_t)t * gridDim.x) * BM + tid;
+      const int64_t gr = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : -1;
+      Rid[b * BM + tid] = (int32_t)gr;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(Fn + b * BM + tid);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa),
+                   "l"(gr >= 0 ? fnorm + gr : fnorm), "r"(gr >= 0 ? 8 : 0));
     }
   };
+  // coalesced loader: 8 threads per row (128 B = one kAK slice), rows from the
+  // tile table (written >= one barrier before the tile's first stage load).
+  // 32-bit stage / tile / ring counters advance incrementally (no 64-bit
+  // division in the loop); the byte offset of a row is one 32x32->64 IMAD.
+  const unsigned ld8 = (unsigned)(ld * (int64_t)sizeof(double));
+  const int vc = tid & 7;
+  int l_st = 0, l_tb = 0, l_buf = 0;  // stage-in-tile, ring slot, buffer of the next load
+  auto load_next = [&]() {
+    const int gc = l_st * kAK + 2 * vc;
+    const bool col_ok = gc < ld;
+    const char *fk = reinterpret_cast<const char *>(f + gc);
+    const int32_t *rid = Rid + l_tb * BM;
+    double *buf = Fs + l_buf * (BM * kAKP);
 #pragma unroll
-  for (int g = 0; g < kStages - 1; ++g) {
-    if (g < total) load_stage(g);
+    for (int q = 0; q < (BM * 8 + NT - 1) / NT; ++q) {
+      const int row = (tid >> 3) + (NT / 8) * q;
+      if (row >= BM) break;
+      const int32_t gr = rid[row];
+      const bool ok = col_ok && gr >= 0;
+      cp_async16(buf + row * kAKP + 2 * vc, ok ? fk + (size_t)(unsigned)gr * ld8 : (const char *)f,
+                 ok);
+    }
+    if (++l_st == nst) {
+      l_st = 0;
+      l_tb = l_tb + 1 == NB ? 0 : l_tb + 1;
+    }
+    l_buf = l_buf + 1 == kStages ? 0 : l_buf + 1;
+  };
+  // Ring safety: tile t's table is written at iteration t*nst - (kStages-1) - 1
+  // (or in the prologue) and last read by its epilogue at t*nst + nst - 1; the
+  // slot is rewritten for tile t + NB at least two iterations (two barriers)
+  // after that epilogue since (NB - 1) * nst >= kStages + 1.
+  constexpr int S = kStages - 1;  // stages in flight ahead of compute
+  const int total_i = (int)total, mt = (int)my_tiles;
+  int p_t = 0;  // next tile to prep
+  for (; p_t < mt && p_t * nst <= S; ++p_t) tile_prep(p_t, p_t % NB);
+  int p_tb = p_t % NB;
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < S; ++g) {
+    if (g < total_i) load_next();
     cp_async_commit();
   }
   double acc[TM][TN];
-  for (int64_t g = 0; g < total; ++g) {
-    if (g + kStages - 1 < total) load_stage(g + kStages - 1);
+  int st = 0, c_buf = 0, c_tb = 0;  // compute: stage-in-tile, stage buffer, ring slot
+  for (int g = 0; g < total_i; ++g) {
+    if (g + S < total_i) load_next();
+    if (p_t < mt && p_t * nst == g + S + 1) {  // tile whose first stage loads next iteration
+      tile_prep(p_t, p_tb);
+      ++p_t;
+      p_tb = p_tb + 1 == NB ? 0 : p_tb + 1;
+    }
     cp_async_commit();
-    cp_async_wait<kStages - 1>();
+    cp_async_wait<S>();
     __syncthreads();
-    const int st = (int)(g % nst);
     if (st == 0) {
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
     }
-    const double *Fb = Fs + (size_t)(g % kStages) * BM * kAKP;
-    const double *Cb = Cs + (size_t)st * kAK * BNP;
+    const double *Fb = Fs + c_buf * (BM * kAKP);
+    const double *Cb = Cs + st * (kAK * BNP);
 #pragma unroll
     for (int kk = 0; kk < kAK; ++kk) {
       double a[TM], b[TN];
@@ -420,46 +463,53 @@ __global__ void __launch_bounds__(RT * CT, 2)
     }
     __syncthreads();
     if (st == nst - 1) {  // epilogue of this row tile
-      const int64_t r0 = tile_row(g);
+      const int tb = c_tb;
       double cn[TN];
 #pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int64_t c = c0 + tx + CT * j;
-        cn[j] = c < k ? cnorm[c] : 0.0;
-      }
+      for (int j = 0; j < TN; ++j) cn[j] = Cn[tx + CT * j];
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
-        const int64_t lr = r0 + ty + RT * i;
-        const int64_t r = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : -1;
-        const double fni = r >= 0 ? fnorm[r] : 0.0;
-        Min3 m[TN];
+        const int row = ty + RT * i;
+        const int64_t r = Rid[tb * BM + row];
+        const double fni = Fn[tb * BM + row];
+        // (min, lowest argmin, second min) of d2 = (|f|^2 - 2 f.c) + |c|^2 over
+        // this thread's columns in ascending order, then across the CT lanes of
+        // the row. fma(-2, acc, |f|^2) rounds once like |f|^2 - (2 acc) (2 acc
+        // is exact). The clamp at 0 only matters when some d2 < 0 (rounding
+        // for a point on a centroid): the unclamped pass is exact otherwise,
+        // and a group with a negative minimum redoes it clamped (features are
+        // finite: FeatureMatrix rejects non-finite values like the reference).
+        double v, v2;
+        int vi;
+        auto reduce_row = [&](bool clamp) {
+          v = INFINITY;
+          v2 = INFINITY;
+          int vj = 0;
 #pragma unroll
-        for (int j = 0; j < TN; ++j) {  // independent: (|f|^2 - 2 f.c) + |c|^2, clamped
-          const double t = __dsub_rn(fni, __dmul_rn(2.0, acc[i][j]));
-          const double d2 = fmax(__dadd_rn(t, cn[j]), 0.0);
-          m[j].v = (c0 + tx + CT * j < k) ? d2 : INFINITY;
-          m[j].i = (int)(c0 + tx + CT * j);
-          m[j].v2 = INFINITY;
-        }
-#pragma unroll
-        for (int w = 1; w < TN; w <<= 1)
-#pragma unroll
-          for (int j = 0; j + w < TN; j += 2 * w) m[j] = min3_merge(m[j], m[j + w]);
-        double v = m[0].v, v2 = m[0].v2;
-        int vi = m[0].i;
-#pragma unroll
-        for (int o = 1; o < CT; o <<= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-          const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-          if (ov < v || (ov == v && oi < vi)) {
-            v2 = fmin(ov2, v);
-            v = ov;
-            vi = oi;
-          } else {
-            v2 = fmin(v2, ov);
+          for (int j = 0; j < TN; ++j) {
+            double d2 = __dadd_rn(fma(-2.0, acc[i][j], fni), cn[j]);
+            if (clamp) d2 = fmax(d2, 0.0);
+            const bool lt = d2 < v, lt2 = d2 < v2;
+            v2 = lt ? v : (lt2 ? d2 : v2);
+            v = lt ? d2 : v;
+            vj = lt ? j : vj;
           }
-        }
+          vi = (int)(c0 + tx + CT * vj);
+#pragma unroll
+          for (int o = 1; o < CT; o <<= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+            const bool take = ov < v || (ov == v && oi < vi);
+            v2 = take ? fmin(ov2, v) : fmin(v2, ov);
+            v = take ? ov : v;
+            vi = take ? oi : vi;
+          }
+        };
+        reduce_row(false);
+        if (__any_sync(0xffffffffu, v < 0.0)) reduce_row(true);  // rare
+        v = fmax(v, 0.0);  // -0.0 -> +0.0 as the clamp gives
+        v2 = fmax(v2, 0.0);
         if (tx == 0 && r >= 0) {
           if (c0 > 0) {  // merge with earlier centroid tiles (smaller indices win ties)
             const double pv = own[r], pv2 = lb[r];
@@ -486,15 +536,155 @@ __global__ void __launch_bounds__(RT * CT, 2)
         }
       }
     }
+    if (++st == nst) {
+      st = 0;
+      c_tb = c_tb + 1 == NB ? 0 : c_tb + 1;
+    }
+    c_buf = c_buf + 1 == kStages ? 0 : c_buf + 1;
   }
+}
+
+// ---------------------------------------------------------------------------
+// assign, small k (k <= 32 * KPL, d <= 128): one warp per R rows, one lane per
+// centroid (KPL per lane). Latency-oriented for small n and candidate subsets
+// (every block reaches its rows after one centroid load, no K pipeline). The
+// per-(row, centroid) arithmetic is assign3's: acc = fma(f_c, c_c, acc) in
+// ascending c from 0.0, then ((|f|^2 - 2 acc) + |c|^2) clamped, and the
+// (min, argmin, second) reduction picks the lowest index on ties, so labels,
+// own distances and bounds are bit-identical to assign3's.
+// ---------------------------------------------------------------------------
+template <int KPL, int R>
+__global__ void __launch_bounds__(256)
+    assign_small_kernel(const double *__restrict__ f, const double *__restrict__ fnorm,
+                        int64_t n, int64_t d, int64_t ld, const double *__restrict__ cent,
+                        int64_t ldc, const double *__restrict__ cnorm, int64_t k,
+                        int32_t *__restrict__ labels, double *__restrict__ own,
+                        int32_t *__restrict__ counts, const int32_t *__restrict__ rows,
+                        const int32_t *__restrict__ nrows_dev, double *__restrict__ ub,
+                        double *__restrict__ lb, const int32_t *__restrict__ gate) {
+  if (gate && *gate == 0) return;
+  extern __shared__ double smem[];
+  const int64_t lds = d | 1;
+  double *Cs = smem;                                  // [32 * KPL][lds]
+  double *Fs = smem + 32 * KPL * lds;                 // [8 warps][R][d]
+  const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;
+  const int64_t ngroups = (nr + R - 1) / R;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if ((int64_t)blockIdx.x * 8 >= ngroups) return;
+  for (int64_t e = threadIdx.x; e < 32 * KPL * d; e += blockDim.x) {
+    const int64_t j = e / d, c = e - j * d;
+    Cs[j * lds + c] = j < k ? cent[j * ldc + c] : 0.0;
+  }
+  double cn[KPL];
+#pragma unroll
+  for (int q = 0; q < KPL; ++q) cn[q] = lane + 32 * q < k ? cnorm[lane + 32 * q] : 0.0;
+  __syncthreads();
+  double *Fw = Fs + (size_t)wid * R * d;
+  for (int64_t g = (int64_t)blockIdx.x * 8 + wid; g < ngroups; g += (int64_t)gridDim.x * 8) {
+    int64_t r[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int64_t lr = g * R + i;
+      r[i] = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      for (int64_t c = lane; c < d; c += 32) Fw[i * d + c] = r[i] >= 0 ? f[r[i] * ld + c] : 0.0;
+    __syncwarp();
+    double acc[R][KPL];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) acc[i][q] = 0.0;
+    for (int64_t c = 0; c < d; ++c) {
+      double b[KPL];
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) b[q] = Cs[(lane + 32 * q) * lds + c];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const double a = Fw[i * d + c];
+#pragma unroll
+        for (int q = 0; q < KPL; ++q) acc[i][q] = fma(a, b[q], acc[i][q]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double fni = r[i] >= 0 ? fnorm[r[i]] : 0.0;
+      Min3 m[KPL];
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) {
+        const double t = __dsub_rn(fni, __dmul_rn(2.0, acc[i][q]));
+        const double d2 = fmax(__dadd_rn(t, cn[q]), 0.0);
+        m[q].v = lane + 32 * q < k ? d2 : INFINITY;
+        m[q].i = lane + 32 * q;
+        m[q].v2 = INFINITY;
+      }
+#pragma unroll
+      for (int q = 1; q < KPL; ++q) m[0] = min3_merge(m[0], m[q]);
+      double v = m[0].v, v2 = m[0].v2;
+      int vi = m[0].i;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+        if (ov < v || (ov == v && oi < vi)) {
+          v2 = fmin(ov2, v);
+          v = ov;
+          vi = oi;
+        } else {
+          v2 = fmin(v2, ov);
+        }
+      }
+      if (lane == 0 && r[i] >= 0) {
+        labels[r[i]] = vi;
+        own[r[i]] = v;
+        if (ub) {
+          ub[r[i]] = sqrt(v);
+          lb[r[i]] = sqrt(v2);
+        }
+        if (counts) atomicAdd(counts + vi, 1);
+      }
+    }
+  }
+}
+
+template <int KPL>
+int launch_assign_small(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
+                        const double *c, int64_t ldc, const double *cnorm, int64_t k,
+                        int32_t *labels, double *own, int32_t *counts, cudaStream_t st,
+                        const int32_t *rows, const int32_t *nrows_dev, double *ub, double *lb,
+                        const int32_t *gate) {
+  constexpr int R = 4;
+  const size_t smem = sizeof(double) * (32 * KPL * (d | 1) + 8 * R * d);
+  static size_t configured = 0;
+  if (smem > configured) {
+    CSC_TRY_CUDA(cudaFuncSetAttribute(assign_small_kernel<KPL, R>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  const int64_t groups = csc::ceil_div(n, (int64_t)R);
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(csc::device_info().sm_count * 4, csc::ceil_div(groups, 8)));
+  assign_small_kernel<KPL, R><<<grid, 256, smem, st>>>(f, fnorm, n, d, ld, c, ldc, cnorm, k,
+                                                        labels, own, counts, rows, nrows_dev, ub,
+                                                        lb, gate);
+  CSC_CHECK_LAUNCH();
+  return CSC_OK;
 }
 
 int g_assign_tn = 8;
 int g_assign_ver = 3;
 
-// 88: 8x8 per thread, 16x8 threads (default: fastest at cfg3/cfg5 scale in
-// tools/ab_assign.py); 48/44/42: 4x8, 4x4 (16x16 threads), 4x4 (32x8 threads)
-int g_assign_tile = 88;
+// 0 (auto): 8x8 per thread, 16x8 threads (fastest at cfg3/cfg5 scale in
+// tools/ab_assign.py), 8x4 when k <= 32; 88/84/48/44/42 force a tile
+int g_assign_tile = 0;
+// 0: fused single-block iteration tail (1024 threads) for small k, 1: same with
+// 256 threads, 2: always the split kernels
+int g_finish_mode = 0;
+// auto: the small-k kernel below this many (row, centroid) pairs
+int64_t kSmallAssignNK = int64_t(1) << 22;
 
 template <int TM, int TN, int RT, int CT>
 int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
@@ -503,11 +693,15 @@ int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d,
                      const int32_t *rows, const int32_t *nrows_dev, double *ub, double *lb,
                      const int32_t *gate) {
   constexpr int BM = RT * TM, BN = CT * TN, NT = RT * CT;
+  CSC_REQUIRE(n < (int64_t(1) << 31) && ld * (int64_t)sizeof(double) < (int64_t(1) << 31),
+              "assign: n and the row stride in bytes must fit int32");
   const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
   const size_t cbytes = sizeof(double) * dpad * (BN + 1), sbytes = sizeof(double) * BM * kAKP;
+  // tile tables (|f|^2 + row id per row, ring of kStages + 2) and |c|^2
+  auto tbytes = [&](int stages) { return (size_t)(stages + 2) * BM * 12 + sizeof(double) * BN; };
   // three stages when two blocks still fit in one SM's shared memory, else two
-  const bool three = 2 * (cbytes + 3 * sbytes + 1024) <= 228 * 1024;
-  const size_t smem = cbytes + (three ? 3 : 2) * sbytes;
+  const bool three = 2 * (cbytes + 3 * sbytes + tbytes(3) + 1024) <= 228 * 1024;
+  const size_t smem = cbytes + (three ? 3 : 2) * sbytes + tbytes(three ? 3 : 2);
   static size_t configured2 = 0, configured3 = 0;
   size_t &configured = three ? configured3 : configured2;
   if (smem > configured) {
@@ -516,11 +710,10 @@ int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  // persistent grid sized to the work (>= 4 row tiles per block), so that small
-  // problems leave SMs free for the concurrently running restarts
+  // persistent grid: two blocks per SM, or one block per row tile when fewer
   const int64_t tiles = csc::ceil_div(n, (int64_t)BM);
   const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>(csc::device_info().sm_count * 2, csc::ceil_div(tiles, 4)));
+      1, std::min<int64_t>(csc::device_info().sm_count * 2, tiles));
   for (int64_t c0 = 0; c0 < k; c0 += BN) {
     const int last = c0 + BN >= k;
     if (three)
@@ -540,6 +733,15 @@ int launch_assign3(const double *f, const double *fnorm, int64_t n, int64_t d, i
                    const double *c, int64_t ldc, const double *cnorm, int64_t k, int32_t *labels,
                    double *own, int32_t *counts, cudaStream_t st, const int32_t *rows,
                    const int32_t *nrows_dev, double *ub, double *lb, const int32_t *gate) {
+  const bool small_ok = k <= 64 && d <= 128;
+  if (g_assign_tile == 1 || (g_assign_tile == 0 && small_ok && n * k <= kSmallAssignNK)) {
+    CSC_REQUIRE(small_ok, "assign_small: needs k <= 64 and d <= 128");
+    if (k <= 32)
+      return launch_assign_small<1>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts, st,
+                                    rows, nrows_dev, ub, lb, gate);
+    return launch_assign_small<2>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts, st,
+                                  rows, nrows_dev, ub, lb, gate);
+  }
   switch (g_assign_tile) {
     case 88:
       return launch_assign3_t<8, 8, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
@@ -553,7 +755,13 @@ int launch_assign3(const double *f, const double *fnorm, int64_t n, int64_t d, i
     case 44:
       return launch_assign3_t<4, 4, 16, 16>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
                                             counts, st, rows, nrows_dev, ub, lb, gate);
+    case 84:
+      return launch_assign3_t<8, 4, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                           counts, st, rows, nrows_dev, ub, lb, gate);
     default:
+      if (k <= 32)  // 128 x 32 tile: no wasted FMAs on padding centroids at small k
+        return launch_assign3_t<8, 4, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                             counts, st, rows, nrows_dev, ub, lb, gate);
       return launch_assign3_t<8, 8, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
                                            counts, st, rows, nrows_dev, ub, lb, gate);
   }
@@ -674,8 +882,21 @@ __global__ void update_partial_kernel(const double *__restrict__ f,
   }
   if (blockIdx.y == 0) {
     for (int64_t r = rbeg + threadIdx.x; r < rend; r += blockDim.x) atomicAdd(scnt + labels[r], 1);
-    if (pq && threadIdx.x == blockDim.x - 1)  // ordered per-cluster |f|^2 sums (extra warp)
-      for (int64_t r = rbeg; r < rend; ++r) sq[labels[r]] += fnorm[r];
+    if (pq && threadIdx.x == blockDim.x - 1) {  // ordered per-cluster |f|^2 sums (extra warp)
+      int64_t r = rbeg;
+      for (; r + 8 <= rend; r += 8) {
+        int32_t l[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          l[u] = __ldg(labels + r + u);
+          v[u] = __ldg(fnorm + r + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sq[l[u]] += v[u];
+      }
+      for (; r < rend; ++r) sq[labels[r]] += fnorm[r];
+    }
   }
   __syncthreads();
   const int64_t nb = gridDim.x;
@@ -1166,8 +1387,11 @@ __global__ void centroid_finish_kernel(const double *__restrict__ S,
 
 // Single-block tail of an iteration for small k: the means, movements,
 // cost terms, scalars and half-separations of centroid_finish + iter_finish +
-// shalf in one graph node (after the multi-block sums_finish_kernel). Also
-// clears the candidate counter for the next pruned iteration.
+// shalf in one graph node (after the multi-block sums_finish_kernel), with the
+// new centroids staged in shared memory (odd row stride: conflict-free) for
+// the pairwise pass. Same per-element arithmetic and summation order as those
+// kernels for the half-separations. Also clears the candidate counter of the
+// next pruned iteration.
 __global__ void __launch_bounds__(1024)
     finish_small_kernel(int64_t d, int64_t k, const double *__restrict__ S,
                         const int32_t *__restrict__ counts, const double *__restrict__ Q,
@@ -1175,8 +1399,11 @@ __global__ void __launch_bounds__(1024)
                         double *__restrict__ delta, double *__restrict__ cterm,
                         double *__restrict__ scal, double *__restrict__ shalf,
                         int32_t *__restrict__ flags) {
+  extern __shared__ double cs[];  // [k][lds] centroids, then [3][k] delta, |c|^2, cost term
+  const int64_t lds = d | 1;
+  double *sdel = cs + k * lds, *snrm = sdel + k, *sct = snrm + k;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  // B: warp per centroid: means, movement, |c|^2, cost term
+  // warp per centroid: means, movement, |c|^2, cost term
   for (int64_t j = wid; j < k; j += nw) {
     const int32_t cnt = counts[j];
     const double denom = (double)(cnt > 1 ? cnt : 1);
@@ -1186,6 +1413,7 @@ __global__ void __launch_bounds__(1024)
       const double mean = __ddiv_rn(sjc, denom);
       const double old = cent[j * ldc + c];
       cent[j * ldc + c] = mean;
+      cs[j * lds + c] = mean;
       mv = fma(mean - old, mean - old, mv);
       nrm = fma(mean, mean, nrm);
       dot = fma(mean, sjc, dot);
@@ -1197,19 +1425,19 @@ __global__ void __launch_bounds__(1024)
       dot += __shfl_xor_sync(0xffffffffu, dot, o);
     }
     if (lane == 0) {
-      delta[j] = sqrt(mv);
-      cnorm[j] = nrm;
-      cterm[j] = cnt > 0 ? (Q[j] - 2.0 * dot) + (double)cnt * nrm : 0.0;
+      const double ct = cnt > 0 ? (Q[j] - 2.0 * dot) + (double)cnt * nrm : 0.0;
+      delta[j] = sdel[j] = sqrt(mv);
+      cnorm[j] = snrm[j] = nrm;
+      cterm[j] = sct[j] = ct;
     }
   }
   __syncthreads();
-  // C: scalars (thread 0), D: half-separations (warp per centroid)
   if (threadIdx.x == 0) {
     double cost = 0.0, d1 = 0.0, d2 = 0.0, cm = 0.0;
     int64_t j1 = 0;
     for (int64_t j = 0; j < k; ++j) {
-      cost += cterm[j];
-      const double dj = delta[j];
+      cost += sct[j];
+      const double dj = sdel[j];
       if (dj > d1) {
         d2 = d1;
         d1 = dj;
@@ -1217,22 +1445,24 @@ __global__ void __launch_bounds__(1024)
       } else if (dj > d2) {
         d2 = dj;
       }
-      cm = fmax(cm, cnorm[j]);
+      cm = fmax(cm, snrm[j]);
     }
     scal[0] = cost > 0.0 ? cost : 0.0;
     scal[1] = d1;
     scal[2] = d2;
     scal[3] = (double)j1;
     scal[4] = sqrt(cm);
-    flags[0] = 0;  // candidate counter of the next pruned iteration
+    flags[3] = flags[0];  // last candidate count, for csc_kmeans_plan_stats
+    flags[0] = 0;
   }
+  // half-separations: lane o of warp j accumulates |c_j - c_o|^2 over c in order
   for (int64_t j = wid; j < k; j += nw) {
     double best = INFINITY;
     for (int64_t o = lane; o < k; o += 32) {
       if (o == j) continue;
       double sacc = 0.0;
       for (int64_t c = 0; c < d; ++c) {
-        const double t = cent[j * ldc + c] - cent[o * ldc + c];
+        const double t = cs[j * lds + c] - cs[o * lds + c];
         sacc = fma(t, t, sacc);
       }
       best = fmin(best, sacc);
@@ -1250,7 +1480,8 @@ __global__ void iter_finish_kernel(int64_t k, const double *__restrict__ cterm,
                                    const double *__restrict__ cnorm, double *__restrict__ scal,
                                    int32_t *__restrict__ flags) {
   if (threadIdx.x != 0) return;
-  flags[0] = 0;  // candidate counter of the next pruned iteration
+  flags[3] = flags[0];  // last candidate count, for csc_kmeans_plan_stats
+  flags[0] = 0;         // candidate counter of the next pruned iteration
   double cost = 0.0, d1 = 0.0, d2 = 0.0, cm = 0.0;
   int64_t j1 = 0;
   for (int64_t j = 0; j < k; ++j) {
@@ -1403,8 +1634,15 @@ int csc_kmeans_assign(const double *f, const double *fnorm, int64_t n, int64_t d
 int csc_kmeans_tuning(const char *key, int64_t value) {
   CSC_REQUIRE(key != nullptr, "csc_kmeans_tuning: NULL key");
   if (std::string(key) == "assign_tile") {
-    CSC_REQUIRE(value == 44 || value == 88 || value == 48 || value == 42, "assign_tile: 44, 88, 48 or 42");
+    CSC_REQUIRE(value == 0 || value == 1 || value == 44 || value == 88 || value == 84 ||
+                    value == 48 || value == 42,
+                "assign_tile: 0 (auto), 1 (small-k), 44, 88, 84, 48 or 42");
     g_assign_tile = (int)value;
+    return CSC_OK;
+  }
+  if (std::string(key) == "finish_mode") {
+    CSC_REQUIRE(value >= 0 && value <= 2, "finish_mode must be 0, 1 or 2");
+    g_finish_mode = (int)value;
     return CSC_OK;
   }
   if (std::string(key) == "assign_ver") {
@@ -1530,7 +1768,7 @@ int csc_kmeans_plan_stats(const csc_kmeans_plan *p, int64_t *candidates, int32_t
   int32_t h[4] = {0, 0, 0, 0};
   CSC_TRY_CUDA(cudaMemcpyAsync(h, p->flags, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
   CSC_TRY_CUDA(cudaStreamSynchronize(p->stream));
-  if (candidates) *candidates = h[0];
+  if (candidates) *candidates = h[3];
   if (gated) *gated = h[1];
   return CSC_OK;
 }
@@ -1602,9 +1840,11 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
   sums_finish_kernel<<<(unsigned)csc::ceil_div(warps, 8), 256, 0, st>>>(
       p->psum, p->pcnt, p->pq, p->nb, d, k, p->S, counts, p->Q);
   CSC_CHECK_LAUNCH();
-  if (k * k * d <= (int64_t(1) << 20)) {
+  if (g_finish_mode != 2 && k * ((d | 1) + 3) * (int64_t)sizeof(double) <= 48 * 1024 &&
+      k * k * d <= (int64_t(1) << 20)) {
     // small k: one single-block node finishes the iteration
-    finish_small_kernel<<<1, 1024, 0, st>>>(d, k, p->S, counts, p->Q, cent, ldc, cnorm,
+    finish_small_kernel<<<1, g_finish_mode == 1 ? 256 : 1024, sizeof(double) * k * ((d | 1) + 3),
+                          st>>>(d, k, p->S, counts, p->Q, cent, ldc, cnorm,
                                             p->delta, p->cterm, p->scal, p->shalf, p->flags);
     CSC_CHECK_LAUNCH();
   } else {

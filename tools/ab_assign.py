@@ -25,8 +25,11 @@ c = torch.zeros((a.k, ld), dtype=torch.float64, device="cuda")
 c[:, :a.d] = torch.randn((a.k, a.d), dtype=torch.float64, device="cuda", generator=g)
 fn = (f * f).sum(1)
 cn = (c * c).sum(1)
-VARIANTS = [("v2", "assign_ver", 2), ("v3-88", "assign_tile", 88), ("v3-48", "assign_tile", 48),
+VARIANTS = [("v2", "assign_ver", 2), ("small", "assign_tile", 1), ("v3-88", "assign_tile", 88), ("v3-84", "assign_tile", 84),
+            ("v3-48", "assign_tile", 48),
             ("v3-44", "assign_tile", 44), ("v3-42", "assign_tile", 42)]
+if a.k > 64 or a.d > 128:
+    VARIANTS = [v for v in VARIANTS if v[0] != "small"]
 labels = {v[0]: torch.empty(a.n, dtype=torch.int32, device="cuda") for v in VARIANTS}
 own = torch.empty(a.n, dtype=torch.float64, device="cuda")
 counts = torch.empty(a.k, dtype=torch.int32, device="cuda")
@@ -50,4 +53,5 @@ for v, _, _ in VARIANTS:
     m = statistics.median(times[v])
     print(f"assign {v}: n={a.n} d={a.d} k={a.k} median {m:.3f} ms ({flop / m / 1e9:.1f} TFLOP/s) "
           f"min {min(times[v]):.3f} max {max(times[v]):.3f}")
+_native.check(lib.csc_kmeans_tuning(b"assign_tile", 0), "tuning")
 print("labels equal:", all(bool(torch.equal(labels["v2"], labels[v[0]])) for v in VARIANTS))
