@@ -180,7 +180,10 @@ int csc_kmeans_run(csc_kmeans_plan *plan, const double *f_dev, const double *row
                    double *c_dev, int64_t ldc, double *cnorm_dev, int32_t *labels_dev,
                    int32_t *counts_dev, int max_iters, double tol, double *out_dev,
                    double *history_dev, void *stream);
-/* k-means tuning knob: "assign_tn" = 4 (default) or 8 centroids per thread */
+/* k-means tuning knobs (performance only; results do not change):
+ * "assign_ver" 2|3, "assign_tn" 4|8 (v2 kernel), "assign_tile" 0 (auto) |
+ * 1 (small-k kernel) | 88 | 84 | 48 | 44 | 42 (v3 register tile),
+ * "finish_mode" 0|1|2 (fused / fused-256 / split iteration tail) */
 int csc_kmeans_tuning(const char *key, int64_t value);
 /* empty-cluster repair (kmeans.py:99-108): for each empty j ascending, move the
  * row with the largest own_d2 (first max) to j and set its own_d2 to -1.

@@ -60,5 +60,6 @@ for it in range(a.iters):
     prev = cost2
     if stop:
         break
-print(json.dumps({"cutoff": cut, "probe_iters": iters, "est": est, "iterations": len(rows),
+tot = sum(r[1] for r in rows)
+print(json.dumps({"total_ms": round(tot, 1), "cutoff": cut, "probe_iters": iters, "est": est, "iterations": len(rows),
                   "per_iter": rows[:5] + rows[5::10] + rows[-3:]}))
