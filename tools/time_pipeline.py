@@ -33,12 +33,19 @@ ap.add_argument("--restarts", type=int, default=10)
 ap.add_argument("--search", default="moments")
 a = ap.parse_args()
 out = {"what": a.what}
+# warm-up on a small graph: module loading, CUB / allocator setup, k-means lanes
+_wq1, _wq2 = G.sbm_probabilities(20000, 20, 16.0, 0.05)
+_wl = P.laplacian(G.graph_from_codes(20000, G.planted_partition_codes(20000, 20, _wq1, _wq2, 1)))
+_wb = device_signals(20000, 32, 0)
+_search_cutoff(_wl, 20, FilteredBlock(_wb, 32), (0.0, 2.0), P.FilterConfig(order=20), None, 1.0)
+torch.cuda.synchronize()
 if a.what == "cfg3":
     n, k, d, m = 1_000_000, 100, 128, 100
     t = tic()
     q1, q2 = G.sbm_probabilities(n, k, 32.0, 0.02)
     g = G.graph_from_codes(n, G.planted_partition_codes(n, k, q1, q2, 3))
     out["gen_s"] = time.perf_counter() - t
+    t = tic(); g.device_edges(); out["edge_upload_ms"] = (tic() - t) * 1e3  # 2 x int64 host -> device
     t = tic(); lap = P.laplacian(g); out["laplacian_ms"] = (tic() - t) * 1e3
     t = tic(); blk = device_signals(n, d, 0); out["signals_ms"] = (tic() - t) * 1e3
     cnt = P.MatvecCounter()
