@@ -315,7 +315,10 @@ def main():
     if rank == 0 or world > 1:
         pinned = torch.from_numpy(r_host).pin_memory()
         x_np = pinned.numpy()
-        P.apply_filter(lap, poly, x_np, precision=args.precision)
+        # warm-up in the same loop shape as the timed one (the previous result is
+        # still alive during each call: steady state holds two pinned host outputs)
+        for _ in range(2):
+            res = P.apply_filter(lap, poly, x_np, precision=args.precision)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 3))
