@@ -45,6 +45,24 @@ METRIC = "filtered nnz*d*order/s"
 UNIT = "nnz*d*order/s"
 
 
+def ncu_traffic(workload: str, precision: str):
+    """DRAM bytes per sweep launch (read + write) from the committed ncu capture of
+    this workload (profiles/r01_sweep_<workload>_<precision>_dram.csv), or None."""
+    path = os.path.join(ROOT, "profiles", f"r01_sweep_{workload}_{precision}_dram.csv")
+    if not os.path.exists(path):
+        return None, None
+    import csv
+    per = {}
+    with open(path) as fh:
+        for r in csv.DictReader(ln for ln in fh if not ln.startswith("==")):
+            if r["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[r["Metric Unit"]]
+                per[r["ID"]] = per.get(r["ID"], 0.0) + float(r["Metric Value"].replace(",", "")) * scale
+    if not per:
+        return None, None
+    return float(np.mean(list(per.values()))), os.path.relpath(path, ROOT)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -301,8 +319,10 @@ def main():
     hbm, peak_kind = peaks()
     sweep_ms = float(sweeps.mean()) if sweeps.size else ms / order
     achieved = b_min / (sweep_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.workload, args.precision)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "peak_kind": peak_kind, "kernel": "sweep_kernel (fused SpMM + recurrence)",
+                "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
+                "kernel": "sweep_kernel (fused SpMM + recurrence)",
                 "sweep_ms_mean": sweep_ms, "sweep_ms_median": float(np.median(sweeps)) if sweeps.size else None,
                 "sweeps_timed": int(sweeps.size), "bytes_min_per_launch": int(b_min),
                 "bytes_full_per_launch": int(b_full), "frac_full": b_full / (sweep_ms / 1e3) / 1e9 / hbm,
