@@ -119,6 +119,18 @@ int csc_cheb_filter(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t
  * work: 2*n*ld elements. */
 int csc_cheb_moments(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t d, int32_t m,
                      double *mu_dev, void *work_dev, void *stream);
+/* Same moments, keeping every order resident for csc_cheb_combine: T_{j+1}
+ * is written to block j of keep_dev (m blocks of n*ld elements; fp64 plans).
+ * Single-pass bisection without a second sweep series:
+ * replaces the final apply_filter at the accepted cutoff (filters.py:176-186). */
+int csc_cheb_moments_keep(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t d,
+                          int32_t m, double *mu_dev, void *keep_dev, void *stream);
+/* out = sum_j c_j T_j from the resident orders of csc_cheb_moments_keep, with
+ * the fused sweep's arithmetic (bit-identical to csc_cheb_filter's output for
+ * the same coefficients); sumsq_dev (nullable) = ||out||_F^2. fp64. */
+int csc_cheb_combine(const void *x_dev, const void *keep_dev, int64_t n, int64_t ld, int64_t d,
+                     const double *coeffs_host, int32_t ncoeffs, void *out_dev,
+                     double *sumsq_dev, void *stream);
 
 /* Tuning knobs (process-wide; defaults are the measured best):
  *   "chunk_bytes"  row-chunk width per sweep series (default 4096)

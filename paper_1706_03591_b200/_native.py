@@ -38,6 +38,8 @@ SIGNATURES = {
     "csc_chebop_info": ([_P, _PI64, _PI64, _PI64, _PI64], _INT),
     "csc_cheb_filter": ([_P, _P, _I64, _I64, _PD, _I32, _P, _P, _P, _P], _INT),
     "csc_cheb_moments": ([_P, _P, _I64, _I64, _I32, _P, _P, _P], _INT),
+    "csc_cheb_moments_keep": ([_P, _P, _I64, _I64, _I32, _P, _P, _P], _INT),
+    "csc_cheb_combine": ([_P, _P, _I64, _I64, _I64, _PD, _I32, _P, _P, _P], _INT),
     "csc_sumsq": ([_P, _I64, _INT, _P, _P, _P], _INT),
     "csc_set_tuning": ([ctypes.c_char_p, _I64], _INT),
     "csc_sweep_timing": ([_INT], _INT),

@@ -1026,7 +1026,7 @@ __global__ void combine_sums_kernel(const double *__restrict__ per_chunk, int64_
 
 template <typename T>
 int cheb_moments_t(const csc_chebop &op, const T *x, int64_t ld, int m, double *mu, T *work,
-                   cudaStream_t st) {
+                   cudaStream_t st, T *keep = nullptr) {
   using VT = typename V16<T>::V;
   constexpr int E = V16<T>::E;
   const int64_t ldv = ld / E;
@@ -1062,7 +1062,10 @@ int cheb_moments_t(const csc_chebop &op, const T *x, int64_t ld, int m, double *
     A.ldv = ldv;
     const VT *t_prev = nullptr;
     const VT *t_cur = xv;
-    VT *t_next = ta;
+    // keep: T_{j+1} goes to block j of `keep` (every order stays resident for
+    // csc_cheb_combine); otherwise a two-buffer ring in `work`
+    auto kept = [&](int j) { return reinterpret_cast<VT *>(keep + (size_t)j * n * ld) + v0; };
+    VT *t_next = keep ? kept(0) : ta;
     for (int j = 0; j < m; ++j) {  // produces T_{j+1}
       A.gat = t_cur;
       A.own = t_cur;
@@ -1076,7 +1079,8 @@ int cheb_moments_t(const csc_chebop &op, const T *x, int64_t ld, int m, double *
       CSC_CHECK_LAUNCH();
       t_prev = t_cur;
       t_cur = t_next;
-      t_next = (j == 0) ? tb : const_cast<VT *>(t_prev);
+      t_next = keep ? (j + 1 < m ? kept(j + 1) : nullptr)
+                    : ((j == 0) ? tb : const_cast<VT *>(t_prev));
     }
   }
   combine_sums_kernel<<<1, 256, 0, st>>>(chunk_sums.as<double>(), nchunks, len, S);
@@ -1278,6 +1282,106 @@ int csc_cheb_filter(const csc_chebop *op, const void *x, int64_t ld, int64_t d,
   return cheb_filter_t<float>(*op, static_cast<const float *>(x), ld, coeffs, ncoeffs,
                               static_cast<float *>(out), static_cast<float *>(work), sumsq_dev,
                               st);
+}
+
+}  // extern "C"
+
+namespace {
+// out = sum_j c_j T_j from resident orders, in the fused sweep's arithmetic:
+// out = fma(c1, T_1, c0 * x), then out = fma(c_j, T_j, out) for j = 2..m, so
+// the features are bit-identical to csc_cheb_filter's. Fused ||out||^2 as
+// per-block partials. HBM-bound: (m + 1) blocks read, one written.
+__global__ void __launch_bounds__(256)
+    combine_kernel(const double2 *__restrict__ x, const double2 *__restrict__ keep,
+                   int64_t nv, const double *__restrict__ c, int nc, double2 *__restrict__ out,
+                   double *__restrict__ parts) {
+  __shared__ double red[32];
+  double s0 = 0.0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const double2 xv = __ldcs(x + v);
+    const double2 t1 = __ldcs(keep + v);
+    double2 o;
+    o.x = fma(c[1], t1.x, c[0] * xv.x);
+    o.y = fma(c[1], t1.y, c[0] * xv.y);
+    int j = 2;
+    for (; j + 4 <= nc; j += 4) {  // four orders in flight
+      double2 t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] = __ldcs(keep + (int64_t)(j + u - 1) * nv + v);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        o.x = fma(c[j + u], t[u].x, o.x);
+        o.y = fma(c[j + u], t[u].y, o.y);
+      }
+    }
+    for (; j < nc; ++j) {
+      const double2 t = __ldcs(keep + (int64_t)(j - 1) * nv + v);
+      o.x = fma(c[j], t.x, o.x);
+      o.y = fma(c[j], t.y, o.y);
+    }
+    __stcs(out + v, o);
+    s0 = fma(o.x, o.x, s0);
+    s0 = fma(o.y, o.y, s0);
+  }
+  if (parts) {
+    s0 = block_sum<256>(s0, red);
+    if (threadIdx.x == 0) parts[blockIdx.x] = s0;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int csc_cheb_moments_keep(const csc_chebop *op, const void *x, int64_t ld, int64_t d, int32_t m,
+                          double *mu_dev, void *keep, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(op != nullptr, "csc_cheb_moments_keep: NULL plan");
+  CSC_REQUIRE(op->dtype == CSC_F64, "csc_cheb_moments_keep: fp64 plans only");
+  CSC_REQUIRE(m >= 1, "csc_cheb_moments_keep: need m >= 1");
+  CSC_REQUIRE(d >= 1 && ld >= d && ld % 2 == 0, "csc_cheb_moments_keep: need 1 <= d <= ld, even ld");
+  CSC_REQUIRE(aligned16(x) && aligned16(keep), "csc_cheb_moments_keep: buffers must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const_cast<csc_chebop *>(op)->stream = st;
+  if (op->n == 0) {
+    CSC_TRY_CUDA(cudaMemsetAsync(mu_dev, 0, sizeof(double) * (2 * m + 1), st));
+    return CSC_OK;
+  }
+  return cheb_moments_t<double>(*op, static_cast<const double *>(x), ld, m, mu_dev, nullptr, st,
+                                static_cast<double *>(keep));
+}
+
+int csc_cheb_combine(const void *x, const void *keep, int64_t n, int64_t ld, int64_t d,
+                     const double *coeffs_host, int32_t ncoeffs, void *out, double *sumsq_dev,
+                     void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(ncoeffs >= 2, "csc_cheb_combine: need at least two coefficients");
+  CSC_REQUIRE(n >= 0 && d >= 1 && ld >= d && ld % 2 == 0, "csc_cheb_combine: bad shape");
+  CSC_REQUIRE(aligned16(x) && aligned16(keep) && aligned16(out),
+              "csc_cheb_combine: buffers must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nv = n * ld / 2;
+  if (nv == 0) {
+    if (sumsq_dev) CSC_TRY_CUDA(cudaMemsetAsync(sumsq_dev, 0, sizeof(double), st));
+    return CSC_OK;
+  }
+  csc::Scratch cs, parts;
+  CSC_TRY_CUDA(cs.alloc(sizeof(double) * ncoeffs, st));
+  CSC_TRY_CUDA(cudaMemcpyAsync(cs.ptr, coeffs_host, sizeof(double) * ncoeffs,
+                               cudaMemcpyHostToDevice, st));
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)csc::device_info().sm_count * 8, csc::ceil_div(nv, 256)));
+  if (sumsq_dev) CSC_TRY_CUDA(parts.alloc(sizeof(double) * grid, st));
+  combine_kernel<<<grid, 256, 0, st>>>(static_cast<const double2 *>(x),
+                                       static_cast<const double2 *>(keep), nv, cs.as<double>(),
+                                       ncoeffs, static_cast<double2 *>(out),
+                                       sumsq_dev ? parts.as<double>() : nullptr);
+  CSC_CHECK_LAUNCH();
+  if (sumsq_dev) {
+    reduce_partials_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), grid, sumsq_dev);
+    CSC_CHECK_LAUNCH();
+  }
+  return CSC_OK;
 }
 
 int csc_cheb_moments(const csc_chebop *op, const void *x, int64_t ld, int64_t d, int32_t m,

@@ -474,8 +474,13 @@ def test_moment_energy_equals_block_energy(P):
         assert abs(moment_energy(mu, poly.coeffs) - ref) <= 1e-11 * max(ref, 1.0)
 
 
+@pytest.mark.parametrize("keep", ["1", "0"])
 @pytest.mark.parametrize("case", ["cfg1", "small"])
-def test_moment_search_equals_probe_search(P, case):
+def test_moment_search_equals_probe_search(P, case, keep, monkeypatch):
+    """Moment bisection == the reference's per-probe refiltering: same cutoff,
+    probes and features bit for bit, with the orders resident in HBM (keep=1:
+    exact features by csc_cheb_combine) or re-swept (keep=0)."""
+    monkeypatch.setenv("CSC_KEEP_ORDERS", keep)
     from paper_1706_03591_b200.filters import _search_cutoff
     if case == "cfg1":
         g = golden("cfg1")
@@ -496,8 +501,10 @@ def test_moment_search_equals_probe_search(P, case):
     assert np.array_equal(fm, fp)
     assert abs(em - ep) <= 1e-12 * abs(ep)
     assert cntm.count == cntp.count == im * order * r.shape[1]
-    assert cntm.physical <= 2 * order * r.shape[1] + cntp.physical  # moment pass + final features
-    assert cntm.physical == 2 * order * r.shape[1] or im == 1
+    if keep == "1":  # one sweep series in total
+        assert cntm.physical == order * r.shape[1]
+    else:  # moment pass + final features (+ guard-band confirmations)
+        assert cntm.physical >= 2 * order * r.shape[1]
 
 
 def test_reference_counter_accepted(P):
@@ -686,3 +693,26 @@ def test_dynamic_cfg2_golden(P):
         print(f"cfg2 step {t}: ARI {ari:.6f} cost {a.feature_cost:.12f} ref {float(g[f's{t}_cost']):.12f}")
         assert ari >= 0.999
         assert abs(a.feature_cost - float(g[f"s{t}_cost"])) <= 1e-9 * float(g[f"s{t}_cost"])
+
+
+def test_combine_equals_filter_bitwise(P):
+    """csc_cheb_combine over resident orders == csc_cheb_filter, bit for bit, and the
+    kept moment pass returns the same moments as the ring-buffer pass."""
+    import torch
+    from paper_1706_03591_b200._device import upload_block
+    from paper_1706_03591_b200.filters import block_moments, block_moments_keep, combine_orders, filter_block
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    blk = upload_block(g["R"])
+    n, ld = blk.shape
+    m = 37
+    keep = torch.empty((m, n, ld), dtype=torch.float64, device=blk.device)
+    mu_keep = block_moments_keep(lap, blk, 40, m, 2.0, keep)
+    mu = block_moments(lap, blk, 40, m, 2.0)
+    assert np.array_equal(mu_keep, mu)
+    for cut in (0.05, 0.4, 1.3):
+        poly = P.cheb_coeffs(cut, 2.0, m)
+        ref, s_ref = filter_block(lap, poly, blk, 40, want_sumsq=True)
+        out, s = combine_orders(blk, keep, 40, poly.coeffs)
+        assert torch.equal(out, ref)
+        assert abs(float(s.item()) - float(s_ref.item())) <= 1e-13 * float(s_ref.item())
