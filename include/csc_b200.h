@@ -249,6 +249,14 @@ int csc_kmeanspp_batch(const double *f_dev, int64_t n, int64_t d, int64_t ld, in
  * disagreement or too few draws; not expected in practice). Bit-identical
  * to numpy except that tail samples (|z| > 3.65) go through the device
  * log1p/exp, which may round the last bit differently. SYNCHRONISES. */
+/* numpy SeedSequence -> PCG64 seeding on the host (signals.py:34-37 builds
+ * default_rng(child) per column): states_out[4c..4c+3] = (state lo, state hi,
+ * inc lo, inc hi) of PCG64(child c) for the children first_child .. + d - 1 of
+ * the SeedSequence with the given run entropy and spawn key (little-endian
+ * uint32 words, as numpy coerces them) and pool size. No device work. */
+int csc_seed_states(const uint32_t *run_entropy, int64_t n_run, const uint32_t *key_prefix,
+                    int64_t n_key, int64_t first_child, int64_t d, int32_t pool_size,
+                    uint64_t *states_out);
 int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
                        double *out_dev, int64_t ld, int64_t col0, int32_t *bad_host, void *stream);
 

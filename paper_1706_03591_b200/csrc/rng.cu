@@ -21,6 +21,8 @@
 // in the last ulp (tail samples, |x| > 3.65, ~3e-4 of draws).
 #include <cub/cub.cuh>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace {
@@ -185,7 +187,101 @@ __global__ void transpose_counts_kernel(const int32_t *__restrict__ in, int64_t 
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// numpy's SeedSequence -> PCG64 seeding, restated on the host (published
+// algorithm: numpy/random/bit_generator.pyx SeedSequence.mix_entropy /
+// generate_state / get_assembled_entropy, _pcg64.pyx + pcg64.h
+// pcg64_set_seed): the per-column (state, inc) of default_rng(child) for the
+// children first..first+d-1 of a SeedSequence, without building the d
+// SeedSequence / PCG64 objects in Python (signals.py:34-37 draws one child per
+// column).
+// ---------------------------------------------------------------------------
+namespace seedseq {
+constexpr uint32_t kInitA = 0x43b0d7e5u, kMultA = 0x931e8875u;
+constexpr uint32_t kInitB = 0x8b51f9ddu, kMultB = 0x58f38dedu;
+constexpr uint32_t kMixL = 0xca01f9ddu, kMixR = 0x4973f715u;
+constexpr int kXShift = 16;
+
+inline uint32_t hashmix(uint32_t value, uint32_t &hc) {
+  value ^= hc;
+  hc *= kMultA;
+  value *= hc;
+  value ^= value >> kXShift;
+  return value;
+}
+inline uint32_t mix(uint32_t x, uint32_t y) {
+  uint32_t r = kMixL * x - kMixR * y;
+  r ^= r >> kXShift;
+  return r;
+}
+void mix_entropy(uint32_t *pool, int ps, const uint32_t *ent, int64_t n) {
+  uint32_t hc = kInitA;
+  for (int i = 0; i < ps; ++i) pool[i] = hashmix(i < n ? ent[i] : 0u, hc);
+  for (int src = 0; src < ps; ++src)
+    for (int dst = 0; dst < ps; ++dst)
+      if (src != dst) pool[dst] = mix(pool[dst], hashmix(pool[src], hc));
+  for (int64_t src = ps; src < n; ++src)
+    for (int dst = 0; dst < ps; ++dst) pool[dst] = mix(pool[dst], hashmix(ent[src], hc));
+}
+}  // namespace seedseq
+
 extern "C" {
+
+int csc_seed_states(const uint32_t *run_entropy, int64_t n_run, const uint32_t *key_prefix,
+                    int64_t n_key, int64_t first_child, int64_t d, int32_t pool_size,
+                    uint64_t *states_out) {
+  csc::clear_error();
+  CSC_REQUIRE(n_run >= 1 && n_key >= 0 && first_child >= 0 && d >= 0 && states_out != nullptr,
+              "csc_seed_states: bad arguments");
+  CSC_REQUIRE(pool_size >= 1 && pool_size <= 1024, "csc_seed_states: pool_size out of range");
+  // assembled entropy of a child: run entropy (zero-padded to the pool size,
+  // since a spawned child always has a spawn key), then the spawn key words:
+  // key_prefix, then the child index as little-endian 32-bit words
+  std::vector<uint32_t> ent;
+  ent.reserve((size_t)std::max<int64_t>(n_run, pool_size) + n_key + 2);
+  std::vector<uint32_t> pool(pool_size);
+  for (int64_t c = 0; c < d; ++c) {
+    ent.assign(run_entropy, run_entropy + n_run);
+    if ((int64_t)ent.size() < pool_size) ent.resize(pool_size, 0u);
+    ent.insert(ent.end(), key_prefix, key_prefix + n_key);
+    uint64_t idx = (uint64_t)(first_child + c);
+    if (idx == 0) ent.push_back(0u);
+    while (idx > 0) {
+      ent.push_back((uint32_t)(idx & 0xffffffffu));
+      idx >>= 32;
+    }
+    seedseq::mix_entropy(pool.data(), pool_size, ent.data(), (int64_t)ent.size());
+    // generate_state(4, uint64): 8 words cycling over the pool
+    uint32_t w[8];
+    uint32_t hc = seedseq::kInitB;
+    for (int i = 0; i < 8; ++i) {
+      uint32_t v = pool[i % pool_size];
+      v ^= hc;
+      hc *= seedseq::kMultB;
+      v *= hc;
+      v ^= v >> seedseq::kXShift;
+      w[i] = v;
+    }
+    const uint64_t val[4] = {w[0] | (uint64_t)w[1] << 32, w[2] | (uint64_t)w[3] << 32,
+                             w[4] | (uint64_t)w[5] << 32, w[6] | (uint64_t)w[7] << 32};
+    // pcg64_set_seed: state0 = (val0 << 64) | val1, seq = (val2 << 64) | val3;
+    // srandom_r: state = 0, inc = seq * 2 + 1, step, state += state0, step
+    const unsigned __int128 mult =
+        ((unsigned __int128)0x2360ed051fc65da4ull << 64) | 0x4385df649fccf645ull;
+    const unsigned __int128 s0 = ((unsigned __int128)val[0] << 64) | val[1];
+    const unsigned __int128 seq = ((unsigned __int128)val[2] << 64) | val[3];
+    const unsigned __int128 inc = (seq << 1) | 1u;
+    unsigned __int128 st = 0;
+    st = st * mult + inc;
+    st += s0;
+    st = st * mult + inc;
+    states_out[4 * c + 0] = (uint64_t)st;
+    states_out[4 * c + 1] = (uint64_t)(st >> 64);
+    states_out[4 * c + 2] = (uint64_t)inc;
+    states_out[4 * c + 3] = (uint64_t)(inc >> 64);
+  }
+  return CSC_OK;
+}
 
 int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
                        double *out, int64_t ld, int64_t col0, int32_t *bad_host, void *stream) {

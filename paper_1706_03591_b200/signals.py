@@ -81,6 +81,41 @@ def random_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> np.n
 RNG_MODE = os.environ.get("CSC_RNG", "device")
 
 
+def _u32_words(x) -> list[int]:
+    """numpy's SeedSequence word coercion (bit_generator.pyx _coerce_to_uint32_array)
+    for integers and (nested) integer sequences: little-endian 32-bit words,
+    [0] for zero."""
+    if isinstance(x, np.ndarray) and x.dtype == np.uint32:
+        return [int(v) for v in x]
+    if isinstance(x, (int, np.integer)):
+        v = int(x)
+        if v < 0:
+            raise ValueError("expected non-negative integer")
+        if v == 0:
+            return [0]
+        words = []
+        while v > 0:
+            words.append(v & 0xFFFFFFFF)
+            v >>= 32
+        return words
+    out: list[int] = []
+    for v in x:
+        out.extend(_u32_words(v))
+    return out
+
+
+def child_states(ss: np.random.SeedSequence, d: int) -> np.ndarray:
+    """column_states(ss.spawn(d)) computed in the library (csc_seed_states) without
+    building the children: (d, 4) uint64 (state lo, hi, inc lo, hi) of
+    PCG64(child) for children ss.n_children_spawned .. + d - 1. Does not advance ss."""
+    run = np.ascontiguousarray(_u32_words(ss.entropy), dtype=np.uint32)
+    key = np.ascontiguousarray(_u32_words(ss.spawn_key), dtype=np.uint32)
+    out = np.empty((d, 4), dtype=np.uint64)
+    _native.call("csc_seed_states", run.ctypes.data, run.size, key.ctypes.data, key.size,
+                 int(ss.n_children_spawned), d, int(ss.pool_size), out.ctypes.data)
+    return out
+
+
 def column_states(children) -> np.ndarray:
     """Initial PCG64 (state, inc) of each child stream as 4 uint64 words per column."""
     words = np.empty((len(children), 4), dtype=np.uint64)
@@ -92,11 +127,15 @@ def column_states(children) -> np.ndarray:
     return words
 
 
-def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None, mode: str | None = None) -> torch.Tensor:
+def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None, mode: str | None = None,
+                   advance: bool = True) -> torch.Tensor:
     """random_signals as a padded (n, ld) float64 device block.
 
     Device mode draws numpy's exact PCG64 streams and ziggurat on the GPU;
-    columns the generator flags are redrawn on the host (the exact path).
+    columns the generator flags are redrawn on the host (the exact path). The
+    per-column PCG64 states come from the library's SeedSequence restatement;
+    a caller's SeedSequence is advanced by d children as ss.spawn(d) would
+    (advance=False skips that for internal, never-reused children).
     """
     if d < 1:
         raise ValueError("need at least one signal column")
@@ -108,15 +147,19 @@ def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None, mode: s
     dev = require_cuda()
     blk = torch.zeros((n, row_stride(d)), dtype=torch.float64, device=dev)
     if (mode or RNG_MODE) == "device":
-        # spawn from a copy so the caller's SeedSequence advances exactly as in signal_columns
-        children = as_seed_sequence(seed).spawn(d)
-        states = np.ascontiguousarray(column_states(children))
+        ss = as_seed_sequence(seed)
+        base = int(ss.n_children_spawned)
+        states = child_states(ss, d)
+        if advance and ss is seed:  # the caller's SeedSequence moves on exactly as in signal_columns
+            ss.spawn(d)
         bad = np.zeros(d, dtype=np.int32)
         sigma = 1.0 / np.sqrt(dim)
         _native.call("csc_normal_columns", states.ctypes.data, d, n, float(sigma), ptr(blk), blk.shape[1], 0,
                      bad.ctypes.data, stream())
         for c in np.flatnonzero(bad):
-            z = np.random.default_rng(children[c]).standard_normal(n) * sigma + 0.0
+            child = np.random.SeedSequence(ss.entropy, spawn_key=tuple(ss.spawn_key) + (base + int(c),),
+                                           pool_size=ss.pool_size)
+            z = np.random.default_rng(child).standard_normal(n) * sigma + 0.0
             blk[:, c].copy_(torch.from_numpy(z))
         return blk
     cols = torch.from_numpy(signal_columns(n, d, seed, scale_dim))

@@ -123,3 +123,23 @@ def test_laplacian_rejects_unknown_variant():
     import paper_1706_03591_b200 as P
     with pytest.raises(ValueError):
         P.laplacian(P.Graph(3, [0], [1], [1.0]), "random-walk")
+
+
+def test_seed_states_match_numpy():
+    """csc_seed_states (host restatement of SeedSequence mixing + PCG64 seeding)
+    == numpy's PCG64(child).state for spawned children, incl. nested spawn keys,
+    big entropy, non-default pool sizes and a partially spawned parent."""
+    import numpy as np
+    from numpy.random.bit_generator import _coerce_to_uint32_array
+    from paper_1706_03591_b200.signals import _u32_words, child_states, column_states
+    cases = [np.random.SeedSequence(0), np.random.SeedSequence(123456789),
+             np.random.SeedSequence(2 ** 200 + 12345), np.random.SeedSequence([1, 2, 2 ** 40]),
+             np.random.SeedSequence(7, pool_size=8), np.random.SeedSequence(5).spawn(3)[2],
+             np.random.SeedSequence(9).spawn(2)[1].spawn(4)[3], np.random.SeedSequence()]
+    for ss in cases:
+        assert _u32_words(ss.entropy) == [int(v) for v in _coerce_to_uint32_array(ss.entropy)]
+        assert _u32_words(ss.spawn_key) == [int(v) for v in _coerce_to_uint32_array(ss.spawn_key)]
+        ss.spawn(5)  # partially spawned parent: children continue from n_children_spawned
+        fast = child_states(ss, 37)
+        ref = column_states(ss.spawn(37))
+        assert np.array_equal(fast, ref)
