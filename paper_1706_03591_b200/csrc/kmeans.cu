@@ -844,62 +844,103 @@ __global__ void repair_kernel(int32_t *__restrict__ labels, double *__restrict__
 
 // partial sums: block (b, y) owns rows [b*chunk, ...) and columns
 // [y*cw, y*cw+cw); smem holds k x cw sums.
+constexpr int kSqLanes = 8;  // lanes of the extra warp summing |f|^2 per cluster
+
 __global__ void update_partial_kernel(const double *__restrict__ f,
                                       const int32_t *__restrict__ labels, int64_t n, int64_t d,
                                       int64_t ld, int64_t k, int64_t chunk, int cw,
                                       double *__restrict__ psum, int32_t *__restrict__ pcnt,
                                       const double *__restrict__ fnorm, double *__restrict__ pq) {
   extern __shared__ double sm[];
-  double *sq = sm + (size_t)k * cw;  // per-cluster sum of |f_i|^2 (y == 0 blocks)
-  int32_t *scnt = reinterpret_cast<int32_t *>(sq + k);
+  double *sq = sm + (size_t)k * cw;  // [kSqLanes][k] per-lane |f|^2 sums (y == 0 blocks)
+  int32_t *scnt = reinterpret_cast<int32_t *>(sq + kSqLanes * k);
   const int64_t b = blockIdx.x;
   const int64_t col0 = (int64_t)blockIdx.y * cw;
   for (int64_t i = threadIdx.x; i < k * cw; i += blockDim.x) sm[i] = 0.0;
-  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
-    scnt[i] = 0;
-    sq[i] = 0.0;
-  }
+  for (int64_t i = threadIdx.x; i < kSqLanes * k; i += blockDim.x) sq[i] = 0.0;
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) scnt[i] = 0;
   __syncthreads();
   const int64_t rbeg = b * chunk, rend = min(n, rbeg + chunk);
   const int c = threadIdx.x;
   const bool active = c < cw && col0 + c < d;
   if (active) {
+    // this thread owns column c of every cluster's partial: rows are added in
+    // order; while consecutive rows share a label the running value stays in a
+    // register (same additions, same order as adding into shared memory)
     const double *fc = f + col0 + c;
-    int64_t r = rbeg;
-    // 8 rows in flight per thread: loads first, then the (ordered) smem adds
-    for (; r + 8 <= rend; r += 8) {
-      int32_t l[8];
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        l[u] = __ldg(labels + r + u);
-        v[u] = __ldg(fc + (r + u) * ld);
+    int cur = -1;
+    double run = 0.0;
+    auto add = [&](int32_t l, double v) {
+      if (l != cur) {
+        if (cur >= 0) sm[(size_t)cur * cw + c] = run;
+        cur = l;
+        run = sm[(size_t)l * cw + c];
       }
+      run += v;
+    };
+    constexpr int U = 16;  // rows per batch; the next batch is loaded before adding this one
+    int64_t r = rbeg;
+    int32_t la[U], lb2[U];
+    double va[U], vb[U];
+    auto load = [&](int64_t r0, int32_t (&l)[U], double (&v)[U]) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) sm[(size_t)l[u] * cw + c] += v[u];
+      for (int u = 0; u < U; ++u) {
+        l[u] = __ldg(labels + r0 + u);
+        v[u] = __ldg(fc + (r0 + u) * ld);
+      }
+    };
+    if (r + U <= rend) load(r, la, va);
+    while (r + U <= rend) {
+      const bool more = r + 2 * U <= rend;
+      if (more) load(r + U, lb2, vb);
+#pragma unroll
+      for (int u = 0; u < U; ++u) add(la[u], va[u]);
+      r += U;
+      if (!more) break;
+      const bool more2 = r + 2 * U <= rend;
+      if (more2) load(r + U, la, va);
+#pragma unroll
+      for (int u = 0; u < U; ++u) add(lb2[u], vb[u]);
+      r += U;
+      if (!more2) break;
     }
-    for (; r < rend; ++r) sm[(size_t)labels[r] * cw + c] += fc[r * ld];
+    for (; r < rend; ++r) add(labels[r], fc[r * ld]);
+    if (cur >= 0) sm[(size_t)cur * cw + c] = run;
   }
   if (blockIdx.y == 0) {
     for (int64_t r = rbeg + threadIdx.x; r < rend; r += blockDim.x) atomicAdd(scnt + labels[r], 1);
-    if (pq && threadIdx.x == blockDim.x - 1) {  // ordered per-cluster |f|^2 sums (extra warp)
-      int64_t r = rbeg;
-      for (; r + 8 <= rend; r += 8) {
+    // per-cluster |f|^2 on kSqLanes lanes of the extra warp: lane l sums rows
+    // rbeg + l, rbeg + l + kSqLanes, ... in order; lanes are combined in order
+    const int lane_sq = (int)threadIdx.x - ((int)blockDim.x - 32);
+    if (pq && lane_sq >= 0 && lane_sq < kSqLanes) {
+      double *mine = sq + (size_t)lane_sq * k;
+      int cur = -1;
+      double run = 0.0;
+      auto add = [&](int32_t l, double v) {  // same register-run scheme as the columns
+        if (l != cur) {
+          if (cur >= 0) mine[cur] = run;
+          cur = l;
+          run = mine[l];
+        }
+        run += v;
+      };
+      int64_t r = rbeg + lane_sq;
+      for (; r + 7 * kSqLanes < rend; r += 8 * kSqLanes) {
         int32_t l[8];
         double v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          l[u] = __ldg(labels + r + u);
-          v[u] = __ldg(fnorm + r + u);
+          l[u] = __ldg(labels + r + u * kSqLanes);
+          v[u] = __ldg(fnorm + r + u * kSqLanes);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) sq[l[u]] += v[u];
+        for (int u = 0; u < 8; ++u) add(l[u], v[u]);
       }
-      for (; r < rend; ++r) sq[labels[r]] += fnorm[r];
+      for (; r < rend; r += kSqLanes) add(labels[r], fnorm[r]);
+      if (cur >= 0) mine[cur] = run;
     }
   }
   __syncthreads();
-  const int64_t nb = gridDim.x;
   for (int64_t i = threadIdx.x; i < k * cw; i += blockDim.x) {
     const int64_t j = i / cw, cc = i % cw;
     if (col0 + cc < d) psum[(b * k + j) * d + col0 + cc] = sm[i];
@@ -907,13 +948,14 @@ __global__ void update_partial_kernel(const double *__restrict__ f,
   if (blockIdx.y == 0)
     for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
       pcnt[b * k + j] = scnt[j];
-      if (pq) pq[b * k + j] = sq[j];
+      if (pq) {
+        double q = 0.0;
+#pragma unroll
+        for (int l = 0; l < kSqLanes; ++l) q += sq[(size_t)l * k + j];
+        pq[b * k + j] = q;
+      }
     }
-  (void)nb;
 }
-
-// one warp per (centroid j, column c): lanes add the block partials b = lane,
-// lane+32, ... in order, then a fixed shuffle tree; means = sum / max(count,1)
 __global__ void update_finish_kernel(const double *__restrict__ psum,
                                      const int32_t *__restrict__ pcnt, int64_t nb, int64_t d,
                                      int64_t k, double *__restrict__ cent, int64_t ldc,
@@ -1677,7 +1719,7 @@ int csc_kmeans_update(const double *f, const int32_t *labels, int64_t n, int64_t
   // columns per block so that k*cw doubles (+ k counts) fit in shared memory
   const int64_t budget = std::max<int64_t>(48 * 1024, (int64_t)info.max_smem_optin) - 1024;
   const int64_t cnt_bytes = sizeof(int32_t) * k;
-  int64_t cw = (budget - cnt_bytes) / (int64_t)(sizeof(double) * k) - 1;
+  int64_t cw = (budget - cnt_bytes) / (int64_t)(sizeof(double) * k) - kSqLanes;
   CSC_REQUIRE(cw >= 1, "csc_kmeans_update: k=%lld too large for shared-memory partials",
               (long long)k);
   cw = std::min<int64_t>(std::min<int64_t>(cw, 256), d);
@@ -1686,7 +1728,7 @@ int csc_kmeans_update(const double *f, const int32_t *labels, int64_t n, int64_t
   const int64_t nb = std::max<int64_t>(
       1, std::min<int64_t>((int64_t)info.sm_count * 8, csc::ceil_div(n, 64)));
   const int64_t chunk = csc::ceil_div(n, nb);
-  const size_t smem = sizeof(double) * k * (cw + 1) + cnt_bytes;
+  const size_t smem = sizeof(double) * k * (cw + kSqLanes) + cnt_bytes;
   CSC_TRY_CUDA(cudaFuncSetAttribute(update_partial_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   csc::Scratch psum, pcnt;
@@ -1721,7 +1763,7 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   p->k = k;
   p->stream = st;
   const int64_t budget = std::max<int64_t>(48 * 1024, (int64_t)info.max_smem_optin) - 1024;
-  int64_t cw = (budget - (int64_t)sizeof(int32_t) * k) / (int64_t)(sizeof(double) * k) - 1;
+  int64_t cw = (budget - (int64_t)sizeof(int32_t) * k) / (int64_t)(sizeof(double) * k) - kSqLanes;
   if (cw < 1) {
     delete p;
     csc::set_error("csc_kmeans_plan_create: k=%lld too large", (long long)k);
@@ -1731,7 +1773,7 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   p->ny = csc::ceil_div(d, p->cw);
   p->nb = std::max<int64_t>(1, std::min<int64_t>((int64_t)info.sm_count * 8, csc::ceil_div(n, 64)));
   p->chunk = csc::ceil_div(n, p->nb);
-  p->smem = sizeof(double) * k * (p->cw + 1) + sizeof(int32_t) * k;
+  p->smem = sizeof(double) * k * (p->cw + kSqLanes) + sizeof(int32_t) * k;
   const size_t nd = (size_t)n, kk = (size_t)k;
   const size_t doubles = 3 * nd + (size_t)p->nb * kk * d + (size_t)p->nb * kk + kk * d + 4 * kk + 8;
   const size_t ints = nd + 4 + (size_t)p->nb * kk;
