@@ -78,9 +78,13 @@ def header_symbols() -> list[str]:
     return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(csc_\w+)\s*\(", text, re.M)))
 
 
-def load(path: str = LIB):
-    """Load the shared library (no device needed) and bind every signature."""
+def load(path: str | None = None):
+    """Load the shared library (no device needed) and bind every signature.
+
+    CSC_LIB overrides the in-tree path (A/B of alternative builds in tools/)."""
     global _lib
+    if path is None:
+        path = os.environ.get("CSC_LIB") or LIB
     if _lib is None:
         if not os.path.exists(path):
             raise ImportError(f"libcscb200.so not built ({path}); run __graft_entry__.build()")

@@ -343,8 +343,18 @@ template <typename T, int LV>
 __device__ __forceinline__ void segment_body(const SweepArgs &A, int64_t first_warp,
                                              int64_t nwarps);
 
+// Narrow row groups (G < 32, <= 2 vectors per lane: d <= 64 fp64) are latency
+// bound at 80 registers (3 blocks/SM); capping them at 64 gives 4 blocks/SM:
+// cfg4 fp64 d=64 7.30 -> 6.62 ms, cfg5 d=48 3.31 -> 3.00 ms per order (interleaved
+// A/B). Wider groups keep the compiler's default (0 = no minimum), which is
+// faster there (an explicit minimum of 1 or 4 slowed cfg3 by 5-16%).
+template <int G, int VPL>
+struct SweepMinBlocks {
+  static constexpr int value = (G < 32 && VPL <= 2) ? 4 : 0;
+};
+
 template <typename T, int G, int VPL, int MODE>
-__global__ void __launch_bounds__(kBlock) sweep_kernel(SweepArgs A) {
+__global__ void __launch_bounds__(kBlock, (SweepMinBlocks<G, VPL>::value)) sweep_kernel(SweepArgs A) {
   using VT = typename V16<T>::V;
   __shared__ double red[kBlock / 32];
   if ((int)blockIdx.x < A.seg_blocks) {  // long-row segments, overlapped with the rows
