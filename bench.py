@@ -180,7 +180,9 @@ def run_reference(args, w, rank):
 
 
 def run_dynamic(args, rank):
-    """ms per dynamic-CSC step on cfg2 shapes (n=20k, k=20, d=80, p=0.5, m=60)."""
+    """ms per dynamic-CSC step on BASELINE configs[1]: SBM n=20k, k=20, mean degree 24,
+    p_out/p_in=0.05, T=10 steps; each step moves 0.5% of nodes to another block
+    (perturb_nodes) and then rewires 1% of edges (perturb_edges); d=80, p=0.5, m=60."""
     import torch
     import paper_1706_03591_b200 as P
     from paper_1706_03591_b200 import generators as G
@@ -191,11 +193,17 @@ def run_dynamic(args, rank):
     g = G.graph_from_codes(n, codes)
     graphs = [g]
     cur = codes
-    steps = 6
-    for t in range(1, steps):
-        dl, il = G.edge_churn(cur, n, labels, q1, q2, 0.01, seed=100 + t)
-        graphs.append(graphs[-1].apply_delta(dl, il))
-        cur = np.union1d(np.setdiff1d(cur, dl, assume_unique=True), il)
+    steps = 10
+
+    def applied(c, dl, il):
+        return np.union1d(np.setdiff1d(c, dl, assume_unique=True), il)
+
+    for t in range(1, steps):  # nodes first, then edges
+        dn, inn, labels = G.node_switch(cur, n, labels, k, q1, q2, 0.005, seed=200 + t)
+        cur = applied(cur, dn, inn)
+        de, ie = G.edge_churn(cur, n, labels, q1, q2, 0.01, seed=100 + t)
+        graphs.append(graphs[-1].apply_delta(dn, inn).apply_delta(de, ie))
+        cur = applied(cur, de, ie)
     cfg = P.DynamicConfig(k=k, d=d, p=0.5, filter=P.FilterConfig(order=60))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -209,7 +217,8 @@ def run_dynamic(args, rank):
         torch.cuda.synchronize()
         ms.append((time.perf_counter() - t0) * 1e3)
         refined += diag.refined
-    out = {"workload": "cfg2: planted partition n=20000 k=20 deg 24 e=0.05, 1% edge churn/step, d=80 p=0.5 m=60, "
+    out = {"workload": "configs[1] / cfg2: SBM n=20000 k=20 mean degree 24 p_out/p_in=0.05, T=10 (init + 9 steps), "
+                       "per step 0.5% of nodes switch block then 1% of edges rewired; d=80 p=0.5 m=60, "
                        "k-means k=20 x 10 restarts", "ms_per_step": statistics.median(ms),
            "steps_timed": len(ms), "init_ms": init_ms, "refined_steps": refined,
            "phase_ms_total": {k2: round(v, 3) for k2, v in phases.items()}}

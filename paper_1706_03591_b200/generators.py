@@ -189,6 +189,9 @@ def edge_churn(codes: np.ndarray, n: int, labels: np.ndarray, q1: float, q2: flo
     k = int(labels.max()) + 1
     sizes = np.bincount(labels, minlength=k)
     offs = np.concatenate([[0], np.cumsum(sizes)])
+    # block members in label order (the identity for contiguous planted blocks;
+    # labels stop being contiguous once nodes switch blocks)
+    members = np.argsort(labels, kind="stable")
     # pair-class weights: same-block pairs and cross pairs
     n_in = float((sizes * (sizes - 1) // 2).sum())
     n_out = float(n) * (n - 1) / 2 - n_in
@@ -201,7 +204,7 @@ def edge_churn(codes: np.ndarray, n: int, labels: np.ndarray, q1: float, q2: flo
         a = rng.integers(0, n, batch)
         b = np.empty(batch, dtype=np.int64)
         la = labels[a]
-        bi = offs[la] + rng.integers(0, sizes[la])
+        bi = members[offs[la] + rng.integers(0, sizes[la])]
         b[inside] = bi[inside]
         bo = rng.integers(0, n, batch)
         b[~inside] = bo[~inside]
@@ -219,3 +222,40 @@ def edge_churn(codes: np.ndarray, n: int, labels: np.ndarray, q1: float, q2: flo
         dels = np.setdiff1d(dels, both, assume_unique=True)
         ins = np.setdiff1d(ins, both, assume_unique=True)
     return dels, ins
+
+
+def node_switch(codes: np.ndarray, n: int, labels: np.ndarray, k: int, q1: float, q2: float,
+                fraction: float, seed=0) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """(deletes, inserts, new_labels) for reassigning round(fraction*n) nodes.
+
+    perturb_nodes semantics (graphs.py:276-319): the selected nodes move to a
+    uniformly drawn other block, all their incident edges are deleted, and
+    every pair with a selected endpoint is then drawn once with the model
+    probability under the new labels (q1 same block, q2 across). Equal in
+    distribution, not stream-identical. O(count * n) host work (cfg2: 100 x 20k
+    pairs); an edge deleted and redrawn is dropped from both lists.
+    """
+    if k < 2:
+        raise ValueError("node reassignment needs k >= 2")
+    rng = np.random.default_rng(seed)
+    new_labels = np.asarray(labels, dtype=np.int64).copy()
+    count = int(round(fraction * n))
+    if count == 0:
+        return np.empty(0, np.int64), np.empty(0, np.int64), new_labels
+    sel = np.sort(rng.choice(n, size=count, replace=False))
+    new_labels[sel] = (new_labels[sel] + rng.integers(1, k, size=count)) % k
+    in_sel = np.zeros(n, dtype=bool)
+    in_sel[sel] = True
+    dels = codes[in_sel[codes // n] | in_sel[codes % n]]
+    uu = np.repeat(sel, n)
+    vv = np.tile(np.arange(n, dtype=np.int64), count)
+    ok = uu != vv
+    cand = np.unique(np.minimum(uu[ok], vv[ok]) * n + np.maximum(uu[ok], vv[ok]))
+    pi, pj = cand // n, cand % n
+    prob = np.where(new_labels[pi] == new_labels[pj], q1, q2)
+    ins = cand[rng.random(cand.size) < prob]
+    both = np.intersect1d(dels, ins, assume_unique=True)
+    if both.size:
+        dels = np.setdiff1d(dels, both, assume_unique=True)
+        ins = np.setdiff1d(ins, both, assume_unique=True)
+    return dels, ins, new_labels

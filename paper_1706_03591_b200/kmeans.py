@@ -256,14 +256,17 @@ def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children)
     pool.F.copy_(blk)
     ws = pool.ws
     _native.call("csc_kmeans_rownorms", ptr(pool.F), n, d, ld, ptr(ws.fnorm), stream())
-    seeds = batched_kmeanspp(ws, children)
-    ready = torch.cuda.Event()
-    ready.record(cur)
-    best = None
+    # seeds are used right away; the rare zero-mass replay is checked at the
+    # first host synchronisation and its restarts re-run (kmeans.py:70-72)
+    seeds, bad_restarts, replay = batched_kmeanspp(ws, children, defer_check=True)
     R = len(children)
-    for w0 in range(0, R, _LloydPool.MAX_LANES):
-        wave = list(range(w0, min(R, w0 + _LloydPool.MAX_LANES)))
-        for li, r in enumerate(wave):
+    costs: dict[int, float] = {}
+    held: dict[int, int] = {}  # restart -> lane whose labels are still current
+
+    def run_wave(restarts):
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        for li, r in enumerate(restarts):
             lane = pool.lanes[li]
             lane.stream.wait_event(ready)
             with torch.cuda.stream(lane.stream):
@@ -272,22 +275,41 @@ def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children)
                              ptr(lane.cnorm), ptr(lane.labels), ptr(lane.counts), int(cfg.max_iters),
                              float(cfg.tol), ptr(lane.out), None, lane.stream.cuda_stream)
                 lane.done.record(lane.stream)
-        for li in range(len(wave)):
+        for li in range(len(restarts)):
             cur.wait_event(pool.lanes[li].done)
-        outs = torch.stack([pool.lanes[li].out for li in range(len(wave))]).cpu().numpy()
-        for li, r in enumerate(wave):
-            cost2 = float(outs[li, 0])
-            if best is None or cost2 < best[0]:
-                best = (cost2, pool.lanes[li].labels.cpu().numpy().astype(np.int64))
-        ready = torch.cuda.Event()
-        ready.record(cur)
-    return best[1], best[0]
+        outs = torch.stack([pool.lanes[li].out[0] for li in range(len(restarts))]).cpu().numpy()
+        held.clear()
+        for li, r in enumerate(restarts):
+            costs[r] = float(outs[li])
+            held[r] = li
+
+    best = None  # (cost2, restart); the reference keeps the earliest on ties (strict <)
+    best_labels = None
+    checked = False
+    for w0 in range(0, R, _LloydPool.MAX_LANES):
+        wave = list(range(w0, min(R, w0 + _LloydPool.MAX_LANES)))
+        run_wave(wave)
+        if not checked:  # the cost read above synchronised: the seeding flags are final
+            checked = True
+            redo = bad_restarts()
+            if redo:
+                replay(redo)  # corrected seeds for every wave
+                if any(r in wave for r in redo):
+                    run_wave(wave)
+        improved = False
+        for r in wave:
+            if best is None or costs[r] < best[0]:
+                best = (costs[r], r)
+                improved = True
+        if improved:  # one labels copy per wave, of the best restart so far
+            best_labels = pool.lanes[held[best[1]]].labels.cpu().numpy().astype(np.int64)
+    return best_labels, best[0]
 
 
 KPP_BATCH = 16  # restarts per batched k-means++ launch series (libcscb200 limit)
 
 
-def batched_kmeanspp(ws: _Workspace, children) -> torch.Tensor:
+def batched_kmeanspp(ws: _Workspace, children, defer_check: bool = False):
     """k-means++ seeds of every restart: (restarts, k, ldc) on the GPU.
 
     Each restart's stream is drawn on the host in the reference's order
@@ -298,19 +320,30 @@ def batched_kmeanspp(ws: _Workspace, children) -> torch.Tensor:
     """
     n, k, R = ws.n, ws.k, len(children)
     seeds = torch.zeros((R, k, ws.ldc), dtype=torch.float64, device=ws.blk.device)
-    flags = torch.empty(KPP_BATCH, dtype=torch.int32, device=ws.blk.device)
-    for g0 in range(0, R, KPP_BATCH):
+    ngroups = (R + KPP_BATCH - 1) // KPP_BATCH
+    flags = torch.empty((ngroups, KPP_BATCH), dtype=torch.int32, device=ws.blk.device)
+    for gidx, g0 in enumerate(range(0, R, KPP_BATCH)):
         grp = list(range(g0, min(R, g0 + KPP_BATCH)))
         rngs = [np.random.default_rng(children[r]) for r in grp]
         first = np.array([int(rng.integers(n)) for rng in rngs], dtype=np.int64)
         unif = np.ascontiguousarray(np.stack([rng.random(k - 1) for rng in rngs]) if k > 1
                                     else np.zeros((len(grp), 1)))
         _native.call("csc_kmeanspp_batch", ptr(ws.blk), n, ws.d, ws.ld, len(grp), k,
-                     first.ctypes.data, unif.ctypes.data, ptr(seeds[g0]), ws.ldc, ptr(flags), stream())
-        bad = flags[: len(grp)].cpu().numpy()
-        for gi in np.flatnonzero(bad >= 0):
-            ws.kmeanspp(np.random.default_rng(children[grp[gi]]))
-            seeds[grp[gi]].copy_(ws.cent)
+                     first.ctypes.data, unif.ctypes.data, ptr(seeds[g0]), ws.ldc, ptr(flags[gidx]), stream())
+
+    def replay(bad_restarts):
+        """Sequential k-means++ (fresh generator) for restarts whose D^2 mass hit 0."""
+        for r in bad_restarts:
+            ws.kmeanspp(np.random.default_rng(children[r]))
+            seeds[r].copy_(ws.cent)
+
+    def bad_restarts():
+        fl = flags.cpu().numpy().reshape(-1)
+        return [r for r in range(R) if fl[r] >= 0]
+
+    if defer_check:  # the caller checks after launching work on the seeds
+        return seeds, bad_restarts, replay
+    replay(bad_restarts())
     return seeds
 
 
@@ -344,7 +377,8 @@ def kmeans(f, k: int, cfg: KmeansConfig | None = None, seed=0) -> Assignment:
     host = not isinstance(f, (FeatureMatrix, tuple, torch.Tensor))
     blk, d = _features_block(f)
     require_cuda()
-    if not host and block_nonfinite(blk) != 0:
+    validated = isinstance(f, FeatureMatrix) and getattr(f, "_finite_checked", False)
+    if not host and not validated and block_nonfinite(blk) != 0:
         raise ValueError("features must be finite")
     n = blk.shape[0]
     if not 1 <= k <= n:

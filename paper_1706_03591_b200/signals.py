@@ -223,6 +223,7 @@ class FeatureMatrix:
             if not finite:
                 raise ValueError("feature values must be finite")
         self._blk, self._d, self._host = blk, int(d), host
+        self._finite_checked = bool(check)  # values validated finite at construction
         self.step_tags, self.stream_tags = steps, streams
 
     @classmethod

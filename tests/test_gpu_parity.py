@@ -716,3 +716,16 @@ def test_combine_equals_filter_bitwise(P):
         out, s = combine_orders(blk, keep, 40, poly.coeffs)
         assert torch.equal(out, ref)
         assert abs(float(s.item()) - float(s_ref.item())) <= 1e-13 * float(s_ref.item())
+
+
+def test_kmeans_zero_mass_replay_through_restarts(P):
+    """Duplicate points exhaust the D^2 mass during seeding (the reference then
+    draws integers(n), kmeans.py:70-72): the deferred replay in run_restarts
+    must give the oracle's labels and cost for every seed."""
+    f = np.array([[0.0, 0.0], [0.0, 0.0], [5.0, 1.0], [5.0, 1.0], [0.0, 0.0], [9.0, -2.0]])
+    for seed in range(6):
+        cfg = P.KmeansConfig(restarts=4, max_iters=20)
+        asg = P.kmeans(f, 3, cfg, seed=seed)
+        ref_labels, _, ref_cost = O.kmeans(f, 3, restarts=4, max_iters=20, tol=1e-6, seed=seed)
+        assert np.array_equal(asg.labels, ref_labels)
+        assert abs(asg.feature_cost - ref_cost) <= 1e-12 * max(ref_cost, 1.0)

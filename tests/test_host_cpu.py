@@ -143,3 +143,36 @@ def test_seed_states_match_numpy():
         fast = child_states(ss, 37)
         ref = column_states(ss.spawn(37))
         assert np.array_equal(fast, ref)
+
+
+def test_node_switch_semantics():
+    """node_switch follows perturb_nodes (graphs.py:276-319): exactly round(f*n)
+    nodes move to another block, every edge touching them is deleted, every
+    insert touches a moved node, and moved nodes regrow their expected degree
+    under the new labels."""
+    import numpy as np
+    from paper_1706_03591_b200 import generators as G
+    n, k = 4000, 8
+    q1, q2 = G.sbm_probabilities(n, k, 24.0, 0.05)
+    codes = G.planted_partition_codes(n, k, q1, q2, 1)
+    labels = np.repeat(np.arange(k), G.block_sizes(n, k))
+    dels, ins, new = G.node_switch(codes, n, labels, k, q1, q2, 0.01, seed=5)
+    moved = np.flatnonzero(new != labels)
+    assert moved.size == 40 and np.all((new[moved] >= 0) & (new[moved] < k))
+    mset = np.zeros(n, bool)
+    mset[moved] = True
+    touch = mset[codes // n] | mset[codes % n]
+    # deletes are touching edges; touching edges not deleted were drawn again (cancelled)
+    assert np.all(np.isin(dels, codes[touch])) and dels.size > 0.8 * touch.sum()
+    assert np.all(mset[ins // n] | mset[ins % n])
+    assert np.intersect1d(dels, ins).size == 0
+    # expected new degree of a moved node: (block size - 1) q1 + (n - block size) q2
+    nxt = np.union1d(np.setdiff1d(codes, dels, assume_unique=True), ins)
+    deg = np.bincount(nxt // n, minlength=n) + np.bincount(nxt % n, minlength=n)
+    sizes = np.bincount(new, minlength=k)
+    expect = (sizes[new[moved]] - 1) * q1 + (n - sizes[new[moved]]) * q2
+    assert abs(deg[moved].mean() - expect.mean()) < 4 * np.sqrt(expect.mean() / moved.size)
+    # edge churn keeps working on the switched (non-contiguous) labels
+    d2, i2 = G.edge_churn(nxt, n, new, q1, q2, 0.01, seed=6)
+    same = new[i2 // n] == new[i2 % n]
+    assert d2.size > 0 and 0.6 < same.mean() < 0.9  # 499 q1 : 3500 q2 -> ~0.74 same-block
