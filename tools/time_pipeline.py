@@ -31,6 +31,7 @@ ap.add_argument("--p", type=float, default=0.5)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--restarts", type=int, default=10)
 ap.add_argument("--search", default="moments")
+ap.add_argument("--ratio", type=float, default=0.05)  # cfg5 p_out/p_in (unspecified in BASELINE)
 a = ap.parse_args()
 out = {"what": a.what}
 # warm-up on a small graph: module loading, CUB / allocator setup, k-means lanes
@@ -66,7 +67,7 @@ if a.what == "cfg3":
 else:
     n, k, d, m = 2_000_000, 64, 96, 80
     t = tic()
-    q1, q2 = G.sbm_probabilities(n, k, 20.0, 0.05)
+    q1, q2 = G.sbm_probabilities(n, k, 20.0, a.ratio)
     codes = G.planted_partition_codes(n, k, q1, q2, 5)
     labels = np.repeat(np.arange(k), G.block_sizes(n, k))
     graphs = [G.graph_from_codes(n, codes)]
@@ -88,7 +89,9 @@ else:
         t = tic()
         asg, state, diag = P.dynamic_step(state, gt, cfg, timings=ph)
         ms = (tic() - t) * 1e3
+        from oracle import csc_oracle as O
         steps.append({"ms": ms, "refined": diag.refined, "iters": diag.search_iters,
+                      "ari_vs_planted": round(O.adjusted_rand(asg.labels, labels), 5),
                       "phases": {kk: round(v, 1) for kk, v in ph.items()}})
     out["steps"] = steps
 print(json.dumps(out))
