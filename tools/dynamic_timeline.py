@@ -18,8 +18,10 @@ labels = np.repeat(np.arange(k), G.block_sizes(n, k))
 graphs = [G.graph_from_codes(n, codes)]
 cur = codes
 for t in range(1, 8):
+    dn, inn, labels = G.node_switch(cur, n, labels, k, q1, q2, 0.005, seed=200 + t)
+    cur = np.union1d(np.setdiff1d(cur, dn, assume_unique=True), inn)
     dl, il = G.edge_churn(cur, n, labels, q1, q2, 0.01, seed=100 + t)
-    graphs.append(graphs[-1].apply_delta(dl, il))
+    graphs.append(graphs[-1].apply_delta(dn, inn).apply_delta(dl, il))
     cur = np.union1d(np.setdiff1d(cur, dl, assume_unique=True), il)
 cfg = P.DynamicConfig(k=k, d=d, p=0.5, filter=P.FilterConfig(order=60))
 _, state, _ = P.dynamic_init(graphs[0], cfg, seed=0)
@@ -64,9 +66,17 @@ if cs is not None:
     busy += ce - cs
 span = (iv[-1][1] - iv[0][0]) / 1e3 if iv else 0.0
 steps = len(graphs) - 4
+merged = []
+for s_, e_ in iv:
+    if merged and s_ <= merged[-1][1]:
+        merged[-1][1] = max(merged[-1][1], e_)
+    else:
+        merged.append([s_, e_])
+
+
 def busy_in(t0, t1):
     tot = 0.0
-    for s_, e_ in iv:
+    for s_, e_ in merged:
         a_, b_ = max(s_, t0), min(e_, t1)
         if b_ > a_:
             tot += b_ - a_
