@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(RT * CT, 2)
   double *Fn = Fs + kStages * BM * kAKP;      // [NB][BM] |f|^2 of the tile's rows
   double *Cn = Fn + NB * BM;                  // [BN] |c|^2 (+inf past k)
   int32_t *Rid = reinterpret_cast<int32_t *>(Cn + BN);  // [NB][BM] row ids (-1: padding)
+  int32_t *Hs = Rid + NB * BM;  // [k] block histogram of the final labels (counts != nullptr)
   const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;
   const int64_t ntiles = (nr + BM - 1) / BM;
   if ((int64_t)blockIdx.x >= ntiles) return;
@@ -374,6 +375,8 @@ __global__ void __launch_bounds__(RT * CT, 2)
   }
   // padding columns get |c|^2 = +inf, so their distance is +inf without a select
   for (int cc = tid; cc < BN; cc += NT) Cn[cc] = c0 + cc < k ? cnorm[c0 + cc] : INFINITY;
+  if (counts)
+    for (int64_t j = tid; j < k; j += NT) Hs[j] = 0;
   // tile table of block-local tile t (ring slot b): row ids, and |f|^2 by
   // cp.async (joins the current commit group, landing with the stage loads)
   auto tile_prep = [&](int t, int b) {
@@ -529,7 +532,7 @@ __global__ void __launch_bounds__(RT * CT, 2)
               ub[r] = sqrt(v);
               lb[r] = sqrt(v2);
             }
-            if (counts) atomicAdd(counts + vi, 1);
+            if (counts) atomicAdd(Hs + vi, 1);
           } else {
             lb[r] = v2;  // carried (squared) second minimum for the next pass
           }
@@ -541,6 +544,11 @@ __global__ void __launch_bounds__(RT * CT, 2)
       c_tb = c_tb + 1 == NB ? 0 : c_tb + 1;
     }
     c_buf = c_buf + 1 == kStages ? 0 : c_buf + 1;
+  }
+  if (counts) {  // one global atomic per (block, cluster) instead of one per row
+    __syncthreads();
+    for (int64_t j = tid; j < k; j += NT)
+      if (Hs[j]) atomicAdd(counts + j, Hs[j]);
   }
 }
 
@@ -698,7 +706,9 @@ int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d,
   const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
   const size_t cbytes = sizeof(double) * dpad * (BN + 1), sbytes = sizeof(double) * BM * kAKP;
   // tile tables (|f|^2 + row id per row, ring of kStages + 2) and |c|^2
-  auto tbytes = [&](int stages) { return (size_t)(stages + 2) * BM * 12 + sizeof(double) * BN; };
+  auto tbytes = [&](int stages) {
+    return (size_t)(stages + 2) * BM * 12 + sizeof(double) * BN + sizeof(int32_t) * (size_t)k;
+  };
   // three stages when two blocks still fit in one SM's shared memory, else two
   const bool three = 2 * (cbytes + 3 * sbytes + tbytes(3) + 1024) <= 228 * 1024;
   const size_t smem = cbytes + (three ? 3 : 2) * sbytes + tbytes(three ? 3 : 2);

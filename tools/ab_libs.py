@@ -20,6 +20,7 @@ ap.add_argument("--n", type=int, default=2_000_000)
 ap.add_argument("--d", type=int, default=96)
 ap.add_argument("--k", type=int, default=64)
 ap.add_argument("--rounds", type=int, default=9)
+ap.add_argument("--no-counts", action="store_true")
 a = ap.parse_args()
 libs = []
 for path in a.libs:
@@ -44,7 +45,7 @@ for r in range(a.rounds):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         rc = lib.csc_kmeans_assign(ptr(f), ptr(fn), a.n, a.d, ld, ptr(c), ld, ptr(cn), a.k, ptr(labels[i]),
-                                   ptr(own), ptr(counts), stream())
+                                   ptr(own), None if a.no_counts else ptr(counts), stream())
         e1.record()
         torch.cuda.synchronize()
         assert rc == 0, rc
