@@ -575,6 +575,7 @@ __global__ void __launch_bounds__(256)
   const int64_t lds = d | 1;
   double *Cs = smem;                                  // [32 * KPL][lds]
   double *Fs = smem + 32 * KPL * lds;                 // [8 warps][R][d]
+  int32_t *Hs = reinterpret_cast<int32_t *>(Fs + 8 * R * d);  // [32 * KPL] block label histogram
   const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;
   const int64_t ngroups = (nr + R - 1) / R;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -586,6 +587,8 @@ __global__ void __launch_bounds__(256)
   double cn[KPL];
 #pragma unroll
   for (int q = 0; q < KPL; ++q) cn[q] = lane + 32 * q < k ? cnorm[lane + 32 * q] : 0.0;
+  if (counts)
+    for (int j = threadIdx.x; j < 32 * KPL; j += blockDim.x) Hs[j] = 0;
   __syncthreads();
   double *Fw = Fs + (size_t)wid * R * d;
   for (int64_t g = (int64_t)blockIdx.x * 8 + wid; g < ngroups; g += (int64_t)gridDim.x * 8) {
@@ -652,9 +655,14 @@ __global__ void __launch_bounds__(256)
           ub[r[i]] = sqrt(v);
           lb[r[i]] = sqrt(v2);
         }
-        if (counts) atomicAdd(counts + vi, 1);
+        if (counts) atomicAdd(Hs + vi, 1);
       }
     }
+  }
+  if (counts) {  // one global atomic per (block, cluster)
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x)
+      if (Hs[j]) atomicAdd(counts + j, Hs[j]);
   }
 }
 
@@ -665,7 +673,7 @@ int launch_assign_small(const double *f, const double *fnorm, int64_t n, int64_t
                         const int32_t *rows, const int32_t *nrows_dev, double *ub, double *lb,
                         const int32_t *gate) {
   constexpr int R = 4;
-  const size_t smem = sizeof(double) * (32 * KPL * (d | 1) + 8 * R * d);
+  const size_t smem = sizeof(double) * (32 * KPL * (d | 1) + 8 * R * d) + sizeof(int32_t) * 32 * KPL;
   static size_t configured = 0;
   if (smem > configured) {
     CSC_TRY_CUDA(cudaFuncSetAttribute(assign_small_kernel<KPL, R>,
