@@ -1301,30 +1301,69 @@ __global__ void gather_cols_kernel(const double *__restrict__ src, int64_t n, in
 // one whose reference argmin cannot change; near-ties are always recomputed.
 // Labels, means and counts therefore follow kmeans.py:96-110.
 
-__global__ void bound_kernel(int64_t n, const int32_t *__restrict__ labels,
-                             double *__restrict__ ub, double *__restrict__ lb,
-                             const double *__restrict__ delta, const double *__restrict__ scal,
-                             const double *__restrict__ shalf, const double *__restrict__ fnorm,
-                             int32_t *__restrict__ cand, int32_t *__restrict__ flags,
-                             int32_t *__restrict__ counts, int64_t k) {
+constexpr int kBoundThreads = 256, kBoundRows = 4;  // rows per thread per chunk
+
+__global__ void __launch_bounds__(kBoundThreads)
+    bound_kernel(int64_t n, const int32_t *__restrict__ labels, double *__restrict__ ub,
+                 double *__restrict__ lb, const double *__restrict__ delta,
+                 const double *__restrict__ scal, const double *__restrict__ shalf,
+                 const double *__restrict__ fnorm, int32_t *__restrict__ cand,
+                 int32_t *__restrict__ flags, int32_t *__restrict__ counts, int64_t k) {
+  typedef cub::BlockScan<int, kBoundThreads> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_base;
   if (blockIdx.x == 0)  // cleared here (stream-ordered before label_hist_kernel)
     for (int64_t j = threadIdx.x; j < k; j += blockDim.x) counts[j] = 0;
   const bool force = flags[2] != 0;
   const double d1 = scal[1], d2 = scal[2], cmax = scal[4];
   const int j1 = (int)scal[3];
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    bool keep = false;
-    if (!force) {
-      const int a = labels[r];
-      const double u = ub[r] + delta[a];
-      const double l = lb[r] - (a == j1 ? d2 : d1);
-      const double eta = 1e-7 * (sqrt(fnorm[r]) + cmax);
-      keep = u + eta <= fmax(l, shalf[a]);
-      ub[r] = u;
-      lb[r] = l;
+  constexpr int U = kBoundRows, CH = kBoundThreads * kBoundRows;
+  // block-sized chunks of rows (lane-contiguous loads, all loads of a thread's
+  // rows issued before use); the candidate list grows by one atomic per chunk
+  // (a single counter: per-warp or per-row atomics serialise on its L2 slice)
+  for (int64_t base = blockIdx.x * (int64_t)CH; base < n; base += (int64_t)gridDim.x * CH) {
+    int64_t r[U];
+    int a[U];
+    double u[U], l[U], fn[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      r[q] = base + (int64_t)kBoundThreads * q + threadIdx.x;
+      if (r[q] < n && !force) {
+        a[q] = labels[r[q]];
+        u[q] = ub[r[q]];
+        l[q] = lb[r[q]];
+        fn[q] = fnorm[r[q]];
+      }
     }
-    if (!keep) cand[atomicAdd(flags, 1)] = (int32_t)r;
+    bool need[U];
+    int mine = 0;
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      need[q] = false;
+      if (r[q] < n) {
+        bool keep = false;
+        if (!force) {
+          const double uq = u[q] + delta[a[q]];
+          const double lq = l[q] - (a[q] == j1 ? d2 : d1);
+          const double eta = 1e-7 * (sqrt(fn[q]) + cmax);
+          keep = uq + eta <= fmax(lq, shalf[a[q]]);
+          ub[r[q]] = uq;
+          lb[r[q]] = lq;
+        }
+        need[q] = !keep;
+        mine += need[q] ? 1 : 0;
+      }
+    }
+    int off, total;
+    Scan(tmp).ExclusiveSum(mine, off, total);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(flags, total) : 0;
+    __syncthreads();
+    const int pos0 = s_base + off;
+    int w = 0;
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+      if (need[q]) cand[pos0 + w++] = (int32_t)r[q];
+    __syncthreads();  // tmp / s_base reuse
   }
 }
 
@@ -1875,7 +1914,8 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
     if ((rc = assign(nullptr, nullptr, counts, nullptr)) != CSC_OK) return rc;
   } else {
     // flags[0] (candidate count) was cleared by the previous iteration's finish
-    bound_kernel<<<grid_cap(csc::ceil_div(n, 256)), 256, 0, st>>>(
+    bound_kernel<<<grid_cap(csc::ceil_div(n, (int64_t)kBoundThreads * kBoundRows)), kBoundThreads, 0,
+                   st>>>(
         n, labels, p->ub, p->lb, p->delta, p->scal, p->shalf, fnorm, p->cand, p->flags, counts, k);
     CSC_CHECK_LAUNCH();
     if ((rc = assign(p->cand, p->flags, nullptr, nullptr)) != CSC_OK) return rc;
