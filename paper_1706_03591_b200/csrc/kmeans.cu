@@ -942,17 +942,34 @@ __global__ void update_partial_kernel(const double *__restrict__ f,
         }
         run += v;
       };
+      // rows rbeg + lane_sq + kSqLanes * t, in order; the next batch of UQ rows
+      // is loaded before the current one is added (16 loads in flight)
+      constexpr int UQ = 8;
       int64_t r = rbeg + lane_sq;
-      for (; r + 7 * kSqLanes < rend; r += 8 * kSqLanes) {
-        int32_t l[8];
-        double v[8];
+      int32_t la[UQ], lbq[UQ];
+      double va[UQ], vb[UQ];
+      auto load = [&](int64_t r0, int32_t (&l)[UQ], double (&v)[UQ]) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          l[u] = __ldg(labels + r + u * kSqLanes);
-          v[u] = __ldg(fnorm + r + u * kSqLanes);
+        for (int u = 0; u < UQ; ++u) {
+          l[u] = __ldg(labels + r0 + u * kSqLanes);
+          v[u] = __ldg(fnorm + r0 + u * kSqLanes);
         }
+      };
+      const int64_t step = (int64_t)UQ * kSqLanes;
+      if (r + step - kSqLanes < rend) load(r, la, va);
+      while (r + step - kSqLanes < rend) {
+        const bool more = r + 2 * step - kSqLanes < rend;
+        if (more) load(r + step, lbq, vb);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) add(l[u], v[u]);
+        for (int u = 0; u < UQ; ++u) add(la[u], va[u]);
+        r += step;
+        if (!more) break;
+        const bool more2 = r + 2 * step - kSqLanes < rend;
+        if (more2) load(r + step, la, va);
+#pragma unroll
+        for (int u = 0; u < UQ; ++u) add(lbq[u], vb[u]);
+        r += step;
+        if (!more2) break;
       }
       for (; r < rend; r += kSqLanes) add(labels[r], fnorm[r]);
       if (cur >= 0) mine[cur] = run;
