@@ -16,6 +16,7 @@ values the reference branches on.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -241,7 +242,16 @@ def _lloyd_pool(n, d, ld, k, dev) -> _LloydPool:
     return _LLOYD_POOL
 
 
+_POOL_LOCK = threading.Lock()  # the lanes / streams / buffers of the pool are shared state
+
+
 def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children):
+    """Thread-safe entry (the reference's kmeans is a pure function): one caller at a time."""
+    with _POOL_LOCK:
+        return _run_restarts(blk, d, k, cfg, children)
+
+
+def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children):
     """Every restart: batched k-means++ seeds, then the Lloyd runs on concurrent lanes.
 
     Each lane runs iteration 1 and a device-resident loop graph
