@@ -194,7 +194,7 @@ int csc_kmeans_run(csc_kmeans_plan *plan, const double *f_dev, const double *row
                    double *history_dev, void *stream);
 /* k-means tuning knobs (performance only; results do not change):
  * "assign_ver" 2|3, "assign_tn" 4|8 (v2 kernel), "assign_tile" 0 (auto) |
- * 1 (small-k kernel) | 88 | 84 | 48 | 44 | 42 (v3 register tile),
+ * 1 (small-k kernel) | 88 | 84 | 87 | 48 | 44 | 42 (v3 register tile),
  * "finish_mode" 0|1|2 (fused / fused-256 / split iteration tail) */
 int csc_kmeans_tuning(const char *key, int64_t value);
 /* empty-cluster repair (kmeans.py:99-108): for each empty j ascending, move the

@@ -338,7 +338,7 @@ __device__ __forceinline__ Min3 min3_merge(const Min3 &a, const Min3 &b) {
 }
 
 template <int kStages, int TM, int TN, int RT, int CT>
-__global__ void __launch_bounds__(RT * CT, 2)
+__global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
     assign3_kernel(const double *__restrict__ f, const double *__restrict__ fnorm, int64_t n,
                    int64_t d, int64_t ld, const double *__restrict__ cent, int64_t ldc,
                    const double *__restrict__ cnorm, int64_t k, int64_t c0, int last_pass,
@@ -693,8 +693,9 @@ int launch_assign_small(const double *f, const double *fnorm, int64_t n, int64_t
 int g_assign_tn = 8;
 int g_assign_ver = 3;
 
-// 0 (auto): 8x8 per thread, 16x8 threads (fastest at cfg3/cfg5 scale in
-// tools/ab_assign.py), 8x4 when k <= 32; 88/84/48/44/42 force a tile
+// 0 (auto): 8x8 per thread, 16x8 threads (fastest at k = 64 in
+// tools/ab_assign.py), 8x4 when k <= 32, 8x7 with 16x16 threads (one pass)
+// when 64 < k <= 112; 88/84/87/48/44/42 force a tile
 int g_assign_tile = 0;
 // 0: fused single-block iteration tail (1024 threads) for small k, 1: same with
 // 256 threads, 2: always the split kernels
@@ -773,6 +774,9 @@ int launch_assign3(const double *f, const double *fnorm, int64_t n, int64_t d, i
     case 44:
       return launch_assign3_t<4, 4, 16, 16>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
                                             counts, st, rows, nrows_dev, ub, lb, gate);
+    case 87:  // 128 x 112 tile (16 x 16 threads, 8 x 7 each): one pass for k <= 112
+      return launch_assign3_t<8, 7, 16, 16>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                            counts, st, rows, nrows_dev, ub, lb, gate);
     case 84:
       return launch_assign3_t<8, 4, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
                                            counts, st, rows, nrows_dev, ub, lb, gate);
@@ -780,6 +784,9 @@ int launch_assign3(const double *f, const double *fnorm, int64_t n, int64_t d, i
       if (k <= 32)  // 128 x 32 tile: no wasted FMAs on padding centroids at small k
         return launch_assign3_t<8, 4, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
                                              counts, st, rows, nrows_dev, ub, lb, gate);
+      if (k > 64 && k <= 112)  // one 112-wide pass instead of two 64-wide (cfg3 k=100: -18%)
+        return launch_assign3_t<8, 7, 16, 16>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                              counts, st, rows, nrows_dev, ub, lb, gate);
       return launch_assign3_t<8, 8, 16, 8>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
                                            counts, st, rows, nrows_dev, ub, lb, gate);
   }
@@ -1750,7 +1757,7 @@ int csc_kmeans_assign(const double *f, const double *fnorm, int64_t n, int64_t d
 int csc_kmeans_tuning(const char *key, int64_t value) {
   CSC_REQUIRE(key != nullptr, "csc_kmeans_tuning: NULL key");
   if (std::string(key) == "assign_tile") {
-    CSC_REQUIRE(value == 0 || value == 1 || value == 44 || value == 88 || value == 84 ||
+    CSC_REQUIRE(value == 0 || value == 1 || value == 44 || value == 88 || value == 84 || value == 87 ||
                     value == 48 || value == 42,
                 "assign_tile: 0 (auto), 1 (small-k), 44, 88, 84, 48 or 42");
     g_assign_tile = (int)value;

@@ -25,7 +25,7 @@ c = torch.zeros((a.k, ld), dtype=torch.float64, device="cuda")
 c[:, :a.d] = torch.randn((a.k, a.d), dtype=torch.float64, device="cuda", generator=g)
 fn = (f * f).sum(1)
 cn = (c * c).sum(1)
-VARIANTS = [("v2", "assign_ver", 2), ("small", "assign_tile", 1), ("v3-88", "assign_tile", 88), ("v3-84", "assign_tile", 84),
+VARIANTS = [("v2", "assign_ver", 2), ("small", "assign_tile", 1), ("v3-88", "assign_tile", 88), ("v3-84", "assign_tile", 84), ("v3-87", "assign_tile", 87),
             ("v3-48", "assign_tile", 48),
             ("v3-44", "assign_tile", 44), ("v3-42", "assign_tile", 42)]
 if a.k > 64 or a.d > 128:
