@@ -16,6 +16,7 @@ values the reference branches on.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from dataclasses import dataclass
 
@@ -296,8 +297,9 @@ def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children
     best = None  # (cost2, restart); the reference keeps the earliest on ties (strict <)
     best_labels = None
     checked = False
-    for w0 in range(0, R, _LloydPool.MAX_LANES):
-        wave = list(range(w0, min(R, w0 + _LloydPool.MAX_LANES)))
+    width = max(1, min(_LloydPool.MAX_LANES, int(os.environ.get("CSC_KMEANS_LANES", _LloydPool.MAX_LANES))))
+    for w0 in range(0, R, width):
+        wave = list(range(w0, min(R, w0 + width)))
         run_wave(wave)
         if not checked:  # the cost read above synchronised: the seeding flags are final
             checked = True
