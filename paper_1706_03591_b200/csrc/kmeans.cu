@@ -1167,9 +1167,10 @@ __global__ void __launch_bounds__(1024)
 
 // closest[r][i] = (first ? d2 : min(closest, d2)), d2 = |f_i - crow_r|^2, for r < R;
 // chunk_sums[r][b] = sum of closest[r] over contiguous chunk b (block b).
+template <int R>  // restarts in the batch (1..16), compile-time: no predicated lanes
 __global__ void __launch_bounds__(128)
     kppb_dist_kernel(const double *__restrict__ f, int64_t n, int64_t d, int64_t ld,
-                     const double *__restrict__ crows, int64_t crow_stride, int R,
+                     const double *__restrict__ crows, int64_t crow_stride,
                      double *__restrict__ closest, int first, int64_t chunk,
                      double *__restrict__ chunk_sums, int64_t nchunks) {
   // thread per row: one pass over the row serves all R restarts (no shuffles)
@@ -1183,41 +1184,37 @@ __global__ void __launch_bounds__(128)
   }
   __syncthreads();
   const int64_t rbeg = blockIdx.x * chunk, rend = min(n, rbeg + chunk);
-  double part[16];
+  double part[R];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) part[r] = 0.0;
+  for (int r = 0; r < R; ++r) part[r] = 0.0;
   for (int64_t i = rbeg + threadIdx.x; i < rend; i += blockDim.x) {
     const double *row = f + i * ld;
-    double acc[16];
+    double acc[R];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
     for (int64_t c = 0; c < d; ++c) {
       const double x = __ldg(row + c);
 #pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if (r < R) {
-          const double t = x - cs[r * d + c];
-          acc[r] = fma(t, t, acc[r]);
-        }
+      for (int r = 0; r < R; ++r) {
+        const double t = x - cs[r * d + c];
+        acc[r] = fma(t, t, acc[r]);
+      }
     }
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if (r < R) {
-        double *slot = closest + (int64_t)r * n + i;
-        const double cl = first ? acc[r] : fmin(*slot, acc[r]);
-        *slot = cl;
-        part[r] += cl;
-      }
+    for (int r = 0; r < R; ++r) {
+      double *slot = closest + (int64_t)r * n + i;
+      const double cl = first ? acc[r] : fmin(*slot, acc[r]);
+      *slot = cl;
+      part[r] += cl;
+    }
   }
   // fixed-order block sums per restart: warp shuffle tree, then warps in order
 #pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    if (r < R) {
-      double v = part[r];
+  for (int r = 0; r < R; ++r) {
+    double v = part[r];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) wsum[wid * R + r] = v;
-    }
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) wsum[wid * R + r] = v;
   }
   __syncthreads();
   if (threadIdx.x < R) {
@@ -2160,9 +2157,22 @@ int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_
       CSC_CHECK_LAUNCH();
     }
     if (j < k - 1) {
-      kppb_dist_kernel<<<(unsigned)nchunks, 128, smem, st>>>(
-          f, n, d, ld, cent + j * ldc, cent_stride, (int)R, closest.as<double>(), j == 0 ? 1 : 0,
-          chunk, sums.as<double>(), nchunks);
+      switch (R) {
+#define CSC_KPPB_CASE(RR)                                                                      \
+  case RR:                                                                                     \
+    kppb_dist_kernel<RR><<<(unsigned)nchunks, 128, smem, st>>>(                                \
+        f, n, d, ld, cent + j * ldc, cent_stride, closest.as<double>(), j == 0 ? 1 : 0, chunk, \
+        sums.as<double>(), nchunks);                                                           \
+    break;
+        CSC_KPPB_CASE(1) CSC_KPPB_CASE(2) CSC_KPPB_CASE(3) CSC_KPPB_CASE(4)
+        CSC_KPPB_CASE(5) CSC_KPPB_CASE(6) CSC_KPPB_CASE(7) CSC_KPPB_CASE(8)
+        CSC_KPPB_CASE(9) CSC_KPPB_CASE(10) CSC_KPPB_CASE(11) CSC_KPPB_CASE(12)
+        CSC_KPPB_CASE(13) CSC_KPPB_CASE(14) CSC_KPPB_CASE(15) CSC_KPPB_CASE(16)
+#undef CSC_KPPB_CASE
+        default:
+          csc::set_error("csc_kmeanspp_batch: R=%lld out of range", (long long)R);
+          return CSC_ERR_ARG;
+      }
       CSC_CHECK_LAUNCH();
     }
   }
