@@ -17,7 +17,9 @@
 //           single-block D^2 draw for one host-supplied uniform
 //           (Generator.choice(n, p) == searchsorted(cumsum(p), u, 'right')).
 #include <cub/cub.cuh>
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -1705,7 +1707,7 @@ struct csc_kmeans_plan {
   int hist_cap = 0;
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
-  const void *key[8] = {};
+  const void *key[12] = {};
 };
 
 extern "C" {
@@ -2005,73 +2007,111 @@ int csc_kmeans_run(csc_kmeans_plan *p, const double *f, const double *fnorm, dou
       p->graph = nullptr;
     }
   }
-  loop_init_kernel<<<1, 1, 0, st>>>(p->loop, tol, max_iters);
-  CSC_CHECK_LAUNCH();
-  // |c_j|^2 of the seeds (the GEMM-form distances of iteration 1 need them)
-  centroid_norms_kernel<<<(unsigned)csc::ceil_div(p->k, 8), 256, 0, st>>>(cent, ldc, p->d, p->k,
-                                                                         cnorm);
-  CSC_CHECK_LAUNCH();
-  if (max_iters >= 1) {
-    int rc = csc_kmeans_iterate(p, f, fnorm, cent, ldc, cnorm, labels, counts, 1, nullptr, st);
-    if (rc != CSC_OK) return rc;
-    loop_check_kernel<<<1, 1, 0, st>>>(p->scal, p->loop, p->history, p->hist_cap, 0, 0);
-    CSC_CHECK_LAUNCH();
-  }
-  if (max_iters >= 2) {
-    const void *key[8] = {f, fnorm, cent, cnorm, labels, counts, (const void *)(intptr_t)ldc,
-                          nullptr};
-    bool same = p->exec != nullptr;
-    for (int i = 0; i < 8 && same; ++i) same = key[i] == p->key[i];
-    if (!same) {
-      if (p->exec) {
-        cudaGraphExecDestroy(p->exec);
-        cudaGraphDestroy(p->graph);
-        p->exec = nullptr;
+  // The whole call is one graph per buffer set (one launch per restart lane):
+  // [init, |c|^2 of the seeds, full iteration 1, stop check] -> while(pruned
+  // iteration + stop check) -> [exact cost, iteration count, history copy].
+  double tol_key = tol;
+  int64_t tol_bits = 0;
+  memcpy(&tol_bits, &tol_key, sizeof(tol_bits));
+  const void *key[12] = {f, fnorm, cent, cnorm, labels, counts, (const void *)(intptr_t)ldc,
+                         out_dev, history_dev, (const void *)(intptr_t)max_iters,
+                         (const void *)(intptr_t)tol_bits, nullptr};
+  bool same = p->exec != nullptr;
+  for (int i = 0; i < 12 && same; ++i) same = key[i] == p->key[i];
+  if (!same) {
+    if (p->exec) {
+      cudaGraphExecDestroy(p->exec);
+      cudaGraphDestroy(p->graph);
+      p->exec = nullptr;
+      p->graph = nullptr;
+    }
+    cudaGraph_t g;
+    CSC_TRY_CUDA(cudaGraphCreate(&g, 0));
+    cudaStream_t cap_st;
+    CSC_TRY_CUDA(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
+    int rc = CSC_OK;
+    cudaError_t ec = cudaSuccess;
+    std::vector<cudaGraphNode_t> tail;
+    auto end_capture = [&]() {
+      const cudaGraphNode_t *deps = nullptr;
+      size_t ndeps = 0;
+      cudaStreamCaptureStatus status;
+      cudaError_t e = cudaStreamGetCaptureInfo(cap_st, &status, nullptr, nullptr, &deps, &ndeps);
+      if (e == cudaSuccess) tail.assign(deps, deps + ndeps);
+      cudaGraph_t captured;
+      const cudaError_t e2 = cudaStreamEndCapture(cap_st, &captured);
+      return e != cudaSuccess ? e : e2;
+    };
+    // prefix
+    ec = cudaStreamBeginCaptureToGraph(cap_st, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+    if (ec == cudaSuccess) {
+      loop_init_kernel<<<1, 1, 0, cap_st>>>(p->loop, tol, max_iters);
+      centroid_norms_kernel<<<(unsigned)csc::ceil_div(p->k, 8), 256, 0, cap_st>>>(cent, ldc, p->d,
+                                                                                 p->k, cnorm);
+      if (max_iters >= 1) {
+        rc = csc_kmeans_iterate(p, f, fnorm, cent, ldc, cnorm, labels, counts, 1, nullptr, cap_st);
+        loop_check_kernel<<<1, 1, 0, cap_st>>>(p->scal, p->loop, p->history, p->hist_cap, 0, 0);
       }
-      cudaGraph_t g;
-      CSC_TRY_CUDA(cudaGraphCreate(&g, 0));
+      ec = end_capture();
+    }
+    // while (stop check says go): pruned iteration + stop check
+    if (ec == cudaSuccess && rc == CSC_OK && max_iters >= 2) {
       cudaGraphConditionalHandle h;
-      CSC_TRY_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+      ec = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
       cudaGraphNodeParams cp = {};
       cp.type = cudaGraphNodeTypeConditional;
       cp.conditional.handle = h;
       cp.conditional.type = cudaGraphCondTypeWhile;
       cp.conditional.size = 1;
       cudaGraphNode_t node;
-      CSC_TRY_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
-      cudaGraph_t body = cp.conditional.phGraph_out[0];
-      cudaStream_t cap_st;
-      CSC_TRY_CUDA(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
-      CSC_TRY_CUDA(cudaStreamBeginCaptureToGraph(cap_st, body, nullptr, nullptr, 0,
-                                                 cudaStreamCaptureModeRelaxed));
-      int rc = csc_kmeans_iterate(p, f, fnorm, cent, ldc, cnorm, labels, counts, 0, nullptr,
-                                  cap_st);
-      loop_check_kernel<<<1, 1, 0, cap_st>>>(p->scal, p->loop, p->history, p->hist_cap, h, 1);
-      cudaGraph_t captured;
-      const cudaError_t ec = cudaStreamEndCapture(cap_st, &captured);
-      cudaStreamDestroy(cap_st);
-      p->stream = st;
-      if (rc != CSC_OK) return rc;
-      CSC_TRY_CUDA(ec);
-      CSC_TRY_CUDA(cudaGraphInstantiate(&p->exec, g, 0));
-      p->graph = g;
-      for (int i = 0; i < 8; ++i) p->key[i] = key[i];
+      if (ec == cudaSuccess) ec = cudaGraphAddNode(&node, g, tail.data(), tail.size(), &cp);
+      if (ec == cudaSuccess) {
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        ec = cudaStreamBeginCaptureToGraph(cap_st, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed);
+        if (ec == cudaSuccess) {
+          rc = csc_kmeans_iterate(p, f, fnorm, cent, ldc, cnorm, labels, counts, 0, nullptr, cap_st);
+          loop_check_kernel<<<1, 1, 0, cap_st>>>(p->scal, p->loop, p->history, p->hist_cap, h, 1);
+          cudaGraph_t captured;
+          ec = cudaStreamEndCapture(cap_st, &captured);
+        }
+        tail.assign(1, node);
+      }
     }
-    CSC_TRY_CUDA(cudaGraphLaunch(p->exec, st));
+    // suffix: out_dev[0] = cost2 of the last iteration in the exact difference
+    // form (kmeans.py:111), out_dev[1] = iterations run (as double)
+    if (ec == cudaSuccess && rc == CSC_OK) {
+      ec = cudaStreamBeginCaptureToGraph(cap_st, g, tail.data(), nullptr, tail.size(),
+                                         cudaStreamCaptureModeRelaxed);
+      if (ec == cudaSuccess) {
+        if (max_iters >= 1) {
+          cost_kernel<<<cost_grid, 256, 0, cap_st>>>(f, labels, cent, ldc, p->n, p->d, p->ld,
+                                                      p->cost_parts);
+          reduce_partials_kernel<<<1, 1024, 0, cap_st>>>(p->cost_parts, cost_grid, out_dev);
+        }
+        if (history_dev)
+          cudaMemcpyAsync(history_dev, p->history, sizeof(double) * cap, cudaMemcpyDeviceToDevice,
+                          cap_st);
+        copy_iters_kernel<<<1, 1, 0, cap_st>>>(p->loop, out_dev + 1, max_iters >= 1);
+        cudaGraph_t captured;
+        ec = cudaStreamEndCapture(cap_st, &captured);
+      }
+    }
+    cudaStreamDestroy(cap_st);
+    p->stream = st;
+    if (rc != CSC_OK) {
+      cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ec != cudaSuccess) {
+      cudaGraphDestroy(g);
+      CSC_TRY_CUDA(ec);
+    }
+    CSC_TRY_CUDA(cudaGraphInstantiate(&p->exec, g, 0));
+    p->graph = g;
+    for (int i = 0; i < 12; ++i) p->key[i] = key[i];
   }
-  // out_dev[0] = cost2 of the last iteration in the exact difference form
-  // (kmeans.py:111), out_dev[1] = iterations run (as double)
-  if (max_iters >= 1) {
-    cost_kernel<<<cost_grid, 256, 0, st>>>(f, labels, cent, ldc, p->n, p->d, p->ld, p->cost_parts);
-    CSC_CHECK_LAUNCH();
-    reduce_partials_kernel<<<1, 1024, 0, st>>>(p->cost_parts, cost_grid, out_dev);
-    CSC_CHECK_LAUNCH();
-  }
-  if (history_dev)
-    CSC_TRY_CUDA(cudaMemcpyAsync(history_dev, p->history, sizeof(double) * cap,
-                                 cudaMemcpyDeviceToDevice, st));
-  copy_iters_kernel<<<1, 1, 0, st>>>(p->loop, out_dev + 1, max_iters >= 1);
-  CSC_CHECK_LAUNCH();
+  CSC_TRY_CUDA(cudaGraphLaunch(p->exec, st));
   return CSC_OK;
 }
 
