@@ -246,13 +246,14 @@ def _lloyd_pool(n, d, ld, k, dev) -> _LloydPool:
 _POOL_LOCK = threading.Lock()  # the lanes / streams / buffers of the pool are shared state
 
 
-def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children):
-    """Thread-safe entry (the reference's kmeans is a pure function): one caller at a time."""
+def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, draws=None):
+    """Thread-safe entry (the reference's kmeans is a pure function): one caller at a time.
+    `draws` (optional) = kmeanspp_draws(children, n, k) made ahead of time."""
     with _POOL_LOCK:
-        return _run_restarts(blk, d, k, cfg, children)
+        return _run_restarts(blk, d, k, cfg, children, draws)
 
 
-def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children):
+def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, draws=None):
     """Every restart: batched k-means++ seeds, then the Lloyd runs on concurrent lanes.
 
     Each lane runs iteration 1 and a device-resident loop graph
@@ -269,7 +270,7 @@ def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children
     _native.call("csc_kmeans_rownorms", ptr(pool.F), n, d, ld, ptr(ws.fnorm), stream())
     # seeds are used right away; the rare zero-mass replay is checked at the
     # first host synchronisation and its restarts re-run (kmeans.py:70-72)
-    seeds, bad_restarts, replay = batched_kmeanspp(ws, children, defer_check=True)
+    seeds, bad_restarts, replay = batched_kmeanspp(ws, children, defer_check=True, draws=draws)
     R = len(children)
     costs: dict[int, float] = {}
     held: dict[int, int] = {}  # restart -> lane whose labels are still current
@@ -321,7 +322,18 @@ def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children
 KPP_BATCH = 16  # restarts per batched k-means++ launch series (libcscb200 limit)
 
 
-def batched_kmeanspp(ws: _Workspace, children, defer_check: bool = False):
+def kmeanspp_draws(children, n: int, k: int):
+    """Host RNG draws of every restart's k-means++ in the reference's order
+    (kmeans.py:67-74): integers(n) for the first centroid, then k-1 random()
+    (what Generator.choice(n, p) consumes). Returns (first int64[R], unif[R, k-1])."""
+    rngs = [np.random.default_rng(c) for c in children]
+    first = np.array([int(rng.integers(n)) for rng in rngs], dtype=np.int64)
+    unif = np.ascontiguousarray(np.stack([rng.random(k - 1) for rng in rngs]) if k > 1
+                                else np.zeros((len(rngs), 1)))
+    return first, unif
+
+
+def batched_kmeanspp(ws: _Workspace, children, defer_check: bool = False, draws=None):
     """k-means++ seeds of every restart: (restarts, k, ldc) on the GPU.
 
     Each restart's stream is drawn on the host in the reference's order
@@ -334,12 +346,11 @@ def batched_kmeanspp(ws: _Workspace, children, defer_check: bool = False):
     seeds = torch.zeros((R, k, ws.ldc), dtype=torch.float64, device=ws.blk.device)
     ngroups = (R + KPP_BATCH - 1) // KPP_BATCH
     flags = torch.empty((ngroups, KPP_BATCH), dtype=torch.int32, device=ws.blk.device)
+    all_first, all_unif = draws if draws is not None else kmeanspp_draws(children, n, k)
     for gidx, g0 in enumerate(range(0, R, KPP_BATCH)):
         grp = list(range(g0, min(R, g0 + KPP_BATCH)))
-        rngs = [np.random.default_rng(children[r]) for r in grp]
-        first = np.array([int(rng.integers(n)) for rng in rngs], dtype=np.int64)
-        unif = np.ascontiguousarray(np.stack([rng.random(k - 1) for rng in rngs]) if k > 1
-                                    else np.zeros((len(grp), 1)))
+        first = np.ascontiguousarray(all_first[g0:g0 + len(grp)])
+        unif = np.ascontiguousarray(all_unif[g0:g0 + len(grp)])
         _native.call("csc_kmeanspp_batch", ptr(ws.blk), n, ws.d, ws.ld, len(grp), k,
                      first.ctypes.data, unif.ctypes.data, ptr(seeds[g0]), ws.ldc, ptr(flags[gidx]), stream())
 
@@ -396,7 +407,14 @@ def kmeans(f, k: int, cfg: KmeansConfig | None = None, seed=0) -> Assignment:
     if not 1 <= k <= n:
         raise ValueError(f"need 1 <= k <= n, got k={k}, n={n}")
     children = as_seed_sequence(seed).spawn(cfg.restarts)
-    labels, cost2 = run_restarts(blk, d, k, cfg, children)
+    return _kmeans_prepared(blk, d, k, cfg, children, None)
+
+
+def _kmeans_prepared(blk, d: int, k: int, cfg: KmeansConfig, children, draws) -> Assignment:
+    """kmeans() after validation, with the restarts' streams (and optionally their
+    k-means++ draws) already made — the dynamic step draws them while the GPU
+    filters."""
+    labels, cost2 = run_restarts(blk, d, k, cfg, children, draws)
     sizes = np.bincount(labels, minlength=k)
     return Assignment(labels, sizes, float(np.sqrt(max(cost2, 0.0))))
 
