@@ -1440,6 +1440,128 @@ __global__ void gated_repair_kernel(int32_t *__restrict__ labels, double *__rest
 
 // warp per (centroid j, column c): S[j][c] = sum of the block partials in
 // order; the extra warp per j adds the counts and the |f|^2 partials.
+// Block partial sums over a label-sorted chunk. A stable counting sort of the
+// chunk's rows by label (shared memory, warp match ranks) makes every
+// cluster's rows one contiguous run in increasing row order, so each column
+// thread sums a run in a register (0.0 + v1 + v2 + ..., the same additions in
+// the same order as update_partial_kernel's per-row shared-memory adds, so
+// psum is bit-identical) with the next rows' loads in flight, and writes the
+// run's total straight to psum. Counts are the run lengths; |f|^2 per cluster
+// is summed over its run in row order by the extra warp.
+constexpr int kSortedMaxChunk = 8192;
+
+__global__ void update_sorted_kernel(const double *__restrict__ f,
+                                     const int32_t *__restrict__ labels, int64_t n, int64_t d,
+                                     int64_t ld, int64_t k, int64_t chunk, int cw,
+                                     double *__restrict__ psum, int32_t *__restrict__ pcnt,
+                                     const double *__restrict__ fnorm, double *__restrict__ pq) {
+  extern __shared__ int32_t us[];
+  int32_t *lab_s = us;             // [chunk] labels in sorted order
+  int32_t *perm_s = lab_s + chunk;  // [chunk] row offsets in sorted order
+  int32_t *cnt_s = perm_s + chunk;  // [k] rows per label
+  int32_t *run_s = cnt_s + k;       // [k] insert position, then end of each run
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t b = blockIdx.x;
+  const int64_t col0 = (int64_t)blockIdx.y * cw;
+  const int64_t rbeg = b * chunk;
+  const int len = (int)max((int64_t)0, min(n, rbeg + chunk) - rbeg);
+  for (int64_t j = tid; j < k; j += blockDim.x) cnt_s[j] = 0;
+  __syncthreads();
+  for (int p = tid; p < len; p += blockDim.x) atomicAdd(cnt_s + labels[rbeg + p], 1);
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int64_t j = 0; j < k; ++j) {
+      run_s[j] = acc;
+      acc += cnt_s[j];
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {  // stable scatter, 32 rows at a time in order
+    for (int g = 0; g < len; g += 32) {
+      const int p = g + lane;
+      const int l = p < len ? labels[rbeg + p] : -1;
+      const unsigned m = __match_any_sync(0xffffffffu, l);
+      const int rank = __popc(m & ((1u << lane) - 1u));
+      if (p < len) {
+        const int pos = run_s[l] + rank;
+        perm_s[pos] = p;
+        lab_s[pos] = l;
+      }
+      __syncwarp();
+      if (p < len && rank == __popc(m) - 1) run_s[l] += __popc(m);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  const int c = tid;
+  if (c < cw && col0 + c < d) {
+    const double *fc = f + col0 + c;
+    double *out = psum + b * k * d + col0 + c;
+    int cur = -1;
+    double run = 0.0;
+    constexpr int U = 16;  // rows per batch; the next batch is loaded before adding this one
+    int p = 0;
+    double va[U], vb[U];
+    int la[U], lb2[U];
+    auto load = [&](int p0, double (&v)[U], int (&l)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = __ldg(fc + (rbeg + perm_s[p0 + u]) * ld);
+        l[u] = lab_s[p0 + u];
+      }
+    };
+    auto add = [&](const double (&v)[U], const int (&l)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (l[u] != cur) {
+          if (cur >= 0) out[(int64_t)cur * d] = run;
+          cur = l[u];
+          run = 0.0;
+        }
+        run += v[u];
+      }
+    };
+    if (p + U <= len) load(p, va, la);
+    while (p + U <= len) {
+      const bool more = p + 2 * U <= len;
+      if (more) load(p + U, vb, lb2);
+      add(va, la);
+      p += U;
+      if (!more) break;
+      const bool more2 = p + 2 * U <= len;
+      if (more2) load(p + U, va, la);
+      add(vb, lb2);
+      p += U;
+      if (!more2) break;
+    }
+    for (; p < len; ++p) {
+      const int l = lab_s[p];
+      const double v = fc[(rbeg + perm_s[p]) * ld];
+      if (l != cur) {
+        if (cur >= 0) out[(int64_t)cur * d] = run;
+        cur = l;
+        run = 0.0;
+      }
+      run += v;
+    }
+    if (cur >= 0) out[(int64_t)cur * d] = run;
+    for (int64_t j = 0; j < k; ++j)
+      if (cnt_s[j] == 0) out[j * d] = 0.0;
+  }
+  if (blockIdx.y == 0 && tid >= (int)blockDim.x - 32) {
+    for (int64_t j = lane; j < k; j += 32) {
+      pcnt[b * k + j] = cnt_s[j];
+      if (pq) {
+        const int end = run_s[j], beg = end - cnt_s[j];
+        double q = 0.0;
+        for (int pp = beg; pp < end; ++pp) q += fnorm[rbeg + perm_s[pp]];
+        pq[b * k + j] = q;
+      }
+    }
+  }
+}
+
 __global__ void sums_finish_kernel(const double *__restrict__ psum,
                                    const int32_t *__restrict__ pcnt,
                                    const double *__restrict__ pq, int64_t nb, int64_t d,
@@ -1881,6 +2003,10 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t) * 4, st));
   CSC_TRY_CUDA(cudaFuncSetAttribute(update_partial_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
+  if (p->chunk <= kSortedMaxChunk)
+    CSC_TRY_CUDA(cudaFuncSetAttribute(
+        update_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (int)(sizeof(int32_t) * (2 * (size_t)p->chunk + 2 * (size_t)k))));
   *out = p;
   return CSC_OK;
 }
@@ -1956,8 +2082,14 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
   CSC_CHECK_LAUNCH();
   // means, counts, movement, cost terms
   const int threads = (int)(csc::ceil_div(p->cw, 32) * 32 + 32);
-  update_partial_kernel<<<dim3((unsigned)p->nb, (unsigned)p->ny), threads, p->smem, st>>>(
-      f, labels, n, d, ld, k, p->chunk, (int)p->cw, p->psum, p->pcnt, fnorm, p->pq);
+  if (p->chunk <= kSortedMaxChunk) {
+    const size_t ssmem = sizeof(int32_t) * (2 * (size_t)p->chunk + 2 * (size_t)k);
+    update_sorted_kernel<<<dim3((unsigned)p->nb, (unsigned)p->ny), threads, ssmem, st>>>(
+        f, labels, n, d, ld, k, p->chunk, (int)p->cw, p->psum, p->pcnt, fnorm, p->pq);
+  } else {
+    update_partial_kernel<<<dim3((unsigned)p->nb, (unsigned)p->ny), threads, p->smem, st>>>(
+        f, labels, n, d, ld, k, p->chunk, (int)p->cw, p->psum, p->pcnt, fnorm, p->pq);
+  }
   CSC_CHECK_LAUNCH();
   const int64_t warps = k * (d + 1);
   sums_finish_kernel<<<(unsigned)csc::ceil_div(warps, 8), 256, 0, st>>>(
