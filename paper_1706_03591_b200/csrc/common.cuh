@@ -46,6 +46,7 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
     if (e_ != cudaSuccess) {                                                           \
       csc::set_error("%s:%d: %s failed: %s", __FILE__, __LINE__, #expr,                \
                      cudaGetErrorString(e_));                                          \
+      (void)cudaGetLastError(); /* consumed: must not resurface in a later call */    \
       return CSC_ERR_CUDA;                                                             \
     }                                                                                  \
   } while (0)

@@ -155,12 +155,20 @@ __global__ void __launch_bounds__(kAssignThreads)
 // cp.async double buffering (zero-fill outside the matrix). FP64-FMA bound.
 // ---------------------------------------------------------------------------
 constexpr int kAM = 128, kAN = 64, kAK = 16, kAKP = kAK + 2, kANP = kAN + 1;
+// assign3 keeps a per-block label histogram in shared memory up to this k
+constexpr int64_t kHistMax = 8192;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
   const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
   const int src_size = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
                "r"(src_size));
+}
+// 16-byte cp.async copying the first `bytes` (0, 8 or 16) and zero-filling the rest
+__device__ __forceinline__ void cp_async_bytes16(void *smem, const void *gmem, int bytes) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -339,7 +347,11 @@ __device__ __forceinline__ Min3 min3_merge(const Min3 &a, const Min3 &b) {
   return r;
 }
 
-template <int kStages, int TM, int TN, int RT, int CT>
+// SC (streamed centroids): when the whole dpad x BN centroid tile does not fit
+// in shared memory (large d), each kAK slice of it rides the cp.async stage
+// ring with the row slices ([kStages][BN][kAKP], same loader) instead of
+// being resident. Same FMA order, so results are bit-identical.
+template <int kStages, int TM, int TN, int RT, int CT, bool SC = false>
 __global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
     assign3_kernel(const double *__restrict__ f, const double *__restrict__ fnorm, int64_t n,
                    int64_t d, int64_t ld, const double *__restrict__ cent, int64_t ldc,
@@ -357,12 +369,14 @@ __global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
   if (gate && *gate == 0) return;
   extern __shared__ __align__(16) double smem[];
   const int64_t dpad = (d + kAK - 1) / kAK * kAK;
-  double *Cs = smem;                          // [dpad][BNP]
-  double *Fs = Cs + dpad * BNP;               // [kStages][BM][kAKP]
+  double *Cs = smem;                          // [dpad][BNP] ([kStages][BN][kAKP] if SC)
+  double *Fs = Cs + (SC ? kStages * BN * kAKP : dpad * BNP);  // [kStages][BM][kAKP]
   double *Fn = Fs + kStages * BM * kAKP;      // [NB][BM] |f|^2 of the tile's rows
   double *Cn = Fn + NB * BM;                  // [BN] |c|^2 (+inf past k)
   int32_t *Rid = reinterpret_cast<int32_t *>(Cn + BN);  // [NB][BM] row ids (-1: padding)
-  int32_t *Hs = Rid + NB * BM;  // [k] block histogram of the final labels (counts != nullptr)
+  // [k] block histogram of the final labels (counts != nullptr and k <= kHistMax)
+  int32_t *Hs = Rid + NB * BM;
+  const bool hist = counts != nullptr && k <= kHistMax;
   const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;
   const int64_t ntiles = (nr + BM - 1) / BM;
   if ((int64_t)blockIdx.x >= ntiles) return;
@@ -371,13 +385,14 @@ __global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
   const int nst = (int)(dpad / kAK);
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int64_t total = my_tiles * nst;
-  for (int64_t e = tid; e < dpad * BN; e += NT) {
-    const int64_t cc = e / dpad, dd = e - cc * dpad;
-    Cs[dd * BNP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
-  }
+  if (!SC)
+    for (int64_t e = tid; e < dpad * BN; e += NT) {
+      const int64_t cc = e / dpad, dd = e - cc * dpad;
+      Cs[dd * BNP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
+    }
   // padding columns get |c|^2 = +inf, so their distance is +inf without a select
   for (int cc = tid; cc < BN; cc += NT) Cn[cc] = c0 + cc < k ? cnorm[c0 + cc] : INFINITY;
-  if (counts)
+  if (hist)
     for (int64_t j = tid; j < k; j += NT) Hs[j] = 0;
   // tile table of block-local tile t (ring slot b): row ids, and |f|^2 by
   // cp.async (joins the current commit group, landing with the stage loads)
@@ -412,6 +427,18 @@ __global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
       const bool ok = col_ok && gr >= 0;
       cp_async16(buf + row * kAKP + 2 * vc, ok ? fk + (size_t)(unsigned)gr * ld8 : (const char *)f,
                  ok);
+    }
+    if (SC) {  // this stage's centroid slice; columns >= d zero-filled
+      const int64_t rem = d - gc;
+      const int cbytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+      double *cb = Cs + l_buf * (BN * kAKP);
+#pragma unroll
+      for (int q = 0; q < (BN * 8 + NT - 1) / NT; ++q) {
+        const int cc = (tid >> 3) + (NT / 8) * q;
+        if (cc >= BN) break;
+        const int nb = c0 + cc < k ? cbytes : 0;
+        cp_async_bytes16(cb + cc * kAKP + 2 * vc, nb ? cent + (c0 + cc) * ldc + gc : cent, nb);
+      }
     }
     if (++l_st == nst) {
       l_st = 0;
@@ -453,14 +480,15 @@ __global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
     }
     const double *Fb = Fs + c_buf * (BM * kAKP);
-    const double *Cb = Cs + st * (kAK * BNP);
+    const double *Cb = SC ? Cs + c_buf * (BN * kAKP) : Cs + st * (kAK * BNP);
 #pragma unroll
     for (int kk = 0; kk < kAK; ++kk) {
       double a[TM], b[TN];
 #pragma unroll
       for (int i = 0; i < TM; ++i) a[i] = Fb[(ty + RT * i) * kAKP + kk];
 #pragma unroll
-      for (int j = 0; j < TN; ++j) b[j] = Cb[kk * BNP + tx + CT * j];
+      for (int j = 0; j < TN; ++j)
+        b[j] = SC ? Cb[(tx + CT * j) * kAKP + kk] : Cb[kk * BNP + tx + CT * j];
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -534,7 +562,10 @@ __global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
               ub[r] = sqrt(v);
               lb[r] = sqrt(v2);
             }
-            if (counts) atomicAdd(Hs + vi, 1);
+            if (hist)
+              atomicAdd(Hs + vi, 1);
+            else if (counts)
+              atomicAdd(counts + vi, 1);
           } else {
             lb[r] = v2;  // carried (squared) second minimum for the next pass
           }
@@ -547,7 +578,7 @@ __global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
     }
     c_buf = c_buf + 1 == kStages ? 0 : c_buf + 1;
   }
-  if (counts) {  // one global atomic per (block, cluster) instead of one per row
+  if (hist) {  // one global atomic per (block, cluster) instead of one per row
     __syncthreads();
     for (int64_t j = tid; j < k; j += NT)
       if (Hs[j]) atomicAdd(counts + j, Hs[j]);
@@ -705,7 +736,18 @@ int g_finish_mode = 0;
 // auto: the small-k kernel below this many (row, centroid) pairs
 int64_t kSmallAssignNK = int64_t(1) << 22;
 
+// dynamic shared memory of assign3<stages, TM, TN, RT, CT, SC>
 template <int TM, int TN, int RT, int CT>
+size_t assign3_smem(int64_t d, int64_t k, int stages, bool sc) {
+  constexpr int BM = RT * TM, BN = CT * TN;
+  const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
+  const size_t cbytes = sc ? sizeof(double) * stages * BN * kAKP : sizeof(double) * dpad * (BN + 1);
+  // row stages, tile tables (|f|^2 + row id per row, ring of stages + 2), |c|^2, histogram
+  return cbytes + sizeof(double) * stages * BM * kAKP + (size_t)(stages + 2) * BM * 12 +
+         sizeof(double) * BN + sizeof(int32_t) * (size_t)(k <= kHistMax ? k : 0);
+}
+
+template <int TM, int TN, int RT, int CT, bool SC = false>
 int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d, int64_t ld,
                      const double *c, int64_t ldc, const double *cnorm, int64_t k,
                      int32_t *labels, double *own, int32_t *counts, cudaStream_t st,
@@ -714,20 +756,21 @@ int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d,
   constexpr int BM = RT * TM, BN = CT * TN, NT = RT * CT;
   CSC_REQUIRE(n < (int64_t(1) << 31) && ld * (int64_t)sizeof(double) < (int64_t(1) << 31),
               "assign: n and the row stride in bytes must fit int32");
-  const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
-  const size_t cbytes = sizeof(double) * dpad * (BN + 1), sbytes = sizeof(double) * BM * kAKP;
-  // tile tables (|f|^2 + row id per row, ring of kStages + 2) and |c|^2
-  auto tbytes = [&](int stages) {
-    return (size_t)(stages + 2) * BM * 12 + sizeof(double) * BN + sizeof(int32_t) * (size_t)k;
-  };
+  if (SC)
+    CSC_REQUIRE(ldc % 2 == 0 && (reinterpret_cast<uintptr_t>(c) & 15u) == 0,
+                "assign (d=%lld): centroids must be 16-byte aligned with an even row stride",
+                (long long)d);
   // three stages when two blocks still fit in one SM's shared memory, else two
-  const bool three = 2 * (cbytes + 3 * sbytes + tbytes(3) + 1024) <= 228 * 1024;
-  const size_t smem = cbytes + (three ? 3 : 2) * sbytes + tbytes(three ? 3 : 2);
+  const bool three = 2 * (assign3_smem<TM, TN, RT, CT>(d, k, 3, SC) + 1024) <= 228 * 1024;
+  const size_t smem = assign3_smem<TM, TN, RT, CT>(d, k, three ? 3 : 2, SC);
+  CSC_REQUIRE((int64_t)smem <= (int64_t)csc::device_info().max_smem_optin,
+              "assign: d=%lld, k=%lld need %zu bytes of shared memory", (long long)d,
+              (long long)k, smem);
   static size_t configured2 = 0, configured3 = 0;
   size_t &configured = three ? configured3 : configured2;
   if (smem > configured) {
-    CSC_TRY_CUDA(cudaFuncSetAttribute(three ? assign3_kernel<3, TM, TN, RT, CT>
-                                            : assign3_kernel<2, TM, TN, RT, CT>,
+    CSC_TRY_CUDA(cudaFuncSetAttribute(three ? assign3_kernel<3, TM, TN, RT, CT, SC>
+                                            : assign3_kernel<2, TM, TN, RT, CT, SC>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
@@ -738,11 +781,11 @@ int launch_assign3_t(const double *f, const double *fnorm, int64_t n, int64_t d,
   for (int64_t c0 = 0; c0 < k; c0 += BN) {
     const int last = c0 + BN >= k;
     if (three)
-      assign3_kernel<3, TM, TN, RT, CT><<<grid, NT, smem, st>>>(
+      assign3_kernel<3, TM, TN, RT, CT, SC><<<grid, NT, smem, st>>>(
           f, fnorm, n, d, ld, c, ldc, cnorm, k, c0, last, labels, own, last ? counts : nullptr,
           rows, nrows_dev, ub, lb, gate);
     else
-      assign3_kernel<2, TM, TN, RT, CT><<<grid, NT, smem, st>>>(
+      assign3_kernel<2, TM, TN, RT, CT, SC><<<grid, NT, smem, st>>>(
           f, fnorm, n, d, ld, c, ldc, cnorm, k, c0, last, labels, own, last ? counts : nullptr,
           rows, nrows_dev, ub, lb, gate);
     CSC_CHECK_LAUNCH();
@@ -762,6 +805,25 @@ int launch_assign3(const double *f, const double *fnorm, int64_t n, int64_t d, i
                                     rows, nrows_dev, ub, lb, gate);
     return launch_assign_small<2>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts, st,
                                   rows, nrows_dev, ub, lb, gate);
+  }
+  // large d: the resident centroid tile does not fit; stream it (any forced tile
+  // maps here too: every tile gives the same bits)
+  auto fits = [&](size_t two_stage) {
+    return (int64_t)two_stage <= (int64_t)csc::device_info().max_smem_optin;
+  };
+  const int tile = g_assign_tile > 1 ? g_assign_tile : (k <= 32 ? 84 : (k <= 112 && k > 64 ? 87 : 88));
+  const size_t need = tile == 87   ? assign3_smem<8, 7, 16, 16>(d, k, 2, false)
+                      : tile == 84 ? assign3_smem<8, 4, 16, 8>(d, k, 2, false)
+                      : tile == 48 ? assign3_smem<4, 8, 16, 8>(d, k, 2, false)
+                      : tile == 42 ? assign3_smem<4, 4, 32, 8>(d, k, 2, false)
+                      : tile == 44 ? assign3_smem<4, 4, 16, 16>(d, k, 2, false)
+                                   : assign3_smem<8, 8, 16, 8>(d, k, 2, false);
+  if (!fits(need)) {
+    if (k <= 32)
+      return launch_assign3_t<8, 4, 16, 8, true>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                                 counts, st, rows, nrows_dev, ub, lb, gate);
+    return launch_assign3_t<8, 8, 16, 8, true>(f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own,
+                                               counts, st, rows, nrows_dev, ub, lb, gate);
   }
   switch (g_assign_tile) {
     case 88:
@@ -808,6 +870,7 @@ int launch_assign2(const double *f, const double *fnorm, int64_t n, int64_t d, i
   }
   assign2_kernel<TN><<<(unsigned)csc::ceil_div(n, kAM), 16 * (kAN / TN), smem, st>>>(
       f, fnorm, n, d, ld, c, ldc, cnorm, k, labels, own, counts, rows, nrows_dev, ub, lb, gate);
+  CSC_CHECK_LAUNCH();
   return CSC_OK;
 }
 
@@ -2043,11 +2106,11 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
   const int64_t n = p->n, d = p->d, ld = p->ld, k = p->k;
   const int64_t dpad = csc::ceil_div(d, kAK) * kAK;
   const size_t asmem = sizeof(double) * (dpad * kANP + 2 * kAM * kAKP);
-  CSC_REQUIRE((ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(f) & 15u) == 0) &&
-                  (int64_t)asmem <= (int64_t)csc::device_info().max_smem_optin,
+  CSC_REQUIRE((ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(f) & 15u) == 0),
               "csc_kmeans_iterate: features must be 16-byte aligned with an even row stride");
+  const bool v2_fits = (int64_t)asmem <= (int64_t)csc::device_info().max_smem_optin;
   auto assign = [&](const int32_t *rows, const int32_t *nrows, int32_t *cnts, const int32_t *gate) {
-    if (g_assign_ver == 3)
+    if (g_assign_ver == 3 || !v2_fits)
       return launch_assign3(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own, cnts, st,
                             rows, nrows, p->ub, p->lb, gate);
     return g_assign_tn == 8
@@ -2319,7 +2382,9 @@ int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_
   kppb_first_kernel<<<(unsigned)R, 128, 0, st>>>(f, d, ld, fidx.as<int64_t>(), cent, cent_stride);
   CSC_CHECK_LAUNCH();
   const size_t smem = sizeof(double) * (R * d + 4 * R);
-  CSC_REQUIRE(smem <= 48 * 1024, "csc_kmeanspp_batch: R*d too large");
+  CSC_REQUIRE((int64_t)smem <= (int64_t)csc::device_info().max_smem_optin,
+              "csc_kmeanspp_batch: R*d too large for shared memory (R=%lld, d=%lld)",
+              (long long)R, (long long)d);
   for (int64_t j = 0; j < k; ++j) {
     if (j > 0) {
       kppb_pick_kernel<<<(unsigned)R, 1024, 0, st>>>(f, n, d, ld, closest.as<double>(),
@@ -2332,6 +2397,9 @@ int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_
       switch (R) {
 #define CSC_KPPB_CASE(RR)                                                                      \
   case RR:                                                                                     \
+    if (smem > 48 * 1024)                                                                      \
+      CSC_TRY_CUDA(cudaFuncSetAttribute(kppb_dist_kernel<RR>,                                  \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     kppb_dist_kernel<RR><<<(unsigned)nchunks, 128, smem, st>>>(                                \
         f, n, d, ld, cent + j * ldc, cent_stride, closest.as<double>(), j == 0 ? 1 : 0, chunk, \
         sums.as<double>(), nchunks);                                                           \

@@ -322,6 +322,12 @@ def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children
 KPP_BATCH = 16  # restarts per batched k-means++ launch series (libcscb200 limit)
 
 
+def kpp_group(d: int) -> int:
+    """Restarts per batched k-means++ series: their R x d centroids share one
+    block's shared memory (<= ~200 KB of the 227 KB opt-in)"""
+    return max(1, min(KPP_BATCH, (200 * 1024) // (8 * d + 32)))
+
+
 def kmeanspp_draws(children, n: int, k: int):
     """Host RNG draws of every restart's k-means++ in the reference's order
     (kmeans.py:67-74): integers(n) for the first centroid, then k-1 random()
@@ -344,11 +350,12 @@ def batched_kmeanspp(ws: _Workspace, children, defer_check: bool = False, draws=
     """
     n, k, R = ws.n, ws.k, len(children)
     seeds = torch.zeros((R, k, ws.ldc), dtype=torch.float64, device=ws.blk.device)
-    ngroups = (R + KPP_BATCH - 1) // KPP_BATCH
-    flags = torch.empty((ngroups, KPP_BATCH), dtype=torch.int32, device=ws.blk.device)
+    per = kpp_group(ws.d)
+    ngroups = (R + per - 1) // per
+    flags = torch.empty((ngroups, per), dtype=torch.int32, device=ws.blk.device)
     all_first, all_unif = draws if draws is not None else kmeanspp_draws(children, n, k)
-    for gidx, g0 in enumerate(range(0, R, KPP_BATCH)):
-        grp = list(range(g0, min(R, g0 + KPP_BATCH)))
+    for gidx, g0 in enumerate(range(0, R, per)):
+        grp = list(range(g0, min(R, g0 + per)))
         first = np.ascontiguousarray(all_first[g0:g0 + len(grp)])
         unif = np.ascontiguousarray(all_unif[g0:g0 + len(grp)])
         _native.call("csc_kmeanspp_batch", ptr(ws.blk), n, ws.d, ws.ld, len(grp), k,
