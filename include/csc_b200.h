@@ -192,6 +192,30 @@ int csc_kmeans_run(csc_kmeans_plan *plan, const double *f_dev, const double *row
                    double *c_dev, int64_t ldc, double *cnorm_dev, int32_t *labels_dev,
                    int32_t *counts_dev, int max_iters, double tol, double *out_dev,
                    double *history_dev, void *stream);
+/* Fused Lloyd for small blocks: ALL R restarts of one kmeans() call
+ * (kmeans.py:120-144, inner loop _lloyd kmeans.py:88-117) in one cooperative
+ * persistent launch, one CTA per SM owning a contiguous row range whose
+ * features stay in shared memory; restarts advance in lock step (two grid
+ * barriers per iteration: Hamerly-pruned GEMM-form assignment + block
+ * partials, then the stop rule and the means). The stop rule uses the exact
+ * difference-form cost of kmeans.py:111. Empty clusters are repaired as in
+ * kmeans.py:99-108 (exact own distances, first-max reseeding).
+ * seeds_dev: R x k x ldc (k-means++ seeds). Outputs (device): labels_dev
+ * R x n int32 (each restart's final labels), cost2_dev[R] (final cost2),
+ * iters_dev[R] (iterations run). Asynchronous. supported() returns 1 when the
+ * shape fits (1 <= k <= 32, d <= 128, R <= 32, max_iters >= 1, the CTA's
+ * rows and per-restart bounds within shared memory), else 0 (no error). */
+int csc_kmeans_fused_supported(int64_t n, int64_t d, int64_t k, int64_t R, int max_iters);
+int csc_kmeans_fused_run(const double *f_dev, const double *rownorm_dev, int64_t n, int64_t d,
+                         int64_t ld, int64_t k, int64_t R, const double *seeds_dev, int64_t ldc,
+                         int max_iters, double tol, int32_t *labels_dev, double *cost2_dev,
+                         int32_t *iters_dev, void *stream);
+/* diagnostics: while trace_dev != NULL, fused runs record CTA 0's
+ * %globaltimer (ns) at the phase boundaries of iteration g into
+ * trace_dev[g * 16 + slot] (slots 0..5: phase 1 start/end, barrier, phase 2
+ * end, barrier, iteration end; 6..10: sub-steps of the first restart's
+ * phase 1; 11: its candidate row count), g < iters_cap. */
+int csc_kmeans_fused_trace(unsigned long long *trace_dev, int64_t iters_cap);
 /* k-means tuning knobs (performance only; results do not change):
  * "assign_ver" 2|3, "assign_tn" 4|8 (v2 kernel), "assign_tile" 0 (auto) |
  * 1 (small-k kernel) | 88 | 84 | 87 | 48 | 44 | 42 (v3 register tile),

@@ -1,0 +1,874 @@
+// Fused Lloyd k-means for small feature blocks: every restart of one
+// kmeans() call (kmeans.py:120-144) in ONE cooperative persistent launch.
+//
+// Why: at configs[1] scale (n = 20k, d = 80, k = 20, 10 restarts) one Lloyd
+// iteration is ~30 us of arithmetic for all restarts together, but the
+// per-restart lane path (csc_kmeans_run) needs ~10 dependent kernel nodes per
+// iteration and the restarts contend for the GPU: ~60-85 us per iteration on
+// the longest restart's critical path. Here each CTA (one per SM) owns a
+// contiguous row range whose features stay resident in shared memory for the
+// whole run; restarts advance in lock step, and an iteration is two grid
+// barriers:
+//
+//   phase 1 (per CTA; the active restarts are spread over 1, 2 or 4 thread
+//   groups, so a lone long-running restart gets the whole CTA)
+//     - exact cost of the previous iteration on the CTA's rows,
+//       sum |f_i - c_{l_i}|^2 with the new means (kmeans.py:111) -> partial
+//     - labels of the previous iteration -> output (the final labels when the
+//       restart stops on this cost)
+//     - Hamerly bounds (ub >= |f - c_a|, lb <= min_{j != a} |f - c_j|, moved
+//       by the centroid movements): rows whose bounds cannot exclude a label
+//       change are recomputed in the reference's GEMM form
+//       max(0, (|f|^2 - 2 f.c) + |c|^2), first-index argmin (kmeans.py:54-61,
+//       96-97; the per-pair arithmetic of assign_small_kernel, so labels are
+//       bit-identical to the lane path's for the same centroids)
+//     - per-cluster sums of the CTA's rows in row order (stable counting sort
+//       by label, one register run per (cluster, column)) and counts
+//   grid barrier
+//   phase 2 (four warps per (restart, cluster), grid-wide)
+//     - cost2 of the previous iteration = fixed-order sum of the partials;
+//       the reference's stop rule (prev - cost2 <= tol * prev, or max_iters;
+//       kmeans.py:112-116), decided identically by every warp of the restart
+//     - means = sums / max(count, 1) (kmeans.py:84): block partials added in
+//       block order (four contiguous block ranges, combined in order);
+//       movement and |c|^2 for the next bounds
+//   grid barrier
+//   rare path (an empty cluster, kmeans.py:99-108): exact reassignment of every
+//   row (own distances), the reference's argmax reseeding in one CTA, updated
+//   partials, means again (four more barriers, only when it happens).
+//
+// Results: labels / cost of every restart. The stop rule uses the exact
+// difference-form cost (the reference's formula; the lane path uses the
+// centroid identity). All reductions have a fixed order: deterministic.
+// No tensor cores (north_star); FP64 SIMT.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kFT = 512;          // threads per CTA (one CTA per SM)
+constexpr int kFW = kFT / 32;     // warps per CTA
+constexpr int kFMaxK = 32;        // one centroid per lane
+constexpr int kFMaxD = 128;       // <= 4 columns per lane in the means pass
+constexpr int kFMaxR = 32;        // restarts
+constexpr int kFMisc = 4 + kFW;   // per-group int scratch
+constexpr int kQuad = 4;          // warps per phase-2 item
+
+struct FusedArgs {
+  const double *F;
+  const double *fnorm;
+  int64_t n, d, ld, k, R, ldc;
+  int max_iters;
+  double tol;
+  int32_t *labels_out;  // [R][n]
+  double *cost_out;     // [R]
+  int32_t *iters_out;   // [R]
+  double *cent;         // [2][R][k][ldc]   centroids by iteration parity
+  double *kvec;         // [2][R][2][k]     |c|^2, movement by iteration parity
+  double *psum;         // [R][G][k][d]     block partial sums
+  double *cpart;        // [R][G]           block partial costs
+  double *hist;         // [R][max_iters + 1]
+  double *own;          // [R][n]           rare path: own distances
+  int32_t *pcnt;        // [R][G][k]
+  int32_t *done;        // [R]
+  int32_t *eflag;       // [R]  = g + 1 when iteration g found an empty cluster
+  int32_t *nrep;        // [R]
+  int32_t *rep_idx;     // [R][k]
+  int32_t *rep_j;       // [R][k]
+  unsigned *bar;        // [2] arrival count, generation
+  unsigned long long *trace;  // optional: CTA 0's globaltimer at phase boundaries [iter][8]
+  int64_t trace_cap;
+  int G, rows_max, ldf, lds, ngmax;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier (all CTAs co-resident: cooperative launch). Writes before
+// it are visible to __ldcg loads after it.
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == G - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire(bar + 1) == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// sum over the warp, lane 0's association broadcast (all lanes equal)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+// A thread group working on one restart at a time (named barrier id + 1).
+struct Grp {
+  int id, GT, GW, gt, gw;
+  __device__ __forceinline__ void sync() const { named_sync(id + 1, GT); }
+};
+
+struct Shared {
+  double *Fs, *fns, *fsq, *ubs, *lbs, *p2;  // CTA-wide
+  int32_t *labs, *act, *p2c;                // CTA-wide
+};
+struct GShared {
+  double *Cs, *cn, *del, *red, *scal;
+  int32_t *cand, *perm, *cnt, *runp, *misc;
+};
+
+__host__ __device__ inline int64_t gstride_d(int lds) { return 32 * (int64_t)lds + 64 + kFW + 4; }
+__host__ __device__ inline int64_t gstride_i(int64_t RM) { return 2 * RM + 64 + kFMisc; }
+
+__device__ __forceinline__ Shared carve(unsigned char *raw, const FusedArgs &a) {
+  const int64_t RM = a.rows_max, R = a.R;
+  Shared s;
+  s.Fs = reinterpret_cast<double *>(raw);
+  s.fns = s.Fs + RM * a.ldf;
+  s.fsq = s.fns + RM;
+  s.ubs = s.fsq + RM;
+  s.lbs = s.ubs + R * RM;
+  s.p2 = s.lbs + R * RM;  // [kFW][d]
+  int32_t *ib = reinterpret_cast<int32_t *>(s.p2 + kFW * a.d + a.ngmax * gstride_d(a.lds));
+  s.labs = ib;
+  s.act = ib + R * RM;  // [kFMaxR + 1]
+  s.p2c = s.act + kFMaxR + 1;  // [kFW]
+  return s;
+}
+
+__device__ __forceinline__ GShared gcarve(unsigned char *raw, const FusedArgs &a, int gi) {
+  const int64_t RM = a.rows_max, R = a.R;
+  GShared g;
+  double *gb = reinterpret_cast<double *>(raw) + RM * a.ldf + 2 * RM + 2 * R * RM + kFW * a.d;
+  g.Cs = gb + gi * gstride_d(a.lds);
+  g.cn = g.Cs + 32 * a.lds;
+  g.del = g.cn + 32;
+  g.red = g.del + 32;
+  g.scal = g.red + kFW;
+  int32_t *ib = reinterpret_cast<int32_t *>(gb + a.ngmax * gstride_d(a.lds)) + R * RM + kFMaxR + 1 +
+                kFW;
+  int32_t *gi32 = ib + gi * gstride_i(RM);
+  g.cand = gi32;
+  g.perm = g.cand + RM;
+  g.cnt = g.perm + RM;
+  g.runp = g.cnt + 32;
+  g.misc = g.runp + 32;
+  return g;
+}
+
+// Centroids of restart r at iteration g into the group's Cs (rows >= k stay
+// zero), |c|^2 (computed for the seeds, else from phase 2) and movements.
+__device__ void group_load(const FusedArgs &a, const GShared &gs, const Grp &G_, int r, int g) {
+  const int64_t k = a.k, d = a.d, R = a.R, kd = k * d;
+  const double *Cc = a.cent + ((int64_t)(g & 1) * R + r) * k * a.ldc;
+  constexpr int U = 8;
+  for (int64_t e0 = G_.gt; e0 < kd; e0 += (int64_t)U * G_.GT) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * G_.GT;
+      if (e < kd) {
+        const int64_t j = e / d, t = e - j * d;
+        v[u] = __ldcg(Cc + j * a.ldc + t);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * G_.GT;
+      if (e < kd) {
+        const int64_t j = e / d, t = e - j * d;
+        gs.Cs[j * a.lds + t] = v[u];
+      }
+    }
+  }
+  if (g > 0) {
+    const double *kv = a.kvec + ((int64_t)(g & 1) * R + r) * 2 * k;
+    if (G_.gt < k) {
+      gs.cn[G_.gt] = __ldcg(kv + G_.gt);
+      gs.del[G_.gt] = __ldcg(kv + k + G_.gt);
+    }
+  }
+  G_.sync();
+  if (g == 0) {  // |c|^2 of the seeds, one thread per centroid
+    if (G_.gt < k) {
+      const double *cr = gs.Cs + (int64_t)G_.gt * a.lds;
+      double v = 0.0;
+      for (int64_t t = 0; t < d; ++t) v = fma(cr[t], cr[t], v);
+      gs.cn[G_.gt] = v;
+    }
+    G_.sync();
+  }
+}
+
+// GEMM-form distances of up to 4 rows to all centroids (lane = centroid):
+// label, own distance, bounds. Same per-pair arithmetic as assign_small_kernel.
+__device__ __forceinline__ void assign_rows(const FusedArgs &a, const Shared &s, const GShared &gs,
+                                            int r, const int (&ii)[4], bool want_own, int64_t rb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t d = a.d, k = a.k, RM = a.rows_max, ldf = a.ldf;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const double *cr = gs.Cs + (int64_t)lane * a.lds;
+  const double *f0 = s.Fs + (int64_t)(ii[0] < 0 ? 0 : ii[0]) * ldf;
+  const double *f1 = s.Fs + (int64_t)(ii[1] < 0 ? 0 : ii[1]) * ldf;
+  const double *f2 = s.Fs + (int64_t)(ii[2] < 0 ? 0 : ii[2]) * ldf;
+  const double *f3 = s.Fs + (int64_t)(ii[3] < 0 ? 0 : ii[3]) * ldf;
+#pragma unroll 4
+  for (int64_t t = 0; t < d; ++t) {
+    const double b = cr[t];
+    acc[0] = fma(f0[t], b, acc[0]);
+    acc[1] = fma(f1[t], b, acc[1]);
+    acc[2] = fma(f2[t], b, acc[2]);
+    acc[3] = fma(f3[t], b, acc[3]);
+  }
+  const double cnl = lane < k ? gs.cn[lane] : 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (ii[q] < 0) continue;  // warp-uniform
+    const int i = ii[q];
+    const double tt = __dsub_rn(s.fns[i], __dmul_rn(2.0, acc[q]));
+    double v = lane < k ? fmax(__dadd_rn(tt, cnl), 0.0) : INFINITY;
+    double v2 = INFINITY;
+    int vi = lane;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+      if (ov < v || (ov == v && oi < vi)) {
+        v2 = fmin(ov2, v);
+        v = ov;
+        vi = oi;
+      } else {
+        v2 = fmin(v2, ov);
+      }
+    }
+    if (lane == 0) {
+      s.labs[(int64_t)r * RM + i] = vi;
+      s.ubs[(int64_t)r * RM + i] = sqrt(v);
+      s.lbs[(int64_t)r * RM + i] = sqrt(v2);
+      if (want_own) a.own[(int64_t)r * a.n + rb + i] = v;
+    }
+  }
+}
+
+// Counting sort of the CTA's rows of restart r by label (stable), then one
+// register run per (cluster, column) in row order -> psum / pcnt.
+__device__ void group_partials(const FusedArgs &a, const Shared &s, const GShared &gs,
+                               const Grp &G_, int r, int nr, bool counts_only) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = a.k, d = a.d, RM = a.rows_max, ldf = a.ldf;
+  const int cta = blockIdx.x;
+  const int32_t *lab = s.labs + (int64_t)r * RM;
+  if (G_.gt < 32) gs.cnt[G_.gt] = 0;
+  G_.sync();
+  for (int i = G_.gt; i < nr; i += G_.GT) atomicAdd(gs.cnt + lab[i], 1);
+  G_.sync();
+  int32_t *pc = a.pcnt + ((int64_t)r * a.G + cta) * k;
+  if (G_.gt < k) pc[G_.gt] = gs.cnt[G_.gt];
+  if (counts_only) {
+    G_.sync();
+    return;
+  }
+  if (G_.gw == 0) {
+    const int v = gs.cnt[lane];
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    gs.runp[lane] = inc - v;
+    __syncwarp();
+    for (int g0 = 0; g0 < nr; g0 += 32) {  // stable scatter, 32 rows at a time
+      const int p = g0 + lane;
+      const int l = p < nr ? lab[p] : -1;
+      const unsigned m = __match_any_sync(0xffffffffu, l);
+      const int rank = __popc(m & ((1u << lane) - 1u));
+      if (p < nr) gs.perm[gs.runp[l] + rank] = p;
+      __syncwarp();
+      if (p < nr && rank == __popc(m) - 1) gs.runp[l] += __popc(m);
+      __syncwarp();
+    }
+  }
+  G_.sync();
+  double *ps = a.psum + ((int64_t)r * a.G + cta) * k * d;
+  for (int64_t e = G_.gt; e < k * d; e += G_.GT) {  // thread per (cluster, column)
+    const int64_t j = e / d, t = e - j * d;
+    const int c = gs.cnt[j];
+    if (c == 0) continue;
+    const int end = gs.runp[j], beg = end - c;
+    double v = 0.0;
+    for (int p = beg; p < end; ++p) v += s.Fs[(int64_t)gs.perm[p] * ldf + t];
+    ps[e] = v;
+  }
+  G_.sync();
+}
+
+__device__ __forceinline__ void submark(const FusedArgs &a, int g, int slot, bool on) {
+  if (on && a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && g < a.trace_cap)
+    a.trace[(int64_t)g * 16 + slot] = gtimer();
+}
+
+__device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, const Grp &G_,
+                       int r, int g, int nr, int64_t rb, bool first) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = a.k, d = a.d, RM = a.rows_max, ldf = a.ldf;
+  const int cta = blockIdx.x;
+  if (G_.gt == 0) gs.misc[0] = 0;
+  group_load(a, gs, G_, r, g);
+  submark(a, g, 6, first);
+  int32_t *lab = s.labs + (int64_t)r * RM;
+  double *ub = s.ubs + (int64_t)r * RM, *lb = s.lbs + (int64_t)r * RM;
+  if (g > 0) {
+    if (G_.gw == 0) {  // largest / second largest movement (first index wins), max |c|
+      const double dj = lane < k ? gs.del[lane] : 0.0;
+      const double cj = lane < k ? gs.cn[lane] : 0.0;
+      double m1 = dj, cm = cj;
+      int i1 = lane;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double om = __shfl_xor_sync(0xffffffffu, m1, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i1, o);
+        if (om > m1 || (om == m1 && oi < i1)) {
+          m1 = om;
+          i1 = oi;
+        }
+        cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+      }
+      double m2 = lane == i1 ? 0.0 : dj;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+      if (lane == 0) {
+        gs.scal[0] = fmax(m1, 0.0);
+        gs.scal[1] = fmax(m2, 0.0);
+        gs.scal[2] = m1 > 0.0 ? (double)i1 : 0.0;
+        gs.scal[3] = sqrt(cm);
+      }
+    }
+    // exact cost of iteration g-1 (labels of g-1, means of g-1), thread per row
+    double acc = 0.0;
+    for (int i = G_.gt; i < nr; i += G_.GT) {
+      const double *fr = s.Fs + (int64_t)i * ldf;
+      const int l = lab[i];
+      const double *cr = gs.Cs + (int64_t)l * a.lds;
+      double v = 0.0;
+      for (int64_t t = 0; t < d; ++t) {
+        const double df = fr[t] - cr[t];
+        v = fma(df, df, v);
+      }
+      acc += v;
+      a.labels_out[(int64_t)r * a.n + rb + i] = l;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) gs.red[G_.gw] = acc;
+    G_.sync();
+    if (G_.gt == 0) {
+      double c = 0.0;
+      for (int w = 0; w < G_.GW; ++w) c += gs.red[w];
+      a.cpart[(int64_t)r * a.G + cta] = c;
+    }
+  }
+  submark(a, g, 7, first);
+  if (g >= a.max_iters) {
+    G_.sync();
+    return;
+  }
+  // rows that need a distance computation
+  int ncand = nr;
+  if (g > 0) {
+    const double d1 = gs.scal[0], d2 = gs.scal[1], cmax = gs.scal[3];
+    const int j1 = (int)gs.scal[2];
+    for (int c0 = 0; c0 < nr; c0 += G_.GT) {
+      const int i = c0 + G_.gt;
+      bool need = false;
+      if (i < nr) {
+        const int l = lab[i];
+        const double u = ub[i] + gs.del[l];
+        const double lw = lb[i] - (l == j1 ? d2 : d1);
+        const double eta = 1e-7 * (s.fsq[i] + cmax);
+        need = !(u + eta <= lw);
+        ub[i] = u;
+        lb[i] = lw;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, need);
+      if (lane == 0) gs.misc[4 + G_.gw] = __popc(bal);
+      G_.sync();
+      int off = gs.misc[0], tot = 0;
+      for (int w = 0; w < G_.GW; ++w) {
+        const int cw = gs.misc[4 + w];
+        if (w < G_.gw) off += cw;
+        tot += cw;
+      }
+      if (need) gs.cand[off + __popc(bal & ((1u << lane) - 1u))] = i;
+      G_.sync();
+      if (G_.gt == 0) gs.misc[0] += tot;
+      G_.sync();
+    }
+    ncand = gs.misc[0];
+  }
+  submark(a, g, 8, first);
+  if (first && a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && g < a.trace_cap)
+    a.trace[(int64_t)g * 16 + 11] = (unsigned long long)ncand;
+  for (int q0 = G_.gw * 4; q0 < ncand; q0 += G_.GW * 4) {
+    int ii[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = q0 + q;
+      ii[q] = p < ncand ? (g == 0 ? p : gs.cand[p]) : -1;
+    }
+    assign_rows(a, s, gs, r, ii, false, rb);
+  }
+  G_.sync();
+  submark(a, g, 9, first);
+  group_partials(a, s, gs, G_, r, nr, false);
+  submark(a, g, 10, first);
+}
+
+// Sum of the cost partials of restart r (identical in every warp that asks).
+__device__ __forceinline__ double cost_sum(const FusedArgs &a, int r) {
+  const int lane = threadIdx.x & 31;
+  const int G = a.G;
+  double v[5];
+#pragma unroll
+  for (int u = 0; u < 5; ++u) {
+    const int b = lane + 32 * u;
+    v[u] = b < G ? __ldcg(a.cpart + (int64_t)r * G + b) : 0.0;
+  }
+  double c = 0.0;
+#pragma unroll
+  for (int u = 0; u < 5; ++u)
+    if (lane + 32 * u < G) c += v[u];
+  for (int b = lane + 160; b < G; b += 32) c += __ldcg(a.cpart + (int64_t)r * G + b);
+  return warp_sum(c);
+}
+
+// Means of (restart r, cluster j) from the block partials, by a quad of warps:
+// warp w4 adds blocks [w4 G/4, (w4+1) G/4) in order (loads batched), warp 0
+// adds the four range sums in order. Movement and |c|^2 for the next bounds.
+__device__ void means_item(const FusedArgs &a, const Shared &s, int w4, int qid, int r, int j,
+                           int g, bool flag_empty) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t k = a.k, d = a.d, R = a.R, G = a.G;
+  const int64_t b_lo = (int64_t)w4 * G / kQuad, b_hi = (int64_t)(w4 + 1) * G / kQuad;
+  int cnt = 0;
+  double sv[4] = {0.0, 0.0, 0.0, 0.0};
+  const double *pbase = a.psum + ((int64_t)r * G * k + j) * d;
+  for (int64_t c0 = b_lo; c0 < b_hi; c0 += 32) {
+    const int64_t b = c0 + lane;
+    const int pc = b < b_hi ? __ldcg(a.pcnt + ((int64_t)r * G + b) * k + j) : 0;
+    cnt += pc;
+    unsigned m = __ballot_sync(0xffffffffu, pc > 0);
+    while (m) {
+      int bb[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        bb[q] = m ? (int)c0 + __ffs(m) - 1 : -1;
+        m &= m ? m - 1 : 0u;
+      }
+      double v[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t t = lane + 32 * u;
+          v[q][u] = (bb[q] >= 0 && t < d) ? __ldcg(pbase + (int64_t)bb[q] * k * d + t) : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (bb[q] >= 0)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sv[u] += v[q][u];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  double *mine = s.p2 + (int64_t)wid * d;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t t = lane + 32 * u;
+    if (t < d) mine[t] = sv[u];
+  }
+  if (lane == 0) s.p2c[wid] = cnt;
+  named_sync(5 + qid, kQuad * 32);
+  if (w4 == 0) {
+    int tot = 0;
+    for (int w = 0; w < kQuad; ++w) tot += s.p2c[wid + w];
+    const double denom = (double)(tot > 1 ? tot : 1);
+    const double *cold = a.cent + ((int64_t)(g & 1) * R + r) * k * a.ldc + j * a.ldc;
+    double *cnew = a.cent + ((int64_t)((g + 1) & 1) * R + r) * k * a.ldc + j * a.ldc;
+    double mv = 0.0, nrm = 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = lane + 32 * u;
+      if (t < d) {
+        double sum = 0.0;
+        for (int w = 0; w < kQuad; ++w) sum += s.p2[(int64_t)(wid + w) * d + t];
+        const double mean = __ddiv_rn(sum, denom);
+        const double old = __ldcg(cold + t);
+        cnew[t] = mean;
+        const double df = mean - old;
+        mv = fma(df, df, mv);
+        nrm = fma(mean, mean, nrm);
+      }
+    }
+    mv = warp_sum(mv);
+    nrm = warp_sum(nrm);
+    if (lane == 0) {
+      double *kv = a.kvec + ((int64_t)((g + 1) & 1) * R + r) * 2 * k;
+      kv[j] = nrm;
+      kv[k + j] = sqrt(mv);
+      if (flag_empty && tot == 0) a.eflag[r] = g + 1;
+    }
+  }
+  named_sync(5 + qid, kQuad * 32);  // p2 reuse
+}
+
+__global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int cta = blockIdx.x, G = a.G;
+  const int64_t n = a.n, d = a.d, k = a.k, R = a.R, RM = a.rows_max, ldf = a.ldf;
+  const int64_t rb = (int64_t)cta * n / G, re = (int64_t)(cta + 1) * n / G;
+  const int nr = (int)(re - rb);
+  const Shared s = carve(smem_raw, a);
+
+  for (int64_t e = tid; e < (int64_t)nr * d; e += kFT) {
+    const int64_t i = e / d, t = e - i * d;
+    s.Fs[i * ldf + t] = a.F[(rb + i) * a.ld + t];
+  }
+  for (int i = tid; i < nr; i += kFT) {
+    const double v = a.fnorm[rb + i];
+    s.fns[i] = v;
+    s.fsq[i] = sqrt(v);
+  }
+  for (int gi = 0; gi < a.ngmax; ++gi) {
+    const GShared gs = gcarve(smem_raw, a, gi);
+    for (int64_t e = tid; e < (32 - k) * a.lds; e += kFT) gs.Cs[k * a.lds + e] = 0.0;
+  }
+  if (tid == 0) {
+    for (int r = 0; r < R; ++r) s.act[r] = r;
+    s.act[kFMaxR] = (int)R;
+  }
+  __syncthreads();
+
+  const bool tr = a.trace != nullptr && cta == 0 && tid == 0;
+  auto mark = [&](int g, int slot) {
+    if (tr && g < a.trace_cap) a.trace[(int64_t)g * 16 + slot] = gtimer();
+  };
+  for (int g = 0;; ++g) {
+    const int A = s.act[kFMaxR];
+    mark(g, 0);
+    // ---- phase 1: cost of g-1, assignment of g, block partials -------------
+    {
+      const int ng = (A >= 4 && a.ngmax >= 4) ? 4 : (A >= 2 && a.ngmax >= 2) ? 2 : 1;
+      Grp G_;
+      G_.GT = kFT / ng;
+      G_.GW = G_.GT / 32;
+      G_.id = tid / G_.GT;
+      G_.gt = tid % G_.GT;
+      G_.gw = G_.gt >> 5;
+      const GShared gs = gcarve(smem_raw, a, G_.id);
+      for (int ai = G_.id; ai < A; ai += ng) phase1(a, s, gs, G_, s.act[ai], g, nr, rb, ai == 0);
+    }
+    __syncthreads();
+    mark(g, 1);
+    grid_sync(a.bar, G);
+    mark(g, 2);
+    // ---- phase 2: stop rule, means ----------------------------------------
+    {
+      const int qid = wid / kQuad, w4 = wid % kQuad;
+      const int nq = G * (kFW / kQuad);
+      for (int64_t q = (int64_t)cta * (kFW / kQuad) + qid; q < (int64_t)A * k; q += nq) {
+        const int r = s.act[q / k], j = (int)(q % k);
+        bool stop = false;
+        if (g > 0) {
+          const double c = cost_sum(a, r);
+          const int64_t hs = a.max_iters + 1;
+          const double prev = g >= 2 ? __ldcg(a.hist + r * hs + g - 2) : INFINITY;
+          stop = (g >= 2 && prev - c <= a.tol * prev) || g >= a.max_iters;
+          if (j == 0 && w4 == 0 && lane == 0) {
+            a.hist[r * hs + g - 1] = c;
+            if (stop) {
+              a.cost_out[r] = c;
+              a.iters_out[r] = g;
+              a.done[r] = 1;
+            }
+          }
+        }
+        if (!stop) means_item(a, s, w4, qid, r, j, g, true);
+      }
+    }
+    __syncthreads();
+    mark(g, 3);
+    grid_sync(a.bar, G);
+    mark(g, 4);
+    // ---- rare path: empty cluster -> exact reassignment + reseeding --------
+    const bool flagged = __syncthreads_or(tid < R && __ldcg(a.eflag + tid) == g + 1);
+    if (flagged) {
+      Grp W;  // the whole CTA as one group
+      W.id = 0;
+      W.GT = kFT;
+      W.GW = kFW;
+      W.gt = tid;
+      W.gw = wid;
+      const GShared gs = gcarve(smem_raw, a, 0);
+      for (int r = 0; r < R; ++r) {
+        if (__ldcg(a.eflag + r) != g + 1) continue;
+        group_load(a, gs, W, r, g);
+        for (int q0 = wid * 4; q0 < nr; q0 += kFW * 4) {
+          int ii[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ii[q] = q0 + q < nr ? q0 + q : -1;
+          assign_rows(a, s, gs, r, ii, true, rb);
+        }
+        W.sync();
+        group_partials(a, s, gs, W, r, nr, true);
+      }
+      grid_sync(a.bar, G);
+      // reseeding (kmeans.py:101-108), one CTA per flagged restart
+      for (int r = cta; r < R; r += G) {
+        if (__ldcg(a.eflag + r) != g + 1) continue;
+        __shared__ int s_cnt[kFMaxK];
+        __shared__ double s_bv[kFW];
+        __shared__ int64_t s_bi[kFW];
+        if (tid < k) {
+          int c = 0;
+          for (int b = 0; b < G; ++b) c += __ldcg(a.pcnt + ((int64_t)r * G + b) * k + tid);
+          s_cnt[tid] = c;
+        }
+        __syncthreads();
+        int nrep = 0;
+        double *own = a.own + (int64_t)r * n;
+        for (int64_t j = 0; j < k; ++j) {
+          if (s_cnt[j] != 0) continue;
+          double bv = -INFINITY;
+          int64_t bi = 0;
+          for (int64_t i = tid; i < n; i += kFT) {
+            const double v = __ldcg(own + i);
+            if (v > bv) {
+              bv = v;
+              bi = i;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+              bv = ov;
+              bi = oi;
+            }
+          }
+          if (lane == 0) {
+            s_bv[wid] = bv;
+            s_bi[wid] = bi;
+          }
+          __syncthreads();
+          if (tid == 0) {
+            for (int w = 1; w < kFW; ++w)
+              if (s_bv[w] > bv || (s_bv[w] == bv && s_bi[w] < bi)) {
+                bv = s_bv[w];
+                bi = s_bi[w];
+              }
+            a.rep_idx[(int64_t)r * k + nrep] = (int32_t)bi;
+            a.rep_j[(int64_t)r * k + nrep] = (int32_t)j;
+            __stcg(own + bi, -1.0);
+            __threadfence();
+          }
+          ++nrep;
+          __syncthreads();
+        }
+        if (tid == 0) a.nrep[r] = nrep;
+        __syncthreads();
+      }
+      grid_sync(a.bar, G);
+      for (int r = 0; r < R; ++r) {
+        if (__ldcg(a.eflag + r) != g + 1) continue;
+        if (tid == 0) {
+          const int m = __ldcg(a.nrep + r);
+          for (int q = 0; q < m; ++q) {
+            const int64_t i = __ldcg(a.rep_idx + (int64_t)r * k + q);
+            if (i >= rb && i < re) {
+              s.labs[(int64_t)r * RM + (i - rb)] = __ldcg(a.rep_j + (int64_t)r * k + q);
+              s.ubs[(int64_t)r * RM + (i - rb)] = INFINITY;  // recomputed next iteration
+              s.lbs[(int64_t)r * RM + (i - rb)] = 0.0;
+            }
+          }
+        }
+        W.sync();
+        group_partials(a, s, gs, W, r, nr, false);
+      }
+      grid_sync(a.bar, G);
+      {
+        const int qid = wid / kQuad, w4 = wid % kQuad;
+        const int nq = G * (kFW / kQuad);
+        for (int64_t q = (int64_t)cta * (kFW / kQuad) + qid; q < R * k; q += nq) {
+          const int r = (int)(q / k), j = (int)(q % k);
+          if (__ldcg(a.eflag + r) == g + 1) means_item(a, s, w4, qid, r, j, g, false);
+        }
+      }
+      grid_sync(a.bar, G);
+    }
+    mark(g, 5);
+    if (tid == 0) {  // restarts still running (identical list on every CTA)
+      int m = 0;
+      for (int r = 0; r < R; ++r)
+        if (!__ldcg(a.done + r)) s.act[m++] = r;
+      s.act[kFMaxR] = m;
+    }
+    __syncthreads();
+    if (s.act[kFMaxR] == 0) break;
+  }
+}
+
+struct FusedGeom {
+  int G = 0, RM = 0, ngmax = 0, ldf = 0, lds = 0;
+  size_t smem = 0;
+};
+
+size_t fused_smem(int64_t RM, int64_t d, int64_t R, int ngmax, int ldf, int lds) {
+  const int64_t dbl = RM * ldf + 2 * RM + 2 * R * RM + kFW * d + ngmax * gstride_d(lds);
+  const int64_t ints = R * RM + kFMaxR + 1 + kFW + ngmax * gstride_i(RM);
+  return (size_t)(dbl * 8 + ints * 4);
+}
+
+bool fused_geometry(int64_t n, int64_t d, int64_t k, int64_t R, int max_iters, FusedGeom &g) {
+  if (n < 1 || d < 1 || d > kFMaxD || k < 1 || k > kFMaxK || k > n || R < 1 || R > kFMaxR ||
+      max_iters < 1)
+    return false;
+  const csc::DeviceInfo &info = csc::device_info();
+  const int64_t smem_cap = info.max_smem_optin > 0 ? info.max_smem_optin : 232448;
+  g.G = (int)std::max<int64_t>(1, std::min<int64_t>(info.sm_count, n / 16));
+  g.RM = (int)csc::ceil_div(n, g.G);
+  g.ldf = (int)(d | 1);
+  g.lds = (int)(d | 1);
+  for (int ng : {4, 2, 1}) {
+    const size_t sm = fused_smem(g.RM, d, R, ng, g.ldf, g.lds);
+    if ((int64_t)sm <= smem_cap - 1024) {  // static shared arrays of the rare path
+      g.ngmax = ng;
+      g.smem = sm;
+      return true;
+    }
+  }
+  return false;
+}
+
+unsigned long long *g_trace = nullptr;
+int64_t g_trace_cap = 0;
+
+}  // namespace
+
+// diagnostics (tools/): the next fused runs record CTA 0's globaltimer at the
+// phase boundaries of every iteration into trace_dev[iter * 16 + slot]
+extern "C" int csc_kmeans_fused_trace(unsigned long long *trace_dev, int64_t iters_cap) {
+  g_trace = trace_dev;
+  g_trace_cap = trace_dev ? iters_cap : 0;
+  return CSC_OK;
+}
+
+extern "C" int csc_kmeans_fused_supported(int64_t n, int64_t d, int64_t k, int64_t R,
+                                          int max_iters) {
+  FusedGeom g;
+  return fused_geometry(n, d, k, R, max_iters, g) ? 1 : 0;
+}
+
+extern "C" int csc_kmeans_fused_run(const double *f, const double *fnorm, int64_t n, int64_t d,
+                                    int64_t ld, int64_t k, int64_t R, const double *seeds,
+                                    int64_t ldc, int max_iters, double tol, int32_t *labels,
+                                    double *cost2, int32_t *iters, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(f && fnorm && seeds && labels && cost2 && iters, "csc_kmeans_fused_run: NULL pointer");
+  CSC_REQUIRE(ld >= d && ldc >= d, "csc_kmeans_fused_run: ld/ldc < d");
+  FusedGeom g;
+  CSC_REQUIRE(fused_geometry(n, d, k, R, max_iters, g),
+              "csc_kmeans_fused_run: shape outside the fused kernel (n=%lld d=%lld k=%lld R=%lld)",
+              (long long)n, (long long)d, (long long)k, (long long)R);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t G = g.G;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t b_cent = al(sizeof(double) * 2 * R * k * ldc);
+  const size_t b_kvec = al(sizeof(double) * 2 * R * 2 * k);
+  const size_t b_psum = al(sizeof(double) * R * G * k * d);
+  const size_t b_cpart = al(sizeof(double) * R * G);
+  const size_t b_hist = al(sizeof(double) * R * (max_iters + 1));
+  const size_t b_own = al(sizeof(double) * R * n);
+  const size_t b_pcnt = al(sizeof(int32_t) * R * G * k);
+  const size_t b_ints = al(sizeof(int32_t) * (3 * R + 2 * R * k) + 2 * sizeof(unsigned));
+  csc::Scratch ws;
+  CSC_TRY_CUDA(ws.alloc(b_cent + b_kvec + b_psum + b_cpart + b_hist + b_own + b_pcnt + b_ints, st));
+  unsigned char *p = ws.as<unsigned char>();
+  FusedArgs a;
+  a.F = f;
+  a.fnorm = fnorm;
+  a.n = n;
+  a.d = d;
+  a.ld = ld;
+  a.k = k;
+  a.R = R;
+  a.ldc = ldc;
+  a.max_iters = max_iters;
+  a.tol = tol;
+  a.labels_out = labels;
+  a.cost_out = cost2;
+  a.iters_out = iters;
+  a.cent = reinterpret_cast<double *>(p);
+  p += b_cent;
+  a.kvec = reinterpret_cast<double *>(p);
+  p += b_kvec;
+  a.psum = reinterpret_cast<double *>(p);
+  p += b_psum;
+  a.cpart = reinterpret_cast<double *>(p);
+  p += b_cpart;
+  a.hist = reinterpret_cast<double *>(p);
+  p += b_hist;
+  a.own = reinterpret_cast<double *>(p);
+  p += b_own;
+  a.pcnt = reinterpret_cast<int32_t *>(p);
+  p += b_pcnt;
+  int32_t *ints = reinterpret_cast<int32_t *>(p);
+  a.done = ints;
+  a.eflag = ints + R;
+  a.nrep = ints + 2 * R;
+  a.rep_idx = ints + 3 * R;
+  a.rep_j = ints + 3 * R + R * k;
+  a.bar = reinterpret_cast<unsigned *>(ints + 3 * R + 2 * R * k);
+  a.trace = g_trace;
+  a.trace_cap = g_trace_cap;
+  a.G = (int)G;
+  a.rows_max = g.RM;
+  a.ldf = g.ldf;
+  a.lds = g.lds;
+  a.ngmax = g.ngmax;
+  CSC_TRY_CUDA(cudaMemcpyAsync(a.cent, seeds, sizeof(double) * R * k * ldc,
+                               cudaMemcpyDeviceToDevice, st));
+  CSC_TRY_CUDA(cudaMemsetAsync(ints, 0, b_ints, st));
+  CSC_TRY_CUDA(cudaFuncSetAttribute(lloyd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)g.smem));
+  void *args[] = {&a};
+  CSC_TRY_CUDA(cudaLaunchCooperativeKernel((const void *)lloyd_fused_kernel, dim3(g.G), dim3(kFT),
+                                           args, g.smem, st));
+  return CSC_OK;
+}

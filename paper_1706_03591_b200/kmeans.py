@@ -246,11 +246,86 @@ def _lloyd_pool(n, d, ld, k, dev) -> _LloydPool:
 _POOL_LOCK = threading.Lock()  # the lanes / streams / buffers of the pool are shared state
 
 
-def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, draws=None):
+def run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, draws=None,
+                 fused: bool | None = None):
     """Thread-safe entry (the reference's kmeans is a pure function): one caller at a time.
-    `draws` (optional) = kmeanspp_draws(children, n, k) made ahead of time."""
+    `draws` (optional) = kmeanspp_draws(children, n, k) made ahead of time.
+    fused=None picks the single-launch fused Lloyd when the shape fits it
+    (CSC_KMEANS_FUSED=0 disables), False forces the per-restart lanes."""
+    n, ld = blk.shape
+    if fused is None:
+        fused = os.environ.get("CSC_KMEANS_FUSED", "1") != "0" and fused_supported(n, d, k, len(children),
+                                                                                   cfg.max_iters)
     with _POOL_LOCK:
+        if fused:
+            return _run_fused(blk, d, k, cfg, children, draws)
         return _run_restarts(blk, d, k, cfg, children, draws)
+
+
+def fused_supported(n: int, d: int, k: int, restarts: int, max_iters: int) -> bool:
+    """Whether csc_kmeans_fused_run takes this shape (features resident in shared memory)."""
+    return bool(_native.lib().csc_kmeans_fused_supported(n, d, k, restarts, max_iters))
+
+
+class _FusedState:
+    """Persistent per-shape buffers of the fused Lloyd path."""
+
+    def __init__(self, n, d, ld, k, dev):
+        self.key = (dev.index, n, d, ld, k)
+        self.F = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+        self.ws = _Workspace(self.F, d, k)
+        self.out = {}
+
+    def outputs(self, R):
+        if R not in self.out:
+            dev = self.F.device
+            self.out[R] = (torch.empty((R, self.ws.n), dtype=torch.int32, device=dev),
+                           torch.empty(R, dtype=torch.float64, device=dev),
+                           torch.empty(R, dtype=torch.int32, device=dev))
+        return self.out[R]
+
+
+_FUSED: _FusedState | None = None
+LAST_FUSED_ITERS: list[int] = []  # diagnostics: Lloyd iterations per restart of the last fused call
+
+
+def _run_fused(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, draws=None):
+    """Every restart in one cooperative launch (csc_kmeans_fused_run): batched
+    k-means++ seeds, then all Lloyd runs in lock step with the features resident
+    in shared memory; best restart by the reference's rule (strictly smaller
+    cost2, earliest on ties). Returns (labels int64 numpy, cost2)."""
+    global _FUSED
+    dev = blk.device
+    n, ld = blk.shape
+    key = (dev.index, n, d, ld, k)
+    if _FUSED is None or _FUSED.key != key:
+        _FUSED = None
+        _FUSED = _FusedState(n, d, ld, k, dev)
+    st = _FUSED
+    ws = st.ws
+    st.F.copy_(blk)
+    _native.call("csc_kmeans_rownorms", ptr(st.F), n, d, ld, ptr(ws.fnorm), stream())
+    seeds, bad_restarts, replay = batched_kmeanspp(ws, children, defer_check=True, draws=draws)
+    R = len(children)
+    labels, cost, iters = st.outputs(R)
+
+    def launch():
+        _native.call("csc_kmeans_fused_run", ptr(st.F), ptr(ws.fnorm), n, d, ld, k, R, ptr(seeds), ws.ldc,
+                     int(cfg.max_iters), float(cfg.tol), ptr(labels), ptr(cost), ptr(iters), stream())
+
+    launch()
+    costs = cost.cpu().numpy()  # synchronises: the seeding flags are final too
+    redo = bad_restarts()
+    if redo:  # zero D^2 mass in some restart's seeding (kmeans.py:70-72): corrected seeds, run again
+        replay(redo)
+        launch()
+        costs = cost.cpu().numpy()
+    LAST_FUSED_ITERS[:] = [int(v) for v in iters.cpu().numpy()]
+    best = 0
+    for r in range(1, R):
+        if costs[r] < costs[best]:
+            best = r
+    return labels[best].cpu().numpy().astype(np.int64), float(costs[best])
 
 
 def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, draws=None):

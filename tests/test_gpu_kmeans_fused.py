@@ -1,0 +1,155 @@
+"""Fused Lloyd (csc_kmeans_fused_run): every restart in one cooperative launch.
+
+Parity bar (north_star): k-means started from the reference's initial
+centroids gives ARI >= 0.999 and cost within 1e-9 relative. Each restart of
+the fused launch is compared with the oracle's Lloyd (kmeans.py:88-117
+restated) started from the same seeds; iteration counts must agree too.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import csc_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+COST_TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def P(cuda_ok):
+    import paper_1706_03591_b200 as P
+    return P
+
+
+def fused_run(f, k, seeds, max_iters=100, tol=1e-6):
+    """Raw C-ABI call: seeds (R, k, d) host -> per-restart (labels, cost2, iters)."""
+    import torch
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import ptr, row_stride, stream, upload_block
+    blk = upload_block(np.ascontiguousarray(f, dtype=np.float64))
+    n, ld = blk.shape
+    d = f.shape[1]
+    R = len(seeds)
+    ldc = row_stride(d)
+    dev = blk.device
+    fn = torch.empty(n, dtype=torch.float64, device=dev)
+    _native.call("csc_kmeans_rownorms", ptr(blk), n, d, ld, ptr(fn), stream())
+    S = torch.zeros((R, k, ldc), dtype=torch.float64, device=dev)
+    S[:, :, :d] = torch.from_numpy(np.stack(seeds).astype(np.float64)).to(dev)
+    labels = torch.full((R, n), -7, dtype=torch.int32, device=dev)
+    cost = torch.empty(R, dtype=torch.float64, device=dev)
+    iters = torch.empty(R, dtype=torch.int32, device=dev)
+    assert _native.lib().csc_kmeans_fused_supported(n, d, k, R, max_iters) == 1
+    _native.call("csc_kmeans_fused_run", ptr(blk), ptr(fn), n, d, ld, k, R, ptr(S), ldc, int(max_iters),
+                 float(tol), ptr(labels), ptr(cost), ptr(iters), stream())
+    return labels.cpu().numpy().astype(np.int64), cost.cpu().numpy(), iters.cpu().numpy()
+
+
+def check_against_oracle(f, k, seeds, max_iters=100, tol=1e-6, exact_labels=False):
+    labels, cost, iters = fused_run(f, k, seeds, max_iters, tol)
+    for r, c0 in enumerate(seeds):
+        ref_labels, ref_cost2, _, ref_it = O.lloyd(f, k, c0, max_iters, tol)
+        assert iters[r] == ref_it, (r, iters[r], ref_it)
+        assert abs(cost[r] - ref_cost2) <= COST_TOL * ref_cost2, (r, cost[r], ref_cost2)
+        if exact_labels:
+            assert np.array_equal(labels[r], ref_labels), r
+        else:
+            assert O.adjusted_rand(labels[r], ref_labels) >= 0.999, r
+    return labels, cost, iters
+
+
+def blobs(n, d, k, spread, seed):
+    rng = np.random.default_rng(seed)
+    centers = rng.normal(size=(k, d))
+    lab = rng.integers(0, k, n)
+    return centers[lab] + spread * rng.normal(size=(n, d))
+
+
+def pp_seeds(f, k, R, seed):
+    return [O.kmeanspp(f, k, np.random.default_rng(c))[0] for c in np.random.SeedSequence(seed).spawn(R)]
+
+
+def test_fused_cfg1_from_reference_init(P):
+    """configs[0]: the reference's k-means++ seeds (golden), 20 iterations cap."""
+    g = golden("cfg1")
+    f = g["features"]
+    labels, cost, iters = fused_run(f, 10, [g["km_init"]], max_iters=20)
+    assert O.adjusted_rand(labels[0], g["km_labels"]) >= 0.999
+    assert abs(cost[0] - float(g["km_cost2"])) <= COST_TOL * float(g["km_cost2"])
+    assert iters[0] == len(g["km_hist"])
+
+
+@pytest.mark.parametrize("n,d,k,R", [(20000, 80, 20, 6), (5000, 40, 10, 10), (3000, 128, 32, 3),
+                                     (997, 7, 5, 16), (40, 3, 4, 2)])
+def test_fused_restarts_match_oracle_lloyd(P, n, d, k, R):
+    f = blobs(n, d, k, 0.8, seed=n + d)
+    check_against_oracle(f, k, pp_seeds(f, k, R, seed=d))
+
+
+def test_fused_iteration_cap_and_k1(P):
+    f = blobs(2000, 16, 6, 1.5, seed=3)
+    check_against_oracle(f, 6, pp_seeds(f, 6, 3, seed=1), max_iters=3, tol=0.0)
+    labels, cost, iters = check_against_oracle(f, 1, pp_seeds(f, 1, 2, seed=2), exact_labels=True)
+    assert (labels == 0).all() and iters[0] == 2  # k=1: the second cost repeats the first
+
+
+def test_fused_empty_cluster_repair(P):
+    """Seeds far from every row leave clusters empty on the first assignment:
+    the reference reseeds each (ascending j) at the row farthest from its
+    centroid (kmeans.py:99-108)."""
+    rng = np.random.default_rng(5)
+    f = rng.normal(size=(3000, 12))
+    seeds = []
+    for far in ([3], [1, 4], [0, 2, 5]):
+        c = f[rng.choice(3000, 6, replace=False)].copy()
+        for j in far:
+            c[j] = 1e3 + 10.0 * j
+        seeds.append(c)
+    check_against_oracle(f, 6, seeds, exact_labels=True)
+
+
+def test_fused_duplicate_rows_through_kmeans(P):
+    """Zero D^2 mass in k-means++ (replayed) and empty clusters through the public kmeans()."""
+    for s in range(6):
+        b = P.kmeans(np.array([[0.0], [0.0], [5.0]]), 3, P.KmeansConfig(restarts=1), seed=s)
+        assert b.cluster_sizes.min() >= 1
+    f = np.repeat(np.arange(5.0)[:, None] * np.ones((1, 3)), 40, axis=0)
+    a = P.kmeans(f, 7, P.KmeansConfig(restarts=4, max_iters=20), seed=9)
+    ref_labels, _, ref_cost = O.kmeans(f, 7, restarts=4, max_iters=20, tol=1e-6, seed=9)
+    assert a.cluster_sizes.min() >= 1
+    assert abs(a.feature_cost - ref_cost) <= 1e-9 * max(ref_cost, 1e-300) + 1e-12
+
+
+def test_fused_public_kmeans_matches_oracle(P):
+    """kmeans() takes the fused path at configs[1]'s shape; best-of-restarts as the reference."""
+    from paper_1706_03591_b200.kmeans import fused_supported
+    f = blobs(20000, 80, 20, 1.0, seed=11)
+    assert fused_supported(20000, 80, 20, 10, 100)
+    a = P.kmeans(f, 20, seed=4)
+    ref_labels, _, ref_cost = O.kmeans(f, 20, restarts=10, max_iters=100, tol=1e-6, seed=4)
+    assert O.adjusted_rand(a.labels, ref_labels) >= 0.999
+    assert abs(a.feature_cost - ref_cost) <= COST_TOL * ref_cost
+
+
+def test_fused_equals_lanes(P):
+    """Fused launch and per-restart lanes agree on the golden case (labels exactly, cost to 1e-9)."""
+    from paper_1706_03591_b200._device import upload_block
+    from paper_1706_03591_b200.kmeans import run_restarts
+    g = golden("kmeans")
+    blk = upload_block(g["b_f"])
+    kids = np.random.SeedSequence(77).spawn(3)
+    cfg = P.KmeansConfig(restarts=3, max_iters=50)
+    lf, cf = run_restarts(blk, 24, 12, cfg, kids, fused=True)
+    ll, cl = run_restarts(blk, 24, 12, cfg, kids, fused=False)
+    assert np.array_equal(lf, ll)
+    assert abs(cf - cl) <= COST_TOL * cl
+    assert np.array_equal(lf, g["b_labels"])
+
+
+def test_fused_shape_gate(P):
+    from paper_1706_03591_b200.kmeans import fused_supported
+    assert not fused_supported(20000, 80, 33, 10, 100)   # k > 32
+    assert not fused_supported(20000, 129, 20, 10, 100)  # d > 128
+    assert not fused_supported(2_000_000, 96, 20, 10, 100)  # rows exceed shared memory
+    assert not fused_supported(20000, 80, 20, 10, 0)

@@ -583,7 +583,7 @@ def test_graph_lloyd_equals_host_driven(P):
     blk = upload_block(f)
     kids = np.random.SeedSequence(77).spawn(3)
     cfg = P.KmeansConfig(restarts=3, max_iters=50)
-    labels, cost2 = run_restarts(blk, 24, 12, cfg, kids)
+    labels, cost2 = run_restarts(blk, 24, 12, cfg, kids, fused=False)
     ws = _Workspace(blk, 24, 12)
     seeds = batched_kmeanspp(ws, kids)
     best = None
