@@ -47,7 +47,7 @@
 
 namespace {
 
-constexpr int kFT = 512;          // threads per CTA (one CTA per SM)
+constexpr int kFT = 384;          // threads per CTA (one CTA per SM; 168 registers)
 constexpr int kFW = kFT / 32;     // warps per CTA
 constexpr int kFMaxK = 32;        // one centroid per lane
 constexpr int kFMaxD = 128;       // <= 4 columns per lane in the means pass
@@ -190,7 +190,7 @@ __device__ void group_load(const FusedArgs &a, const GShared &gs, const Grp &G_,
     for (int u = 0; u < U; ++u) {
       const int64_t e = e0 + (int64_t)u * G_.GT;
       if (e < kd) {
-        const int64_t j = e / d, t = e - j * d;
+        const int j = (int)e / (int)d, t = (int)e - j * (int)d;
         v[u] = __ldcg(Cc + j * a.ldc + t);
       }
     }
@@ -198,7 +198,7 @@ __device__ void group_load(const FusedArgs &a, const GShared &gs, const Grp &G_,
     for (int u = 0; u < U; ++u) {
       const int64_t e = e0 + (int64_t)u * G_.GT;
       if (e < kd) {
-        const int64_t j = e / d, t = e - j * d;
+        const int j = (int)e / (int)d, t = (int)e - j * (int)d;
         gs.Cs[j * a.lds + t] = v[u];
       }
     }
@@ -222,71 +222,174 @@ __device__ void group_load(const FusedArgs &a, const GShared &gs, const Grp &G_,
   }
 }
 
-// GEMM-form distances of up to 4 rows to all centroids (lane = centroid):
-// label, own distance, bounds. Same per-pair arithmetic as assign_small_kernel.
-__device__ __forceinline__ void assign_rows(const FusedArgs &a, const Shared &s, const GShared &gs,
-                                            int r, const int (&ii)[4], bool want_own, int64_t rb) {
-  const int lane = threadIdx.x & 31;
-  const int64_t d = a.d, k = a.k, RM = a.rows_max, ldf = a.ldf;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const double *cr = gs.Cs + (int64_t)lane * a.lds;
-  const double *f0 = s.Fs + (int64_t)(ii[0] < 0 ? 0 : ii[0]) * ldf;
-  const double *f1 = s.Fs + (int64_t)(ii[1] < 0 ? 0 : ii[1]) * ldf;
-  const double *f2 = s.Fs + (int64_t)(ii[2] < 0 ? 0 : ii[2]) * ldf;
-  const double *f3 = s.Fs + (int64_t)(ii[3] < 0 ? 0 : ii[3]) * ldf;
-#pragma unroll 4
+// GEMM-form distances of a 32-row tile to all centroids, register-tiled:
+// lane = (row group rg = lane/4, centroid group cg = lane%4); the lane owns
+// rows p0 + rg + 8q (q < 4) and, per pass of 16 centroids, centroids
+// c0 + cg + 4c (c < TC <= 4), so each shared load feeds 4 or TC FMAs and is
+// conflict-free (8 consecutive rows / 4 consecutive centroids at odd
+// strides). Per pair the arithmetic is assign_small_kernel's: acc =
+// fma(f_t, c_t, acc) in ascending t from 0.0, then
+// max(0, (|f|^2 - 2 acc) + |c|^2); the (min, argmin, second) merge keeps the
+// lowest index on ties. Labels, bounds and own distances are therefore
+// bit-identical to the lane path's. cand == nullptr: rows p0.. themselves.
+template <int TR, int TC>
+__device__ __forceinline__ void assign_pass(const FusedArgs &a, const GShared &gs, int c0,
+                                            const double *const (&fp)[TR], const double (&fn)[TR],
+                                            double (&v)[TR], double (&v2)[TR], int (&vi)[TR]) {
+  const int cg = threadIdx.x & 3;
+  const int64_t d = a.d, k = a.k, lds = a.lds;
+  const double *cp = gs.Cs + (int64_t)(c0 + cg) * lds;
+  double acc[TR][TC];
+#pragma unroll
+  for (int q = 0; q < TR; ++q)
+#pragma unroll
+    for (int c = 0; c < TC; ++c) acc[q][c] = 0.0;
+#pragma unroll (TR == 4 ? 2 : 4)
   for (int64_t t = 0; t < d; ++t) {
-    const double b = cr[t];
-    acc[0] = fma(f0[t], b, acc[0]);
-    acc[1] = fma(f1[t], b, acc[1]);
-    acc[2] = fma(f2[t], b, acc[2]);
-    acc[3] = fma(f3[t], b, acc[3]);
+    double f[TR], cv[TC];
+#pragma unroll
+    for (int q = 0; q < TR; ++q) f[q] = fp[q][t];
+#pragma unroll
+    for (int c = 0; c < TC; ++c) cv[c] = cp[(int64_t)(4 * c) * lds + t];
+#pragma unroll
+    for (int q = 0; q < TR; ++q)
+#pragma unroll
+      for (int c = 0; c < TC; ++c) acc[q][c] = fma(f[q], cv[c], acc[q][c]);
   }
-  const double cnl = lane < k ? gs.cn[lane] : 0.0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (ii[q] < 0) continue;  // warp-uniform
-    const int i = ii[q];
-    const double tt = __dsub_rn(s.fns[i], __dmul_rn(2.0, acc[q]));
-    double v = lane < k ? fmax(__dadd_rn(tt, cnl), 0.0) : INFINITY;
-    double v2 = INFINITY;
-    int vi = lane;
+  for (int c = 0; c < TC; ++c) {
+    const int j = c0 + cg + 4 * c;
+    if (j < k) {
+      const double cnj = gs.cn[j];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-      if (ov < v || (ov == v && oi < vi)) {
-        v2 = fmin(ov2, v);
-        v = ov;
-        vi = oi;
-      } else {
-        v2 = fmin(v2, ov);
+      for (int q = 0; q < TR; ++q) {
+        const double tt = __dsub_rn(fn[q], __dmul_rn(2.0, acc[q][c]));
+        const double d2 = fmax(__dadd_rn(tt, cnj), 0.0);
+        if (d2 < v[q]) {  // ascending j within the lane: a tie keeps the earlier index
+          v2[q] = v[q];
+          v[q] = d2;
+          vi[q] = j;
+        } else {
+          v2[q] = fmin(v2[q], d2);
+        }
       }
     }
-    if (lane == 0) {
-      s.labs[(int64_t)r * RM + i] = vi;
-      s.ubs[(int64_t)r * RM + i] = sqrt(v);
-      s.lbs[(int64_t)r * RM + i] = sqrt(v2);
-      if (want_own) a.own[(int64_t)r * a.n + rb + i] = v;
+  }
+}
+
+// rows p0 + rg + 8q (q < TR) of the candidate list (or of the CTA's rows);
+// marks the clusters a changed row left or joined in gs.misc[1] (bit mask)
+template <int TR>
+__device__ __forceinline__ void assign_rows(const FusedArgs &a, const Shared &s, const GShared &gs,
+                                            int r, int p0, int ncand, const int32_t *cand,
+                                            bool want_own, int64_t rb, bool fresh) {
+  const int lane = threadIdx.x & 31, rg = lane >> 2, cg = lane & 3;
+  const int64_t k = a.k, RM = a.rows_max, ldf = a.ldf;
+  int row[TR];
+  const double *fp[TR];
+  double fn[TR], v[TR], v2[TR];
+  int vi[TR];
+#pragma unroll
+  for (int q = 0; q < TR; ++q) {
+    const int p = p0 + rg + 8 * q;
+    row[q] = p < ncand ? (cand ? cand[p] : p) : -1;
+    fp[q] = s.Fs + (int64_t)(row[q] < 0 ? 0 : row[q]) * ldf;
+    fn[q] = row[q] >= 0 ? s.fns[row[q]] : 0.0;
+    v[q] = INFINITY;
+    v2[q] = INFINITY;
+    vi[q] = 0x7fffffff;
+  }
+  // one pass over d when the TR x TC accumulators fit (the chain of d FMAs per
+  // pair is the latency of a call), else two passes of <= 16 centroids
+  const int tc = (int)((k + 3) / 4);
+  if (TR * tc <= 20) {
+    switch (tc) {
+      case 1: assign_pass<TR, 1>(a, gs, 0, fp, fn, v, v2, vi); break;
+      case 2: assign_pass<TR, 2>(a, gs, 0, fp, fn, v, v2, vi); break;
+      case 3: assign_pass<TR, 3>(a, gs, 0, fp, fn, v, v2, vi); break;
+      case 4: assign_pass<TR, 4>(a, gs, 0, fp, fn, v, v2, vi); break;
+      case 5: assign_pass<TR, 5>(a, gs, 0, fp, fn, v, v2, vi); break;
+      case 6: assign_pass<TR, (TR <= 2 ? 6 : 1)>(a, gs, 0, fp, fn, v, v2, vi); break;
+      case 7: assign_pass<TR, (TR <= 2 ? 7 : 1)>(a, gs, 0, fp, fn, v, v2, vi); break;
+      default: assign_pass<TR, (TR <= 2 ? 8 : 1)>(a, gs, 0, fp, fn, v, v2, vi); break;
     }
+  } else {
+    for (int c0 = 0; c0 < k; c0 += 16) {
+      const int64_t tcn = (k - c0 + 3) / 4;
+      switch (tcn < 4 ? (int)tcn : 4) {
+        case 1: assign_pass<TR, 1>(a, gs, c0, fp, fn, v, v2, vi); break;
+        case 2: assign_pass<TR, 2>(a, gs, c0, fp, fn, v, v2, vi); break;
+        case 3: assign_pass<TR, 3>(a, gs, c0, fp, fn, v, v2, vi); break;
+        default: assign_pass<TR, 4>(a, gs, c0, fp, fn, v, v2, vi); break;
+      }
+    }
+  }
+  unsigned moved = 0;
+#pragma unroll
+  for (int q = 0; q < TR; ++q) {
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v[q], o);
+      const double ov2 = __shfl_xor_sync(0xffffffffu, v2[q], o);
+      const int oi = __shfl_xor_sync(0xffffffffu, vi[q], o);
+      if (ov < v[q] || (ov == v[q] && oi < vi[q])) {
+        v2[q] = fmin(ov2, v[q]);
+        v[q] = ov;
+        vi[q] = oi;
+      } else {
+        v2[q] = fmin(v2[q], ov);
+      }
+    }
+    if (cg == 0 && row[q] >= 0) {
+      const int i = row[q];
+      const int old = s.labs[(int64_t)r * RM + i];
+      if (!fresh && old != vi[q]) moved |= (1u << old) | (1u << vi[q]);
+      s.labs[(int64_t)r * RM + i] = vi[q];
+      s.ubs[(int64_t)r * RM + i] = sqrt(v[q]);
+      s.lbs[(int64_t)r * RM + i] = sqrt(v2[q]);
+      if (want_own) a.own[(int64_t)r * a.n + rb + i] = v[q];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) moved |= __shfl_xor_sync(0xffffffffu, moved, o);
+  if (lane == 0 && moved) atomicOr(reinterpret_cast<unsigned *>(gs.misc + 1), moved);
+}
+
+// All rows of the list with the warps of the group: the widest row tile that
+// still gives every warp work (latency-bound when few rows are candidates).
+__device__ __forceinline__ void assign_list(const FusedArgs &a, const Shared &s, const GShared &gs,
+                                            int r, int ncand, const int32_t *cand, bool want_own,
+                                            int64_t rb, bool fresh, int gw, int GW) {
+  if (ncand >= 32 * GW) {
+    for (int p0 = gw * 32; p0 < ncand; p0 += GW * 32)
+      assign_rows<4>(a, s, gs, r, p0, ncand, cand, want_own, rb, fresh);
+  } else if (ncand >= 16 * GW) {
+    for (int p0 = gw * 16; p0 < ncand; p0 += GW * 16)
+      assign_rows<2>(a, s, gs, r, p0, ncand, cand, want_own, rb, fresh);
+  } else {
+    for (int p0 = gw * 8; p0 < ncand; p0 += GW * 8)
+      assign_rows<1>(a, s, gs, r, p0, ncand, cand, want_own, rb, fresh);
   }
 }
 
 // Counting sort of the CTA's rows of restart r by label (stable), then one
 // register run per (cluster, column) in row order -> psum / pcnt.
 __device__ void group_partials(const FusedArgs &a, const Shared &s, const GShared &gs,
-                               const Grp &G_, int r, int nr, bool counts_only) {
+                               const Grp &G_, int r, int nr, bool counts_only, unsigned dirty) {
   const int lane = threadIdx.x & 31;
   const int64_t k = a.k, d = a.d, RM = a.rows_max, ldf = a.ldf;
   const int cta = blockIdx.x;
   const int32_t *lab = s.labs + (int64_t)r * RM;
+  if (dirty == 0) {  // no row of this block changed cluster: its partials stand
+    G_.sync();
+    return;
+  }
   if (G_.gt < 32) gs.cnt[G_.gt] = 0;
   G_.sync();
   for (int i = G_.gt; i < nr; i += G_.GT) atomicAdd(gs.cnt + lab[i], 1);
   G_.sync();
   int32_t *pc = a.pcnt + ((int64_t)r * a.G + cta) * k;
-  if (G_.gt < k) pc[G_.gt] = gs.cnt[G_.gt];
+  if (G_.gt < k && ((dirty >> G_.gt) & 1u)) pc[G_.gt] = gs.cnt[G_.gt];
   if (counts_only) {
     G_.sync();
     return;
@@ -315,9 +418,9 @@ __device__ void group_partials(const FusedArgs &a, const Shared &s, const GShare
   G_.sync();
   double *ps = a.psum + ((int64_t)r * a.G + cta) * k * d;
   for (int64_t e = G_.gt; e < k * d; e += G_.GT) {  // thread per (cluster, column)
-    const int64_t j = e / d, t = e - j * d;
+    const int j = (int)e / (int)d, t = (int)e - j * (int)d;
     const int c = gs.cnt[j];
-    if (c == 0) continue;
+    if (c == 0 || !((dirty >> j) & 1u)) continue;
     const int end = gs.runp[j], beg = end - c;
     double v = 0.0;
     for (int p = beg; p < end; ++p) v += s.Fs[(int64_t)gs.perm[p] * ldf + t];
@@ -336,7 +439,10 @@ __device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, c
   const int lane = threadIdx.x & 31;
   const int64_t k = a.k, d = a.d, RM = a.rows_max, ldf = a.ldf;
   const int cta = blockIdx.x;
-  if (G_.gt == 0) gs.misc[0] = 0;
+  if (G_.gt == 0) {
+    gs.misc[0] = 0;  // candidate count
+    gs.misc[1] = 0;  // clusters whose membership changed in this block
+  }
   group_load(a, gs, G_, r, g);
   submark(a, g, 6, first);
   int32_t *lab = s.labs + (int64_t)r * RM;
@@ -367,19 +473,29 @@ __device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, c
         gs.scal[3] = sqrt(cm);
       }
     }
-    // exact cost of iteration g-1 (labels of g-1, means of g-1), thread per row
+    // exact cost of iteration g-1 (labels of g-1, means of g-1): SP adjacent
+    // threads per row (columns split in SP contiguous parts, added by a fixed
+    // xor tree), rows in rounds of GT / SP
+    int SP = 1;
+    while (SP < 8 && nr * SP * 2 <= G_.GT) SP *= 2;
+    const int part = G_.gt % SP;
+    const int t0 = part * (int)d / SP, t1 = (part + 1) * (int)d / SP;
     double acc = 0.0;
-    for (int i = G_.gt; i < nr; i += G_.GT) {
-      const double *fr = s.Fs + (int64_t)i * ldf;
-      const int l = lab[i];
-      const double *cr = gs.Cs + (int64_t)l * a.lds;
+    for (int i0 = 0; i0 < nr; i0 += G_.GT / SP) {
+      const int i = i0 + G_.gt / SP;
       double v = 0.0;
-      for (int64_t t = 0; t < d; ++t) {
-        const double df = fr[t] - cr[t];
-        v = fma(df, df, v);
+      if (i < nr && G_.gt < (G_.GT / SP) * SP) {
+        const double *fr = s.Fs + (int64_t)i * ldf;
+        const int l = lab[i];
+        const double *cr = gs.Cs + (int64_t)l * a.lds;
+        for (int64_t t = t0; t < t1; ++t) {
+          const double df = fr[t] - cr[t];
+          v = fma(df, df, v);
+        }
+        if (part == 0) a.labels_out[(int64_t)r * a.n + rb + i] = l;
       }
-      acc += v;
-      a.labels_out[(int64_t)r * a.n + rb + i] = l;
+      for (int o = 1; o < SP; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (part == 0) acc += v;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -432,18 +548,10 @@ __device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, c
   submark(a, g, 8, first);
   if (first && a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && g < a.trace_cap)
     a.trace[(int64_t)g * 16 + 11] = (unsigned long long)ncand;
-  for (int q0 = G_.gw * 4; q0 < ncand; q0 += G_.GW * 4) {
-    int ii[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int p = q0 + q;
-      ii[q] = p < ncand ? (g == 0 ? p : gs.cand[p]) : -1;
-    }
-    assign_rows(a, s, gs, r, ii, false, rb);
-  }
+  assign_list(a, s, gs, r, ncand, g == 0 ? nullptr : gs.cand, false, rb, g == 0, G_.gw, G_.GW);
   G_.sync();
   submark(a, g, 9, first);
-  group_partials(a, s, gs, G_, r, nr, false);
+  group_partials(a, s, gs, G_, r, nr, false, g == 0 ? ~0u : (unsigned)gs.misc[1]);
   submark(a, g, 10, first);
 }
 
@@ -465,43 +573,52 @@ __device__ __forceinline__ double cost_sum(const FusedArgs &a, int r) {
   return warp_sum(c);
 }
 
-// Means of (restart r, cluster j) from the block partials, by a quad of warps:
-// warp w4 adds blocks [w4 G/4, (w4+1) G/4) in order (loads batched), warp 0
-// adds the four range sums in order. Movement and |c|^2 for the next bounds.
-__device__ void means_item(const FusedArgs &a, const Shared &s, int w4, int qid, int r, int j,
-                           int g, bool flag_empty) {
+// Means of (restart r, cluster j) from the block partials, by a whole CTA:
+// warp w adds the partials of blocks [w G / kFW, (w+1) G / kFW) in block order
+// (loads issued in batches of 4 ahead of the adds), warp 0 adds the kFW range
+// sums in order. Movement and |c|^2 for the next bounds. Called uniformly by
+// every thread of the CTA.
+__device__ void means_item(const FusedArgs &a, const Shared &s, int r, int j, int g,
+                           bool flag_empty) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t k = a.k, d = a.d, R = a.R, G = a.G;
-  const int64_t b_lo = (int64_t)w4 * G / kQuad, b_hi = (int64_t)(w4 + 1) * G / kQuad;
-  int cnt = 0;
+  const int b_lo = (int)((int64_t)wid * G / kFW), b_hi = (int)((int64_t)(wid + 1) * G / kFW);
+  const double *cold = a.cent + ((int64_t)(g & 1) * R + r) * k * a.ldc + j * a.ldc;
+  double old[4];
+  if (wid == 0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = lane + 32 * u;
+      old[u] = t < d ? __ldcg(cold + t) : 0.0;
+    }
+  }
+  const int b = b_lo + lane;  // kFW >= 12 warps: a range has <= 13 blocks
+  const int pc = b < b_hi ? __ldcg(a.pcnt + ((int64_t)r * G + b) * k + j) : 0;
+  int cnt = pc;
   double sv[4] = {0.0, 0.0, 0.0, 0.0};
   const double *pbase = a.psum + ((int64_t)r * G * k + j) * d;
-  for (int64_t c0 = b_lo; c0 < b_hi; c0 += 32) {
-    const int64_t b = c0 + lane;
-    const int pc = b < b_hi ? __ldcg(a.pcnt + ((int64_t)r * G + b) * k + j) : 0;
-    cnt += pc;
-    unsigned m = __ballot_sync(0xffffffffu, pc > 0);
-    while (m) {
-      int bb[4];
+  unsigned m = __ballot_sync(0xffffffffu, pc > 0);
+  constexpr int NB = 3;  // nonzero blocks whose loads are in flight together
+  while (m) {
+    int bb[NB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        bb[q] = m ? (int)c0 + __ffs(m) - 1 : -1;
-        m &= m ? m - 1 : 0u;
-      }
-      double v[4][4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t t = lane + 32 * u;
-          v[q][u] = (bb[q] >= 0 && t < d) ? __ldcg(pbase + (int64_t)bb[q] * k * d + t) : 0.0;
-        }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (bb[q] >= 0)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) sv[u] += v[q][u];
+    for (int q = 0; q < NB; ++q) {
+      bb[q] = m ? b_lo + __ffs(m) - 1 : -1;
+      m &= m ? m - 1 : 0u;
     }
+    double v[NB][4];
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t t = lane + 32 * u;
+        v[q][u] = (bb[q] >= 0 && t < d) ? __ldcg(pbase + (int64_t)bb[q] * k * d + t) : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      if (bb[q] >= 0)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sv[u] += v[q][u];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -512,12 +629,11 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int w4, int qid,
     if (t < d) mine[t] = sv[u];
   }
   if (lane == 0) s.p2c[wid] = cnt;
-  named_sync(5 + qid, kQuad * 32);
-  if (w4 == 0) {
+  __syncthreads();
+  if (wid == 0) {
     int tot = 0;
-    for (int w = 0; w < kQuad; ++w) tot += s.p2c[wid + w];
+    for (int w = 0; w < kFW; ++w) tot += s.p2c[w];
     const double denom = (double)(tot > 1 ? tot : 1);
-    const double *cold = a.cent + ((int64_t)(g & 1) * R + r) * k * a.ldc + j * a.ldc;
     double *cnew = a.cent + ((int64_t)((g + 1) & 1) * R + r) * k * a.ldc + j * a.ldc;
     double mv = 0.0, nrm = 0.0;
 #pragma unroll
@@ -525,11 +641,10 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int w4, int qid,
       const int64_t t = lane + 32 * u;
       if (t < d) {
         double sum = 0.0;
-        for (int w = 0; w < kQuad; ++w) sum += s.p2[(int64_t)(wid + w) * d + t];
+        for (int w = 0; w < kFW; ++w) sum += s.p2[(int64_t)w * d + t];
         const double mean = __ddiv_rn(sum, denom);
-        const double old = __ldcg(cold + t);
         cnew[t] = mean;
-        const double df = mean - old;
+        const double df = mean - old[u];
         mv = fma(df, df, mv);
         nrm = fma(mean, mean, nrm);
       }
@@ -543,7 +658,7 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int w4, int qid,
       if (flag_empty && tot == 0) a.eflag[r] = g + 1;
     }
   }
-  named_sync(5 + qid, kQuad * 32);  // p2 reuse
+  __syncthreads();  // p2 reuse
 }
 
 __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) {
@@ -591,35 +706,33 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
       G_.gt = tid % G_.GT;
       G_.gw = G_.gt >> 5;
       const GShared gs = gcarve(smem_raw, a, G_.id);
-      for (int ai = G_.id; ai < A; ai += ng) phase1(a, s, gs, G_, s.act[ai], g, nr, rb, ai == 0);
+      for (int ai = G_.id; ai < A; ai += ng) {
+        phase1(a, s, gs, G_, s.act[ai], g, nr, rb, ai == 0);
+      }
     }
     __syncthreads();
     mark(g, 1);
     grid_sync(a.bar, G);
     mark(g, 2);
-    // ---- phase 2: stop rule, means ----------------------------------------
-    {
-      const int qid = wid / kQuad, w4 = wid % kQuad;
-      const int nq = G * (kFW / kQuad);
-      for (int64_t q = (int64_t)cta * (kFW / kQuad) + qid; q < (int64_t)A * k; q += nq) {
-        const int r = s.act[q / k], j = (int)(q % k);
-        bool stop = false;
-        if (g > 0) {
-          const double c = cost_sum(a, r);
-          const int64_t hs = a.max_iters + 1;
-          const double prev = g >= 2 ? __ldcg(a.hist + r * hs + g - 2) : INFINITY;
-          stop = (g >= 2 && prev - c <= a.tol * prev) || g >= a.max_iters;
-          if (j == 0 && w4 == 0 && lane == 0) {
-            a.hist[r * hs + g - 1] = c;
-            if (stop) {
-              a.cost_out[r] = c;
-              a.iters_out[r] = g;
-              a.done[r] = 1;
-            }
+    // ---- phase 2: stop rule, means (one CTA per (restart, cluster)) --------
+    for (int q = cta; q < A * (int)k; q += G) {
+      const int r = s.act[q / (int)k], j = q % (int)k;
+      bool stop = false;
+      if (g > 0) {
+        const double c = cost_sum(a, r);  // identical in every warp
+        const int64_t hs = a.max_iters + 1;
+        const double prev = g >= 2 ? __ldcg(a.hist + r * hs + g - 2) : INFINITY;
+        stop = (g >= 2 && prev - c <= a.tol * prev) || g >= a.max_iters;
+        if (j == 0 && tid == 0) {
+          a.hist[r * hs + g - 1] = c;
+          if (stop) {
+            a.cost_out[r] = c;
+            a.iters_out[r] = g;
+            a.done[r] = 1;
           }
         }
-        if (!stop) means_item(a, s, w4, qid, r, j, g, true);
       }
+      if (!stop) means_item(a, s, r, j, g, true);
     }
     __syncthreads();
     mark(g, 3);
@@ -638,14 +751,9 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
       for (int r = 0; r < R; ++r) {
         if (__ldcg(a.eflag + r) != g + 1) continue;
         group_load(a, gs, W, r, g);
-        for (int q0 = wid * 4; q0 < nr; q0 += kFW * 4) {
-          int ii[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) ii[q] = q0 + q < nr ? q0 + q : -1;
-          assign_rows(a, s, gs, r, ii, true, rb);
-        }
+        assign_list(a, s, gs, r, nr, nullptr, true, rb, true, wid, kFW);
         W.sync();
-        group_partials(a, s, gs, W, r, nr, true);
+        group_partials(a, s, gs, W, r, nr, true, ~0u);
       }
       grid_sync(a.bar, G);
       // reseeding (kmeans.py:101-108), one CTA per flagged restart
@@ -719,16 +827,12 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
           }
         }
         W.sync();
-        group_partials(a, s, gs, W, r, nr, false);
+        group_partials(a, s, gs, W, r, nr, false, ~0u);
       }
       grid_sync(a.bar, G);
-      {
-        const int qid = wid / kQuad, w4 = wid % kQuad;
-        const int nq = G * (kFW / kQuad);
-        for (int64_t q = (int64_t)cta * (kFW / kQuad) + qid; q < R * k; q += nq) {
-          const int r = (int)(q / k), j = (int)(q % k);
-          if (__ldcg(a.eflag + r) == g + 1) means_item(a, s, w4, qid, r, j, g, false);
-        }
+      for (int q = cta; q < (int)(R * k); q += G) {
+        const int r = q / (int)k, j = q % (int)k;
+        if (__ldcg(a.eflag + r) == g + 1) means_item(a, s, r, j, g, false);
       }
       grid_sync(a.bar, G);
     }
