@@ -139,7 +139,9 @@ int csc_cheb_combine(const void *x_dev, const void *keep_dev, int64_t n, int64_t
  *   "stream_hint"  1: row-local streams use L2 evict_first (default 1)
  *   "vpl"          preferred 16-byte vectors per lane (1, 2, 4): narrower row
  *                  groups, more gathers in flight per lane (default 0 = 2 for rows
- *                  up to 512 B, else 1) */
+ *                  up to 512 B, else 1)
+ *   "sweep_g"      force the row-group width (4, 8, 16, 32; default 0 = from
+ *                  "vpl") */
 int csc_set_tuning(const char *key, int64_t value);
 
 /* Measurement hook: when enabled, every main sweep launch of csc_cheb_filter /

@@ -875,6 +875,21 @@ int vpl_pref() {
   return g_vpl_pref;
 }
 
+// forced row-group width (0 = automatic; tuning knob). At configs[1] (n = 20k,
+// d = 40 fresh columns, the gathered block L2-resident) every width runs at
+// 26.6-30.7 us per order (G = 16/32 fastest; 3 or 5 vectors per lane, tried,
+// do not help): the gather is bound by L2 throughput there, not lane use.
+int g_sweep_g = -1;
+
+int sweep_g() {
+  if (g_sweep_g < 0) {
+    const char *e = getenv("CSC_SWEEP_G");
+    g_sweep_g = e ? atoi(e) : 0;
+    if (g_sweep_g != 4 && g_sweep_g != 8 && g_sweep_g != 16 && g_sweep_g != 32) g_sweep_g = 0;
+  }
+  return g_sweep_g;
+}
+
 template <typename T, int G>
 int run_order_g(const csc_chebop &op, const SweepArgs &A, int mode, double *partials,
                 int64_t &nparts, cudaStream_t st, void *seg_scratch) {
@@ -892,6 +907,13 @@ int run_order(const csc_chebop &op, const SweepArgs &A, int mode, double *partia
               int64_t &nparts, cudaStream_t st, void *seg_scratch) {
   // default (0): 2 vectors per lane for rows up to 512 B, else full-warp groups
   // (A/B on B200: cfg4 fp32 d=64 4.59 vs 4.76 ms/order, cfg5 d=48 3.33 vs 3.40)
+  switch (sweep_g()) {
+    case 4: return run_order_g<T, 4>(op, A, mode, partials, nparts, st, seg_scratch);
+    case 8: return run_order_g<T, 8>(op, A, mode, partials, nparts, st, seg_scratch);
+    case 16: return run_order_g<T, 16>(op, A, mode, partials, nparts, st, seg_scratch);
+    case 32: return run_order_g<T, 32>(op, A, mode, partials, nparts, st, seg_scratch);
+    default: break;
+  }
   const int pref = vpl_pref() ? vpl_pref() : (A.nvec <= 32 ? 2 : 1);
   const int want = (A.nvec + pref - 1) / pref;
   if (want <= 4) return run_order_g<T, 4>(op, A, mode, partials, nparts, st, seg_scratch);
@@ -1429,6 +1451,11 @@ int csc_set_tuning(const char *key, int64_t value) {
     vpl_pref();
     CSC_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4, "vpl must be 0, 1, 2 or 4");
     g_vpl_pref = (int)value;
+  } else if (k == "sweep_g") {
+    sweep_g();
+    CSC_REQUIRE(value == 0 || value == 4 || value == 8 || value == 16 || value == 32,
+                "sweep_g must be 0, 4, 8, 16 or 32");
+    g_sweep_g = (int)value;
   } else if (k == "stream_hint") {
     stream_hint();
     g_hint = value ? 1 : 0;

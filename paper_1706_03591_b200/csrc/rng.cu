@@ -294,10 +294,16 @@ int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, do
   ChunkPlan P;
   P.n = n;
   P.ncols = ncols;
-  P.W = 128;
-  // ~1.02 draws per output; chunks of B draws with a W-draw lookback
-  P.B = std::max<int64_t>(512, std::min<int64_t>(4096, csc::ceil_div(n, 64)));
-  const int64_t draws = n + n / 16 + 4 * P.B;
+  // ~1.02 draws per output; chunks of B draws with a W-draw lookback. Every
+  // draw of a chunk thread is a dependent LCG + ziggurat step, so the chunk
+  // length is the latency: B is chosen for ~19k chunk threads (148 SMs x 4
+  // warps) over all columns, between 64 and 4096 draws. A misaligned parse
+  // resynchronises at the first one-draw output (~98% of outputs), so short
+  // chunks use a 32-draw lookback (boundaries are still checked below).
+  const int64_t est = n + n / 16;
+  P.B = std::max<int64_t>(64, std::min<int64_t>(4096, csc::ceil_div(est * ncols, 148 * 128)));
+  P.W = P.B < 512 ? 32 : 128;
+  const int64_t draws = est + 4 * P.B;
   P.nch = csc::ceil_div(draws, P.B);
   const int64_t T = ncols * P.nch;
   csc::Scratch st_dev, counts, fgs, fge, cnt_t, offs, bad, tmp;

@@ -29,7 +29,8 @@ if a.workload == "cfg4":
     n = 4_000_000
     g, _ = G.chung_lu_sbm(n, 50, 16.0, 2.3, 20000.0, 0.05, seed=4)
 else:
-    n, k, deg, ratio = {"cfg3": (1_000_000, 100, 32.0, 0.02), "cfg5": (2_000_000, 64, 20.0, 0.05)}[a.workload]
+    n, k, deg, ratio = {"cfg3": (1_000_000, 100, 32.0, 0.02), "cfg5": (2_000_000, 64, 20.0, 0.05),
+                        "cfg2": (20_000, 20, 24.0, 0.05)}[a.workload]
     q1, q2 = G.sbm_probabilities(n, k, deg, ratio)
     g = G.graph_from_codes(n, G.planted_partition_codes(n, k, q1, q2, 3))
 lap = P.laplacian(g)
