@@ -212,6 +212,22 @@ int csc_kmeans_fused_run(const double *f_dev, const double *rownorm_dev, int64_t
                          int64_t ld, int64_t k, int64_t R, const double *seeds_dev, int64_t ldc,
                          int max_iters, double tol, int32_t *labels_dev, double *cost2_dev,
                          int32_t *iters_dev, void *stream);
+/* The same fused launch with the k-means++ seeding inside (kmeans.py:64-77):
+ * first_idx_host[r] = restart r's integers(n) draw, uniforms_host[r*(k-1)+j-1]
+ * = its j-th random() draw (host arrays, the reference's consumption order).
+ * Each draw takes searchsorted(cumsum(D^2), u * total) over the rows in
+ * order (fixed-order block prefixes), D^2 in the difference form. seeds_dev
+ * (nullable, R x k x ldc) receives the seeds; flags_dev[r] (int32) = the first
+ * draw whose D^2 mass was 0 (the reference then draws integers(n): the caller
+ * must re-seed that restart sequentially and rerun with
+ * csc_kmeans_fused_run), else -1. |f|^2 is computed in the kernel with
+ * csc_kmeans_rownorms' association. Asynchronous. */
+int csc_kmeans_fused_kpp_run(const double *f_dev, int64_t n, int64_t d, int64_t ld, int64_t k,
+                             int64_t R, const int64_t *first_idx_host,
+                             const double *uniforms_host, int64_t ldc, int max_iters,
+                             double tol, int32_t *labels_dev, double *cost2_dev,
+                             int32_t *iters_dev, double *seeds_dev, int32_t *flags_dev,
+                             void *stream);
 /* diagnostics: while trace_dev != NULL, fused runs record CTA 0's
  * %globaltimer (ns) at the phase boundaries of iteration g into
  * trace_dev[g * 16 + slot] (slots 0..5: phase 1 start/end, barrier, phase 2

@@ -57,6 +57,8 @@ SIGNATURES = {
     "csc_kmeans_cost": ([_P, _P, _P, _I64, _I64, _I64, _I64, _P, _P], _INT),
     "csc_kmeans_fused_supported": ([_I64, _I64, _I64, _I64, _INT], _INT),
     "csc_kmeans_fused_trace": ([_P, _I64], _INT),
+    "csc_kmeans_fused_kpp_run": ([_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _INT, _D, _P, _P, _P, _P, _P, _P],
+                                 _INT),
     "csc_kmeans_fused_run": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _P, _I64, _INT, _D, _P, _P, _P, _P], _INT),
     "csc_kmeanspp_nchunks": ([_I64], _INT),
     "csc_kmeanspp_dist": ([_P, _I64, _I64, _I64, _P, _P, _INT, _P, _I64, _P, _P], _INT),

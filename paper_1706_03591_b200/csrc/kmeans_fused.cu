@@ -77,6 +77,14 @@ struct FusedArgs {
   int32_t *rep_idx;     // [R][k]
   int32_t *rep_j;       // [R][k]
   unsigned *bar;        // [2] arrival count, generation
+  // in-kernel k-means++ (kmeans.py:64-77), when kpp_first != nullptr
+  const int64_t *kpp_first;  // [R] the restart's integers(n) draw
+  const double *kpp_unif;    // [R][k-1] its random() draws
+  double *kpp_part;          // [R][G] block sums of the D^2 weights
+  int32_t *kpp_pick;         // [R] row drawn by the current step
+  int32_t *kpp_ready;        // [R] = j + 1 once draw j's pick is written (zeroed)
+  int32_t *kpp_flag;         // [R] first j whose D^2 mass was 0 (host replays), else -1
+  double *seeds_out;         // [R][k][ldc] the seeds (nullable)
   unsigned long long *trace;  // optional: CTA 0's globaltimer at phase boundaries [iter][8]
   int64_t trace_cap;
   int G, rows_max, ldf, lds, ngmax;
@@ -86,6 +94,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ int ld_acquire_i(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int32_t *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -141,6 +159,11 @@ struct GShared {
 
 __host__ __device__ inline int64_t gstride_d(int lds) { return 32 * (int64_t)lds + 64 + kFW + 4; }
 __host__ __device__ inline int64_t gstride_i(int64_t RM) { return 2 * RM + 64 + kFMisc; }
+// double offset of the per-group area: after Fs, |f|^2, sqrt, ub, lb and the
+// phase-2 scratch, rounded to 16 bytes (the k-means++ staging reads double2)
+__host__ __device__ inline int64_t group_base(int64_t RM, int64_t ldf, int64_t R, int64_t d) {
+  return (RM * ldf + 2 * RM + 2 * R * RM + kFW * d + 1) & ~int64_t(1);
+}
 
 __device__ __forceinline__ Shared carve(unsigned char *raw, const FusedArgs &a) {
   const int64_t RM = a.rows_max, R = a.R;
@@ -151,7 +174,8 @@ __device__ __forceinline__ Shared carve(unsigned char *raw, const FusedArgs &a) 
   s.ubs = s.fsq + RM;
   s.lbs = s.ubs + R * RM;
   s.p2 = s.lbs + R * RM;  // [kFW][d]
-  int32_t *ib = reinterpret_cast<int32_t *>(s.p2 + kFW * a.d + a.ngmax * gstride_d(a.lds));
+  int32_t *ib = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(raw) + group_base(RM, a.ldf, R, a.d) +
+                                            a.ngmax * gstride_d(a.lds));
   s.labs = ib;
   s.act = ib + R * RM;  // [kFMaxR + 1]
   s.p2c = s.act + kFMaxR + 1;  // [kFW]
@@ -161,7 +185,7 @@ __device__ __forceinline__ Shared carve(unsigned char *raw, const FusedArgs &a) 
 __device__ __forceinline__ GShared gcarve(unsigned char *raw, const FusedArgs &a, int gi) {
   const int64_t RM = a.rows_max, R = a.R;
   GShared g;
-  double *gb = reinterpret_cast<double *>(raw) + RM * a.ldf + 2 * RM + 2 * R * RM + kFW * a.d;
+  double *gb = reinterpret_cast<double *>(raw) + group_base(RM, a.ldf, R, a.d);
   g.Cs = gb + gi * gstride_d(a.lds);
   g.cn = g.Cs + 32 * a.lds;
   g.del = g.cn + 32;
@@ -661,6 +685,161 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int r, int j, in
   __syncthreads();  // p2 reuse
 }
 
+__device__ __forceinline__ void kmark(const FusedArgs &a, int j, int slot) {
+  if (a.trace && a.trace_cap >= 128 && blockIdx.x == 0 && threadIdx.x == 0)
+    a.trace[(int64_t)(96 + j) * 16 + slot] = gtimer();
+}
+
+// k-means++ seeds of every restart (kmeans.py:64-77) before the Lloyd loop:
+// per draw j, the D^2 weights closest_i = min over chosen centroids of
+// |f_i - c|^2 (difference form, ascending column order, as kppb_dist_kernel)
+// stay in shared memory; each block's inclusive prefix of its weights (warp
+// scan, fixed order) gives a block sum; after a grid barrier every block forms
+// the same prefix over the block sums, the draw u * total
+// (Generator.choice(n, p) == searchsorted(cumsum(p), u, 'right')) selects the
+// block whose prefix first exceeds it, and that block selects the first row
+// with a positive weight whose prefix exceeds it. A zero D^2 mass (the
+// reference then draws integers(n)) is flagged for the host to replay.
+// Closest weights live in s.ubs, prefixes in s.lbs (free before Lloyd).
+__device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShared &g0, int nr,
+                               int64_t rb) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int cta = blockIdx.x, G = a.G;
+  const int64_t k = a.k, d = a.d, R = a.R, RM = a.rows_max, ldf = a.ldf, lds = a.lds;
+  const int di = (int)d, ki = (int)k;
+  double *cl = s.ubs, *pre = s.lbs;
+  // centroid j of every restart, transposed into g0.Cs as [t][RP] (RP = R
+  // rounded up to 4: one 32-byte pair of loads feeds 4 restarts' chains)
+  const int RP = ((int)R + 3) & ~3;
+  auto stage = [&](int j) {
+    for (int e = tid; e < (int)R * di; e += kFT) {
+      const int r = e / di, t = e - r * di;
+      const int64_t idx = j == 0 ? a.kpp_first[r] : (int64_t)__ldcg(a.kpp_pick + r);
+      const double v = __ldg(a.F + idx * a.ld + t);
+      g0.Cs[(int64_t)t * RP + r] = v;
+      if (cta == 0) {
+        a.cent[((int64_t)r * k + j) * a.ldc + t] = v;  // buffer 0: the Lloyd seeds
+        if (a.seeds_out) a.seeds_out[((int64_t)r * k + j) * a.ldc + t] = v;
+      }
+    }
+    __syncthreads();
+  };
+  stage(0);
+  for (int j = 0; j + 1 < ki; ++j) {
+    kmark(a, j, 0);
+    for (int e = tid; e < nr * (RP / 4); e += kFT) {  // (row, 4 restarts) per item
+      const int i = e / (RP / 4), c4 = (e - i * (RP / 4)) * 4;
+      const double *fr = s.Fs + (int64_t)i * ldf;
+      const double2 *cr = reinterpret_cast<const double2 *>(g0.Cs + c4);
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+      for (int t = 0; t < di; ++t) {
+        const double f = fr[t];
+        const double2 c01 = cr[(t * RP) >> 1], c23 = cr[((t * RP) >> 1) + 1];
+        const double x0 = f - c01.x, x1 = f - c01.y, x2 = f - c23.x, x3 = f - c23.y;
+        acc[0] = fma(x0, x0, acc[0]);
+        acc[1] = fma(x1, x1, acc[1]);
+        acc[2] = fma(x2, x2, acc[2]);
+        acc[3] = fma(x3, x3, acc[3]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (c4 + q >= R) break;
+        double *c = cl + (int64_t)(c4 + q) * RM + i;
+        *c = j == 0 ? acc[q] : fmin(*c, acc[q]);
+      }
+    }
+    __syncthreads();
+    for (int r = wid; r < R; r += kFW) {
+      double carry = 0.0;
+      for (int i0 = 0; i0 < nr; i0 += 32) {
+        const int i = i0 + lane;
+        double x = i < nr ? cl[(int64_t)r * RM + i] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        x += carry;
+        if (i < nr) pre[(int64_t)r * RM + i] = x;
+        carry = __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) a.kpp_part[(int64_t)r * G + cta] = carry;
+    }
+    kmark(a, j, 1);
+    grid_sync(a.bar, G);
+    for (int r = wid; r < R; r += kFW) {
+      double p[5], loc[5], sl = 0.0;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const int c = 5 * lane + q;
+        p[q] = c < G ? __ldcg(a.kpp_part + (int64_t)r * G + c) : 0.0;
+        sl += p[q];
+        loc[q] = sl;
+      }
+      double incl = sl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (lane == 0) excl = 0.0;
+      const double total = __shfl_sync(0xffffffffu, incl, 31);
+      if (!(total > 0.0)) {
+        if (cta == 0 && lane == 0 && __ldcg(a.kpp_flag + r) < 0) a.kpp_flag[r] = j + 1;
+        if (cta == 0 && lane == 0) {
+          a.kpp_pick[r] = 0;
+          __threadfence();
+          st_release(a.kpp_ready + r, j + 1);
+        }
+        continue;
+      }
+      const double target = a.kpp_unif[(int64_t)r * (k - 1) + j] * total;
+      int qf = -1;
+#pragma unroll
+      for (int q = 4; q >= 0; --q)
+        if (5 * lane + q < G && excl + loc[q] > target) qf = q;
+      const unsigned hit = __ballot_sync(0xffffffffu, qf >= 0);
+      // the last block always reaches the total (its prefix is the total)
+      const int lf = hit ? __ffs(hit) - 1 : (G - 1) / 5;
+      const int qsel = __shfl_sync(0xffffffffu, hit ? qf : (G - 1) % 5, lf);
+      const int cstar = 5 * lf + qsel;
+      if (cstar != cta) continue;
+      double base = excl;
+      if (qsel > 0) base = excl + loc[qsel - 1];
+      base = __shfl_sync(0xffffffffu, base, lf);
+      int found = -1, lastpos = -1;
+      for (int i0 = 0; i0 < nr && found < 0; i0 += 32) {
+        const int i = i0 + lane;
+        const double w = i < nr ? cl[(int64_t)r * RM + i] : 0.0;
+        const bool pos = i < nr && w > 0.0;
+        const bool ok = pos && base + pre[(int64_t)r * RM + i] > target;
+        const unsigned hb = __ballot_sync(0xffffffffu, ok);
+        const unsigned pb = __ballot_sync(0xffffffffu, pos);
+        if (hb) found = i0 + __ffs(hb) - 1;
+        if (pb) lastpos = i0 + 31 - __clz(pb);
+      }
+      if (found < 0) found = lastpos >= 0 ? lastpos : 0;  // rounding fallback
+      if (lane == 0) {
+        a.kpp_pick[r] = (int32_t)(rb + found);
+        __threadfence();
+        st_release(a.kpp_ready + r, j + 1);
+      }
+    }
+    kmark(a, j, 2);
+    // wait for every restart's pick (one writer block each) instead of a barrier
+    __syncthreads();
+    if (tid < R)
+      while (ld_acquire_i(a.kpp_ready + tid) != j + 1) __nanosleep(20);
+    __syncthreads();
+    kmark(a, j, 3);
+    stage(j + 1);
+    kmark(a, j, 4);
+  }
+  grid_sync(a.bar, G);  // buffer 0 (written by block 0) before the first Lloyd phase
+}
+
 __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -674,15 +853,22 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
     const int64_t i = e / d, t = e - i * d;
     s.Fs[i * ldf + t] = a.F[(rb + i) * a.ld + t];
   }
-  for (int i = tid; i < nr; i += kFT) {
-    const double v = a.fnorm[rb + i];
-    s.fns[i] = v;
-    s.fsq[i] = sqrt(v);
+  if (a.fnorm) {
+    for (int i = tid; i < nr; i += kFT) s.fns[i] = a.fnorm[rb + i];
+  } else {  // |f|^2 with csc_kmeans_rownorms' association (lane-strided, xor tree)
+    __syncthreads();
+    for (int i = wid; i < nr; i += kFW) {
+      const double *fr = s.Fs + (int64_t)i * ldf;
+      double v = 0.0;
+      for (int64_t t = lane; t < d; t += 32) v = fma(fr[t], fr[t], v);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) s.fns[i] = v;
+    }
   }
-  for (int gi = 0; gi < a.ngmax; ++gi) {
-    const GShared gs = gcarve(smem_raw, a, gi);
-    for (int64_t e = tid; e < (32 - k) * a.lds; e += kFT) gs.Cs[k * a.lds + e] = 0.0;
-  }
+  __syncthreads();
+  for (int i = tid; i < nr; i += kFT) s.fsq[i] = sqrt(s.fns[i]);
+  if (a.kpp_first) kmeanspp_phase(a, s, gcarve(smem_raw, a, 0), nr, rb);
   if (tid == 0) {
     for (int r = 0; r < R; ++r) s.act[r] = r;
     s.act[kFMaxR] = (int)R;
@@ -854,7 +1040,7 @@ struct FusedGeom {
 };
 
 size_t fused_smem(int64_t RM, int64_t d, int64_t R, int ngmax, int ldf, int lds) {
-  const int64_t dbl = RM * ldf + 2 * RM + 2 * R * RM + kFW * d + ngmax * gstride_d(lds);
+  const int64_t dbl = group_base(RM, ldf, R, d) + ngmax * gstride_d(lds);
   const int64_t ints = R * RM + kFMaxR + 1 + kFW + ngmax * gstride_i(RM);
   return (size_t)(dbl * 8 + ints * 4);
 }
@@ -899,19 +1085,21 @@ extern "C" int csc_kmeans_fused_supported(int64_t n, int64_t d, int64_t k, int64
   return fused_geometry(n, d, k, R, max_iters, g) ? 1 : 0;
 }
 
-extern "C" int csc_kmeans_fused_run(const double *f, const double *fnorm, int64_t n, int64_t d,
-                                    int64_t ld, int64_t k, int64_t R, const double *seeds,
-                                    int64_t ldc, int max_iters, double tol, int32_t *labels,
-                                    double *cost2, int32_t *iters, void *stream) {
-  csc::clear_error();
-  CSC_REQUIRE(f && fnorm && seeds && labels && cost2 && iters, "csc_kmeans_fused_run: NULL pointer");
-  CSC_REQUIRE(ld >= d && ldc >= d, "csc_kmeans_fused_run: ld/ldc < d");
+namespace {
+
+// Shared launcher: seeds (device, R x k x ldc) or the k-means++ draws (host).
+int fused_launch(const char *who, const double *f, const double *fnorm, int64_t n, int64_t d,
+                 int64_t ld, int64_t k, int64_t R, const double *seeds,
+                 const int64_t *first_host, const double *unif_host, double *seeds_out,
+                 int32_t *flags, int64_t ldc, int max_iters, double tol, int32_t *labels,
+                 double *cost2, int32_t *iters, cudaStream_t st) {
+  CSC_REQUIRE(ld >= d && ldc >= d, "%s: ld/ldc < d", who);
   FusedGeom g;
   CSC_REQUIRE(fused_geometry(n, d, k, R, max_iters, g),
-              "csc_kmeans_fused_run: shape outside the fused kernel (n=%lld d=%lld k=%lld R=%lld)",
+              "%s: shape outside the fused kernel (n=%lld d=%lld k=%lld R=%lld)", who,
               (long long)n, (long long)d, (long long)k, (long long)R);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t G = g.G;
+  const bool kpp = first_host != nullptr;
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t b_cent = al(sizeof(double) * 2 * R * k * ldc);
   const size_t b_kvec = al(sizeof(double) * 2 * R * 2 * k);
@@ -921,8 +1109,14 @@ extern "C" int csc_kmeans_fused_run(const double *f, const double *fnorm, int64_
   const size_t b_own = al(sizeof(double) * R * n);
   const size_t b_pcnt = al(sizeof(int32_t) * R * G * k);
   const size_t b_ints = al(sizeof(int32_t) * (3 * R + 2 * R * k) + 2 * sizeof(unsigned));
+  const size_t b_kfirst = kpp ? al(sizeof(int64_t) * R) : 0;
+  const size_t b_kunif = kpp ? al(sizeof(double) * R * std::max<int64_t>(1, k - 1)) : 0;
+  const size_t b_kpart = kpp ? al(sizeof(double) * R * G) : 0;
+  const size_t b_kpick = kpp ? al(sizeof(int32_t) * 2 * R) : 0;
   csc::Scratch ws;
-  CSC_TRY_CUDA(ws.alloc(b_cent + b_kvec + b_psum + b_cpart + b_hist + b_own + b_pcnt + b_ints, st));
+  CSC_TRY_CUDA(ws.alloc(b_cent + b_kvec + b_psum + b_cpart + b_hist + b_own + b_pcnt + b_ints +
+                            b_kfirst + b_kunif + b_kpart + b_kpick,
+                        st));
   unsigned char *p = ws.as<unsigned char>();
   FusedArgs a;
   a.F = f;
@@ -953,12 +1147,41 @@ extern "C" int csc_kmeans_fused_run(const double *f, const double *fnorm, int64_
   a.pcnt = reinterpret_cast<int32_t *>(p);
   p += b_pcnt;
   int32_t *ints = reinterpret_cast<int32_t *>(p);
+  p += b_ints;
   a.done = ints;
   a.eflag = ints + R;
   a.nrep = ints + 2 * R;
   a.rep_idx = ints + 3 * R;
   a.rep_j = ints + 3 * R + R * k;
   a.bar = reinterpret_cast<unsigned *>(ints + 3 * R + 2 * R * k);
+  a.kpp_first = nullptr;
+  a.kpp_unif = nullptr;
+  a.kpp_part = nullptr;
+  a.kpp_pick = nullptr;
+  a.kpp_ready = nullptr;
+  a.kpp_flag = flags;
+  a.seeds_out = seeds_out;
+  if (kpp) {
+    int64_t *kf = reinterpret_cast<int64_t *>(p);
+    p += b_kfirst;
+    double *ku = reinterpret_cast<double *>(p);
+    p += b_kunif;
+    a.kpp_part = reinterpret_cast<double *>(p);
+    p += b_kpart;
+    a.kpp_pick = reinterpret_cast<int32_t *>(p);
+    a.kpp_ready = a.kpp_pick + R;
+    CSC_TRY_CUDA(cudaMemsetAsync(a.kpp_ready, 0, sizeof(int32_t) * R, st));
+    CSC_TRY_CUDA(cudaMemcpyAsync(kf, first_host, sizeof(int64_t) * R, cudaMemcpyHostToDevice, st));
+    if (k > 1)
+      CSC_TRY_CUDA(cudaMemcpyAsync(ku, unif_host, sizeof(double) * R * (k - 1),
+                                   cudaMemcpyHostToDevice, st));
+    CSC_TRY_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(int32_t) * R, st));
+    a.kpp_first = kf;
+    a.kpp_unif = ku;
+  } else {
+    CSC_TRY_CUDA(cudaMemcpyAsync(a.cent, seeds, sizeof(double) * R * k * ldc,
+                                 cudaMemcpyDeviceToDevice, st));
+  }
   a.trace = g_trace;
   a.trace_cap = g_trace_cap;
   a.G = (int)G;
@@ -966,8 +1189,6 @@ extern "C" int csc_kmeans_fused_run(const double *f, const double *fnorm, int64_
   a.ldf = g.ldf;
   a.lds = g.lds;
   a.ngmax = g.ngmax;
-  CSC_TRY_CUDA(cudaMemcpyAsync(a.cent, seeds, sizeof(double) * R * k * ldc,
-                               cudaMemcpyDeviceToDevice, st));
   CSC_TRY_CUDA(cudaMemsetAsync(ints, 0, b_ints, st));
   CSC_TRY_CUDA(cudaFuncSetAttribute(lloyd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)g.smem));
@@ -975,4 +1196,35 @@ extern "C" int csc_kmeans_fused_run(const double *f, const double *fnorm, int64_
   CSC_TRY_CUDA(cudaLaunchCooperativeKernel((const void *)lloyd_fused_kernel, dim3(g.G), dim3(kFT),
                                            args, g.smem, st));
   return CSC_OK;
+}
+
+}  // namespace
+
+extern "C" int csc_kmeans_fused_run(const double *f, const double *fnorm, int64_t n, int64_t d,
+                                    int64_t ld, int64_t k, int64_t R, const double *seeds,
+                                    int64_t ldc, int max_iters, double tol, int32_t *labels,
+                                    double *cost2, int32_t *iters, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(f && fnorm && seeds && labels && cost2 && iters, "csc_kmeans_fused_run: NULL pointer");
+  return fused_launch("csc_kmeans_fused_run", f, fnorm, n, d, ld, k, R, seeds, nullptr, nullptr,
+                      nullptr, nullptr, ldc, max_iters, tol, labels, cost2, iters,
+                      static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int csc_kmeans_fused_kpp_run(const double *f, int64_t n, int64_t d, int64_t ld,
+                                        int64_t k, int64_t R, const int64_t *first_idx_host,
+                                        const double *uniforms_host, int64_t ldc, int max_iters,
+                                        double tol, int32_t *labels, double *cost2,
+                                        int32_t *iters, double *seeds_out, int32_t *flags,
+                                        void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(f && first_idx_host && labels && cost2 && iters && flags &&
+                  (k < 2 || uniforms_host),
+              "csc_kmeans_fused_kpp_run: NULL pointer");
+  for (int64_t r = 0; r < R; ++r)
+    CSC_REQUIRE(first_idx_host[r] >= 0 && first_idx_host[r] < n,
+                "csc_kmeans_fused_kpp_run: first index out of range");
+  return fused_launch("csc_kmeans_fused_kpp_run", f, nullptr, n, d, ld, k, R, nullptr,
+                      first_idx_host, uniforms_host, seeds_out, flags, ldc, max_iters, tol, labels,
+                      cost2, iters, static_cast<cudaStream_t>(stream));
 }

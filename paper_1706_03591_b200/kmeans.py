@@ -268,19 +268,20 @@ def fused_supported(n: int, d: int, k: int, restarts: int, max_iters: int) -> bo
 
 
 class _FusedState:
-    """Persistent per-shape buffers of the fused Lloyd path."""
+    """Persistent per-shape output buffers of the fused Lloyd path."""
 
     def __init__(self, n, d, ld, k, dev):
         self.key = (dev.index, n, d, ld, k)
-        self.F = torch.zeros((n, ld), dtype=torch.float64, device=dev)
-        self.ws = _Workspace(self.F, d, k)
+        self.n, self.k, self.ldc, self.dev = n, k, row_stride(d), dev
         self.out = {}
 
     def outputs(self, R):
         if R not in self.out:
-            dev = self.F.device
-            self.out[R] = (torch.empty((R, self.ws.n), dtype=torch.int32, device=dev),
+            dev, n, k = self.dev, self.n, self.k
+            self.out[R] = (torch.empty((R, n), dtype=torch.int32, device=dev),
                            torch.empty(R, dtype=torch.float64, device=dev),
+                           torch.empty(R, dtype=torch.int32, device=dev),
+                           torch.zeros((R, k, self.ldc), dtype=torch.float64, device=dev),
                            torch.empty(R, dtype=torch.int32, device=dev))
         return self.out[R]
 
@@ -290,10 +291,13 @@ LAST_FUSED_ITERS: list[int] = []  # diagnostics: Lloyd iterations per restart of
 
 
 def _run_fused(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, draws=None):
-    """Every restart in one cooperative launch (csc_kmeans_fused_run): batched
-    k-means++ seeds, then all Lloyd runs in lock step with the features resident
-    in shared memory; best restart by the reference's rule (strictly smaller
-    cost2, earliest on ties). Returns (labels int64 numpy, cost2)."""
+    """Every restart in one cooperative launch (csc_kmeans_fused_kpp_run): the
+    k-means++ seeds from the restarts' host draws (integers(n), then k-1
+    random(); kmeans.py:67-74) and all Lloyd runs in lock step, with the
+    features resident in shared memory; best restart by the reference's rule
+    (strictly smaller cost2, earliest on ties). A restart whose D^2 mass hit 0
+    (the reference then draws integers(n)) is re-seeded on the sequential path
+    and the launch repeated with explicit seeds. Returns (labels int64 numpy, cost2)."""
     global _FUSED
     dev = blk.device
     n, ld = blk.shape
@@ -301,24 +305,25 @@ def _run_fused(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, d
     if _FUSED is None or _FUSED.key != key:
         _FUSED = None
         _FUSED = _FusedState(n, d, ld, k, dev)
-    st = _FUSED
-    ws = st.ws
-    st.F.copy_(blk)
-    _native.call("csc_kmeans_rownorms", ptr(st.F), n, d, ld, ptr(ws.fnorm), stream())
-    seeds, bad_restarts, replay = batched_kmeanspp(ws, children, defer_check=True, draws=draws)
     R = len(children)
-    labels, cost, iters = st.outputs(R)
-
-    def launch():
-        _native.call("csc_kmeans_fused_run", ptr(st.F), ptr(ws.fnorm), n, d, ld, k, R, ptr(seeds), ws.ldc,
+    labels, cost, iters, seeds, flags = _FUSED.outputs(R)
+    ldc = _FUSED.ldc
+    first, unif = draws if draws is not None else kmeanspp_draws(children, n, k)
+    first = np.ascontiguousarray(first, dtype=np.int64)
+    unif = np.ascontiguousarray(unif, dtype=np.float64)
+    _native.call("csc_kmeans_fused_kpp_run", ptr(blk), n, d, ld, k, R, first.ctypes.data, unif.ctypes.data, ldc,
+                 int(cfg.max_iters), float(cfg.tol), ptr(labels), ptr(cost), ptr(iters), ptr(seeds), ptr(flags),
+                 stream())
+    costs = cost.cpu().numpy()  # synchronises
+    fl = flags.cpu().numpy()
+    bad = [r for r in range(R) if fl[r] >= 0]
+    if bad:  # zero D^2 mass (kmeans.py:70-72): sequential seeding for those restarts, explicit seeds
+        ws = _Workspace(blk, d, k)
+        for r in bad:
+            ws.kmeanspp(np.random.default_rng(children[r]))
+            seeds[r].copy_(ws.cent)
+        _native.call("csc_kmeans_fused_run", ptr(blk), ptr(ws.fnorm), n, d, ld, k, R, ptr(seeds), ldc,
                      int(cfg.max_iters), float(cfg.tol), ptr(labels), ptr(cost), ptr(iters), stream())
-
-    launch()
-    costs = cost.cpu().numpy()  # synchronises: the seeding flags are final too
-    redo = bad_restarts()
-    if redo:  # zero D^2 mass in some restart's seeding (kmeans.py:70-72): corrected seeds, run again
-        replay(redo)
-        launch()
         costs = cost.cpu().numpy()
     LAST_FUSED_ITERS[:] = [int(v) for v in iters.cpu().numpy()]
     best = 0

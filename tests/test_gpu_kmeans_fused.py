@@ -153,3 +153,40 @@ def test_fused_shape_gate(P):
     assert not fused_supported(20000, 129, 20, 10, 100)  # d > 128
     assert not fused_supported(2_000_000, 96, 20, 10, 100)  # rows exceed shared memory
     assert not fused_supported(20000, 80, 20, 10, 0)
+
+
+def test_fused_kpp_seeds_match_reference_picks(P):
+    """In-kernel k-means++ (csc_kmeans_fused_kpp_run): the seeds are the
+    reference's picks for the same streams (kmeans.py:64-77), and every
+    restart's Lloyd run then matches the oracle from those seeds."""
+    import torch
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import ptr, row_stride, stream, upload_block
+    from paper_1706_03591_b200.kmeans import kmeanspp_draws
+    for n, d, k, R, seed in [(1000, 40, 10, 1, 0), (20000, 80, 20, 10, 5), (997, 7, 5, 16, 2)]:
+        f = blobs(n, d, k, 0.9, seed=seed)
+        blk = upload_block(f)
+        ld = blk.shape[1]
+        ldc = row_stride(d)
+        kids = np.random.SeedSequence(seed).spawn(R)
+        first, unif = kmeanspp_draws(kids, n, k)
+        dev = blk.device
+        labels = torch.empty((R, n), dtype=torch.int32, device=dev)
+        cost = torch.empty(R, dtype=torch.float64, device=dev)
+        iters = torch.empty(R, dtype=torch.int32, device=dev)
+        seeds = torch.zeros((R, k, ldc), dtype=torch.float64, device=dev)
+        flags = torch.empty(R, dtype=torch.int32, device=dev)
+        first = np.ascontiguousarray(first)
+        unif = np.ascontiguousarray(unif)
+        _native.call("csc_kmeans_fused_kpp_run", ptr(blk), n, d, ld, k, R, first.ctypes.data, unif.ctypes.data,
+                     ldc, 100, 1e-6, ptr(labels), ptr(cost), ptr(iters), ptr(seeds), ptr(flags), stream())
+        assert (flags.cpu().numpy() < 0).all()
+        S = seeds[:, :, :d].cpu().numpy()
+        lab, cst, its = labels.cpu().numpy(), cost.cpu().numpy(), iters.cpu().numpy()
+        for r, child in enumerate(kids):
+            ref_cent, ref_picks = O.kmeanspp(f, k, np.random.default_rng(child))
+            assert np.array_equal(S[r], ref_cent), (n, r)
+            ref_labels, ref_cost2, _, ref_it = O.lloyd(f, k, ref_cent, 100, 1e-6)
+            assert its[r] == ref_it
+            assert abs(cst[r] - ref_cost2) <= COST_TOL * ref_cost2
+            assert O.adjusted_rand(lab[r], ref_labels) >= 0.999

@@ -65,3 +65,10 @@ for which in range(len(captured)):
         print(f"  g={g:3d} active={act:2d} " + " ".join(f"{n}={v:7.1f}" for n, v in zip(names, row))
               + "  [first restart: load %.1f cost %.1f bounds %.1f assign %.1f (%d rows) sums %.1f]"
               % (sub[0], sub[1], sub[2], sub[3], int(t[g, 11]), sub[4]))
+    kp = t_all = trace.cpu().numpy().reshape(cap, 16).astype(np.float64)[96:96 + 32]
+    for j in range(32):
+        if kp[j, 0] == 0:
+            break
+        print("  kpp draw %2d: dist+prefix %.1f  bar1 %.1f  draw %.1f  bar2 %.1f  stage %.1f" % (
+            j, (kp[j, 1] - kp[j, 0]) / 1e3, 0.0, (kp[j, 2] - kp[j, 1]) / 1e3, (kp[j, 3] - kp[j, 2]) / 1e3,
+            (kp[j, 4] - kp[j, 3]) / 1e3))
