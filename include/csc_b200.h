@@ -301,6 +301,11 @@ int csc_seed_states(const uint32_t *run_entropy, int64_t n_run, const uint32_t *
                     uint64_t *states_out);
 int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
                        double *out_dev, int64_t ld, int64_t col0, int32_t *bad_host, void *stream);
+/* The same without synchronising: the flags go to bad_dev (ncols int32,
+ * device) for the caller to read at its next synchronisation. */
+int csc_normal_columns_async(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
+                             double *out_dev, int64_t ld, int64_t col0, int32_t *bad_dev,
+                             void *stream);
 
 /* ---- dense helpers ------------------------------------------------------ */
 /* dst[:, j] = src[:, cols[j]] for j < ncols (row-major, f64), the Theta

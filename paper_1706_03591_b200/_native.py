@@ -66,6 +66,7 @@ SIGNATURES = {
     "csc_kmeanspp_batch": ([_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _P, _P], _INT),
     "csc_seed_states": ([_P, _I64, _P, _I64, _I64, _I64, _I32, _P], _INT),
     "csc_normal_columns": ([_P, _I64, _I64, _D, _P, _I64, _I64, _P, _P], _INT),
+    "csc_normal_columns_async": ([_P, _I64, _I64, _D, _P, _I64, _I64, _P, _P], _INT),
     "csc_gather_columns": ([_P, _I64, _I64, _P, _I64, _P, _I64, _I64, _P], _INT),
 }
 

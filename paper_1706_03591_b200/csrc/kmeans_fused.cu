@@ -77,6 +77,8 @@ struct FusedArgs {
   int32_t *rep_idx;     // [R][k]
   int32_t *rep_j;       // [R][k]
   unsigned *bar;        // [2] arrival count, generation
+  unsigned *arrive;     // [R] blocks' phase-1 arrivals per restart (monotonic: G per iteration)
+  unsigned *readycnt;   // [R] finished phase-2 items per restart (monotonic: k per iteration)
   // in-kernel k-means++ (kmeans.py:64-77), when kpp_first != nullptr
   const int64_t *kpp_first;  // [R] the restart's integers(n) draw
   const double *kpp_unif;    // [R][k-1] its random() draws
@@ -894,15 +896,25 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
       const GShared gs = gcarve(smem_raw, a, G_.id);
       for (int ai = G_.id; ai < A; ai += ng) {
         phase1(a, s, gs, G_, s.act[ai], g, nr, rb, ai == 0);
+        // this block's partials of the restart are written (phase1 ends on a
+        // group barrier): release them with one arrival on the restart's count
+        if (G_.gt == 0) {
+          __threadfence();
+          atomicAdd(a.arrive + s.act[ai], 1u);
+        }
       }
     }
     __syncthreads();
     mark(g, 1);
-    grid_sync(a.bar, G);
-    mark(g, 2);
-    // ---- phase 2: stop rule, means (one CTA per (restart, cluster)) --------
+    // ---- phase 2: stop rule, means; (restart, cluster) items spread over the
+    // blocks, each waiting only for the arrivals of its restart; no grid barrier
     for (int q = cta; q < A * (int)k; q += G) {
       const int r = s.act[q / (int)k], j = q % (int)k;
+      if (tid == 0) {
+        const unsigned want = (unsigned)G * (unsigned)(g + 1);
+        while (ld_acquire(a.arrive + r) < want) __nanosleep(20);
+      }
+      __syncthreads();
       bool stop = false;
       if (g > 0) {
         const double c = cost_sum(a, r);  // identical in every warp
@@ -919,10 +931,21 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
         }
       }
       if (!stop) means_item(a, s, r, j, g, true);
+      __syncthreads();
+      if (tid == 0) {  // the mean (or the stop decision) of (r, j) is published
+        __threadfence();
+        atomicAdd(a.readycnt + r, 1u);
+      }
     }
     __syncthreads();
+    mark(g, 2);
     mark(g, 3);
-    grid_sync(a.bar, G);
+    // every active restart's k items of this iteration are done
+    if (tid < A) {
+      const unsigned want = (unsigned)k * (unsigned)(g + 1);
+      while (ld_acquire(a.readycnt + s.act[tid]) < want) __nanosleep(20);
+    }
+    __syncthreads();
     mark(g, 4);
     // ---- rare path: empty cluster -> exact reassignment + reseeding --------
     const bool flagged = __syncthreads_or(tid < R && __ldcg(a.eflag + tid) == g + 1);
@@ -1108,7 +1131,7 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   const size_t b_hist = al(sizeof(double) * R * (max_iters + 1));
   const size_t b_own = al(sizeof(double) * R * n);
   const size_t b_pcnt = al(sizeof(int32_t) * R * G * k);
-  const size_t b_ints = al(sizeof(int32_t) * (3 * R + 2 * R * k) + 2 * sizeof(unsigned));
+  const size_t b_ints = al(sizeof(int32_t) * (3 * R + 2 * R * k) + (2 + 2 * R) * sizeof(unsigned));
   const size_t b_kfirst = kpp ? al(sizeof(int64_t) * R) : 0;
   const size_t b_kunif = kpp ? al(sizeof(double) * R * std::max<int64_t>(1, k - 1)) : 0;
   const size_t b_kpart = kpp ? al(sizeof(double) * R * G) : 0;
@@ -1154,6 +1177,8 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   a.rep_idx = ints + 3 * R;
   a.rep_j = ints + 3 * R + R * k;
   a.bar = reinterpret_cast<unsigned *>(ints + 3 * R + 2 * R * k);
+  a.arrive = a.bar + 2;
+  a.readycnt = a.arrive + R;
   a.kpp_first = nullptr;
   a.kpp_unif = nullptr;
   a.kpp_part = nullptr;

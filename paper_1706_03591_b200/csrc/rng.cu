@@ -283,13 +283,17 @@ int csc_seed_states(const uint32_t *run_entropy, int64_t n_run, const uint32_t *
   return CSC_OK;
 }
 
-int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
-                       double *out, int64_t ld, int64_t col0, int32_t *bad_host, void *stream) {
-  csc::clear_error();
+}  // extern "C"
+
+namespace {
+
+// bad_host != nullptr: flags copied back and the stream synchronised;
+// otherwise they stay in bad_dev (ncols int32) and nothing synchronises.
+int normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
+                   double *out, int64_t ld, int64_t col0, int32_t *bad_host, int32_t *bad_dev,
+                   cudaStream_t st) {
   CSC_REQUIRE(ncols >= 1 && n >= 1 && col0 >= 0 && col0 + ncols <= ld,
               "csc_normal_columns: bad shape");
-  CSC_REQUIRE(bad_host != nullptr, "csc_normal_columns: NULL bad_host");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   csc::device_info();
   ChunkPlan P;
   P.n = n;
@@ -313,8 +317,14 @@ int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, do
   CSC_TRY_CUDA(offs.alloc(sizeof(int32_t) * T, st));
   CSC_TRY_CUDA(fgs.alloc(sizeof(int64_t) * T, st));
   CSC_TRY_CUDA(fge.alloc(sizeof(int64_t) * T, st));
-  CSC_TRY_CUDA(bad.alloc(sizeof(int32_t) * ncols, st));
-  CSC_TRY_CUDA(cudaMemsetAsync(bad.ptr, 0, sizeof(int32_t) * ncols, st));
+  int32_t *badp = nullptr;
+  if (bad_dev) {
+    badp = bad_dev;  // caller-owned
+  } else {
+    CSC_TRY_CUDA(bad.alloc(sizeof(int32_t) * ncols, st));
+    badp = bad.as<int32_t>();
+  }
+  CSC_TRY_CUDA(cudaMemsetAsync(badp, 0, sizeof(int32_t) * ncols, st));
   CSC_TRY_CUDA(cudaMemcpyAsync(st_dev.ptr, states_host, sizeof(uint64_t) * 4 * ncols,
                                cudaMemcpyHostToDevice, st));
   const int threads = 128;
@@ -333,16 +343,37 @@ int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, do
                                              T, st));
   // offsets in [col][ch] order; the kernels index them as col * nch + ch
   zig_check_kernel<<<blocks, threads, 0, st>>>(P, counts.as<int32_t>(), fgs.as<int64_t>(),
-                                              fge.as<int64_t>(), offs.as<int32_t>(),
-                                              bad.as<int32_t>());
+                                              fge.as<int64_t>(), offs.as<int32_t>(), badp);
   CSC_CHECK_LAUNCH();
   zig_chunk_kernel<<<blocks, threads, 0, st>>>(P, st_dev.as<uint64_t>(), 1, nullptr, nullptr,
                                               nullptr, offs.as<int32_t>(), sigma, out, ld, col0);
   CSC_CHECK_LAUNCH();
-  CSC_TRY_CUDA(cudaMemcpyAsync(bad_host, bad.ptr, sizeof(int32_t) * ncols, cudaMemcpyDeviceToHost,
+  if (bad_dev) return CSC_OK;
+  CSC_TRY_CUDA(cudaMemcpyAsync(bad_host, badp, sizeof(int32_t) * ncols, cudaMemcpyDeviceToHost,
                                st));
   CSC_TRY_CUDA(cudaStreamSynchronize(st));
   return CSC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int csc_normal_columns(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
+                       double *out, int64_t ld, int64_t col0, int32_t *bad_host, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(bad_host != nullptr, "csc_normal_columns: NULL bad_host");
+  return normal_columns(states_host, ncols, n, sigma, out, ld, col0, bad_host, nullptr,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int csc_normal_columns_async(const uint64_t *states_host, int64_t ncols, int64_t n, double sigma,
+                             double *out, int64_t ld, int64_t col0, int32_t *bad_dev,
+                             void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(bad_dev != nullptr, "csc_normal_columns_async: NULL bad_dev");
+  return normal_columns(states_host, ncols, n, sigma, out, ld, col0, nullptr, bad_dev,
+                        static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -128,7 +128,7 @@ def column_states(children) -> np.ndarray:
 
 
 def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None, mode: str | None = None,
-                   advance: bool = True) -> torch.Tensor:
+                   advance: bool = True, defer: bool = False):
     """random_signals as a padded (n, ld) float64 device block.
 
     Device mode draws numpy's exact PCG64 streams and ziggurat on the GPU;
@@ -136,6 +136,10 @@ def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None, mode: s
     per-column PCG64 states come from the library's SeedSequence restatement;
     a caller's SeedSequence is advanced by d children as ss.spawn(d) would
     (advance=False skips that for internal, never-reused children).
+    defer=True (device mode): returns (block, fix) without synchronising;
+    fix() reads the device flags, redraws flagged columns on the host and
+    returns whether it changed any (the caller then recomputes what it built
+    from the block).
     """
     if d < 1:
         raise ValueError("need at least one signal column")
@@ -152,19 +156,29 @@ def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None, mode: s
         states = child_states(ss, d)
         if advance and ss is seed:  # the caller's SeedSequence moves on exactly as in signal_columns
             ss.spawn(d)
-        bad = np.zeros(d, dtype=np.int32)
         sigma = 1.0 / np.sqrt(dim)
+
+        def redraw(bad):  # flagged columns: the exact host generator
+            for c in np.flatnonzero(bad):
+                child = np.random.SeedSequence(ss.entropy, spawn_key=tuple(ss.spawn_key) + (base + int(c),),
+                                               pool_size=ss.pool_size)
+                z = np.random.default_rng(child).standard_normal(n) * sigma + 0.0
+                blk[:, c].copy_(torch.from_numpy(z))
+            return bool(np.any(bad))
+
+        if defer:  # no synchronisation here: the caller runs fix() at its next one
+            bad_dev = torch.empty(d, dtype=torch.int32, device=dev)
+            _native.call("csc_normal_columns_async", states.ctypes.data, d, n, float(sigma), ptr(blk),
+                         blk.shape[1], 0, ptr(bad_dev), stream())
+            return blk, lambda: redraw(bad_dev.cpu().numpy())
+        bad = np.zeros(d, dtype=np.int32)
         _native.call("csc_normal_columns", states.ctypes.data, d, n, float(sigma), ptr(blk), blk.shape[1], 0,
                      bad.ctypes.data, stream())
-        for c in np.flatnonzero(bad):
-            child = np.random.SeedSequence(ss.entropy, spawn_key=tuple(ss.spawn_key) + (base + int(c),),
-                                           pool_size=ss.pool_size)
-            z = np.random.default_rng(child).standard_normal(n) * sigma + 0.0
-            blk[:, c].copy_(torch.from_numpy(z))
+        redraw(bad)
         return blk
     cols = torch.from_numpy(signal_columns(n, d, seed, scale_dim))
     blk[:, :d].copy_(cols.to(dev).t())
-    return blk
+    return (blk, lambda: False) if defer else blk
 
 
 def block_nonfinite(blk: torch.Tensor) -> int:

@@ -36,3 +36,10 @@ for e in evs:
 print(f"GPU span {busy_end - t0:.1f} us, idle gaps {gaps:.1f} us")
 for name, (c, us) in sorted(tot.items(), key=lambda x: -x[1][1])[:25]:
     print(f"{us:9.1f} us  x{c:4d}  {name}")
+print("gaps > 15 us (after kernel -> before kernel):")
+prev = None
+for e in evs:
+    if prev is not None and e.time_range.start - prev.time_range.end > 15:
+        print(f"  {e.time_range.start - prev.time_range.end:7.1f} us  after {prev.name[:50]}  before {e.name[:50]}")
+    if prev is None or e.time_range.end > prev.time_range.end:
+        prev = e
