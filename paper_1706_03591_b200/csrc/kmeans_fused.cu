@@ -209,25 +209,30 @@ __device__ __forceinline__ GShared gcarve(unsigned char *raw, const FusedArgs &a
 __device__ void group_load(const FusedArgs &a, const GShared &gs, const Grp &G_, int r, int g) {
   const int64_t k = a.k, d = a.d, R = a.R, kd = k * d;
   const double *Cc = a.cent + ((int64_t)(g & 1) * R + r) * k * a.ldc;
+  // element e = gt + u GT of the k x d tile as (row, column), stepped without
+  // divisions in the loop (integer division is a long instruction sequence)
   constexpr int U = 8;
-  for (int64_t e0 = G_.gt; e0 < kd; e0 += (int64_t)U * G_.GT) {
+  const int di = (int)d, GT = G_.GT;
+  const int dj = GT / di, dt = GT - dj * di;
+  int j0 = G_.gt / di, t0 = G_.gt - j0 * di;
+  for (int64_t e0 = G_.gt; e0 < kd; e0 += (int64_t)U * GT) {
     double v[U];
+    int jj[U], tt[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t e = e0 + (int64_t)u * G_.GT;
-      if (e < kd) {
-        const int j = (int)e / (int)d, t = (int)e - j * (int)d;
-        v[u] = __ldcg(Cc + j * a.ldc + t);
+      jj[u] = j0;
+      tt[u] = t0;
+      if (e0 + (int64_t)u * GT < kd) v[u] = __ldcg(Cc + j0 * a.ldc + t0);
+      t0 += dt;
+      j0 += dj;
+      if (t0 >= di) {
+        t0 -= di;
+        ++j0;
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = e0 + (int64_t)u * G_.GT;
-      if (e < kd) {
-        const int j = (int)e / (int)d, t = (int)e - j * (int)d;
-        gs.Cs[j * a.lds + t] = v[u];
-      }
-    }
+    for (int u = 0; u < U; ++u)
+      if (e0 + (int64_t)u * GT < kd) gs.Cs[jj[u] * a.lds + tt[u]] = v[u];
   }
   if (g > 0) {
     const double *kv = a.kvec + ((int64_t)(g & 1) * R + r) * 2 * k;
@@ -443,14 +448,24 @@ __device__ void group_partials(const FusedArgs &a, const Shared &s, const GShare
   }
   G_.sync();
   double *ps = a.psum + ((int64_t)r * a.G + cta) * k * d;
-  for (int64_t e = G_.gt; e < k * d; e += G_.GT) {  // thread per (cluster, column)
-    const int j = (int)e / (int)d, t = (int)e - j * (int)d;
-    const int c = gs.cnt[j];
-    if (c == 0 || !((dirty >> j) & 1u)) continue;
-    const int end = gs.runp[j], beg = end - c;
-    double v = 0.0;
-    for (int p = beg; p < end; ++p) v += s.Fs[(int64_t)gs.perm[p] * ldf + t];
-    ps[e] = v;
+  {
+    const int di = (int)d, GT = G_.GT, dj = GT / di, dt = GT - dj * di;
+    int j = G_.gt / di, t = G_.gt - j * di;
+    for (int64_t e = G_.gt; e < k * d; e += GT) {  // thread per (cluster, column)
+      const int c = gs.cnt[j];
+      if (c > 0 && ((dirty >> j) & 1u)) {
+        const int end = gs.runp[j], beg = end - c;
+        double v = 0.0;
+        for (int p = beg; p < end; ++p) v += s.Fs[(int64_t)gs.perm[p] * ldf + t];
+        ps[e] = v;
+      }
+      t += dt;
+      j += dj;
+      if (t >= di) {
+        t -= di;
+        ++j;
+      }
+    }
   }
   G_.sync();
 }
