@@ -234,6 +234,21 @@ int csc_kmeans_fused_kpp_run(const double *f_dev, int64_t n, int64_t d, int64_t 
  * end, barrier, iteration end; 6..10: sub-steps of the first restart's
  * phase 1; 11: its candidate row count), g < iters_cap. */
 int csc_kmeans_fused_trace(unsigned long long *trace_dev, int64_t iters_cap);
+/* FP32 screen of the Lloyd assignment (csrc/kmeans_screen.cu): the plan's
+ * assignments first compute the GEMM-form distances in FP32; a row whose FP32
+ * best/second gap exceeds 2 (d+5) 2^-24 (|f| + max|c|)^2 provably has the same
+ * FP64 first-argmin and is decided there (Hamerly bounds widened by that
+ * error), every other row is recomputed by the FP64 kernels — labels, means
+ * and costs are identical to the FP64-only plan. supported(): 1 if (d, k)
+ * fit the screen tile. prepare(): f32 = (float)f with row stride ld32
+ * (multiple of 4, 16-byte aligned), fn32 = |f32 row|^2 (n floats); call it
+ * whenever f changes. set_screen(): the plan uses these buffers from now on
+ * (NULL f32 disables); they must stay valid while the plan runs. */
+int csc_kmeans_screen_supported(int64_t d, int64_t k);
+int csc_kmeans_screen_prepare(const double *f_dev, int64_t n, int64_t d, int64_t ld,
+                              float *f32_dev, int64_t ld32, float *fn32_dev, void *stream);
+int csc_kmeans_plan_set_screen(csc_kmeans_plan *plan, const float *f32_dev, int64_t ld32,
+                               const float *fn32_dev);
 /* k-means tuning knobs (performance only; results do not change):
  * "assign_ver" 2|3, "assign_tn" 4|8 (v2 kernel), "assign_tile" 0 (auto) |
  * 1 (small-k kernel) | 88 | 84 | 87 | 48 | 44 | 42 (v3 register tile),

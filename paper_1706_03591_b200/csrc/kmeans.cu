@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "kmeans_screen.cuh"
 
 namespace {
 
@@ -1893,6 +1894,13 @@ struct csc_kmeans_plan {
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   const void *key[12] = {};
+  // FP32 screen (kmeans_screen.cu): caller's fp32 features, plan-owned scratch
+  const float *f32 = nullptr, *fn32 = nullptr;
+  int64_t ld32 = 0;
+  float *c32t = nullptr, *cn32 = nullptr;
+  double *cmax = nullptr;
+  int32_t *amb = nullptr, *namb = nullptr;
+  void *screen_base = nullptr;
 };
 
 extern "C" {
@@ -2074,6 +2082,55 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   return CSC_OK;
 }
 
+int csc_kmeans_screen_supported(int64_t d, int64_t k) {
+  return csc::screen_supported(d, k) ? 1 : 0;
+}
+
+int csc_kmeans_screen_prepare(const double *f, int64_t n, int64_t d, int64_t ld, float *f32,
+                              int64_t ld32, float *fn32, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(f && f32 && fn32 && n >= 1 && d >= 1 && ld >= d && ld32 >= d && ld32 % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(f32) & 15u) == 0,
+              "csc_kmeans_screen_prepare: bad arguments (ld32 must be a multiple of 4, f32 16-byte aligned)");
+  return csc::screen_convert_features(f, n, d, ld, f32, ld32, fn32,
+                                      static_cast<cudaStream_t>(stream));
+}
+
+int csc_kmeans_plan_set_screen(csc_kmeans_plan *p, const float *f32, int64_t ld32,
+                               const float *fn32) {
+  csc::clear_error();
+  CSC_REQUIRE(p != nullptr, "csc_kmeans_plan_set_screen: NULL plan");
+  if (f32 == nullptr) {
+    p->f32 = nullptr;
+    return CSC_OK;
+  }
+  CSC_REQUIRE(fn32 != nullptr && ld32 >= p->d && ld32 % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(f32) & 15u) == 0,
+              "csc_kmeans_plan_set_screen: bad arguments");
+  CSC_REQUIRE(csc::screen_supported(p->d, p->k),
+              "csc_kmeans_plan_set_screen: (d=%lld, k=%lld) outside the screen kernel",
+              (long long)p->d, (long long)p->k);
+  if (!p->screen_base) {
+    const int64_t kpad = csc::screen_kpad(p->k);
+    const size_t bytes = sizeof(float) * (p->d * kpad + kpad) + 16 + sizeof(double) +
+                         sizeof(int32_t) * (p->n + 4) + 64;
+    CSC_TRY_CUDA(cudaMallocAsync(&p->screen_base, bytes, p->stream));
+    char *b = static_cast<char *>(p->screen_base);
+    p->cmax = reinterpret_cast<double *>(b);
+    b += 16;
+    p->c32t = reinterpret_cast<float *>(b);
+    b += sizeof(float) * p->d * kpad;
+    p->cn32 = reinterpret_cast<float *>(b);
+    b += sizeof(float) * kpad;
+    p->namb = reinterpret_cast<int32_t *>(b);
+    p->amb = p->namb + 4;
+  }
+  p->f32 = f32;
+  p->fn32 = fn32;
+  p->ld32 = ld32;
+  return CSC_OK;
+}
+
 int csc_kmeans_plan_stats(const csc_kmeans_plan *p, int64_t *candidates, int32_t *gated) {
   CSC_REQUIRE(p != nullptr, "csc_kmeans_plan_stats: NULL plan");
   int32_t h[4] = {0, 0, 0, 0};
@@ -2092,6 +2149,7 @@ int csc_kmeans_plan_destroy(csc_kmeans_plan *p) {
   if (p->cost_parts) cudaFreeAsync(p->cost_parts, p->stream);
   if (p->history) cudaFreeAsync(p->history, p->stream);
   if (p->base) cudaFreeAsync(p->base, p->stream);
+  if (p->screen_base) cudaFreeAsync(p->screen_base, p->stream);
   delete p;
   return CSC_OK;
 }
@@ -2119,18 +2177,30 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
                : launch_assign2<4>(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own, cnts,
                                    asmem, st, rows, nrows, p->ub, p->lb, gate);
   };
+  // FP32 screen first when enabled: provably decided rows there, the rest
+  // (listed in p->amb) by the FP64 assignment — the same labels either way
+  auto screened = [&](const int32_t *rows, const int32_t *nrows, int32_t *cnts) -> int {
+    if (!p->f32) return assign(rows, nrows, cnts, nullptr);
+    CSC_TRY_CUDA(cudaMemsetAsync(p->namb, 0, sizeof(int32_t), st));
+    int r2 = csc::screen_convert_centroids(cent, k, d, ldc, cnorm, p->c32t, p->cn32, p->cmax, st);
+    if (r2 != CSC_OK) return r2;
+    r2 = csc::screen_assign(p->f32, p->ld32, p->fn32, fnorm, n, d, p->c32t, p->cn32, k, p->cmax,
+                            rows, nrows, labels, p->ub, p->lb, cnts, p->amb, p->namb, st);
+    if (r2 != CSC_OK) return r2;
+    return assign(p->amb, p->namb, cnts, nullptr);
+  };
   int rc;
   if (full) {
     CSC_TRY_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * k, st));
     CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t) * 4, st));
-    if ((rc = assign(nullptr, nullptr, counts, nullptr)) != CSC_OK) return rc;
+    if ((rc = screened(nullptr, nullptr, counts)) != CSC_OK) return rc;
   } else {
     // flags[0] (candidate count) was cleared by the previous iteration's finish
     bound_kernel<<<grid_cap(csc::ceil_div(n, (int64_t)kBoundThreads * kBoundRows)), kBoundThreads, 0,
                    st>>>(
         n, labels, p->ub, p->lb, p->delta, p->scal, p->shalf, fnorm, p->cand, p->flags, counts, k);
     CSC_CHECK_LAUNCH();
-    if ((rc = assign(p->cand, p->flags, nullptr, nullptr)) != CSC_OK) return rc;
+    if ((rc = screened(p->cand, p->flags, nullptr)) != CSC_OK) return rc;
     label_hist_kernel<<<grid_cap(csc::ceil_div(n, 256), 4), 256, sizeof(int32_t) * k, st>>>(
         n, k, labels, counts);
     CSC_CHECK_LAUNCH();
@@ -2210,7 +2280,7 @@ int csc_kmeans_run(csc_kmeans_plan *p, const double *f, const double *fnorm, dou
   memcpy(&tol_bits, &tol_key, sizeof(tol_bits));
   const void *key[12] = {f, fnorm, cent, cnorm, labels, counts, (const void *)(intptr_t)ldc,
                          out_dev, history_dev, (const void *)(intptr_t)max_iters,
-                         (const void *)(intptr_t)tol_bits, nullptr};
+                         (const void *)(intptr_t)tol_bits, p->f32};
   bool same = p->exec != nullptr;
   for (int i = 0; i < 12 && same; ++i) same = key[i] == p->key[i];
   if (!same) {

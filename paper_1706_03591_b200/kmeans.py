@@ -229,6 +229,21 @@ class _LloydPool:
         self.F = torch.zeros((n, ld), dtype=torch.float64, device=dev)
         self.ws = _Workspace(self.F, d, k)  # persistent row norms etc.: stable graph keys
         self.lanes = [_Lane(self, dev) for _ in range(self.MAX_LANES)]
+        # FP32 screen of the assignment (same labels; csc_kmeans_plan_set_screen)
+        self.screen = (os.environ.get("CSC_KMEANS_SCREEN", "1") != "0"
+                       and bool(_native.lib().csc_kmeans_screen_supported(d, k)))
+        if self.screen:
+            self.ld32 = (d + 3) // 4 * 4
+            self.F32 = torch.zeros((n, self.ld32), dtype=torch.float32, device=dev)
+            self.fn32 = torch.empty(n, dtype=torch.float32, device=dev)
+            for lane in self.lanes:
+                _native.call("csc_kmeans_plan_set_screen", lane.plan, ptr(self.F32), self.ld32, ptr(self.fn32))
+
+    def prepare(self, stream_handle):
+        """Refresh the FP32 copy of F (after F changed)."""
+        if self.screen:
+            _native.call("csc_kmeans_screen_prepare", ptr(self.F), self.n, self.d, self.ld, ptr(self.F32),
+                         self.ld32, ptr(self.fn32), stream_handle)
 
 
 _LLOYD_POOL: _LloydPool | None = None
@@ -348,6 +363,7 @@ def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children
     pool.F.copy_(blk)
     ws = pool.ws
     _native.call("csc_kmeans_rownorms", ptr(pool.F), n, d, ld, ptr(ws.fnorm), stream())
+    pool.prepare(stream())
     # seeds are used right away; the rare zero-mass replay is checked at the
     # first host synchronisation and its restarts re-run (kmeans.py:70-72)
     seeds, bad_restarts, replay = batched_kmeanspp(ws, children, defer_check=True, draws=draws)

@@ -190,3 +190,33 @@ def test_fused_kpp_seeds_match_reference_picks(P):
             assert its[r] == ref_it
             assert abs(cst[r] - ref_cost2) <= COST_TOL * ref_cost2
             assert O.adjusted_rand(lab[r], ref_labels) >= 0.999
+
+
+@pytest.mark.parametrize("n,d,k", [(60000, 64, 48), (30000, 128, 100), (20000, 24, 40)])
+def test_fp32_screen_same_labels_as_fp64(P, n, d, k):
+    """The FP32 screen of the lane path (csc_kmeans_plan_set_screen) decides
+    only rows whose FP64 argmin it provably knows: labels and cost equal the
+    FP64-only plan bit for bit, and match the oracle."""
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import upload_block
+    import importlib
+    KM = importlib.import_module("paper_1706_03591_b200.kmeans")
+    f = blobs(n, d, k, 1.2, seed=k)
+    blk = upload_block(f)
+    kids = np.random.SeedSequence(k).spawn(3)
+    cfg = P.KmeansConfig(restarts=3, max_iters=40)
+    la, ca = KM.run_restarts(blk, d, k, cfg, kids, fused=False)
+    pool = KM._LLOYD_POOL
+    assert pool.screen
+    for lane in pool.lanes:
+        _native.call("csc_kmeans_plan_set_screen", lane.plan, None, 0, None)
+    try:
+        lb, cb = KM.run_restarts(blk, d, k, cfg, kids, fused=False)
+    finally:
+        for lane in pool.lanes:
+            _native.call("csc_kmeans_plan_set_screen", lane.plan, KM.ptr(pool.F32), pool.ld32, KM.ptr(pool.fn32))
+    assert np.array_equal(la, lb)
+    assert ca == cb
+    ref_labels, _, ref_cost = O.kmeans(f, k, restarts=3, max_iters=40, tol=1e-6, seed=k)
+    assert O.adjusted_rand(la, ref_labels) >= 0.999
+    assert abs(np.sqrt(ca) - ref_cost) <= COST_TOL * ref_cost

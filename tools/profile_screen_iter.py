@@ -1,0 +1,51 @@
+"""Per-kernel times of host-driven pruned Lloyd iterations with and without the FP32 screen (torch.profiler)."""
+import collections
+import importlib
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+import paper_1706_03591_b200 as P  # noqa: E402
+from paper_1706_03591_b200 import _native  # noqa: E402
+from paper_1706_03591_b200 import generators as G  # noqa: E402
+from paper_1706_03591_b200._device import ptr, stream  # noqa: E402
+from paper_1706_03591_b200.filters import FilteredBlock, _search_cutoff  # noqa: E402
+from paper_1706_03591_b200.signals import device_signals  # noqa: E402
+
+KM = importlib.import_module("paper_1706_03591_b200.kmeans")
+n, k, d, m = 2_000_000, 64, 96, 80
+q1, q2 = G.sbm_probabilities(n, k, 20.0, 0.05)
+g = G.graph_from_codes(n, G.planted_partition_codes(n, k, q1, q2, 5))
+lap = P.laplacian(g)
+blk = device_signals(n, d, 0)
+cut, filt, poly, iters, est = _search_cutoff(lap, k, FilteredBlock(blk, d), (0.0, 2.0),
+                                             P.FilterConfig(order=m), None, 1.0)
+F = filt.blk
+ws = KM._Workspace(F, d, k)
+seeds = KM.batched_kmeanspp(ws, np.random.SeedSequence(1).spawn(1))
+plan = ws._plan()
+ld32 = (d + 3) // 4 * 4
+F32 = torch.zeros((n, ld32), dtype=torch.float32, device=F.device)
+fn32 = torch.empty(n, dtype=torch.float32, device=F.device)
+_native.call("csc_kmeans_screen_prepare", ptr(F), n, d, F.shape[1], ptr(F32), ld32, ptr(fn32), stream())
+for on in (False, True):
+    if on:
+        _native.call("csc_kmeans_plan_set_screen", plan, ptr(F32), ld32, ptr(fn32))
+    ws.cent.copy_(seeds[0])
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        c2 = ws.lloyd(12, 1e-6)
+        torch.cuda.synchronize()
+    tot = collections.defaultdict(lambda: [0, 0.0])
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA:
+            tot[e.name[:60]][0] += 1
+            tot[e.name[:60]][1] += e.time_range.elapsed_us()
+    print(f"screen={on}: cost2 {c2!r}")
+    for name, (c, us) in sorted(tot.items(), key=lambda x: -x[1][1])[:12]:
+        print(f"   {us:9.1f} us x{c:4d}  {name}")
+    cand = ctypes_c = None
