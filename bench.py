@@ -144,6 +144,12 @@ def cpu_filter_sample(indptr, indices, data, r, coeffs, orders=2, threads=0):
     return time.perf_counter() - t0, (threads or ON.num_threads())
 
 
+def workload_desc(name, w, n, d, order):
+    """config.workload of both arms (the same string)."""
+    return (f"{name}: planted partition n={n} k={w['k']} mean degree {w['deg']} p_out/p_in={w['ratio']:.4g}; "
+            f"d={d}; Chebyshev order {order}; one step = one apply_filter of a device-resident block")
+
+
 def run_reference(args, w, rank):
     """--impl reference: the CPU path on the host cores, rank 0 only."""
     if rank != 0:
@@ -171,8 +177,8 @@ def run_reference(args, w, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "n": n, "nnz_L": int(nnz), "d": w["d"], "order": w["order"],
-                   "sample": sample},
+        "config": {"workload": workload_desc(args.workload, w, n, w["d"], w["order"]), "n": n,
+                   "nnz_L": int(nnz), "d": w["d"], "order": w["order"], "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -408,9 +414,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if dtype == torch.float64 else "f32", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: planted partition n={n} k={w['k']} mean degree {w['deg']} "
-                                   f"p_out/p_in={w['ratio']:.4g}; d={d}; Chebyshev order {order}; one step = one "
-                                   "apply_filter of a device-resident block",
+            "config": {"workload": workload_desc(args.workload, w, n, d, order),
                        "n": n, "nnz_L": int(nnz_L), "d": d, "order": order, "precision": args.precision,
                        "l2": "inputs (n*d*8 B per block, 3 blocks) exceed the 126 MB L2; no flush",
                        "parallelism": f"column shards x{world}, no exchange"},
