@@ -291,13 +291,15 @@ class _FusedState:
         self.out = {}
 
     def outputs(self, R):
+        """(labels R x n, packed bytes, cost R, iters R, seeds R x k x ldc, flags R): cost,
+        iters and flags are views of one byte buffer, read back with one copy."""
         if R not in self.out:
             dev, n, k = self.dev, self.n, self.k
-            self.out[R] = (torch.empty((R, n), dtype=torch.int32, device=dev),
-                           torch.empty(R, dtype=torch.float64, device=dev),
-                           torch.empty(R, dtype=torch.int32, device=dev),
+            packed = torch.empty(16 * R, dtype=torch.uint8, device=dev)
+            self.out[R] = (torch.empty((R, n), dtype=torch.int32, device=dev), packed,
+                           packed[:8 * R].view(torch.float64), packed[8 * R:12 * R].view(torch.int32),
                            torch.zeros((R, k, self.ldc), dtype=torch.float64, device=dev),
-                           torch.empty(R, dtype=torch.int32, device=dev))
+                           packed[12 * R:].view(torch.int32))
         return self.out[R]
 
 
@@ -321,7 +323,7 @@ def _run_fused(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, d
         _FUSED = None
         _FUSED = _FusedState(n, d, ld, k, dev)
     R = len(children)
-    labels, cost, iters, seeds, flags = _FUSED.outputs(R)
+    labels, packed, cost, iters, seeds, flags = _FUSED.outputs(R)
     ldc = _FUSED.ldc
     first, unif = draws if draws is not None else kmeanspp_draws(children, n, k)
     first = np.ascontiguousarray(first, dtype=np.int64)
@@ -329,8 +331,8 @@ def _run_fused(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, d
     _native.call("csc_kmeans_fused_kpp_run", ptr(blk), n, d, ld, k, R, first.ctypes.data, unif.ctypes.data, ldc,
                  int(cfg.max_iters), float(cfg.tol), ptr(labels), ptr(cost), ptr(iters), ptr(seeds), ptr(flags),
                  stream())
-    costs = cost.cpu().numpy()  # synchronises
-    fl = flags.cpu().numpy()
+    host = packed.cpu().numpy()  # one synchronising copy: costs, iterations, seeding flags
+    costs, its, fl = host[:8 * R].view(np.float64), host[8 * R:12 * R].view(np.int32), host[12 * R:].view(np.int32)
     bad = [r for r in range(R) if fl[r] >= 0]
     if bad:  # zero D^2 mass (kmeans.py:70-72): sequential seeding for those restarts, explicit seeds
         ws = _Workspace(blk, d, k)
@@ -339,8 +341,9 @@ def _run_fused(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, d
             seeds[r].copy_(ws.cent)
         _native.call("csc_kmeans_fused_run", ptr(blk), ptr(ws.fnorm), n, d, ld, k, R, ptr(seeds), ldc,
                      int(cfg.max_iters), float(cfg.tol), ptr(labels), ptr(cost), ptr(iters), stream())
-        costs = cost.cpu().numpy()
-    LAST_FUSED_ITERS[:] = [int(v) for v in iters.cpu().numpy()]
+        host = packed.cpu().numpy()
+        costs, its = host[:8 * R].view(np.float64), host[8 * R:12 * R].view(np.int32)
+    LAST_FUSED_ITERS[:] = [int(v) for v in its]
     best = 0
     for r in range(1, R):
         if costs[r] < costs[best]:

@@ -222,9 +222,15 @@ class FeatureMatrix:
             self._set(None, host.shape[1], host, step_tags, stream_tags, check=True)
 
     @classmethod
-    def _from_block(cls, blk: torch.Tensor, d: int, step_tags, stream_tags, check: bool = True):
+    def _from_block(cls, blk: torch.Tensor, d: int, step_tags, stream_tags, check: bool = True,
+                    proven_finite: bool = False):
+        """Wrap a device block. proven_finite: the caller knows every value is
+        finite (e.g. from finite sums of squares of its parts), so the check is
+        skipped but recorded as done."""
         fm = cls.__new__(cls)
-        fm._set(blk, d, None, step_tags, stream_tags, check)
+        fm._set(blk, d, None, step_tags, stream_tags, check and not proven_finite)
+        if proven_finite:
+            fm._finite_checked = True
         return fm
 
     def _set(self, blk, d, host, step_tags, stream_tags, check):
