@@ -7,39 +7,39 @@
 // iteration and the restarts contend for the GPU: ~60-85 us per iteration on
 // the longest restart's critical path. Here each CTA (one per SM) owns a
 // contiguous row range whose features stay resident in shared memory for the
-// whole run; restarts advance in lock step, and an iteration is two grid
-// barriers:
+// whole run; restarts advance in lock step (one counter handshake per phase,
+// no grid barrier in the steady state):
 //
 //   phase 1 (per CTA; the active restarts are spread over 1, 2 or 4 thread
 //   groups, so a lone long-running restart gets the whole CTA)
-//     - exact cost of the previous iteration on the CTA's rows,
-//       sum |f_i - c_{l_i}|^2 with the new means (kmeans.py:111) -> partial
-//     - labels of the previous iteration -> output (the final labels when the
-//       restart stops on this cost)
+//     - the stop rule (prev - cost2 <= tol * prev, or max_iters;
+//       kmeans.py:112-116) on the previous iteration's cost by the centroid
+//       identity (the lane path's form), decided identically in every block;
+//       a stopping restart instead computes its exact difference-form cost
+//       sum |f_i - c_{l_i}|^2 (kmeans.py:111, the returned value) and writes
+//       its final labels
 //     - Hamerly bounds (ub >= |f - c_a|, lb <= min_{j != a} |f - c_j|, moved
 //       by the centroid movements): rows whose bounds cannot exclude a label
 //       change are recomputed in the reference's GEMM form
 //       max(0, (|f|^2 - 2 f.c) + |c|^2), first-index argmin (kmeans.py:54-61,
 //       96-97; the per-pair arithmetic of assign_small_kernel, so labels are
 //       bit-identical to the lane path's for the same centroids)
-//     - per-cluster sums of the CTA's rows in row order (stable counting sort
-//       by label, one register run per (cluster, column)) and counts
-//   grid barrier
-//   phase 2 (four warps per (restart, cluster), grid-wide)
-//     - cost2 of the previous iteration = fixed-order sum of the partials;
-//       the reference's stop rule (prev - cost2 <= tol * prev, or max_iters;
-//       kmeans.py:112-116), decided identically by every warp of the restart
+//     - per-cluster sums (and |f|^2 sums) of the CTA's rows in row order for
+//       the clusters whose membership changed (stable counting sort by label)
+//   one arrival per (block, restart)
+//   phase 2 ((restart, cluster) items over the blocks, each waiting for its
+//   restart's arrivals only)
 //     - means = sums / max(count, 1) (kmeans.py:84): block partials added in
-//       block order (four contiguous block ranges, combined in order);
-//       movement and |c|^2 for the next bounds
-//   grid barrier
+//       block order; movement, |c|^2 and the cluster's identity cost term
+//     - a stopping restart: the fixed-order sum of the blocks' exact costs
+//   every block waits for the k items of every active restart
 //   rare path (an empty cluster, kmeans.py:99-108): exact reassignment of every
 //   row (own distances), the reference's argmax reseeding in one CTA, updated
-//   partials, means again (four more barriers, only when it happens).
+//   partials, means again (four grid barriers, only when it happens).
 //
-// Results: labels / cost of every restart. The stop rule uses the exact
-// difference-form cost (the reference's formula; the lane path uses the
-// centroid identity). All reductions have a fixed order: deterministic.
+// Results: labels / cost of every restart. As in the lane path, the stop rule
+// uses the centroid-identity cost and the returned cost the exact difference
+// form. All reductions have a fixed order: deterministic.
 // No tensor cores (north_star); FP64 SIMT.
 #include <cmath>
 
@@ -67,7 +67,10 @@ struct FusedArgs {
   double *cent;         // [2][R][k][ldc]   centroids by iteration parity
   double *kvec;         // [2][R][2][k]     |c|^2, movement by iteration parity
   double *psum;         // [R][G][k][d]     block partial sums
-  double *cpart;        // [R][G]           block partial costs
+  double *cpart;        // [R][G]           block partial exact costs (final iteration)
+  double *pq;           // [R][G][k]        block partial sums of |f|^2 per cluster
+  double *cterm;        // [2][R][k]        centroid-identity cost terms by iteration parity
+  int32_t *stopping;    // [R] iteration whose phase 1 decided the stop (-1 before)
   double *hist;         // [R][max_iters + 1]
   double *own;          // [R][n]           rare path: own distances
   int32_t *pcnt;        // [R][G][k]
@@ -151,7 +154,7 @@ struct Grp {
 };
 
 struct Shared {
-  double *Fs, *fns, *fsq, *ubs, *lbs, *p2;  // CTA-wide
+  double *Fs, *fns, *fsq, *ubs, *lbs, *p2, *p2q;  // CTA-wide
   int32_t *labs, *act, *p2c;                // CTA-wide
 };
 struct GShared {
@@ -164,7 +167,7 @@ __host__ __device__ inline int64_t gstride_i(int64_t RM) { return 2 * RM + 64 + 
 // double offset of the per-group area: after Fs, |f|^2, sqrt, ub, lb and the
 // phase-2 scratch, rounded to 16 bytes (the k-means++ staging reads double2)
 __host__ __device__ inline int64_t group_base(int64_t RM, int64_t ldf, int64_t R, int64_t d) {
-  return (RM * ldf + 2 * RM + 2 * R * RM + kFW * d + 1) & ~int64_t(1);
+  return (RM * ldf + 2 * RM + 2 * R * RM + kFW * (d + 1) + 1) & ~int64_t(1);
 }
 
 __device__ __forceinline__ Shared carve(unsigned char *raw, const FusedArgs &a) {
@@ -176,6 +179,7 @@ __device__ __forceinline__ Shared carve(unsigned char *raw, const FusedArgs &a) 
   s.ubs = s.fsq + RM;
   s.lbs = s.ubs + R * RM;
   s.p2 = s.lbs + R * RM;  // [kFW][d]
+  s.p2q = s.p2 + kFW * a.d;  // [kFW]
   int32_t *ib = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(raw) + group_base(RM, a.ldf, R, a.d) +
                                             a.ngmax * gstride_d(a.lds));
   s.labs = ib;
@@ -448,6 +452,12 @@ __device__ void group_partials(const FusedArgs &a, const Shared &s, const GShare
   }
   G_.sync();
   double *ps = a.psum + ((int64_t)r * a.G + cta) * k * d;
+  if (G_.gt < k && ((dirty >> G_.gt) & 1u) && gs.cnt[G_.gt] > 0) {  // |f|^2 of the run, row order
+    const int j = G_.gt, end = gs.runp[j], beg = end - gs.cnt[j];
+    double q = 0.0;
+    for (int p = beg; p < end; ++p) q += s.fns[gs.perm[p]];
+    a.pq[((int64_t)r * a.G + cta) * k + j] = q;
+  }
   {
     const int di = (int)d, GT = G_.GT, dj = GT / di, dt = GT - dj * di;
     int j = G_.gt / di, t = G_.gt - j * di;
@@ -507,13 +517,36 @@ __device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, c
       double m2 = lane == i1 ? 0.0 : dj;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+      // stop rule (kmeans.py:112-116) on the centroid-identity cost of
+      // iteration g-1 (sum of its k cluster terms in order) and of g-2
+      const double term = lane < k ? __ldcg(a.cterm + ((int64_t)((g - 1) & 1) * a.R + r) * k + lane) : 0.0;
+      double cost = term;
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, cost, o);
+        if (lane >= o) cost += y;  // inclusive prefix in lane order: the total is lane 31's
+      }
+      cost = __shfl_sync(0xffffffffu, cost, 31);
+      cost = cost > 0.0 ? cost : 0.0;
+      const int64_t hs = a.max_iters + 1;
+      const double prev = g >= 2 ? __ldcg(a.hist + r * hs + g - 2) : INFINITY;
+      const bool stop = (g >= 2 && prev - cost <= a.tol * prev) || g >= a.max_iters;
       if (lane == 0) {
         gs.scal[0] = fmax(m1, 0.0);
         gs.scal[1] = fmax(m2, 0.0);
         gs.scal[2] = m1 > 0.0 ? (double)i1 : 0.0;
         gs.scal[3] = sqrt(cm);
+        gs.misc[3] = stop ? 1 : 0;
+        if (cta == 0) {
+          a.hist[r * hs + g - 1] = cost;
+          if (stop) a.stopping[r] = g;
+        }
       }
     }
+    G_.sync();
+  }
+  if (g > 0 && gs.misc[3]) {
+    // the restart stops after iteration g-1: the returned cost2 in the
+    // reference's difference form (kmeans.py:111) and the final labels
     // exact cost of iteration g-1 (labels of g-1, means of g-1): SP adjacent
     // threads per row (columns split in SP contiguous parts, added by a fixed
     // xor tree), rows in rounds of GT / SP
@@ -547,12 +580,10 @@ __device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, c
       for (int w = 0; w < G_.GW; ++w) c += gs.red[w];
       a.cpart[(int64_t)r * a.G + cta] = c;
     }
-  }
-  submark(a, g, 7, first);
-  if (g >= a.max_iters) {
     G_.sync();
     return;
   }
+  submark(a, g, 7, first);
   // rows that need a distance computation
   int ncand = nr;
   if (g > 0) {
@@ -637,6 +668,7 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int r, int j, in
   const int pc = b < b_hi ? __ldcg(a.pcnt + ((int64_t)r * G + b) * k + j) : 0;
   int cnt = pc;
   double sv[4] = {0.0, 0.0, 0.0, 0.0};
+  double qv = 0.0;  // sum of the blocks' |f|^2 partials (same value in every lane)
   const double *pbase = a.psum + ((int64_t)r * G * k + j) * d;
   unsigned m = __ballot_sync(0xffffffffu, pc > 0);
   constexpr int NB = 3;  // nonzero blocks whose loads are in flight together
@@ -647,19 +679,23 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int r, int j, in
       bb[q] = m ? b_lo + __ffs(m) - 1 : -1;
       m &= m ? m - 1 : 0u;
     }
-    double v[NB][4];
+    double v[NB][4], vq[NB];
 #pragma unroll
-    for (int q = 0; q < NB; ++q)
+    for (int q = 0; q < NB; ++q) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t t = lane + 32 * u;
         v[q][u] = (bb[q] >= 0 && t < d) ? __ldcg(pbase + (int64_t)bb[q] * k * d + t) : 0.0;
       }
+      vq[q] = bb[q] >= 0 ? __ldcg(a.pq + ((int64_t)r * G + bb[q]) * k + j) : 0.0;
+    }
 #pragma unroll
     for (int q = 0; q < NB; ++q)
-      if (bb[q] >= 0)
+      if (bb[q] >= 0) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) sv[u] += v[q][u];
+        qv += vq[q];
+      }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -669,14 +705,17 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int r, int j, in
     const int64_t t = lane + 32 * u;
     if (t < d) mine[t] = sv[u];
   }
-  if (lane == 0) s.p2c[wid] = cnt;
+  if (lane == 0) {
+    s.p2c[wid] = cnt;
+    s.p2q[wid] = qv;
+  }
   __syncthreads();
   if (wid == 0) {
     int tot = 0;
     for (int w = 0; w < kFW; ++w) tot += s.p2c[w];
     const double denom = (double)(tot > 1 ? tot : 1);
     double *cnew = a.cent + ((int64_t)((g + 1) & 1) * R + r) * k * a.ldc + j * a.ldc;
-    double mv = 0.0, nrm = 0.0;
+    double mv = 0.0, nrm = 0.0, dot = 0.0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t t = lane + 32 * u;
@@ -688,14 +727,21 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int r, int j, in
         const double df = mean - old[u];
         mv = fma(df, df, mv);
         nrm = fma(mean, mean, nrm);
+        dot = fma(mean, sum, dot);
       }
     }
     mv = warp_sum(mv);
     nrm = warp_sum(nrm);
+    dot = warp_sum(dot);
     if (lane == 0) {
       double *kv = a.kvec + ((int64_t)((g + 1) & 1) * R + r) * 2 * k;
       kv[j] = nrm;
       kv[k + j] = sqrt(mv);
+      // this cluster's cost term by the centroid identity (as the lane path):
+      // sum |f - m|^2 = Q - 2 m.S + n |m|^2 with the rounded mean m
+      double q = 0.0;
+      for (int w = 0; w < kFW; ++w) q += s.p2q[w];
+      a.cterm[((int64_t)(g & 1) * R + r) * k + j] = tot > 0 ? (q - 2.0 * dot) + (double)tot * nrm : 0.0;
       if (flag_empty && tot == 0) a.eflag[r] = g + 1;
     }
   }
@@ -930,22 +976,22 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
         while (ld_acquire(a.arrive + r) < want) __nanosleep(20);
       }
       __syncthreads();
-      bool stop = false;
-      if (g > 0) {
-        const double c = cost_sum(a, r);  // identical in every warp
-        const int64_t hs = a.max_iters + 1;
-        const double prev = g >= 2 ? __ldcg(a.hist + r * hs + g - 2) : INFINITY;
-        stop = (g >= 2 && prev - c <= a.tol * prev) || g >= a.max_iters;
-        if (j == 0 && tid == 0) {
-          a.hist[r * hs + g - 1] = c;
-          if (stop) {
+      // phase 1 of this iteration decided (identically in every block) whether
+      // the restart stopped after iteration g-1; then its blocks computed the
+      // exact cost instead of assigning
+      const bool stop = g > 0 && __ldcg(a.stopping + r) == g;
+      if (stop) {
+        if (j == 0) {
+          const double c = cost_sum(a, r);  // identical in every warp
+          if (tid == 0) {
             a.cost_out[r] = c;
             a.iters_out[r] = g;
             a.done[r] = 1;
           }
         }
+      } else {
+        means_item(a, s, r, j, g, true);
       }
-      if (!stop) means_item(a, s, r, j, g, true);
       __syncthreads();
       if (tid == 0) {  // the mean (or the stop decision) of (r, j) is published
         __threadfence();
@@ -1143,6 +1189,9 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   const size_t b_kvec = al(sizeof(double) * 2 * R * 2 * k);
   const size_t b_psum = al(sizeof(double) * R * G * k * d);
   const size_t b_cpart = al(sizeof(double) * R * G);
+  const size_t b_pq = al(sizeof(double) * R * G * k);
+  const size_t b_cterm = al(sizeof(double) * 2 * R * k);
+  const size_t b_stop = al(sizeof(int32_t) * R);
   const size_t b_hist = al(sizeof(double) * R * (max_iters + 1));
   const size_t b_own = al(sizeof(double) * R * n);
   const size_t b_pcnt = al(sizeof(int32_t) * R * G * k);
@@ -1152,8 +1201,8 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   const size_t b_kpart = kpp ? al(sizeof(double) * R * G) : 0;
   const size_t b_kpick = kpp ? al(sizeof(int32_t) * 2 * R) : 0;
   csc::Scratch ws;
-  CSC_TRY_CUDA(ws.alloc(b_cent + b_kvec + b_psum + b_cpart + b_hist + b_own + b_pcnt + b_ints +
-                            b_kfirst + b_kunif + b_kpart + b_kpick,
+  CSC_TRY_CUDA(ws.alloc(b_cent + b_kvec + b_psum + b_cpart + b_pq + b_cterm + b_stop + b_hist + b_own +
+                            b_pcnt + b_ints + b_kfirst + b_kunif + b_kpart + b_kpick,
                         st));
   unsigned char *p = ws.as<unsigned char>();
   FusedArgs a;
@@ -1178,6 +1227,13 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   p += b_psum;
   a.cpart = reinterpret_cast<double *>(p);
   p += b_cpart;
+  a.pq = reinterpret_cast<double *>(p);
+  p += b_pq;
+  a.cterm = reinterpret_cast<double *>(p);
+  p += b_cterm;
+  a.stopping = reinterpret_cast<int32_t *>(p);
+  p += b_stop;
+  CSC_TRY_CUDA(cudaMemsetAsync(a.stopping, 0xff, sizeof(int32_t) * R, st));
   a.hist = reinterpret_cast<double *>(p);
   p += b_hist;
   a.own = reinterpret_cast<double *>(p);
