@@ -17,17 +17,14 @@
 // On configs[4]-shape features (tools/fp32_screen_sim.py) 99.9% of rows are
 // decided and the largest observed |E - D| is 3% of delta.
 //
-// No tensor cores (north_star): SIMT FFMA, 64 rows x 64 centroids per pass,
-// 4 x 4 per thread, row tiles double-buffered with cp.async.
+// No tensor cores (north_star): SIMT FFMA, 256 rows x 64 centroids per block
+// pass, 8 x 8 per thread, 16-column row stages through a cp.async ring.
 #include "common.cuh"
 #include "kmeans_screen.cuh"
 
 namespace {
 
-constexpr int kSRT = 16, kSCT = 16, kSTM = 4, kSTN = 4;
-constexpr int kSThreads = kSRT * kSCT;  // 256
-constexpr int kSBM = kSRT * kSTM;       // 64 rows per tile
-constexpr int kSBN = kSCT * kSTN;       // 64 centroids per pass
+constexpr int kSBN = 64;  // centroid padding unit (kpad)
 
 // F (fp64, ld) -> F32 (ld32, zero padding to ld32), fn32 = |F32 row|^2 (fp32)
 __global__ void f32_convert_kernel(const double *__restrict__ f, int64_t n, int64_t d, int64_t ld,
@@ -88,13 +85,27 @@ __device__ __forceinline__ void cp_async16_s(void *smem, const void *gmem, bool 
                "r"(valid ? 16 : 0));
 }
 __device__ __forceinline__ void cp_async_commit_s() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1_s() { asm volatile("cp.async.wait_group 1;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_s() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
-// 64-row tiles, double-buffered with cp.async (rows stay row-major: 16-byte
-// copies straight from the FP32 features); per thread 4 rows x 4 centroids,
-// per 4 columns four float4 row loads and four float4 centroid loads feed 64
-// FFMAs. Centroids resident, transposed [d][kpad].
-__global__ void __launch_bounds__(kSThreads, 2)
+// 256 rows x 64 centroids per block pass, 32 x 8 threads, 8 x 8 per thread
+// (rows ty + 32 i: the 4 row groups of a warp hit disjoint banks; centroids
+// 8 tx .. 8 tx + 7). The row tile streams
+// through a 3-stage cp.async ring of 16-column slices kept row-major ([row][20]
+// floats: one float4 per row and 4 columns), so per 4 columns eight float4 row
+// loads and eight float4 centroid loads feed 256 FFMAs; the centroid tile is
+// resident, transposed [d][kpad].
+constexpr int kS3RT = 32, kS3CT = 8, kS3TM = 8, kS3TN = 8;
+constexpr int kS3Threads = kS3RT * kS3CT;  // 256
+constexpr int kS3BM = kS3RT * kS3TM;       // 256 rows per tile
+constexpr int kS3BN = kS3CT * kS3TN;       // 64 centroids per pass
+constexpr int kS3KS = 32;                  // columns per stage
+constexpr int kS3KP = kS3KS + 4;           // padded stage row (floats)
+constexpr int kS3NS = 3;                   // stages in the ring
+
+__global__ void __launch_bounds__(kS3Threads, 1)
     screen_kernel(const float *__restrict__ f32, int64_t ld32, const float *__restrict__ fn32,
                   const double *__restrict__ fn64, int64_t n, int d,
                   const float *__restrict__ c32t, const float *__restrict__ cn32, int k, int kpad,
@@ -103,94 +114,102 @@ __global__ void __launch_bounds__(kSThreads, 2)
                   double *__restrict__ ub, double *__restrict__ lb, int32_t *__restrict__ counts,
                   int32_t *__restrict__ amb, int32_t *__restrict__ namb) {
   extern __shared__ __align__(16) float ssm[];
-  const int d4 = (d + 3) / 4, ldp = 4 * d4 + 4;   // padded row stride (floats)
-  float *Cs = ssm;                                 // [4*d4][kpad] transposed centroids
-  float *Cn = Cs + (int64_t)4 * d4 * kpad;         // [kpad]
-  float *Fs = Cn + kpad;                           // [2][kSBM][ldp]
-  float *Fn = Fs + 2 * kSBM * ldp;                 // [2][kSBM]
-  int32_t *Rid = reinterpret_cast<int32_t *>(Fn + 2 * kSBM);  // [2][kSBM]
-  int32_t *Hs = Rid + 2 * kSBM;                    // [kpad]
-  const int tid = threadIdx.x, tx = tid % kSCT, ty = tid / kSCT;
+  const int nst = (d + kS3KS - 1) / kS3KS, dpad = nst * kS3KS;
+  float *Cs = ssm;                              // [dpad][kpad] transposed centroids
+  float *Cn = Cs + (int64_t)dpad * kpad;        // [kpad]
+  float *Fs = Cn + kpad;                        // [kS3NS][kS3BM][kS3KP] row stages
+  float *Fn = Fs + kS3NS * kS3BM * kS3KP;       // [kS3BM]
+  int32_t *Rid = reinterpret_cast<int32_t *>(Fn + kS3BM);  // [kS3BM]
+  int32_t *Hs = Rid + kS3BM;                    // [kpad]
+  const int tid = threadIdx.x, tx = tid % kS3CT, ty = tid / kS3CT;
   const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : n;
-  const int64_t ntiles = (nr + kSBM - 1) / kSBM;
+  const int64_t ntiles = (nr + kS3BM - 1) / kS3BM;
   if ((int64_t)blockIdx.x >= ntiles) return;
-  for (int64_t e = tid; e < (int64_t)4 * d4 * kpad; e += kSThreads)
+  for (int64_t e = tid; e < (int64_t)dpad * kpad; e += kS3Threads)
     Cs[e] = e < (int64_t)d * kpad ? c32t[e] : 0.0f;
-  for (int j = tid; j < kpad; j += kSThreads) {
+  for (int j = tid; j < kpad; j += kS3Threads) {
     Cn[j] = cn32[j];
     Hs[j] = 0;
   }
   const double cmax = *cmax_dev;
   const double dscale = (double)(d + 5) * 5.9604644775390625e-8;  // (d + 5) * 2^-24
-  // stage tile t into buffer b: row ids / |f|^2 by plain loads, rows by cp.async
-  auto prep = [&](int64_t t, int b) {
-    int32_t *rid = Rid + b * kSBM;
-    if (tid < kSBM) {
-      const int64_t lr = t * kSBM + tid;
-      const int64_t gr = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : -1;
-      rid[tid] = (int32_t)gr;
-      Fn[b * kSBM + tid] = gr >= 0 ? fn32[gr] : 0.0f;
-    }
-    float *fs = Fs + (int64_t)b * kSBM * ldp;
-    // kSThreads / kSBM threads per row (no division, one row id load each)
-    constexpr int TPR = kSThreads / kSBM;
-    const int row = tid / TPR, part = tid % TPR;
-    const int64_t lr = t * kSBM + row;
-    const int64_t gr = lr < nr ? (rows ? (int64_t)__ldg(rows + lr) : lr) : -1;
-    const float *src = gr >= 0 ? f32 + gr * ld32 : f32;
-    for (int q = part; q < d4; q += TPR) cp_async16_s(fs + row * ldp + 4 * q, src + 4 * q, gr >= 0);
-  };
-  int buf = 0;
-  prep(blockIdx.x, 0);
-  cp_async_commit_s();
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if (tile + gridDim.x < ntiles) prep(tile + gridDim.x, buf ^ 1);
-    cp_async_commit_s();
-    cp_async_wait1_s();
-    __syncthreads();
-    const float *fs = Fs + (int64_t)buf * kSBM * ldp + (ty * kSTM) * ldp;
-    const float *fnb = Fn + buf * kSBM;
-    float bv[kSTM], bv2[kSTM];
-    int bi[kSTM];
+  // stage st of the current tile into ring slot b: 256 rows x KS/4 float4
+  // (e = tid + 256 u: row e / (KS/4), column group e % (KS/4)); columns past d
+  // (and padding rows) are zero-filled
+  constexpr int kQ = kS3KS / 4, kU = kS3BM * kQ / kS3Threads;
+  auto stage = [&](int st, int b) {
+    float *fs = Fs + b * kS3BM * kS3KP;
 #pragma unroll
-    for (int i = 0; i < kSTM; ++i) {
+    for (int u = 0; u < kU; ++u) {
+      const int e = tid + kS3Threads * u, row = e / kQ, q = e % kQ;
+      const int32_t gr = Rid[row];
+      const int col = st * kS3KS + 4 * q;
+      const bool ok = gr >= 0 && col < d;
+      cp_async16_s(fs + row * kS3KP + 4 * q, ok ? f32 + (int64_t)gr * ld32 + col : f32, ok);
+    }
+  };
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();  // previous tile's Rid / Fn / stages consumed
+    {
+      const int64_t lr = tile * kS3BM + tid;
+      const int64_t gr = lr < nr ? (rows ? (int64_t)rows[lr] : lr) : -1;
+      Rid[tid] = (int32_t)gr;
+      Fn[tid] = gr >= 0 ? fn32[gr] : 0.0f;
+    }
+    __syncthreads();
+    float bv[kS3TM], bv2[kS3TM];
+    int bi[kS3TM];
+#pragma unroll
+    for (int i = 0; i < kS3TM; ++i) {
       bv[i] = INFINITY;
       bv2[i] = INFINITY;
       bi[i] = 0x7fffffff;
     }
-    for (int c0 = 0; c0 < kpad; c0 += kSBN) {
-      float acc[kSTM][kSTN];
+    for (int c0 = 0; c0 < kpad; c0 += kS3BN) {
+      float acc[kS3TM][kS3TN];
 #pragma unroll
-      for (int i = 0; i < kSTM; ++i)
+      for (int i = 0; i < kS3TM; ++i)
 #pragma unroll
-        for (int j = 0; j < kSTN; ++j) acc[i][j] = 0.0f;
-      const float *cb = Cs + c0 + tx * kSTN;
-#pragma unroll 2
-      for (int q = 0; q < d4; ++q) {
-        float4 a[kSTM], b[4];
+        for (int j = 0; j < kS3TN; ++j) acc[i][j] = 0.0f;
 #pragma unroll
-        for (int i = 0; i < kSTM; ++i) a[i] = *reinterpret_cast<const float4 *>(fs + i * ldp + 4 * q);
+      for (int p = 0; p < kS3NS - 1; ++p) {
+        if (p < nst) stage(p, p);
+        cp_async_commit_s();
+      }
+      for (int st = 0; st < nst; ++st) {
+        if (st + kS3NS - 1 < nst) stage(st + kS3NS - 1, (st + kS3NS - 1) % kS3NS);
+        cp_async_commit_s();
+        cp_async_wait_s<kS3NS - 1>();
+        __syncthreads();
+        const float *fs = Fs + (st % kS3NS) * kS3BM * kS3KP + ty * kS3KP;
+        const float *cb = Cs + (int64_t)st * kS3KS * kpad + c0 + tx * kS3TN;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          b[u] = *reinterpret_cast<const float4 *>(cb + (int64_t)(4 * q + u) * kpad);
+        for (int k4 = 0; k4 < kS3KS / 4; ++k4) {
+          float4 a[kS3TM];
 #pragma unroll
-        for (int i = 0; i < kSTM; ++i) {
-          const float av[4] = {a[i].x, a[i].y, a[i].z, a[i].w};
+          for (int i = 0; i < kS3TM; ++i)
+            a[i] = *reinterpret_cast<const float4 *>(fs + i * kS3RT * kS3KP + 4 * k4);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            acc[i][0] = fmaf(av[u], b[u].x, acc[i][0]);
-            acc[i][1] = fmaf(av[u], b[u].y, acc[i][1]);
-            acc[i][2] = fmaf(av[u], b[u].z, acc[i][2]);
-            acc[i][3] = fmaf(av[u], b[u].w, acc[i][3]);
+            const float4 b0 = *reinterpret_cast<const float4 *>(cb + (int64_t)(4 * k4 + u) * kpad);
+            const float4 b1 = *reinterpret_cast<const float4 *>(cb + (int64_t)(4 * k4 + u) * kpad + 4);
+            const float bw[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < kS3TM; ++i) {
+              const float av = u == 0 ? a[i].x : u == 1 ? a[i].y : u == 2 ? a[i].z : a[i].w;
+#pragma unroll
+              for (int j = 0; j < kS3TN; ++j) acc[i][j] = fmaf(av, bw[j], acc[i][j]);
+            }
           }
         }
+        __syncthreads();  // slot st % NS is refilled by the next iteration's stage()
       }
 #pragma unroll
-      for (int i = 0; i < kSTM; ++i) {
-        const float fni = fnb[ty * kSTM + i];
+      for (int i = 0; i < kS3TM; ++i) {
+        const float fni = Fn[ty + kS3RT * i];
 #pragma unroll
-        for (int j = 0; j < kSTN; ++j) {
-          const int cj = c0 + tx * kSTN + j;
+        for (int j = 0; j < kS3TN; ++j) {
+          const int cj = c0 + tx * kS3TN + j;
           const float e = fmaf(-2.0f, acc[i][j], fni) + Cn[cj];
           if (e < bv[i]) {  // ascending centroid index within the thread
             bv2[i] = bv[i];
@@ -202,12 +221,15 @@ __global__ void __launch_bounds__(kSThreads, 2)
         }
       }
     }
-    // across the 16 threads of a row group (a half warp), lowest index on ties
-    const int32_t *rid = Rid + buf * kSBM;
+    // across the 8 threads of a row group (lanes 8m .. 8m+7), lowest index on
+    // ties; afterwards every lane of the group holds all 8 rows' results and
+    // lane tx settles row ty + 32 tx
+    float myv = INFINITY, myv2 = INFINITY;
+    int myi = 0;
 #pragma unroll
-    for (int i = 0; i < kSTM; ++i) {
+    for (int i = 0; i < kS3TM; ++i) {
 #pragma unroll
-      for (int o = 1; o < kSCT; o <<= 1) {
+      for (int o = 1; o < kS3CT; o <<= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, bv[i], o);
         const float ov2 = __shfl_xor_sync(0xffffffffu, bv2[i], o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi[i], o);
@@ -219,29 +241,31 @@ __global__ void __launch_bounds__(kSThreads, 2)
           bv2[i] = fminf(bv2[i], ov);
         }
       }
-      if (tx == 0) {
-        const int32_t r = rid[ty * kSTM + i];
-        if (r >= 0) {
-          const double fr = sqrt(fn64[r]) + cmax;
-          const double delta = dscale * fr * fr * (1.0 + 1e-6);
-          const double e1 = (double)bv[i], e2 = (double)bv2[i];
-          if (e2 - e1 > 2.0 * delta) {
-            labels[r] = bi[i];
-            ub[r] = sqrt(fmax(e1 + delta, 0.0));
-            lb[r] = sqrt(fmax(e2 - delta, 0.0));
-            if (counts) atomicAdd(Hs + bi[i], 1);
-          } else {
-            amb[atomicAdd(namb, 1)] = r;
-          }
-        }
+      if (tx == i) {
+        myv = bv[i];
+        myv2 = bv2[i];
+        myi = bi[i];
       }
     }
-    __syncthreads();  // buffer `buf` is refilled two tiles later
-    buf ^= 1;
+    const int32_t r = Rid[ty + kS3RT * tx];
+    if (r >= 0) {
+      // |f| from the FP32 norm (relative error < 1e-5 for d <= 256), inflated
+      const double fr = sqrt((double)Fn[ty + kS3RT * tx] * (1.0 + 2e-5)) + cmax;
+      const double delta = dscale * fr * fr * (1.0 + 1e-6);
+      const double e1 = (double)myv, e2 = (double)myv2;
+      if (e2 - e1 > 2.0 * delta) {
+        labels[r] = myi;
+        ub[r] = sqrt(fmax(e1 + delta, 0.0));
+        lb[r] = sqrt(fmax(e2 - delta, 0.0));
+        if (counts) atomicAdd(Hs + myi, 1);
+      } else {
+        amb[atomicAdd(namb, 1)] = r;
+      }
+    }
   }
   if (counts) {
     __syncthreads();
-    for (int j = tid; j < k; j += kSThreads)
+    for (int j = tid; j < k; j += kS3Threads)
       if (Hs[j]) atomicAdd(counts + j, Hs[j]);
   }
 }
@@ -258,9 +282,9 @@ bool screen_supported(int64_t d, int64_t k) {
 
 size_t screen_smem(int64_t d, int64_t k) {
   const int64_t kpad = (k + kSBN - 1) / kSBN * kSBN;
-  const int64_t d4 = (d + 3) / 4, ldp = 4 * d4 + 4;
-  return sizeof(float) * (4 * d4 * kpad + kpad + 2 * kSBM * ldp + 2 * kSBM) +
-         sizeof(int32_t) * (2 * kSBM + kpad);
+  const int64_t dpad = (d + kS3KS - 1) / kS3KS * kS3KS;
+  return sizeof(float) * (dpad * kpad + kpad + kS3NS * kS3BM * kS3KP + kS3BM) +
+         sizeof(int32_t) * (kS3BM + kpad);
 }
 
 int64_t screen_kpad(int64_t k) { return (k + kSBN - 1) / kSBN * kSBN; }
@@ -295,12 +319,12 @@ int screen_assign(const float *f32, int64_t ld32, const float *fn32, const doubl
     configured = smem;
   }
   int occ = 0;
-  CSC_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, screen_kernel, kSThreads, smem));
-  const int64_t tiles = ceil_div(n, kSBM);
+  CSC_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, screen_kernel, kS3Threads, smem));
+  const int64_t tiles = ceil_div(n, kS3BM);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(occ, 1) *
                                                                   csc::device_info().sm_count,
                                                               tiles));
-  screen_kernel<<<(unsigned)grid, kSThreads, smem, st>>>(
+  screen_kernel<<<(unsigned)grid, kS3Threads, smem, st>>>(
       f32, ld32, fn32, fn64, n, (int)d, c32t, cn32, (int)k, (int)screen_kpad(k), cmax, rows,
       nrows_dev, labels, ub, lb, counts, amb, namb);
   CSC_CHECK_LAUNCH();
