@@ -53,7 +53,6 @@ constexpr int kFMaxK = 32;        // one centroid per lane
 constexpr int kFMaxD = 128;       // <= 4 columns per lane in the means pass
 constexpr int kFMaxR = 32;        // restarts
 constexpr int kFMisc = 4 + kFW;   // per-group int scratch
-constexpr int kQuad = 4;          // warps per phase-2 item
 
 struct FusedArgs {
   const double *F;

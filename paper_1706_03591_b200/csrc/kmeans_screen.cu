@@ -19,6 +19,10 @@
 //
 // No tensor cores (north_star): SIMT FFMA, 256 rows x 64 centroids per block
 // pass, 8 x 8 per thread, 16-column row stages through a cp.async ring.
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 #include "kmeans_screen.cuh"
 
@@ -312,14 +316,24 @@ int screen_assign(const float *f32, int64_t ld32, const float *fn32, const doubl
                   int32_t *labels, double *ub, double *lb, int32_t *counts, int32_t *amb,
                   int32_t *namb, cudaStream_t st) {
   const size_t smem = screen_smem(d, k);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    CSC_TRY_CUDA(cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    configured = smem;
-  }
+  // per-device launch setup (dynamic shared memory opt-in, occupancy), cached
+  static std::mutex mu;
+  static std::vector<std::pair<size_t, int>> setup;  // [device] (configured smem, blocks/SM)
+  int dev = 0;
+  CSC_TRY_CUDA(cudaGetDevice(&dev));
   int occ = 0;
-  CSC_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, screen_kernel, kS3Threads, smem));
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)setup.size() <= dev) setup.resize(dev + 1, {0, 0});
+    if (smem > setup[dev].first) {
+      CSC_TRY_CUDA(cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+      CSC_TRY_CUDA(
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, screen_kernel, kS3Threads, smem));
+      setup[dev] = {smem, occ};
+    }
+    occ = setup[dev].second;
+  }
   const int64_t tiles = ceil_div(n, kS3BM);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(occ, 1) *
                                                                   csc::device_info().sm_count,
