@@ -1,5 +1,7 @@
 """Kernel timeline of one configs[1] dynamic step (torch.profiler / CUPTI): per-kernel totals and GPU idle gaps."""
 import collections
+
+import numpy as np
 import os
 import sys
 
@@ -43,3 +45,8 @@ for e in evs:
         print(f"  {e.time_range.start - prev.time_range.end:7.1f} us  after {prev.name[:50]}  before {e.name[:50]}")
     if prev is None or e.time_range.end > prev.time_range.end:
         prev = e
+sw = [e for e in evs if "sweep_kernel" in e.name]
+gaps = [b.time_range.start - a.time_range.end for a, b in zip(sw, sw[1:])]
+if gaps:
+    print(f"sweeps: {len(sw)}, mean duration {np.mean([e.time_range.elapsed_us() for e in sw]):.1f} us, "
+          f"gap between consecutive sweeps median {np.median(gaps):.1f} us, total gaps {np.sum(gaps):.0f} us")
