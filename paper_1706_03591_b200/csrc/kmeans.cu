@@ -1253,17 +1253,28 @@ __global__ void __launch_bounds__(128)
   double part[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) part[r] = 0.0;
-  for (int64_t i = rbeg + threadIdx.x; i < rend; i += blockDim.x) {
+  // two of the thread's rows (i and i + blockDim) per pass: each centroid
+  // value loaded from shared memory feeds both; the block partials still add
+  // the thread's rows in ascending order (identical bits)
+  for (int64_t i = rbeg + threadIdx.x; i < rend; i += 2 * (int64_t)blockDim.x) {
+    const int64_t i2 = i + blockDim.x;
+    const bool two = i2 < rend;
     const double *row = f + i * ld;
-    double acc[R];
+    const double *row2 = f + (two ? i2 : i) * ld;
+    double acc[R], acc2[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    for (int r = 0; r < R; ++r) {
+      acc[r] = 0.0;
+      acc2[r] = 0.0;
+    }
     for (int64_t c = 0; c < d; ++c) {
-      const double x = __ldg(row + c);
+      const double x = __ldg(row + c), x2 = __ldg(row2 + c);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const double t = x - cs[r * d + c];
+        const double cv = cs[r * d + c];
+        const double t = x - cv, t2 = x2 - cv;
         acc[r] = fma(t, t, acc[r]);
+        acc2[r] = fma(t2, t2, acc2[r]);
       }
     }
 #pragma unroll
@@ -1272,6 +1283,15 @@ __global__ void __launch_bounds__(128)
       const double cl = first ? acc[r] : fmin(*slot, acc[r]);
       *slot = cl;
       part[r] += cl;
+    }
+    if (two) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double *slot = closest + (int64_t)r * n + i2;
+        const double cl = first ? acc2[r] : fmin(*slot, acc2[r]);
+        *slot = cl;
+        part[r] += cl;
+      }
     }
   }
   // fixed-order block sums per restart: warp shuffle tree, then warps in order
