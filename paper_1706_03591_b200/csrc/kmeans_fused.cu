@@ -42,6 +42,7 @@
 // form. All reductions have a fixed order: deterministic.
 // No tensor cores (north_star); FP64 SIMT.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -1284,6 +1285,10 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   a.ldf = g.ldf;
   a.lds = g.lds;
   a.ngmax = g.ngmax;
+  if (const char *e = getenv("CSC_FUSED_GROUPS")) {  // A/B knob: cap the thread groups
+    const int cap = atoi(e);
+    if (cap == 1 || cap == 2) a.ngmax = std::min(a.ngmax, cap);
+  }
   CSC_TRY_CUDA(cudaMemsetAsync(ints, 0, b_ints, st));
   CSC_TRY_CUDA(cudaFuncSetAttribute(lloyd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)g.smem));

@@ -192,7 +192,7 @@ def test_fused_kpp_seeds_match_reference_picks(P):
             assert O.adjusted_rand(lab[r], ref_labels) >= 0.999
 
 
-@pytest.mark.parametrize("n,d,k", [(60000, 64, 48), (30000, 128, 100), (20000, 24, 40)])
+@pytest.mark.parametrize("n,d,k", [(60000, 64, 48), (30000, 128, 100), (20000, 24, 40), (8000, 37, 50)])
 def test_fp32_screen_same_labels_as_fp64(P, n, d, k):
     """The FP32 screen of the lane path (csc_kmeans_plan_set_screen) decides
     only rows whose FP64 argmin it provably knows: labels and cost equal the
