@@ -19,7 +19,7 @@ _, state, _ = P.dynamic_init(graphs[0], cfg, seed=0)
 for gt in graphs[1:4]:
     _, state, _ = P.dynamic_step(state, gt, cfg)
 torch.cuda.synchronize()
-with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
     ph = {}
     _, state, _ = P.dynamic_step(state, graphs[4], cfg, timings=ph)
     torch.cuda.synchronize()
