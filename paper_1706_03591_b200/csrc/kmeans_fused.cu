@@ -155,7 +155,7 @@ struct Grp {
 
 struct Shared {
   double *Fs, *fns, *fsq, *ubs, *lbs, *p2, *p2q;  // CTA-wide
-  int32_t *labs, *act, *p2c;                // CTA-wide
+  int32_t *labs, *act, *p2c, *work;         // CTA-wide
 };
 struct GShared {
   double *Cs, *cn, *del, *red, *scal;
@@ -185,6 +185,7 @@ __device__ __forceinline__ Shared carve(unsigned char *raw, const FusedArgs &a) 
   s.labs = ib;
   s.act = ib + R * RM;  // [kFMaxR + 1]
   s.p2c = s.act + kFMaxR + 1;  // [kFW]
+  s.work = s.p2c + kFW;        // [1] phase-1 restart counter (groups take the next restart)
   return s;
 }
 
@@ -198,7 +199,7 @@ __device__ __forceinline__ GShared gcarve(unsigned char *raw, const FusedArgs &a
   g.red = g.del + 32;
   g.scal = g.red + kFW;
   int32_t *ib = reinterpret_cast<int32_t *>(gb + a.ngmax * gstride_d(a.lds)) + R * RM + kFMaxR + 1 +
-                kFW;
+                kFW + 1;
   int32_t *gi32 = ib + gi * gstride_i(RM);
   g.cand = gi32;
   g.perm = g.cand + RM;
@@ -935,6 +936,7 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
   if (tid == 0) {
     for (int r = 0; r < R; ++r) s.act[r] = r;
     s.act[kFMaxR] = (int)R;
+    *s.work = 0;
   }
   __syncthreads();
 
@@ -955,7 +957,14 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
       G_.gt = tid % G_.GT;
       G_.gw = G_.gt >> 5;
       const GShared gs = gcarve(smem_raw, a, G_.id);
-      for (int ai = G_.id; ai < A; ai += ng) {
+      // groups take the next active restart from a block counter (restarts'
+      // costs differ with their candidate counts)
+      for (;;) {
+        if (G_.gt == 0) gs.misc[2] = atomicAdd(s.work, 1);
+        G_.sync();
+        const int ai = gs.misc[2];
+        G_.sync();
+        if (ai >= A) break;
         phase1(a, s, gs, G_, s.act[ai], g, nr, rb, ai == 0);
         // this block's partials of the restart are written (phase1 ends on a
         // group barrier): release them with one arrival on the restart's count
@@ -1108,6 +1117,7 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
     }
     mark(g, 5);
     if (tid == 0) {  // restarts still running (identical list on every CTA)
+      *s.work = 0;
       int m = 0;
       for (int r = 0; r < R; ++r)
         if (!__ldcg(a.done + r)) s.act[m++] = r;
@@ -1125,7 +1135,7 @@ struct FusedGeom {
 
 size_t fused_smem(int64_t RM, int64_t d, int64_t R, int ngmax, int ldf, int lds) {
   const int64_t dbl = group_base(RM, ldf, R, d) + ngmax * gstride_d(lds);
-  const int64_t ints = R * RM + kFMaxR + 1 + kFW + ngmax * gstride_i(RM);
+  const int64_t ints = R * RM + kFMaxR + 1 + kFW + 1 + ngmax * gstride_i(RM);
   return (size_t)(dbl * 8 + ints * 4);
 }
 
