@@ -147,6 +147,15 @@ __device__ __forceinline__ double warp_sum(double v) {
   return __shfl_sync(0xffffffffu, v, 0);
 }
 
+// Global row of the block's local row i: start + stride * i. k-means++ uses
+// contiguous ranges (its D^2 draw scans rows in order); the Lloyd phases use an
+// interleaved map (row = block + G i) so every block holds a sample of every
+// community and the blocks' candidate counts (their phase-1 work) balance.
+struct RowMap {
+  int64_t start, stride;
+  __device__ __forceinline__ int64_t operator()(int64_t i) const { return start + stride * i; }
+};
+
 // A thread group working on one restart at a time (named barrier id + 1).
 struct Grp {
   int id, GT, GW, gt, gw;
@@ -318,7 +327,7 @@ __device__ __forceinline__ void assign_pass(const FusedArgs &a, const GShared &g
 template <int TR>
 __device__ __forceinline__ void assign_rows(const FusedArgs &a, const Shared &s, const GShared &gs,
                                             int r, int p0, int ncand, const int32_t *cand,
-                                            bool want_own, int64_t rb, bool fresh) {
+                                            bool want_own, RowMap rm, bool fresh) {
   const int lane = threadIdx.x & 31, rg = lane >> 2, cg = lane & 3;
   const int64_t k = a.k, RM = a.rows_max, ldf = a.ldf;
   int row[TR];
@@ -383,7 +392,7 @@ __device__ __forceinline__ void assign_rows(const FusedArgs &a, const Shared &s,
       s.labs[(int64_t)r * RM + i] = vi[q];
       s.ubs[(int64_t)r * RM + i] = sqrt(v[q]);
       s.lbs[(int64_t)r * RM + i] = sqrt(v2[q]);
-      if (want_own) a.own[(int64_t)r * a.n + rb + i] = v[q];
+      if (want_own) a.own[(int64_t)r * a.n + rm(i)] = v[q];
     }
   }
 #pragma unroll
@@ -395,16 +404,16 @@ __device__ __forceinline__ void assign_rows(const FusedArgs &a, const Shared &s,
 // still gives every warp work (latency-bound when few rows are candidates).
 __device__ __forceinline__ void assign_list(const FusedArgs &a, const Shared &s, const GShared &gs,
                                             int r, int ncand, const int32_t *cand, bool want_own,
-                                            int64_t rb, bool fresh, int gw, int GW) {
+                                            RowMap rm, bool fresh, int gw, int GW) {
   if (ncand >= 32 * GW) {
     for (int p0 = gw * 32; p0 < ncand; p0 += GW * 32)
-      assign_rows<4>(a, s, gs, r, p0, ncand, cand, want_own, rb, fresh);
+      assign_rows<4>(a, s, gs, r, p0, ncand, cand, want_own, rm, fresh);
   } else if (ncand >= 16 * GW) {
     for (int p0 = gw * 16; p0 < ncand; p0 += GW * 16)
-      assign_rows<2>(a, s, gs, r, p0, ncand, cand, want_own, rb, fresh);
+      assign_rows<2>(a, s, gs, r, p0, ncand, cand, want_own, rm, fresh);
   } else {
     for (int p0 = gw * 8; p0 < ncand; p0 += GW * 8)
-      assign_rows<1>(a, s, gs, r, p0, ncand, cand, want_own, rb, fresh);
+      assign_rows<1>(a, s, gs, r, p0, ncand, cand, want_own, rm, fresh);
   }
 }
 
@@ -487,7 +496,7 @@ __device__ __forceinline__ void submark(const FusedArgs &a, int g, int slot, boo
 }
 
 __device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, const Grp &G_,
-                       int r, int g, int nr, int64_t rb, bool first) {
+                       int r, int g, int nr, RowMap rm, bool first) {
   const int lane = threadIdx.x & 31;
   const int64_t k = a.k, d = a.d, RM = a.rows_max, ldf = a.ldf;
   const int cta = blockIdx.x;
@@ -567,7 +576,7 @@ __device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, c
           const double df = fr[t] - cr[t];
           v = fma(df, df, v);
         }
-        if (part == 0) a.labels_out[(int64_t)r * a.n + rb + i] = l;
+        if (part == 0) a.labels_out[(int64_t)r * a.n + rm(i)] = l;
       }
       for (int o = 1; o < SP; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (part == 0) acc += v;
@@ -621,7 +630,7 @@ __device__ void phase1(const FusedArgs &a, const Shared &s, const GShared &gs, c
   submark(a, g, 8, first);
   if (first && a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && g < a.trace_cap)
     a.trace[(int64_t)g * 16 + 11] = (unsigned long long)ncand;
-  assign_list(a, s, gs, r, ncand, g == 0 ? nullptr : gs.cand, false, rb, g == 0, G_.gw, G_.GW);
+  assign_list(a, s, gs, r, ncand, g == 0 ? nullptr : gs.cand, false, rm, g == 0, G_.gw, G_.GW);
   G_.sync();
   submark(a, g, 9, first);
   group_partials(a, s, gs, G_, r, nr, false, g == 0 ? ~0u : (unsigned)gs.misc[1]);
@@ -909,30 +918,43 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int cta = blockIdx.x, G = a.G;
   const int64_t n = a.n, d = a.d, k = a.k, R = a.R, RM = a.rows_max, ldf = a.ldf;
-  const int64_t rb = (int64_t)cta * n / G, re = (int64_t)(cta + 1) * n / G;
-  const int nr = (int)(re - rb);
   const Shared s = carve(smem_raw, a);
-
-  for (int64_t e = tid; e < (int64_t)nr * d; e += kFT) {
-    const int64_t i = e / d, t = e - i * d;
-    s.Fs[i * ldf + t] = a.F[(rb + i) * a.ld + t];
-  }
-  if (a.fnorm) {
-    for (int i = tid; i < nr; i += kFT) s.fns[i] = a.fnorm[rb + i];
-  } else {  // |f|^2 with csc_kmeans_rownorms' association (lane-strided, xor tree)
+  // the block's rows into shared memory: features, |f|^2, |f|
+  auto load_rows = [&](RowMap m, int cnt) {
     __syncthreads();
-    for (int i = wid; i < nr; i += kFW) {
-      const double *fr = s.Fs + (int64_t)i * ldf;
-      double v = 0.0;
-      for (int64_t t = lane; t < d; t += 32) v = fma(fr[t], fr[t], v);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) s.fns[i] = v;
+    for (int64_t e = tid; e < (int64_t)cnt * d; e += kFT) {
+      const int64_t i = e / d, t = e - i * d;
+      s.Fs[i * ldf + t] = a.F[m(i) * a.ld + t];
     }
+    if (a.fnorm) {
+      for (int i = tid; i < cnt; i += kFT) s.fns[i] = a.fnorm[m(i)];
+    } else {  // |f|^2 with csc_kmeans_rownorms' association (lane-strided, xor tree)
+      __syncthreads();
+      for (int i = wid; i < cnt; i += kFW) {
+        const double *fr = s.Fs + (int64_t)i * ldf;
+        double v = 0.0;
+        for (int64_t t = lane; t < d; t += 32) v = fma(fr[t], fr[t], v);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s.fns[i] = v;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < cnt; i += kFT) s.fsq[i] = sqrt(s.fns[i]);
+    __syncthreads();
+  };
+  if (a.kpp_first) {  // k-means++ over contiguous row ranges (draws scan rows in order)
+    const int64_t rb = (int64_t)cta * n / G, re = (int64_t)(cta + 1) * n / G;
+    load_rows(RowMap{rb, 1}, (int)(re - rb));
+    kmeanspp_phase(a, s, gcarve(smem_raw, a, 0), (int)(re - rb), rb);
   }
-  __syncthreads();
-  for (int i = tid; i < nr; i += kFT) s.fsq[i] = sqrt(s.fns[i]);
-  if (a.kpp_first) kmeanspp_phase(a, s, gcarve(smem_raw, a, 0), nr, rb);
+  const RowMap rm{cta, G};
+  const int nr = (int)((n - cta + G - 1) / G);
+  load_rows(rm, nr);
+  for (int gi = 0; gi < a.ngmax; ++gi) {  // centroid rows >= k read as zero
+    const GShared gs = gcarve(smem_raw, a, gi);
+    for (int64_t e = tid; e < (32 - k) * a.lds; e += kFT) gs.Cs[k * a.lds + e] = 0.0;
+  }
   if (tid == 0) {
     for (int r = 0; r < R; ++r) s.act[r] = r;
     s.act[kFMaxR] = (int)R;
@@ -965,7 +987,7 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
         const int ai = gs.misc[2];
         G_.sync();
         if (ai >= A) break;
-        phase1(a, s, gs, G_, s.act[ai], g, nr, rb, ai == 0);
+        phase1(a, s, gs, G_, s.act[ai], g, nr, rm, ai == 0);
         // this block's partials of the restart are written (phase1 ends on a
         // group barrier): release them with one arrival on the restart's count
         if (G_.gt == 0) {
@@ -1030,7 +1052,7 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
       for (int r = 0; r < R; ++r) {
         if (__ldcg(a.eflag + r) != g + 1) continue;
         group_load(a, gs, W, r, g);
-        assign_list(a, s, gs, r, nr, nullptr, true, rb, true, wid, kFW);
+        assign_list(a, s, gs, r, nr, nullptr, true, rm, true, wid, kFW);
         W.sync();
         group_partials(a, s, gs, W, r, nr, true, ~0u);
       }
@@ -1098,10 +1120,11 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
           const int m = __ldcg(a.nrep + r);
           for (int q = 0; q < m; ++q) {
             const int64_t i = __ldcg(a.rep_idx + (int64_t)r * k + q);
-            if (i >= rb && i < re) {
-              s.labs[(int64_t)r * RM + (i - rb)] = __ldcg(a.rep_j + (int64_t)r * k + q);
-              s.ubs[(int64_t)r * RM + (i - rb)] = INFINITY;  // recomputed next iteration
-              s.lbs[(int64_t)r * RM + (i - rb)] = 0.0;
+            if (i % G == cta) {  // this block's row (interleaved map)
+              const int64_t li = i / G;
+              s.labs[(int64_t)r * RM + li] = __ldcg(a.rep_j + (int64_t)r * k + q);
+              s.ubs[(int64_t)r * RM + li] = INFINITY;  // recomputed next iteration
+              s.lbs[(int64_t)r * RM + li] = 0.0;
             }
           }
         }
