@@ -1171,17 +1171,13 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
   if (scan_tmp.alloc(tmp_bytes, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
   cub::DeviceScan::ExclusiveSum(scan_tmp.ptr, tmp_bytes, counts.as<int32_t>(), op->indptr, n + 1,
                                 st);
-  int32_t mnnz = 0;
-  if (cudaMemcpyAsync(&mnnz, op->indptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+  // M has at most the entries of L plus a diagonal for rows L leaves empty
+  // (isolated nodes; exact zeros are dropped): allocate nnz + n now and read
+  // M's count back together with the long-row count below (one
+  // synchronisation instead of two)
+  if (cudaMallocAsync((void **)&op->indices, sizeof(int32_t) * std::max<int64_t>(nnz + n, 1), st) !=
           cudaSuccess ||
-      cudaStreamSynchronize(st) != cudaSuccess) {
-    csc::set_error("csc_chebop_create: %s", cudaGetErrorString(cudaGetLastError()));
-    return fail(CSC_ERR_CUDA);
-  }
-  op->nnz = mnnz;
-  if (cudaMallocAsync((void **)&op->indices, sizeof(int32_t) * std::max<int64_t>(mnnz, 1), st) !=
-          cudaSuccess ||
-      cudaMallocAsync(&op->vals, esz * std::max<int64_t>(mnnz, 1), st) != cudaSuccess) {
+      cudaMallocAsync(&op->vals, esz * std::max<int64_t>(nnz + n, 1), st) != cudaSuccess) {
     csc::set_error("csc_chebop_create: allocation failed");
     return fail(CSC_ERR_CUDA);
   }
@@ -1212,13 +1208,18 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
   if (sel_tmp.alloc(sel_bytes, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
   cub::DeviceSelect::If(sel_tmp.ptr, sel_bytes, rows_it, op->long_rows, nsel.as<int32_t>(), n,
                         pred, st);
-  int32_t n_long = 0;
-  if (cudaMemcpyAsync(&n_long, nsel.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+  // nsel[1] <- nnz(M) = indptr[n]; one copy of both counts
+  int32_t cnt[2] = {0, 0};
+  if (cudaMemcpyAsync(nsel.as<int32_t>() + 1, op->indptr + n, sizeof(int32_t),
+                      cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(cnt, nsel.ptr, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, st) !=
           cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess) {
     csc::set_error("csc_chebop_create: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(CSC_ERR_CUDA);
   }
+  const int32_t n_long = cnt[0];
+  op->nnz = cnt[1];
   op->n_long = n_long;
   if (n_long > 0) {
     if (segcnt.alloc(sizeof(int32_t) * (n_long + 1), st) != cudaSuccess ||
