@@ -758,6 +758,39 @@ __device__ void means_item(const FusedArgs &a, const Shared &s, int r, int j, in
   __syncthreads();  // p2 reuse
 }
 
+// k-means++ D^2 update for (row, Q restarts) items: difference form in
+// ascending columns per (row, restart) chain, closest = min over the draws
+template <int Q>
+__device__ __forceinline__ void kpp_dist_items(const Shared &s, const GShared &g0, double *cl,
+                                               int nr, int RP, int R, int di, int64_t ldf,
+                                               int64_t RM, int j) {
+  for (int e = threadIdx.x; e < nr * (RP / Q); e += kFT) {
+    const int i = e / (RP / Q), c0 = (e - i * (RP / Q)) * Q;
+    const double *fr = s.Fs + (int64_t)i * ldf;
+    const double2 *cr = reinterpret_cast<const double2 *>(g0.Cs + c0);
+    double acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+#pragma unroll 2
+    for (int t = 0; t < di; ++t) {
+      const double f = fr[t];
+#pragma unroll
+      for (int h = 0; h < Q / 2; ++h) {
+        const double2 c = cr[((t * RP) >> 1) + h];
+        const double x0 = f - c.x, x1 = f - c.y;
+        acc[2 * h] = fma(x0, x0, acc[2 * h]);
+        acc[2 * h + 1] = fma(x1, x1, acc[2 * h + 1]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (c0 + q >= R) break;
+      double *c = cl + (int64_t)(c0 + q) * RM + i;
+      *c = j == 0 ? acc[q] : fmin(*c, acc[q]);
+    }
+  }
+}
+
 __device__ __forceinline__ void kmark(const FusedArgs &a, int j, int slot) {
   if (a.trace && a.trace_cap >= 128 && blockIdx.x == 0 && threadIdx.x == 0)
     a.trace[(int64_t)(96 + j) * 16 + slot] = gtimer();
@@ -783,7 +816,10 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
   double *cl = s.ubs, *pre = s.lbs;
   // centroid j of every restart, transposed into g0.Cs as [t][RP] (RP = R
   // rounded up to 4: one 32-byte pair of loads feeds 4 restarts' chains)
-  const int RP = ((int)R + 3) & ~3;
+  // restarts per distance item: 4, or 8 when (row, 4 restarts) items would
+  // need a second round of the block's threads
+  const int Q = (nr * (((int)R + 3) / 4) > kFT) ? 8 : 4;
+  const int RP = ((int)R + Q - 1) / Q * Q;
   auto stage = [&](int j) {
     for (int e = tid; e < (int)R * di; e += kFT) {
       const int r = e / di, t = e - r * di;
@@ -800,28 +836,10 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
   stage(0);
   for (int j = 0; j + 1 < ki; ++j) {
     kmark(a, j, 0);
-    for (int e = tid; e < nr * (RP / 4); e += kFT) {  // (row, 4 restarts) per item
-      const int i = e / (RP / 4), c4 = (e - i * (RP / 4)) * 4;
-      const double *fr = s.Fs + (int64_t)i * ldf;
-      const double2 *cr = reinterpret_cast<const double2 *>(g0.Cs + c4);
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-      for (int t = 0; t < di; ++t) {
-        const double f = fr[t];
-        const double2 c01 = cr[(t * RP) >> 1], c23 = cr[((t * RP) >> 1) + 1];
-        const double x0 = f - c01.x, x1 = f - c01.y, x2 = f - c23.x, x3 = f - c23.y;
-        acc[0] = fma(x0, x0, acc[0]);
-        acc[1] = fma(x1, x1, acc[1]);
-        acc[2] = fma(x2, x2, acc[2]);
-        acc[3] = fma(x3, x3, acc[3]);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (c4 + q >= R) break;
-        double *c = cl + (int64_t)(c4 + q) * RM + i;
-        *c = j == 0 ? acc[q] : fmin(*c, acc[q]);
-      }
-    }
+    if (Q == 8)
+      kpp_dist_items<8>(s, g0, cl, nr, RP, (int)R, di, ldf, RM, j);
+    else
+      kpp_dist_items<4>(s, g0, cl, nr, RP, (int)R, di, ldf, RM, j);
     __syncthreads();
     for (int r = wid; r < R; r += kFW) {
       double carry = 0.0;
