@@ -814,11 +814,13 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
   const int64_t k = a.k, d = a.d, R = a.R, RM = a.rows_max, ldf = a.ldf, lds = a.lds;
   const int di = (int)d, ki = (int)k;
   double *cl = s.ubs, *pre = s.lbs;
-  // centroid j of every restart, transposed into g0.Cs as [t][RP] (RP = R
-  // rounded up to 4: one 32-byte pair of loads feeds 4 restarts' chains)
-  // restarts per distance item: 4, or 8 when (row, 4 restarts) items would
-  // need a second round of the block's threads
-  const int Q = (nr * (((int)R + 3) / 4) > kFT) ? 8 : 4;
+  // centroid j of every restart, transposed into g0.Cs as [t][RP], RP = R
+  // rounded up to Q, the restarts one (row, Q restarts) distance item covers:
+  // the smallest even Q >= 4 whose items fit one round of the block's threads
+  // (and RP <= 32: g0.Cs holds 32 x lds doubles)
+  int Q = 4;
+  while (Q < 8 && nr * (((int)R + Q - 1) / Q) > kFT) Q += 2;
+  if (((int)R + Q - 1) / Q * Q > 32) Q = 4;
   const int RP = ((int)R + Q - 1) / Q * Q;
   auto stage = [&](int j) {
     for (int e = tid; e < (int)R * di; e += kFT) {
@@ -838,6 +840,8 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
     kmark(a, j, 0);
     if (Q == 8)
       kpp_dist_items<8>(s, g0, cl, nr, RP, (int)R, di, ldf, RM, j);
+    else if (Q == 6)
+      kpp_dist_items<6>(s, g0, cl, nr, RP, (int)R, di, ldf, RM, j);
     else
       kpp_dist_items<4>(s, g0, cl, nr, RP, (int)R, di, ldf, RM, j);
     __syncthreads();

@@ -163,7 +163,10 @@ def test_fused_kpp_seeds_match_reference_picks(P):
     from paper_1706_03591_b200 import _native
     from paper_1706_03591_b200._device import ptr, row_stride, stream, upload_block
     from paper_1706_03591_b200.kmeans import kmeanspp_draws
-    for n, d, k, R, seed in [(1000, 40, 10, 1, 0), (20000, 80, 20, 10, 5), (997, 7, 5, 16, 2)]:
+    # restarts per distance item (kmeans_fused.cu kmeanspp_phase): 4 (997 rows),
+    # 6 (20000 x R=10), 8 (20000 x R=13), back to 4 where 6 would pad past 32 (8000 x R=32)
+    for n, d, k, R, seed in [(1000, 40, 10, 1, 0), (20000, 80, 20, 10, 5), (997, 7, 5, 16, 2),
+                             (20000, 24, 6, 13, 3), (8000, 16, 8, 32, 4)]:
         f = blobs(n, d, k, 0.9, seed=seed)
         blk = upload_block(f)
         ld = blk.shape[1]
