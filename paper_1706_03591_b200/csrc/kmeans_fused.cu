@@ -86,8 +86,8 @@ struct FusedArgs {
   const int64_t *kpp_first;  // [R] the restart's integers(n) draw
   const double *kpp_unif;    // [R][k-1] its random() draws
   double *kpp_part;          // [R][G] block sums of the D^2 weights
-  int32_t *kpp_pick;         // [R] row drawn by the current step
-  int32_t *kpp_ready;        // [R] = j + 1 once draw j's pick is written (zeroed)
+  double *kpp_w;             // [2][R][G][rows_max] blocks' D^2 weights (draw parity)
+  double *kpp_pre;           // [2][R][G][rows_max] their in-block prefix sums
   int32_t *kpp_flag;         // [R] first j whose D^2 mass was 0 (host replays), else -1
   double *seeds_out;         // [R][k][ldc] the seeds (nullable)
   unsigned long long *trace;  // optional: CTA 0's globaltimer at phase boundaries [iter][8]
@@ -825,7 +825,7 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
   auto stage = [&](int j) {
     for (int e = tid; e < (int)R * di; e += kFT) {
       const int r = e / di, t = e - r * di;
-      const int64_t idx = j == 0 ? a.kpp_first[r] : (int64_t)__ldcg(a.kpp_pick + r);
+      const int64_t idx = j == 0 ? a.kpp_first[r] : (int64_t)s.act[r];
       const double v = __ldg(a.F + idx * a.ld + t);
       g0.Cs[(int64_t)t * RP + r] = v;
       if (cta == 0) {
@@ -845,18 +845,24 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
     else
       kpp_dist_items<4>(s, g0, cl, nr, RP, (int)R, di, ldf, RM, j);
     __syncthreads();
+    // the weights and their in-block prefix to global memory as well: after
+    // the barrier every block finds every restart's pick itself
+    const int64_t GRM = (int64_t)G * RM;
+    double *gw = a.kpp_w + (int64_t)(j & 1) * R * GRM, *gp = a.kpp_pre + (int64_t)(j & 1) * R * GRM;
     for (int r = wid; r < R; r += kFW) {
       double carry = 0.0;
+      double *wr = gw + r * GRM + (int64_t)cta * RM, *pr = gp + r * GRM + (int64_t)cta * RM;
       for (int i0 = 0; i0 < nr; i0 += 32) {
         const int i = i0 + lane;
         double x = i < nr ? cl[(int64_t)r * RM + i] : 0.0;
+        if (i < nr) wr[i] = x;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const double y = __shfl_up_sync(0xffffffffu, x, o);
           if (lane >= o) x += y;
         }
         x += carry;
-        if (i < nr) pre[(int64_t)r * RM + i] = x;
+        if (i < nr) pr[i] = x;
         carry = __shfl_sync(0xffffffffu, x, 31);
       }
       if (lane == 0) a.kpp_part[(int64_t)r * G + cta] = carry;
@@ -883,11 +889,7 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
       const double total = __shfl_sync(0xffffffffu, incl, 31);
       if (!(total > 0.0)) {
         if (cta == 0 && lane == 0 && __ldcg(a.kpp_flag + r) < 0) a.kpp_flag[r] = j + 1;
-        if (cta == 0 && lane == 0) {
-          a.kpp_pick[r] = 0;
-          __threadfence();
-          st_release(a.kpp_ready + r, j + 1);
-        }
+        if (lane == 0) s.act[r] = 0;
         continue;
       }
       const double target = a.kpp_unif[(int64_t)r * (k - 1) + j] * total;
@@ -900,33 +902,40 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
       const int lf = hit ? __ffs(hit) - 1 : (G - 1) / 5;
       const int qsel = __shfl_sync(0xffffffffu, hit ? qf : (G - 1) % 5, lf);
       const int cstar = 5 * lf + qsel;
-      if (cstar != cta) continue;
       double base = excl;
       if (qsel > 0) base = excl + loc[qsel - 1];
       base = __shfl_sync(0xffffffffu, base, lf);
+      // block cstar's rows (a contiguous range), 256 per batch of loads
+      const int64_t cb = (int64_t)cstar * a.n / G;
+      const int ncs = (int)((int64_t)(cstar + 1) * a.n / G - cb);
+      const double *wc = gw + r * GRM + (int64_t)cstar * RM, *pc = gp + r * GRM + (int64_t)cstar * RM;
       int found = -1, lastpos = -1;
-      for (int i0 = 0; i0 < nr && found < 0; i0 += 32) {
-        const int i = i0 + lane;
-        const double w = i < nr ? cl[(int64_t)r * RM + i] : 0.0;
-        const bool pos = i < nr && w > 0.0;
-        const bool ok = pos && base + pre[(int64_t)r * RM + i] > target;
-        const unsigned hb = __ballot_sync(0xffffffffu, ok);
-        const unsigned pb = __ballot_sync(0xffffffffu, pos);
-        if (hb) found = i0 + __ffs(hb) - 1;
-        if (pb) lastpos = i0 + 31 - __clz(pb);
+      for (int i0 = 0; i0 < ncs && found < 0; i0 += 256) {
+        double w[8], pv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + 32 * u + lane;
+          w[u] = i < ncs ? __ldcg(wc + i) : 0.0;
+          pv[u] = i < ncs ? __ldcg(pc + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + 32 * u + lane;
+          const bool pos = i < ncs && w[u] > 0.0;
+          const bool ok = pos && base + pv[u] > target;
+          const unsigned hb = __ballot_sync(0xffffffffu, ok);
+          const unsigned pb = __ballot_sync(0xffffffffu, pos);
+          if (pb) lastpos = i0 + 32 * u + 31 - __clz(pb);
+          if (hb) {
+            found = i0 + 32 * u + __ffs(hb) - 1;
+            break;
+          }
+        }
       }
       if (found < 0) found = lastpos >= 0 ? lastpos : 0;  // rounding fallback
-      if (lane == 0) {
-        a.kpp_pick[r] = (int32_t)(rb + found);
-        __threadfence();
-        st_release(a.kpp_ready + r, j + 1);
-      }
+      if (lane == 0) s.act[r] = (int32_t)(cb + found);
     }
     kmark(a, j, 2);
-    // wait for every restart's pick (one writer block each) instead of a barrier
-    __syncthreads();
-    if (tid < R)
-      while (ld_acquire_i(a.kpp_ready + tid) != j + 1) __nanosleep(20);
     __syncthreads();
     kmark(a, j, 3);
     stage(j + 1);
@@ -1254,7 +1263,7 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   const size_t b_kfirst = kpp ? al(sizeof(int64_t) * R) : 0;
   const size_t b_kunif = kpp ? al(sizeof(double) * R * std::max<int64_t>(1, k - 1)) : 0;
   const size_t b_kpart = kpp ? al(sizeof(double) * R * G) : 0;
-  const size_t b_kpick = kpp ? al(sizeof(int32_t) * 2 * R) : 0;
+  const size_t b_kpick = kpp ? al(sizeof(double) * 4 * R * G * g.RM) : 0;
   csc::Scratch ws;
   CSC_TRY_CUDA(ws.alloc(b_cent + b_kvec + b_psum + b_cpart + b_pq + b_cterm + b_stop + b_hist + b_own +
                             b_pcnt + b_ints + b_kfirst + b_kunif + b_kpart + b_kpick,
@@ -1308,8 +1317,8 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   a.kpp_first = nullptr;
   a.kpp_unif = nullptr;
   a.kpp_part = nullptr;
-  a.kpp_pick = nullptr;
-  a.kpp_ready = nullptr;
+  a.kpp_w = nullptr;
+  a.kpp_pre = nullptr;
   a.kpp_flag = flags;
   a.seeds_out = seeds_out;
   if (kpp) {
@@ -1319,9 +1328,8 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
     p += b_kunif;
     a.kpp_part = reinterpret_cast<double *>(p);
     p += b_kpart;
-    a.kpp_pick = reinterpret_cast<int32_t *>(p);
-    a.kpp_ready = a.kpp_pick + R;
-    CSC_TRY_CUDA(cudaMemsetAsync(a.kpp_ready, 0, sizeof(int32_t) * R, st));
+    a.kpp_w = reinterpret_cast<double *>(p);
+    a.kpp_pre = a.kpp_w + 2 * R * G * g.RM;
     CSC_TRY_CUDA(cudaMemcpyAsync(kf, first_host, sizeof(int64_t) * R, cudaMemcpyHostToDevice, st));
     if (k > 1)
       CSC_TRY_CUDA(cudaMemcpyAsync(ku, unif_host, sizeof(double) * R * (k - 1),
