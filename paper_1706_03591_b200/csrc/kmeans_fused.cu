@@ -120,17 +120,14 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
 // Grid-wide barrier (all CTAs co-resident: cooperative launch). Writes before
 // it are visible to __ldcg loads after it.
 __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned G) {
+  // one monotonic arrival counter (zeroed per launch): the e-th barrier of
+  // every block returns old in [eG, (e+1)G) and releases at (e+1)G -- one
+  // atomic per block, no reset round trip
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire(bar + 1);
     __threadfence();
-    if (atomicAdd(bar, 1u) == G - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (ld_acquire(bar + 1) == gen) __nanosleep(20);
-    }
+    const unsigned target = (atomicAdd(bar, 1u) / G + 1) * G;
+    while (ld_acquire(bar) < target) __nanosleep(20);
     __threadfence();
   }
   __syncthreads();
