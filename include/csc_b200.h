@@ -150,6 +150,12 @@ int csc_set_tuning(const char *key, int64_t value);
 int csc_sweep_timing(int enable);
 int csc_sweep_times(float *ms_host, int max_count, int *count_out);
 
+/* rows x width_bytes strided copy (cudaMemcpy2DAsync, direction from the
+ * pointers): the column-chunk staging of apply_filter's host pipeline
+ * (filters.py apply_filter; reference filters.py:155-178 takes a host matrix). */
+int csc_copy2d_async(void *dst, int64_t dpitch, const void *src, int64_t spitch,
+                     int64_t width_bytes, int64_t rows, void *stream);
+
 /* sum of squares of a dense n x ld block (dtype) into out_dev[0] (double) and
  * the count of non-finite entries into nonfinite_dev[0] (int64, nullable). */
 int csc_sumsq(const void *x_dev, int64_t count, int dtype, double *out_dev,

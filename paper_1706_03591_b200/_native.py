@@ -41,6 +41,7 @@ SIGNATURES = {
     "csc_cheb_moments_keep": ([_P, _P, _I64, _I64, _I32, _P, _P, _P], _INT),
     "csc_cheb_combine": ([_P, _P, _I64, _I64, _I64, _PD, _I32, _P, _P, _P], _INT),
     "csc_sumsq": ([_P, _I64, _INT, _P, _P, _P], _INT),
+    "csc_copy2d_async": ([_P, _I64, _P, _I64, _I64, _I64, _P], _INT),
     "csc_set_tuning": ([ctypes.c_char_p, _I64], _INT),
     "csc_sweep_timing": ([_INT], _INT),
     "csc_sweep_times": ([ctypes.POINTER(ctypes.c_float), _INT, ctypes.POINTER(_INT)], _INT),

@@ -89,4 +89,14 @@ int csc_device_info(int *sm_count, int *cc_major, int *cc_minor) {
   return CSC_OK;
 }
 
+int csc_copy2d_async(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width_bytes,
+                     int64_t rows, void *stream) {
+  CSC_REQUIRE(rows >= 0 && width_bytes >= 0, "csc_copy2d_async: negative extent");
+  CSC_REQUIRE(dpitch >= width_bytes && spitch >= width_bytes, "csc_copy2d_async: pitch below width");
+  if (rows == 0 || width_bytes == 0) return CSC_OK;
+  CSC_TRY_CUDA(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width_bytes,
+                                 (size_t)rows, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return CSC_OK;
+}
+
 }  // extern "C"

@@ -729,3 +729,35 @@ def test_kmeans_zero_mass_replay_through_restarts(P):
         ref_labels, _, ref_cost = O.kmeans(f, 3, restarts=4, max_iters=20, tol=1e-6, seed=seed)
         assert np.array_equal(asg.labels, ref_labels)
         assert abs(asg.feature_cost - ref_cost) <= 1e-12 * max(ref_cost, 1.0)
+
+
+def test_filter_host_pipeline(P, monkeypatch):
+    """apply_filter's pinned-host pipeline (column chunks, copies overlapped with
+    the filter on a side stream) returns the device path's features and charges
+    the same matvecs."""
+    import torch
+    from paper_1706_03591_b200 import filters as PF
+    g = golden("cfg1")
+    lap = P.laplacian(graph_from(g, "g", P))
+    poly = P.cheb_coeffs(0.5, 2.0, 50)
+    x = torch.from_numpy(np.ascontiguousarray(g["R"], dtype=np.float64)).pin_memory().numpy()
+    monkeypatch.setattr(PF, "PIPE_MIN_BYTES", 0)
+    monkeypatch.setattr(PF, "PIPE_MIN_COLS", 4)
+    for chunks in (2, 3):
+        monkeypatch.setattr(PF, "PIPE_CHUNKS", chunks)
+        counter = P.MatvecCounter()
+        out = P.apply_filter(lap, poly, x, counter)
+        assert rel(out, g["filt_05"]) <= FEAT_TOL
+        assert counter.count == 50 * x.shape[1]
+    # a larger block: pipelined host result equals the device-tensor path
+    rng = np.random.default_rng(7)
+    n, d = 60000, 96
+    a, b = rng.integers(0, n, 8 * n), rng.integers(0, n, 8 * n)
+    pairs = np.unique(np.stack([np.minimum(a, b), np.maximum(a, b)], 1)[a != b], axis=0)
+    big = P.laplacian(P.Graph(n, pairs[:, 0], pairs[:, 1], rng.uniform(0.5, 2.0, len(pairs))))
+    poly = P.cheb_coeffs(0.7, big.lambda_max_bound, 40)
+    xb = torch.from_numpy(rng.normal(size=(n, d))).pin_memory()
+    monkeypatch.setattr(PF, "PIPE_CHUNKS", 2)
+    host = P.apply_filter(big, poly, xb.numpy())
+    dev = P.apply_filter(big, poly, xb.cuda()).cpu().numpy()
+    assert rel(host, dev) <= 1e-13

@@ -36,3 +36,21 @@ for rep in range(3):
     print(f"apply_filter {total:.1f} ms | upload {(t1 - t0) * 1e3:.1f} filter {(t2 - t1) * 1e3:.1f} "
           f"download {(t3 - t2) * 1e3:.1f} ms")
     del res, h, out, blk
+
+# host pipeline chunk counts (PIPE_CHUNKS = 1: the unpipelined path)
+from paper_1706_03591_b200 import filters as PF  # noqa: E402
+ref = P.apply_filter(lap, poly, torch.from_numpy(x_np).cuda()).cpu().numpy()
+for chunks in (1, 2, 3, 4):
+    PF.PIPE_CHUNKS = chunks
+    PF.PIPE_MIN_BYTES = 1 << 28 if chunks > 1 else 1 << 62
+    res = P.apply_filter(lap, poly, x_np)
+    torch.cuda.synchronize()
+    ts = []
+    for rep in range(3):
+        t0 = time.perf_counter()
+        res = P.apply_filter(lap, poly, x_np)
+        torch.cuda.synchronize()
+        ts.append((time.perf_counter() - t0) * 1e3)
+    err = float(np.abs(res - ref).max())
+    print(f"chunks {chunks}: apply_filter {min(ts):.1f} / {np.median(ts):.1f} ms (min / median), "
+          f"max |host - device| {err:.2e}")
