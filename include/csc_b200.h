@@ -97,6 +97,15 @@ int csc_chebop_destroy(csc_chebop *op);
 int csc_chebop_info(const csc_chebop *op, int64_t *n, int64_t *nnz, int64_t *n_long,
                     int64_t *n_segments);
 
+/* host outputs: *binned = 1 when the plan orders its rows by stored length
+ * (skewed degrees, e.g. configs[3]'s Chung-Lu graph: row groups of a warp
+ * then gather rows of similar length), and the squared coefficient of
+ * variation of M's row lengths the decision used (threshold 1.0; tuning key
+ * "row_binning"). Replaces nothing in the reference (SciPy's csr_matvecs,
+ * filters.py:176, walks rows in index order); results do not depend on it
+ * beyond the fixed per-row accumulation order. */
+int csc_chebop_schedule(const csc_chebop *op, int32_t *binned, double *len_cv2);
+
 /* copy the plan's M (CSR) and long-row schedule into caller buffers
  * (sizes from csc_chebop_info; any pointer may be NULL) — for tests/tools */
 int csc_chebop_export(const csc_chebop *op, int32_t *indptr_dev, int32_t *indices_dev,
@@ -141,7 +150,9 @@ int csc_cheb_combine(const void *x_dev, const void *keep_dev, int64_t n, int64_t
  *                  groups, more gathers in flight per lane (default 0 = 2 for rows
  *                  up to 512 B, else 1)
  *   "sweep_g"      force the row-group width (4, 8, 16, 32; default 0 = from
- *                  "vpl") */
+ *                  "vpl")
+ *   "row_binning"  row order of plans created afterwards: -1 auto (by the
+ *                  row-length CV^2), 0 index order, 1 length order */
 int csc_set_tuning(const char *key, int64_t value);
 
 /* Measurement hook: when enabled, every main sweep launch of csc_cheb_filter /

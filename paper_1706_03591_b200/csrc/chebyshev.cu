@@ -247,6 +247,10 @@ struct SweepArgs {
   const int32_t *indices;
   const void *vals;
   int64_t n;
+  // row schedule: nullptr = rows 0..n-1 in order (long rows skipped inside);
+  // else the nrows short rows in perm order (long rows already excluded)
+  const int32_t *perm;
+  int64_t nrows;
   int nvec;       // 16-byte vectors per row actually used (chunk width)
   int64_t ldv;    // row stride in 16-byte vectors
   const void *gat;   // T_j (gathered)
@@ -325,15 +329,31 @@ __device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
 #pragma unroll
         for (int q = 0; q < VPL; ++q) vfma(acc[q], a[t], x[t][q]);
     }
-    for (; u < cnt; ++u) {
-      const int c0 = __shfl_sync(gmask, my_col, u, G);
-      const T a0 = __shfl_sync(gmask, my_val, u, G);
-      const VT *src = gat + (int64_t)c0 * ldv;
+    if (u < cnt) {  // 1..3 remaining entries: their gathers issued together
+      const int rem = cnt - u;
+      int c[3];
+      T a[3];
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int v = glane + q * G;
-        if (v < nvec) vfma(acc[q], a0, __ldg(src + v));
+      for (int t = 0; t < 3; ++t) {
+        const int src_lane = min(u + t, cnt - 1);
+        c[t] = __shfl_sync(gmask, my_col, src_lane, G);
+        a[t] = __shfl_sync(gmask, my_val, src_lane, G);
       }
+      VT x[3][VPL];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const VT *src = gat + (int64_t)c[t] * ldv;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const int v = glane + q * G;
+          x[t][q] = (t < rem && v < nvec) ? __ldg(src + v) : vzero(VT());
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+        if (t < rem)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) vfma(acc[q], a[t], x[t][q]);
     }
   }
 }
@@ -382,9 +402,26 @@ __global__ void __launch_bounds__(kBlock, (SweepMinBlocks<G, VPL>::value)) sweep
   const uint64_t pol = make_policy(A.hint);
   const uint64_t pnear = make_gather_policy(1), pfar = make_gather_policy(0);
 
-  for (int64_t row = bid * groups_per_block + threadIdx.x / G; row < A.n; row += ngroups) {
-    const int beg = __ldg(A.indptr + row), end = __ldg(A.indptr + row + 1);
-    if (end - beg > kLongThr) continue;  // segment path
+  const int64_t nrows = A.perm ? A.nrows : A.n;
+  int64_t i = bid * groups_per_block + threadIdx.x / G;
+  // the row, and its extent, one grid stride ahead: the next row's indptr
+  // loads are in flight while this row gathers
+  int64_t nrow = 0;
+  int nbeg = 0, nend = 0;
+  if (i < nrows) {
+    nrow = A.perm ? __ldg(A.perm + i) : i;
+    nbeg = __ldg(A.indptr + nrow);
+    nend = __ldg(A.indptr + nrow + 1);
+  }
+  for (; i < nrows; i += ngroups) {
+    const int64_t row = nrow;
+    const int beg = nbeg, end = nend;
+    if (i + ngroups < nrows) {
+      nrow = A.perm ? __ldg(A.perm + i + ngroups) : i + ngroups;
+      nbeg = __ldg(A.indptr + nrow);
+      nend = __ldg(A.indptr + nrow + 1);
+    }
+    if (!A.perm && end - beg > kLongThr) continue;  // segment path
     VT acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = vzero(VT());
@@ -727,6 +764,33 @@ __global__ void sumsq_f32_kernel(const float4 *__restrict__ x4, int64_t nvec4,
   if (nonfinite && bad) atomicAdd(nonfinite, bad);
 }
 
+// sum and sum of squares of the row lengths (exact integer sums)
+__global__ void len_stats_kernel(const int32_t *__restrict__ counts, int64_t n,
+                                 unsigned long long *__restrict__ out) {
+  unsigned long long s1 = 0, s2 = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long c = (unsigned long long)counts[r];
+    s1 += c;
+    s2 += c * c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, s1);
+    atomicAdd(out + 1, s2);
+  }
+}
+
+__global__ void iota_kernel(int32_t *__restrict__ v, int64_t n) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    v[r] = (int32_t)r;
+}
+
 // mu from the per-order moment sums (see csc_cheb_moments):
 //   mu_{2j}   = 2 <T_j,T_j>     - mu_0
 //   mu_{2j+1} = 2 <T_{j+1},T_j> - mu_1
@@ -770,6 +834,12 @@ struct csc_chebop {
   int32_t *long_rows = nullptr;
   int32_t *seg_off = nullptr;
   int64_t n_long = 0, n_seg = 0;
+  // Skewed degrees: all rows ordered by stored length, longest first (stable),
+  // so the row groups of a warp gather rows of similar length; the first
+  // n_long entries are the segment path's rows. nullptr: rows in index order
+  // (the graph's own ordering keeps community gathers L2-local).
+  int32_t *perm = nullptr;
+  double len_cv2 = 0.0;  // squared coefficient of variation of the row lengths
   cudaStream_t stream = nullptr;  // last stream used (for stream-ordered free)
 };
 
@@ -807,6 +877,8 @@ int run_order_gv(const csc_chebop &op, SweepArgs A, int mode, double *partials,
   int grid = (int)std::min<int64_t>(sweep_grid<T, G, VPL>(),
                                     std::max<int64_t>(1, csc::ceil_div(op.n, groups_per_block)));
   A.partials = partials;
+  A.perm = op.perm ? op.perm + op.n_long : nullptr;
+  A.nrows = op.perm ? op.n - op.n_long : op.n;
   A.seg_blocks = 0;
   if (op.n_long > 0) {
     A.seg_blocks = (int)std::min<int64_t>(csc::device_info().sm_count * 4,
@@ -925,6 +997,21 @@ int run_order(const csc_chebop &op, const SweepArgs &A, int mode, double *partia
 constexpr int kMaxVecChunk = 256;  // widest row chunk one sweep handles
 
 int g_near = -1, g_hint = -1;
+int g_binning = -2;  // -1 auto, 0 off, 1 on (applied when a plan is created)
+
+int row_binning() {
+  if (g_binning == -2) {
+    const char *e = getenv("CSC_ROW_BINNING");
+    g_binning = e ? atoi(e) : -1;
+    if (g_binning < -1 || g_binning > 1) g_binning = -1;
+  }
+  return g_binning;
+}
+
+// Rows are ordered by length when the lengths vary widely: CV^2 of the stored
+// row lengths above this (Poisson-degree SBMs such as configs[2]/[4] sit near
+// 1/mean degree; the Chung-Lu configs[3] graph far above).
+constexpr double kBinCv2 = 1.0;
 int64_t g_chunk_vectors = -1;
 
 int near_window() {
@@ -1208,12 +1295,21 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
   if (sel_tmp.alloc(sel_bytes, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
   cub::DeviceSelect::If(sel_tmp.ptr, sel_bytes, rows_it, op->long_rows, nsel.as<int32_t>(), n,
                         pred, st);
+  // row-length statistics for the schedule decision
+  csc::Scratch stats;
+  if (stats.alloc(sizeof(unsigned long long) * 2, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
+  cudaMemsetAsync(stats.ptr, 0, sizeof(unsigned long long) * 2, st);
+  if (n > 0)
+    len_stats_kernel<<<grid, threads, 0, st>>>(counts.as<int32_t>(), n,
+                                               stats.as<unsigned long long>());
   // nsel[1] <- nnz(M) = indptr[n]; one copy of both counts
   int32_t cnt[2] = {0, 0};
+  unsigned long long lst[2] = {0, 0};
   if (cudaMemcpyAsync(nsel.as<int32_t>() + 1, op->indptr + n, sizeof(int32_t),
                       cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
       cudaMemcpyAsync(cnt, nsel.ptr, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, st) !=
           cudaSuccess ||
+      cudaMemcpyAsync(lst, stats.ptr, sizeof(lst), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess) {
     csc::set_error("csc_chebop_create: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(CSC_ERR_CUDA);
@@ -1240,6 +1336,28 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
       return fail(CSC_ERR_CUDA);
     op->n_seg = nseg;
   }
+  if (n > 0 && lst[0] > 0) {
+    const double mean = (double)lst[0] / (double)n;
+    op->len_cv2 = (double)lst[1] / (double)n / (mean * mean) - 1.0;
+  }
+  const int bin = row_binning();
+  if (n > 0 && (bin == 1 || (bin == -1 && op->len_cv2 > kBinCv2))) {
+    // stable descending sort of (length, row): longest rows first, ties in row order
+    csc::Scratch keys_out, ids, sort_tmp;
+    if (keys_out.alloc(sizeof(int32_t) * n, st) != cudaSuccess ||
+        ids.alloc(sizeof(int32_t) * n, st) != cudaSuccess ||
+        cudaMallocAsync((void **)&op->perm, sizeof(int32_t) * n, st) != cudaSuccess)
+      return fail(CSC_ERR_CUDA);
+    iota_kernel<<<grid, threads, 0, st>>>(ids.as<int32_t>(), n);
+    size_t sb = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, counts.as<int32_t>(),
+                                              keys_out.as<int32_t>(), ids.as<int32_t>(), op->perm,
+                                              (int)n, 0, 32, st);
+    if (sort_tmp.alloc(sb, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
+    cub::DeviceRadixSort::SortPairsDescending(sort_tmp.ptr, sb, counts.as<int32_t>(),
+                                              keys_out.as<int32_t>(), ids.as<int32_t>(), op->perm,
+                                              (int)n, 0, 32, st);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     csc::set_error("csc_chebop_create: %s", cudaGetErrorString(e));
@@ -1257,6 +1375,7 @@ int csc_chebop_destroy(csc_chebop *op) {
   if (op->vals) cudaFreeAsync(op->vals, st);
   if (op->long_rows) cudaFreeAsync(op->long_rows, st);
   if (op->seg_off) cudaFreeAsync(op->seg_off, st);
+  if (op->perm) cudaFreeAsync(op->perm, st);
   delete op;
   return CSC_OK;
 }
@@ -1290,6 +1409,13 @@ int csc_chebop_info(const csc_chebop *op, int64_t *n, int64_t *nnz, int64_t *n_l
   if (nnz) *nnz = op->nnz;
   if (n_long) *n_long = op->n_long;
   if (n_segments) *n_segments = op->n_seg;
+  return CSC_OK;
+}
+
+int csc_chebop_schedule(const csc_chebop *op, int32_t *binned, double *len_cv2) {
+  CSC_REQUIRE(op != nullptr, "csc_chebop_schedule: NULL plan");
+  if (binned) *binned = op->perm != nullptr ? 1 : 0;
+  if (len_cv2) *len_cv2 = op->len_cv2;
   return CSC_OK;
 }
 
@@ -1457,6 +1583,10 @@ int csc_set_tuning(const char *key, int64_t value) {
     CSC_REQUIRE(value == 0 || value == 4 || value == 8 || value == 16 || value == 32,
                 "sweep_g must be 0, 4, 8, 16 or 32");
     g_sweep_g = (int)value;
+  } else if (k == "row_binning") {
+    row_binning();
+    CSC_REQUIRE(value >= -1 && value <= 1, "row_binning must be -1 (auto), 0 or 1");
+    g_binning = (int)value;
   } else if (k == "stream_hint") {
     stream_hint();
     g_hint = value ? 1 : 0;

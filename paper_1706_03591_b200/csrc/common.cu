@@ -1,7 +1,6 @@
 // Library-level entry points and shared helpers.
 #include <mutex>
 #include <string>
-#include <vector>
 
 #include "common.cuh"
 
@@ -20,17 +19,18 @@ void set_error(const char *fmt, ...) {
 
 void clear_error() { g_last_error.clear(); }
 
+// Fixed-size table: references handed out stay valid when another thread
+// first touches a higher device id (a resized vector would move them).
+constexpr int kMaxDevices = 64;
+
 const DeviceInfo &device_info() {
   static std::mutex mu;
-  static std::vector<DeviceInfo> cache;
-  static std::vector<bool> pool_ready;
+  static DeviceInfo cache[kMaxDevices];
+  static bool pool_ready[kMaxDevices] = {};
   int dev = 0;
   cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
   std::lock_guard<std::mutex> lock(mu);
-  if ((int)cache.size() <= dev) {
-    cache.resize(dev + 1);
-    pool_ready.resize(dev + 1, false);
-  }
   DeviceInfo &info = cache[dev];
   if (info.sm_count == 0) {
     cudaDeviceGetAttribute(&info.sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -40,9 +40,13 @@ const DeviceInfo &device_info() {
     if (info.sm_count <= 0) info.sm_count = 148;
   }
   if (!pool_ready[dev]) {
+    // The stream-ordered pool keeps up to 2 GiB of freed scratch for reuse
+    // (per-call partials, segment buffers, k-means lanes) and returns the rest
+    // to the driver at synchronisation points, so it does not hold HBM that
+    // PyTorch's caching allocator needs.
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
+      uint64_t thr = 2ull << 30;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();

@@ -85,7 +85,7 @@ struct FusedArgs {
   // in-kernel k-means++ (kmeans.py:64-77), when kpp_first != nullptr
   const int64_t *kpp_first;  // [R] the restart's integers(n) draw
   const double *kpp_unif;    // [R][k-1] its random() draws
-  double *kpp_part;          // [R][G] block sums of the D^2 weights
+  double *kpp_part;          // [2][R][G] block sums of the D^2 weights (draw parity)
   double *kpp_w;             // [2][R][G][rows_max] blocks' D^2 weights (draw parity)
   double *kpp_pre;           // [2][R][G][rows_max] their in-block prefix sums
   int32_t *kpp_flag;         // [R] first j whose D^2 mass was 0 (host replays), else -1
@@ -862,7 +862,7 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
         if (i < nr) pr[i] = x;
         carry = __shfl_sync(0xffffffffu, x, 31);
       }
-      if (lane == 0) a.kpp_part[(int64_t)r * G + cta] = carry;
+      if (lane == 0) a.kpp_part[((int64_t)(j & 1) * R + r) * G + cta] = carry;
     }
     kmark(a, j, 1);
     grid_sync(a.bar, G);
@@ -871,7 +871,7 @@ __device__ void kmeanspp_phase(const FusedArgs &a, const Shared &s, const GShare
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
         const int c = 5 * lane + q;
-        p[q] = c < G ? __ldcg(a.kpp_part + (int64_t)r * G + c) : 0.0;
+        p[q] = c < G ? __ldcg(a.kpp_part + ((int64_t)(j & 1) * R + r) * G + c) : 0.0;
         sl += p[q];
         loc[q] = sl;
       }
@@ -1196,7 +1196,8 @@ bool fused_geometry(int64_t n, int64_t d, int64_t k, int64_t R, int max_iters, F
     return false;
   const csc::DeviceInfo &info = csc::device_info();
   const int64_t smem_cap = info.max_smem_optin > 0 ? info.max_smem_optin : 232448;
-  g.G = (int)std::max<int64_t>(1, std::min<int64_t>(info.sm_count, n / 16));
+  // the k-means++ pick reads the block sums as 5 per lane of one warp: G <= 160
+  g.G = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(info.sm_count, 5 * 32), n / 16));
   g.RM = (int)csc::ceil_div(n, g.G);
   g.ldf = (int)(d | 1);
   g.lds = (int)(d | 1);
@@ -1259,7 +1260,9 @@ int fused_launch(const char *who, const double *f, const double *fnorm, int64_t 
   const size_t b_ints = al(sizeof(int32_t) * (3 * R + 2 * R * k) + (2 + 2 * R) * sizeof(unsigned));
   const size_t b_kfirst = kpp ? al(sizeof(int64_t) * R) : 0;
   const size_t b_kunif = kpp ? al(sizeof(double) * R * std::max<int64_t>(1, k - 1)) : 0;
-  const size_t b_kpart = kpp ? al(sizeof(double) * R * G) : 0;
+  // double-buffered by draw parity: a block that leaves barrier j early writes
+  // draw j+1's sums while slower blocks still read draw j's
+  const size_t b_kpart = kpp ? al(sizeof(double) * 2 * R * G) : 0;
   const size_t b_kpick = kpp ? al(sizeof(double) * 4 * R * G * g.RM) : 0;
   csc::Scratch ws;
   CSC_TRY_CUDA(ws.alloc(b_cent + b_kvec + b_psum + b_cpart + b_pq + b_cterm + b_stop + b_hist + b_own +

@@ -16,10 +16,23 @@
 // and a second pass writes them. Each chunk also reports its first output
 // start at/after its own start and at/after its end; neighbouring chunks
 // must agree (checked on device), otherwise the column is flagged and the
-// caller regenerates it on the host. Uniform/exp/log1p paths use the
-// device's libm: wedge decisions and tail values can differ from glibc only
-// in the last ulp (tail samples, |x| > 3.65, ~3e-4 of draws).
+// caller regenerates it on the host.
+//
+// Bit-exactness of the tail and wedge. numpy calls the C library's log1p
+// (npy_log1p) in the tail loop; on x86-64 with FMA, glibc 2.39 dispatches to
+// its FMA build of the fdlibm log1p. glibc_log1p below restates that
+// published algorithm (argument reduction 1+x = 2^k (1+f), s = f/(2+f),
+// log(1+f) = 2s + s R(s^2) with the fdlibm Lp1..Lp7 minimax coefficients,
+// R evaluated in the split form z*Lp1 + z^2 (Lp2 + z Lp3) + z^4 (...) + z^6
+// (...)) with every fused multiply-add placed where that build has one and
+// all other operations in non-contractible _rn intrinsics; it equals the
+// host log1p bit for bit (1e8 inputs over (-1, 0] and arbitrary doubles,
+// tools/log1p_check.c). The wedge test and the tail arithmetic use _rn
+// intrinsics too (numpy's build has no FMA there). exp() in the wedge test
+// only decides a comparison, whose outcome could differ only for a left side
+// within one ulp of exp (probability ~1e-16 per wedge draw).
 #include <cub/cub.cuh>
+#include <math_constants.h>
 
 #include <vector>
 
@@ -76,6 +89,85 @@ struct Pcg {
   }
 };
 
+// glibc's log1p (fdlibm algorithm, FMA build) restated; see the header.
+__device__ __forceinline__ int32_t hi_word(double x) {
+  return (int32_t)(__double_as_longlong(x) >> 32);
+}
+__device__ __forceinline__ double with_hi_word(double x, int32_t h) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return __longlong_as_double((long long)((u & 0xffffffffull) | ((unsigned long long)(uint32_t)h << 32)));
+}
+
+__device__ __noinline__ double glibc_log1p(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double two54 = 1.80143985094819840000e+16;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01,
+               Lp3 = 2.857142874366239149e-01, Lp4 = 2.222219843214978396e-01,
+               Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  double f = 0.0, c = 0.0, u;
+  int32_t k = 1, hu = 0;
+  const int32_t hx = hi_word(x), ax = hx & 0x7fffffff;
+  if (hx < 0x3FDA827A) {  // 1 + x < sqrt(2)
+    if (ax >= 0x3ff00000) return x == -1.0 ? -CUDART_INF : CUDART_NAN;
+    if (ax < 0x3e200000) {  // |x| < 2^-29
+      if (__dadd_rn(two54, x) > 0.0 && ax < 0x3c900000) return x;
+      return fma(-__dmul_rn(x, x), 0.5, x);
+    }
+    if (hx > 0 || hx <= (int32_t)0xbfd2bec3) {  // -0.2929 < x < 0.41422
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  }
+  if (hx >= 0x7ff00000) return __dadd_rn(x, x);
+  if (k != 0) {
+    if (hx < 0x43400000) {
+      u = __dadd_rn(1.0, x);
+      hu = hi_word(u);
+      k = (hu >> 20) - 1023;
+      c = (k > 0) ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+      c = __ddiv_rn(c, u);
+    } else {
+      u = x;
+      hu = hi_word(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = with_hi_word(u, hu | 0x3ff00000);
+    } else {
+      k += 1;
+      u = with_hi_word(u, hu | 0x3fe00000);
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+  const double dk = (double)k;
+  if (hu == 0) {  // |f| < 2^-20
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      c = fma(dk, ln2_lo, c);
+      return fma(dk, ln2_hi, c);
+    }
+    const double R = __dmul_rn(fma(-f, 0.66666666666666666, 1.0), hfsq);
+    if (k == 0) return __dsub_rn(f, R);
+    return fma(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, fma(dk, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+  const double z = __dmul_rn(s, s);
+  const double R2 = fma(Lp3, z, Lp2), R3 = fma(Lp5, z, Lp4), R4 = fma(Lp7, z, Lp6);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z4, z2);
+  double R = fma(z, Lp1, __dmul_rn(z2, R2));
+  R = fma(z4, R3, R);
+  R = fma(z6, R4, R);
+  const double t = __dmul_rn(s, __dadd_rn(R, hfsq));
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
+  return fma(dk, ln2_hi, -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(fma(dk, ln2_lo, c), t)), f));
+}
+
 // one standard normal; `pos` counts consumed draws
 __device__ __forceinline__ double zig_normal(Pcg &g, int64_t &pos, const double *W,
                                              const unsigned long long *K, const double *F) {
@@ -91,15 +183,18 @@ __device__ __forceinline__ double zig_normal(Pcg &g, int64_t &pos, const double 
     if (rabs < K[idx]) return x;
     if (idx == 0) {
       for (;;) {
-        const double xx = -ZIG_INV_R * log1p(-g.next_double());
-        const double yy = -log1p(-g.next_double());
+        const double xx = __dmul_rn(-ZIG_INV_R, glibc_log1p(-g.next_double()));
+        const double yy = -glibc_log1p(-g.next_double());
         pos += 2;
-        if (yy + yy > xx * xx) return ((rabs >> 8) & 1) ? -(ZIG_R + xx) : ZIG_R + xx;
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx))
+          return ((rabs >> 8) & 1) ? -__dadd_rn(ZIG_R, xx) : __dadd_rn(ZIG_R, xx);
       }
     }
     const double u = g.next_double();
     ++pos;
-    if ((F[idx - 1] - F[idx]) * u + F[idx] < exp(-0.5 * x * x)) return x;
+    if (__dadd_rn(__dmul_rn(__dsub_rn(F[idx - 1], F[idx]), u), F[idx]) <
+        exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
+      return x;
   }
 }
 

@@ -25,8 +25,6 @@ from . import _native
 from ._device import dtype_code, ptr, require_cuda, stream
 
 LAPLACIAN_VARIANTS = ("combinatorial", "normalized")
-# graphs at least this large are canonicalised on the GPU when one is present
-DEVICE_CANON_MIN_EDGES = 1 << 16
 
 
 class Graph:
@@ -34,8 +32,10 @@ class Graph:
 
     Construction canonicalizes endpoint order, sorts edges by code i*n+j and
     rejects self-loops, duplicates, nonpositive weights and out-of-range
-    indices (graphs.py:29-54). Graphs produced by ``apply_delta`` hold their
-    edges on the GPU and materialise the host arrays only when asked.
+    indices (graphs.py:29-54) — on the GPU (csc_graph_canonicalize: validation
+    flags, stable radix sort of the codes, duplicate scan), for every non-empty
+    edge list. The graph then holds its edges on the GPU and materialises the
+    host arrays only when asked.
     """
 
     def __init__(self, n: int, edge_i, edge_j, edge_w):
@@ -46,25 +46,10 @@ class Graph:
         w = np.asarray(edge_w, dtype=np.float64).ravel()
         if not (i.shape == j.shape == w.shape):
             raise ValueError("edge arrays must have equal length")
-        if i.size >= DEVICE_CANON_MIN_EDGES and torch.cuda.is_available():
+        if i.size:  # K9 runs on the GPU (no CPU fallback: raises without CUDA)
             self._canonicalize_on_device(int(n), i, j, w)
             return
-        if i.size:
-            if i.min() < 0 or j.min() < 0 or max(i.max(), j.max()) >= n:
-                raise ValueError("edge endpoint out of range [0, n)")
-            if np.any(i == j):
-                raise ValueError("self-loops are not allowed")
-            if np.any(w <= 0):
-                raise ValueError("edge weights must be positive")
-            lo = np.minimum(i, j)
-            hi = np.maximum(i, j)
-            code = lo * n + hi
-            order = np.argsort(code, kind="stable")
-            code = code[order]
-            if code.size > 1 and np.any(code[1:] == code[:-1]):
-                raise ValueError("duplicate edges (after canonicalizing endpoint order)")
-            i, j, w = lo[order], hi[order], w[order]
-        self._init(int(n), i, j, w, None, int(i.size))
+        self._init(int(n), i, j, w, None, 0)
 
     def _canonicalize_on_device(self, n, i, j, w):
         """K9 on the GPU: validation flags, stable radix sort of the codes, duplicate check."""
@@ -234,6 +219,9 @@ class _ChebPlan:
     def __init__(self, handle, n, nnz, n_long, n_seg, dtype):
         self.handle, self.n, self.nnz, self.n_long, self.n_seg, self.dtype = \
             handle, n, nnz, n_long, n_seg, dtype
+        b, cv2 = ctypes.c_int32(0), ctypes.c_double(0.0)
+        _native.call("csc_chebop_schedule", handle, ctypes.byref(b), ctypes.byref(cv2))
+        self.binned, self.len_cv2 = bool(b.value), float(cv2.value)
 
     def __del__(self):
         h = getattr(self, "handle", None)

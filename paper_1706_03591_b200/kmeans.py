@@ -534,11 +534,22 @@ def _kmeans_prepared(blk, d: int, k: int, cfg: KmeansConfig, children, draws) ->
 
 def kmeans_cost(f, assignment: Assignment) -> float:
     """Cost ||F - X X^T F||_F of an existing assignment, in centroid form."""
+    labels = np.asarray(assignment.labels)
+    # the device kernels index shared memory and centroids by label: check the
+    # range on the host first, with the reference's exception types
+    # (np.bincount raises ValueError on negatives, np.add.at IndexError past k;
+    # kmeans.py:80-85)
+    if labels.ndim != 1 or (labels.size and not np.issubdtype(labels.dtype, np.integer)):
+        raise ValueError("assignment labels must be a 1-D integer array")
+    if labels.size and labels.min() < 0:
+        raise ValueError("'list' argument must have no negative elements")
+    if labels.size and labels.max() >= assignment.k:
+        raise IndexError(f"index {int(labels.max())} is out of bounds for axis 0 with size {assignment.k}")
     blk, d = _features_block(f)
     if blk.shape[0] != assignment.n:
         raise ValueError("feature rows and assignment length differ")
     ws = _Workspace(blk, d, assignment.k)
-    ws.labels.copy_(torch.from_numpy(np.asarray(assignment.labels, dtype=np.int32)))
+    ws.labels.copy_(torch.from_numpy(labels.astype(np.int32)))
     s = stream()
     _native.call("csc_kmeans_update", ptr(blk), ptr(ws.labels), ws.n, d, ws.ld, ws.k, ptr(ws.cent), ws.ldc,
                  ptr(ws.cnorm), ptr(ws.counts), s)

@@ -79,6 +79,9 @@ def random_signals(n: int, d: int, seed=0, scale_dim: int | None = None) -> np.n
 # "device": PCG64 + ziggurat on the GPU (csc_normal_columns); "host": numpy in
 # a thread pool + H2D (bit-exact by construction). CSC_RNG=host selects the latter.
 RNG_MODE = os.environ.get("CSC_RNG", "device")
+# columns the device generator flagged (chunk boundaries that did not agree)
+# and the host regenerated; reported by bench.py, asserted zero in the tests
+RNG_STATS = {"device_columns": 0, "redrawn_columns": 0}
 
 
 def _u32_words(x) -> list[int]:
@@ -158,7 +161,10 @@ def device_signals(n: int, d: int, seed=0, scale_dim: int | None = None, mode: s
             ss.spawn(d)
         sigma = 1.0 / np.sqrt(dim)
 
+        RNG_STATS["device_columns"] += d
+
         def redraw(bad):  # flagged columns: the exact host generator
+            RNG_STATS["redrawn_columns"] += int(np.count_nonzero(bad))
             for c in np.flatnonzero(bad):
                 child = np.random.SeedSequence(ss.entropy, spawn_key=tuple(ss.spawn_key) + (base + int(c),),
                                                pool_size=ss.pool_size)

@@ -597,12 +597,30 @@ def test_graph_lloyd_equals_host_driven(P):
     assert np.array_equal(labels, g["b_labels"])
 
 
+def test_graph_small_canonical_order(P):
+    """Small graphs are canonicalised on the device too (no host branch)."""
+    g = P.Graph(4, [2, 0, 3], [0, 1, 1], [1.0, 2.0, 3.0])
+    assert g._i is None  # built on the device
+    assert g.edge_i.tolist() == [0, 0, 1] and g.edge_j.tolist() == [1, 2, 3]
+    assert g.edge_w.tolist() == [2.0, 1.0, 3.0]
+    assert g.m == 3 and np.array_equal(g.edge_codes(), [1, 2, 7])
+    assert np.array_equal(g.degrees, [3.0, 5.0, 1.0, 3.0])
+    for bad in [(4, [0], [0], [1.0]), (4, [0], [5], [1.0]), (4, [0], [1], [0.0]),
+                (4, [0, 1], [1, 0], [1.0, 1.0]), (4, [0, 1], [1], [1.0]), (-1, [], [], [])]:
+        with pytest.raises(ValueError):
+            P.Graph(*bad)
+    with pytest.raises(AttributeError):
+        g.n = 5
+    assert P.graphs_equal(g, P.Graph(4, [0, 2, 1], [1, 0, 3], [2.0, 1.0, 3.0]))
+    e = P.Graph(5, [], [], [])
+    assert e.m == 0 and P.laplacian(e).nnz == 0
+
+
 def test_graph_device_canonicalisation(P):
     """K9 on device (graphs.py:29-54): same canonical order, weights and errors as the reference."""
-    from paper_1706_03591_b200.graphs import DEVICE_CANON_MIN_EDGES
     rng = np.random.default_rng(11)
     n = 50000
-    m = DEVICE_CANON_MIN_EDGES * 3
+    m = 3 << 16
     a = rng.integers(0, n, m)
     b = rng.integers(0, n, m)
     ok = a != b
