@@ -11,6 +11,20 @@ Chebyshev order m=100. One step = one apply_filter (100 fused SpMM sweeps) of
 the device-resident block. Inputs (1 GB signals + 2 GB recurrence buffers)
 exceed the 126 MB L2, so no explicit flush is needed between steps.
 
+Also on the same line (each untimed by the headline's clock):
+  * e2e: the public apply_filter with host numpy in / numpy out, pinned
+    (the contract's headline e2e) and pageable (an ordinary numpy array), >= 5
+    calls each;
+  * variants.fp32 (cfg3) and variants.cfg4_fp32 / cfg4_fp64 (BASELINE
+    configs[3]: Chung-Lu n = 4M, skewed degrees, d = 64, m = 80): throughput,
+    sweep roofline on the minimum bytes, fp32 error vs fp64;
+  * dynamic (configs[1]) and dynamic_cfg5 (configs[4], p = 0.5, 1% churn):
+    ms per step with the host insert/delete lists merged on the device inside
+    the timed step, phase split, and one refined step;
+  * cpu_baseline: the C restatement on all host cores (the `--impl reference`
+    arm) and the unmodified reference's own apply_filter (SciPy, installed in
+    baseline/_ref) on the same sample.
+
 Multi-GPU (torchrun): the filter shards by columns with no exchange
 (filters.py:159-161); every rank filters its own d=128 block of the same
 graph ("scaling": "weak"), time = max over ranks.
@@ -23,6 +37,7 @@ orders per step, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -41,26 +56,31 @@ WORKLOADS = {
     "cfg1": dict(n=1000, k=10, deg=19.62, ratio=1 / 90, d=40, order=50, cutoff=0.5, seed=0),
     "cfg5": dict(n=2_000_000, k=64, deg=20.0, ratio=0.05, d=96, order=80, cutoff=0.05, seed=5),
 }
+CFG4 = dict(n=4_000_000, k=50, deg=16.0, exponent=2.3, max_degree=20000.0, ratio=0.05, d=64, order=80,
+            cutoff=0.05, seed=4)
 METRIC = "filtered nnz*d*order/s"
 UNIT = "nnz*d*order/s"
 
 
-def ncu_traffic(workload: str, precision: str):
-    """DRAM bytes per sweep launch (read + write) from the committed ncu capture of
-    this workload (profiles/r01_sweep_<workload>_<precision>_dram.csv), or None."""
-    path = os.path.join(ROOT, "profiles", f"r01_sweep_{workload}_{precision}_dram.csv")
+def traffic_capture(workload: str, precision: str):
+    """The committed ncu capture of this workload's sweep: DRAM bytes per launch
+    plus the kernel instance, grid and commit it was taken of
+    (profiles/r02_sweep_<workload>_<precision>.json, written by
+    tools/capture_traffic.py), or None."""
+    path = os.path.join(ROOT, "profiles", f"r02_sweep_{workload}_{precision}.json")
     if not os.path.exists(path):
-        return None, None
-    import csv
-    per = {}
+        return None
     with open(path) as fh:
-        for r in csv.DictReader(ln for ln in fh if not ln.startswith("==")):
-            if r["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[r["Metric Unit"]]
-                per[r["ID"]] = per.get(r["ID"], 0.0) + float(r["Metric Value"].replace(",", "")) * scale
-    if not per:
-        return None, None
-    return float(np.mean(list(per.values()))), os.path.relpath(path, ROOT)
+        cap = json.load(fh)
+    cap["source"] = os.path.relpath(path, ROOT)
+    return cap
+
+
+def last_launch(lib):
+    buf = ctypes.create_string_buffer(128)
+    grid = ctypes.c_int(0)
+    lib.csc_sweep_last_launch(buf, 128, ctypes.byref(grid))
+    return buf.value.decode(), int(grid.value)
 
 
 def peaks():
@@ -76,6 +96,12 @@ def make_graph_codes(w):
     from paper_1706_03591_b200 import generators as G
     q1, q2 = G.sbm_probabilities(w["n"], w["k"], w["deg"], w["ratio"])
     return G.planted_partition_codes(w["n"], w["k"], q1, q2, w["seed"]), (q1, q2)
+
+
+def b_min(n, nnz, d, s):
+    """SURVEY 8(d) minimum bytes of one sweep: CSR (indptr, indices, values),
+    one gathered d-row per stored entry, the written T_{j+1} rows."""
+    return 4 * (n + 1) + nnz * (4 + s) + nnz * d * s + n * d * s
 
 
 class ClockSampler:
@@ -144,6 +170,28 @@ def cpu_filter_sample(indptr, indices, data, r, coeffs, orders=2, threads=0):
     return time.perf_counter() - t0, (threads or ON.num_threads())
 
 
+def reference_scipy_sample(matrix, r, coeffs, orders=2):
+    """Time `orders` SpMM blocks of the UNMODIFIED reference's apply_filter
+    (cscluster from baseline/_ref: SciPy csr_matvecs, single-threaded), or None
+    when the reference is not installed."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "cscluster")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    try:
+        import cscluster as cc
+        from cscluster.graphs import LaplacianMatrix as RefLap
+    except Exception:
+        return None
+    lap = RefLap(matrix, "normalized", 2.0)
+    c = np.ascontiguousarray(coeffs[: orders + 1])
+    poly = cc.FilterPoly(orders, c, 0.05, 2.0, "jackson")
+    t0 = time.perf_counter()
+    cc.apply_filter(lap, poly, r)
+    return time.perf_counter() - t0
+
+
 def workload_desc(name, w, n, d, order):
     """config.workload of both arms (the same string)."""
     return (f"{name}: planted partition n={n} k={w['k']} mean degree {w['deg']} p_out/p_in={w['ratio']:.4g}; "
@@ -185,10 +233,88 @@ def run_reference(args, w, rank):
     print(json.dumps(line), flush=True)
 
 
+def sweep_times(lib):
+    buf = (ctypes.c_float * 4096)()
+    cnt = ctypes.c_int(0)
+    lib.csc_sweep_times(buf, 4096, ctypes.byref(cnt))
+    return np.array(buf[: cnt.value], dtype=np.float64)
+
+
+def timed_filter(lap, poly, blk, d, out, work, reps, lib):
+    """(ms per filter by CUDA events on the launching stream, per-sweep ms)."""
+    import torch
+    from paper_1706_03591_b200.filters import filter_block
+    filter_block(lap, poly, blk, d, out=out, work=work)
+    torch.cuda.synchronize()
+    lib.csc_sweep_timing(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        filter_block(lap, poly, blk, d, out=out, work=work)
+    e1.record()
+    torch.cuda.synchronize()
+    lib.csc_sweep_timing(0)
+    return e0.elapsed_time(e1) / reps, sweep_times(lib)
+
+
+def run_cfg4(hbm, lib):
+    """BASELINE configs[3]: skewed-degree Chung-Lu graph, fp32 primary with an fp64 check."""
+    import torch
+    import paper_1706_03591_b200 as P
+    from paper_1706_03591_b200 import generators as G
+    from paper_1706_03591_b200._device import row_stride
+    from paper_1706_03591_b200.signals import device_signals
+    w = CFG4
+    t0 = time.perf_counter()
+    g, _ = G.chung_lu_sbm(w["n"], w["k"], w["deg"], w["exponent"], w["max_degree"], w["ratio"], seed=w["seed"])
+    gen_s = time.perf_counter() - t0
+    lap = P.laplacian(g)
+    n, d, order, nnz = w["n"], w["d"], w["order"], lap.nnz
+    poly = P.cheb_coeffs(w["cutoff"], lap.lambda_max_bound, order)
+    x64 = device_signals(n, d, w["seed"])
+    res = {"workload": (f"configs[3]: Chung-Lu / degree-corrected SBM n={n} k={w['k']} power-law exponent "
+                        f"{w['exponent']} mean degree {w['deg']} max ~{int(w['max_degree'])} "
+                        f"p_out/p_in={w['ratio']}; d={d}; Chebyshev order {order}"),
+           "n": n, "nnz_L": int(nnz), "d": d, "order": order, "graph_gen_s": round(gen_s, 1)}
+    outs = {}
+    for prec, dt in (("fp32", torch.float32), ("fp64", torch.float64)):
+        plan = lap.plan(1.0, dt)
+        ld = row_stride(d, dt)
+        blk = torch.zeros((n, ld), dtype=dt, device=x64.device)
+        blk[:, :d].copy_(x64[:, :d])
+        out = torch.empty_like(blk)
+        work = torch.empty((2 * n, ld), dtype=dt, device=blk.device)
+        ms, sw = timed_filter(lap, poly, blk, d, out, work, 2, lib)
+        s = 8 if dt == torch.float64 else 4
+        bm = b_min(n, nnz, d, s)
+        sweep_ms = float(sw.mean())
+        name, grid = last_launch(lib)
+        entry = {"value": nnz * d * order / (ms / 1e3), "ms_per_step": ms, "sweep_ms_mean": sweep_ms,
+                 "roofline_frac": bm / (sweep_ms / 1e3) / 1e9 / hbm, "bytes_min_per_launch": int(bm),
+                 "schedule": "length_order" if plan.binned else "index_order",
+                 "row_length_cv2": round(plan.len_cv2, 2), "long_rows": int(plan.n_long),
+                 "kernel": name, "grid": grid}
+        cap = traffic_capture("cfg4", prec)
+        if cap is not None:
+            entry["traffic"] = cap.get("dram_bytes_per_launch")
+            entry["dram_frac"] = cap.get("dram_bytes_per_launch", 0) / (sweep_ms / 1e3) / 1e9 / hbm
+            entry["traffic_source"] = cap["source"]
+            entry["traffic_capture_matches"] = cap.get("kernel") == name and cap.get("grid") == grid
+        res[prec] = entry
+        outs[prec] = out[:, :d].double()
+        del blk, work
+    res["fp32_rel_frobenius_vs_fp64"] = float((outs["fp32"] - outs["fp64"]).norm() / outs["fp64"].norm())
+    del outs, x64, lap
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_dynamic(args, rank):
     """ms per dynamic-CSC step on BASELINE configs[1]: SBM n=20k, k=20, mean degree 24,
     p_out/p_in=0.05, T=10 steps; each step moves 0.5% of nodes to another block
-    (perturb_nodes) and then rewires 1% of edges (perturb_edges); d=80, p=0.5, m=60."""
+    (perturb_nodes) and then rewires 1% of edges (perturb_edges); d=80, p=0.5, m=60.
+    The timed step includes merging that step's host insert/delete lists into the
+    device edge set (Graph.apply_delta -> csc_edge_delta)."""
     import torch
     import paper_1706_03591_b200 as P
     from paper_1706_03591_b200 import generators as G
@@ -196,43 +322,64 @@ def run_dynamic(args, rank):
     q1, q2 = G.sbm_probabilities(n, k, 24.0, 0.05)
     codes = G.planted_partition_codes(n, k, q1, q2, 7)
     labels = np.repeat(np.arange(k), G.block_sizes(n, k))
-    g = G.graph_from_codes(n, codes)
-    graphs = [g]
+    g0 = G.graph_from_codes(n, codes)
     cur = codes
     steps = 10
 
     def applied(c, dl, il):
         return np.union1d(np.setdiff1d(c, dl, assume_unique=True), il)
 
+    deltas = []
     for t in range(1, steps):  # nodes first, then edges
         dn, inn, labels = G.node_switch(cur, n, labels, k, q1, q2, 0.005, seed=200 + t)
         cur = applied(cur, dn, inn)
         de, ie = G.edge_churn(cur, n, labels, q1, q2, 0.01, seed=100 + t)
-        graphs.append(graphs[-1].apply_delta(dn, inn).apply_delta(de, ie))
         cur = applied(cur, de, ie)
+        deltas.append((dn, inn, de, ie))
     cfg = P.DynamicConfig(k=k, d=d, p=0.5, filter=P.FilterConfig(order=60))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    _, state, diag0 = P.dynamic_init(graphs[0], cfg, seed=rank)
+    _, state, diag0 = P.dynamic_init(g0, cfg, seed=rank)
+    torch.cuda.synchronize()
     init_ms = (time.perf_counter() - t0) * 1e3
     ms, phases, refined = [], {}, 0
-    for gt in graphs[1:]:
+    g = g0
+    for dn, inn, de, ie in deltas:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _, state, diag = P.dynamic_step(state, gt, cfg, timings=phases)
+        g = g.apply_delta(dn, inn).apply_delta(de, ie)  # host lists -> device merge
+        t1 = time.perf_counter()
+        _, state, diag = P.dynamic_step(state, g, cfg, timings=phases)
         torch.cuda.synchronize()
-        ms.append((time.perf_counter() - t0) * 1e3)
+        t2 = time.perf_counter()
+        ms.append((t2 - t0) * 1e3)
+        phases["edge_delta"] = phases.get("edge_delta", 0.0) + (t1 - t0) * 1e3
         refined += diag.refined
+    # one refined step: the communities split (k 20 -> 26 planted blocks), the
+    # validation eigencount leaves the tolerance band and the cutoff is re-bisected
+    q1s, q2s = G.sbm_probabilities(n, 26, 24.0, 0.05)
+    g_split = G.graph_from_codes(n, G.planted_partition_codes(n, 26, q1s, q2s, 9))
+    g_split.device_codes()
+    ph = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, _, diag_r = P.dynamic_step(state, g_split, cfg, timings=ph)
+    torch.cuda.synchronize()
+    refine_sample = {"ms": (time.perf_counter() - t0) * 1e3, "refined": bool(diag_r.refined),
+                     "search_iters": diag_r.search_iters, "phase_ms": {k2: round(v, 3) for k2, v in ph.items()},
+                     "graph": "SBM with 26 planted blocks (communities split); whole new edge set, not a delta"}
     out = {"workload": "configs[1] / cfg2: SBM n=20000 k=20 mean degree 24 p_out/p_in=0.05, T=10 (init + 9 steps), "
                        "per step 0.5% of nodes switch block then 1% of edges rewired; d=80 p=0.5 m=60, "
-                       "k-means k=20 x 10 restarts", "ms_per_step": statistics.median(ms),
+                       "k-means k=20 x 10 restarts; the step's insert/delete lists are merged on the device "
+                       "inside the timed step", "ms_per_step": statistics.median(ms),
            "steps_timed": len(ms), "init_ms": init_ms, "refined_steps": refined,
-           "phase_ms_total": {k2: round(v, 3) for k2, v in phases.items()}}
+           "phase_ms_total": {k2: round(v, 3) for k2, v in phases.items()},
+           "refined_step": refine_sample}
     if rank == 0 and not args.no_cpu_baseline:
         # bounded CPU sample: one dynamic step through the oracle (C-port filter + numpy k-means)
         from oracle import csc_oracle as O
         from oracle import native as ON
-        lap = P.laplacian(graphs[1])
+        lap = P.laplacian(g)
         m = lap.matrix
         r = O.random_signals(n, 40, 1, scale_dim=d)
         coeffs = state.filter.coeffs
@@ -246,6 +393,66 @@ def run_dynamic(args, rank):
     return out
 
 
+def run_dynamic_cfg5(args, rank, steps=4):
+    """BASELINE configs[4] at p = 0.5 and 1% edge churn: planted partition n=2M,
+    k=64, mean degree 20, p_out/p_in=0.05 (unspecified in BASELINE),
+    d=96, m=80, fp64, k-means k=64 x 10 restarts. Timed step = device merge of
+    the host insert/delete lists + dynamic_step (CSR rebuild, fresh signals,
+    validation filter, (refine), Theta, k-means)."""
+    import torch
+    import paper_1706_03591_b200 as P
+    from paper_1706_03591_b200 import generators as G
+    w = WORKLOADS["cfg5"]
+    n, k, d = w["n"], w["k"], w["d"]
+    q1, q2 = G.sbm_probabilities(n, k, w["deg"], w["ratio"])
+    codes = G.planted_partition_codes(n, k, q1, q2, w["seed"])
+    labels = np.repeat(np.arange(k), G.block_sizes(n, k))
+    g = G.graph_from_codes(n, codes)
+    deltas, cur = [], codes
+    for s in range(steps):
+        dl, il = G.edge_churn(cur, n, labels, q1, q2, 0.01, seed=50 + s)
+        deltas.append((dl, il))
+        cur = np.union1d(np.setdiff1d(cur, dl, assume_unique=True), il)
+    cfg = P.DynamicConfig(k=k, d=d, p=0.5, filter=P.FilterConfig(order=w["order"]))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, state, diag0 = P.dynamic_init(g, cfg, seed=rank)
+    torch.cuda.synchronize()
+    init_ms = (time.perf_counter() - t0) * 1e3
+    ms, phases, refined = [], {}, 0
+    for dl, il in deltas:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g = g.apply_delta(dl, il)
+        t1 = time.perf_counter()
+        _, state, diag = P.dynamic_step(state, g, cfg, timings=phases)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        ms.append((t2 - t0) * 1e3)
+        phases["edge_delta"] = phases.get("edge_delta", 0.0) + (t1 - t0) * 1e3
+        refined += diag.refined
+    return {"workload": (f"configs[4] / cfg5: planted partition n={n} k={k} mean degree {w['deg']} "
+                         f"p_out/p_in={w['ratio']}; d={d} p=0.5 m={w['order']} fp64; 1% edge churn per step "
+                         f"(insert/delete lists merged on the device inside the timed step); "
+                         f"k-means k={k} x 10 restarts"),
+            "ms_per_step": statistics.median(ms), "ms_all": [round(v, 1) for v in ms], "steps_timed": len(ms),
+            "init_ms": init_ms, "init_search_iters": diag0.search_iters, "refined_steps": refined,
+            "phase_ms_mean": {k2: round(v / len(ms), 2) for k2, v in phases.items()}}
+
+
+def e2e_calls(P, lap, poly, x_np, precision, calls):
+    """Mean seconds per public apply_filter call (host numpy in, host numpy out)."""
+    import torch
+    for _ in range(2):  # steady state holds the previous result while the next call runs
+        res = P.apply_filter(lap, poly, x_np, precision=precision)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(calls):
+        res = P.apply_filter(lap, poly, x_np, precision=precision)
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / calls, res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -257,6 +464,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dynamic", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-cfg4", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.workload]
@@ -270,6 +479,7 @@ def main():
     import torch.distributed as dist
     import paper_1706_03591_b200 as P
     from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200 import signals as S
     from paper_1706_03591_b200._device import row_stride
     from paper_1706_03591_b200.filters import filter_block
     from paper_1706_03591_b200 import generators as G
@@ -314,10 +524,8 @@ def main():
         end.record()
         torch.cuda.synchronize()
     lib.csc_sweep_timing(0)
-    buf = (__import__("ctypes").c_float * 4096)()
-    cnt = __import__("ctypes").c_int(0)
-    lib.csc_sweep_times(buf, 4096, __import__("ctypes").byref(cnt))
-    sweeps = np.array(buf[: cnt.value], dtype=np.float64)
+    sweeps = sweep_times(lib)
+    launch_name, launch_grid = last_launch(lib)
     ms = start.elapsed_time(end) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -329,74 +537,60 @@ def main():
 
     # roofline of the dominant kernel (the fused sweep), algorithmic bytes per launch
     s = 8 if dtype == torch.float64 else 4
-    b_min = 4 * (n + 1) + nnz_L * (4 + s) + nnz_L * d * s + n * d * s
-    b_full = b_min + 3 * n * d * s
+    bm = b_min(n, nnz_L, d, s)
+    b_full = bm + 3 * n * d * s
     hbm, peak_kind = peaks()
     sweep_ms = float(sweeps.mean()) if sweeps.size else ms / order
-    achieved = b_min / (sweep_ms / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic(args.workload, args.precision)
+    achieved = bm / (sweep_ms / 1e3) / 1e9
+    cap = traffic_capture(args.workload, args.precision)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
-                "kernel": "sweep_kernel (fused SpMM + recurrence)",
+                "traffic": cap.get("dram_bytes_per_launch") if cap else None, "peak_kind": peak_kind,
+                "kernel": launch_name, "grid": launch_grid,
                 "sweep_ms_mean": sweep_ms, "sweep_ms_median": float(np.median(sweeps)) if sweeps.size else None,
-                "sweeps_timed": int(sweeps.size), "bytes_min_per_launch": int(b_min),
+                "sweeps_timed": int(sweeps.size), "bytes_min_per_launch": int(bm),
                 "bytes_full_per_launch": int(b_full), "frac_full": b_full / (sweep_ms / 1e3) / 1e9 / hbm,
                 "sweep_share_of_step": float(sweeps.sum() / (ms * args.steps)) if sweeps.size else None,
-                "nnz_M": int(plan.nnz)}
-    launches_per_step = order + (2 * order if plan.n_long else 0)
+                "nnz_M": int(plan.nnz), "schedule": "length_order" if plan.binned else "index_order"}
+    if cap:
+        roofline["traffic_source"] = cap["source"]
+        roofline["traffic_capture"] = {k2: cap.get(k2) for k2 in ("kernel", "grid", "commit", "when")}
+        roofline["traffic_capture_matches"] = cap.get("kernel") == launch_name and cap.get("grid") == launch_grid
+        roofline["dram_frac"] = cap["dram_bytes_per_launch"] / (sweep_ms / 1e3) / 1e9 / hbm
 
-    # end to end through the public API: pinned host signals in, host features out
+    # end to end through the public API: host numpy in, host numpy out
     e2e = None
     if rank == 0 or world > 1:
+        calls = max(5, args.steps)
         pinned = torch.from_numpy(r_host).pin_memory()
-        x_np = pinned.numpy()
-        # warm-up in the same loop shape as the timed one (the previous result is
-        # still alive during each call: steady state holds two pinned host outputs)
-        for _ in range(2):
-            res = P.apply_filter(lap, poly, x_np, precision=args.precision)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e2e_steps = max(1, min(args.steps, 3))
-        for _ in range(e2e_steps):
-            res = P.apply_filter(lap, poly, x_np, precision=args.precision)
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        e2e_s, res = e2e_calls(P, lap, poly, pinned.numpy(), args.precision, calls)
+        e2e_pg, _ = e2e_calls(P, lap, poly, np.ascontiguousarray(r_host), args.precision, calls)
         if world > 1:
-            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            t = torch.tensor([e2e_s, e2e_pg], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+            e2e_s, e2e_pg = (float(v) for v in t.tolist())
         e2e = {"value": units * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(n * d * 8),
-               "d2h_bytes_per_step": int(res.nbytes), "ms_per_step": e2e_s * 1e3,
-               "api": "paper_1706_03591_b200.apply_filter(L, poly, numpy pinned) -> numpy"}
+               "d2h_bytes_per_step": int(res.nbytes), "ms_per_step": e2e_s * 1e3, "calls": calls,
+               "api": "paper_1706_03591_b200.apply_filter(L, poly, numpy pinned) -> numpy",
+               "pageable": {"value": units * world / e2e_pg, "ms_per_step": e2e_pg * 1e3, "calls": calls,
+                            "api": "apply_filter(L, poly, ordinary numpy array) -> numpy (pinned staging "
+                                   "ring, host threads)"}}
+        del pinned, res
 
-    # fp32 variant of the same workload (reported separately; error in DESIGN.md)
+    # fp32 variant of the same workload, and configs[3]
     variants = {}
     if dtype == torch.float64 and not args.no_variants:
-        blk32 = blk.to(torch.float32)
-        ld32 = row_stride(d, torch.float32)
-        if ld32 != blk32.shape[1]:
-            b2 = torch.zeros((n, ld32), dtype=torch.float32, device=dev)
-            b2[:, :d] = blk32[:, :d]
-            blk32 = b2
+        blk32 = torch.zeros((n, row_stride(d, torch.float32)), dtype=torch.float32, device=dev)
+        blk32[:, :d].copy_(blk[:, :d])
         out32 = torch.empty_like(blk32)
         work32 = torch.empty((2 * n, blk32.shape[1]), dtype=torch.float32, device=dev)
         lap.plan(1.0, torch.float32)
-        filter_block(lap, poly, blk32, d, out=out32, work=work32)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(2):
-            filter_block(lap, poly, blk32, d, out=out32, work=work32)
-        e1.record()
-        torch.cuda.synchronize()
-        ms32 = e0.elapsed_time(e1) / 2
-        b32 = 4 * (n + 1) + nnz_L * 8 + nnz_L * d * 4 + n * d * 4
+        ms32, sw32 = timed_filter(lap, poly, blk32, d, out32, work32, 2, lib)
+        b32 = b_min(n, nnz_L, d, 4)
         variants["fp32"] = {"value": units * world / (ms32 / 1e3), "ms_per_step": ms32,
-                            "roofline_frac": b32 / (ms32 / order / 1e3) / 1e9 / hbm,
+                            "roofline_frac": b32 / (float(sw32.mean()) / 1e3) / 1e9 / hbm,
                             "rel_frobenius_vs_fp64": float((out[:, :d] - out32[:, :d].double()).norm()
                                                            / out[:, :d].norm())}
         del blk32, out32, work32
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         m = lap.matrix
@@ -404,10 +598,25 @@ def main():
         cpu = {"value": nnz_L * d * 2 / dt, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"2 of {order} SpMM orders of apply_filter, C restatement on {cores} host threads "
                          f"(same graph and signals); {dt:.2f} s"}
+        dt_ref = reference_scipy_sample(m, r_host, poly.coeffs, orders=2)
+        if dt_ref is not None:
+            cpu["reference_scipy"] = {
+                "value": nnz_L * d * 2 / dt_ref, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"2 of {order} SpMM orders of the unmodified reference apply_filter "
+                          f"(cscluster from baseline/_ref, SciPy csr_matvecs), same graph and signals, "
+                          f"extrapolated per order; {dt_ref:.1f} s"}
+    del blk, out, work
+    torch.cuda.empty_cache()
+    if dtype == torch.float64 and not args.no_variants and not args.no_cfg4:
+        variants["cfg4"] = run_cfg4(hbm, lib)
 
-    dyn = None
+    dyn = dyn5 = None
     if not args.no_dynamic:
         dyn = run_dynamic(args, rank)
+        if not args.no_cfg5:
+            del lap, plan
+            torch.cuda.empty_cache()
+            dyn5 = run_dynamic_cfg5(args, rank)
 
     if rank == 0:
         line = {
@@ -419,12 +628,16 @@ def main():
                        "l2": "inputs (n*d*8 B per block, 3 blocks) exceed the 126 MB L2; no flush",
                        "parallelism": f"column shards x{world}, no exchange"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches_per_step * args.steps), "clocks": clk.summary(),
+            "gpu_launches": int(sweeps.size) if sweeps.size else int(order * args.steps),
+            "clocks": clk.summary(),
+            "rng": dict(S.RNG_STATS),
         }
         if variants:
             line["variants"] = variants
         if dyn is not None:
             line["dynamic"] = dyn
+        if dyn5 is not None:
+            line["dynamic_cfg5"] = dyn5
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

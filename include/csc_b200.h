@@ -143,8 +143,6 @@ int csc_cheb_combine(const void *x_dev, const void *keep_dev, int64_t n, int64_t
 
 /* Tuning knobs (process-wide; defaults are the measured best):
  *   "chunk_bytes"  row-chunk width per sweep series (default 4096)
- *   "near_window"  >0: gathers within +-window rows of the output row use
- *                  L2 evict_last, others evict_first (default 0 = off)
  *   "stream_hint"  1: row-local streams use L2 evict_first (default 1)
  *   "vpl"          preferred 16-byte vectors per lane (1, 2, 4): narrower row
  *                  groups, more gathers in flight per lane (default 0 = 2 for rows
@@ -159,6 +157,10 @@ int csc_set_tuning(const char *key, int64_t value);
  * csc_cheb_moments is bracketed by CUDA events on its stream (up to 4096
  * launches); csc_sweep_times returns their durations in ms and resets. */
 int csc_sweep_timing(int enable);
+/* Measurement hook: the kernel instance ("sweep_kernel<f64,G=32,VPL=2,mid,
+ * index_order>") and grid of the most recent main sweep launch, so a bench
+ * can check that a committed ncu capture was taken of the same launch. */
+int csc_sweep_last_launch(char *name_out, int cap, int *grid_out);
 int csc_sweep_times(float *ms_host, int max_count, int *count_out);
 
 /* rows x width_bytes strided copy (cudaMemcpy2DAsync, direction from the

@@ -45,6 +45,7 @@ SIGNATURES = {
     "csc_copy2d_async": ([_P, _I64, _P, _I64, _I64, _I64, _P], _INT),
     "csc_set_tuning": ([ctypes.c_char_p, _I64], _INT),
     "csc_sweep_timing": ([_INT], _INT),
+    "csc_sweep_last_launch": ([ctypes.c_char_p, _INT, ctypes.POINTER(_INT)], _INT),
     "csc_sweep_times": ([ctypes.POINTER(ctypes.c_float), _INT, ctypes.POINTER(_INT)], _INT),
     "csc_kmeans_rownorms": ([_P, _I64, _I64, _I64, _P, _P], _INT),
     "csc_kmeans_assign": ([_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P], _INT),

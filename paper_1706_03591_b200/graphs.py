@@ -188,8 +188,8 @@ class Graph:
         if not self.unit_weights():
             raise ValueError("apply_delta supports unit-weight graphs only")
         dev = require_cuda()
-        dl = np.unique(np.asarray(deletes, dtype=np.int64).ravel())
-        il = np.unique(np.asarray(inserts, dtype=np.int64).ravel())
+        dl = _sorted_codes(deletes)
+        il = _sorted_codes(inserts)
         if il.size:
             lo, hi = il // self.n, il % self.n
             if il.min() < 0 or np.any(lo >= hi) or hi.max() >= self.n:
@@ -206,6 +206,15 @@ class Graph:
         g._init(self.n, None, None, None, out[:m_new], int(got.value))
         object.__setattr__(g, "_unit", True)
         return g
+
+
+def _sorted_codes(codes) -> np.ndarray:
+    """Sorted unique int64 codes; lists that already are (the generators' and
+    set-difference outputs) pass with one O(m) check instead of a sort."""
+    c = np.asarray(codes, dtype=np.int64).ravel()
+    if c.size > 1 and not np.all(c[1:] > c[:-1]):
+        c = np.unique(c)
+    return c
 
 
 def graphs_equal(a: Graph, b: Graph) -> bool:

@@ -286,13 +286,55 @@ def make_cfg2(steps=2):
     print(f"cfg2 total: {time.time() - t0:.1f}s", flush=True)
 
 
+def make_high_order():
+    """High-order filters of the reference's own tests: m = 300 eigencounts on the
+    sbm300 fixture (pkg/tests/test_filters.py:178-184, conftest.py:33-38) and the
+    m = 250 approximation of the ideal projector (test_filters.py:277-291)."""
+    out = {}
+    params = cc.SbmParams(n=300, k=4, s=25, e=1 / 6)
+    g, _ = cc.sbm_generate(params, seed=2024)
+    lap = cc.laplacian(g)
+    out.update(graph_arrays("g300", g))
+    out.update(lap_arrays("l300", lap))
+    basis = cc.eigendecompose(lap, 4)
+    cut = 0.5 * (basis.eigenvalues[-1] + basis.lambda_next)
+    out["g300_cut"] = np.float64(cut)
+    ests, feats = [], []
+    for s in range(5):
+        est, fm = cc.eigencount(lap, cut, d=100, m=300, seed=s)
+        ests.append(est)
+        if s == 0:
+            feats = fm.values
+    out["g300_ests"] = np.array(ests)
+    out["g300_feats0"] = feats
+    poly = cc.cheb_coeffs(cut, lap.lambda_max_bound, 300)
+    out["g300_coeffs"] = poly.coeffs
+    params = cc.SbmParams(n=120, k=3, s=12, e=0.1)
+    g, _ = cc.sbm_generate(params, 11)
+    lap = cc.laplacian(g)
+    out.update(graph_arrays("g120", g))
+    out.update(lap_arrays("l120", lap))
+    basis = cc.eigendecompose(lap, 3)
+    r = cc.random_signals(120, 40, seed=12)
+    grid = np.linspace(0.0, lap.lambda_max_bound, 4000)
+    for tag, cut in (("mid", 0.5 * (basis.eigenvalues[-1] + basis.lambda_next)), ("eig", basis.eigenvalues[-1])):
+        poly = cc.cheb_coeffs(cut, lap.lambda_max_bound, m=250, damping="jackson")
+        out[f"g120_{tag}_cut"] = np.float64(cut)
+        out[f"g120_{tag}_approx"] = cc.apply_filter(lap, poly, r)
+        out[f"g120_{tag}_ideal"] = cc.ideal_projector_apply(basis, r)
+        step = (grid <= cut).astype(np.float64)
+        out[f"g120_{tag}_worst"] = np.float64(np.abs(poly.evaluate(grid) - step).max())
+    out["g120_r"] = r
+    np.savez_compressed(os.path.join(HERE, "high_order.npz"), **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-cfg2", action="store_true")
     ap.add_argument("--only", default="")
     args = ap.parse_args()
     jobs = {"cfg1": make_cfg1, "small": make_small, "kmeans": make_kmeans,
-            "dynamic_small": make_dynamic_small, "cfg2": make_cfg2}
+            "dynamic_small": make_dynamic_small, "cfg2": make_cfg2, "high_order": make_high_order}
     for name, fn in jobs.items():
         if args.only and name not in args.only.split(","):
             continue

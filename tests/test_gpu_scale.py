@@ -1,0 +1,223 @@
+"""Parity at BASELINE.json's full sizes against the C / numpy oracle.
+
+Each test runs the production GPU path on the whole configs[2..4] workload and
+checks a bounded subset against the oracle restatement (oracle/, pinned to the
+live reference's goldens by tests/test_oracle_golden.py):
+  * cfg3 (configs[2]): the order-100 filter of the production d = 128 block,
+    8 of its columns through the C restatement of apply_filter
+    (filters.py:155-187): rel. Frobenius <= 1e-10 (fp64); fp32 error printed;
+  * cfg4 (configs[3], Chung-Lu n = 4M, rows up to ~18k entries, the
+    length-ordered schedule and the long-row segments): fp64 <= 1e-10 on 8
+    columns, fp32 error printed and bounded; the length-ordered and the
+    index-ordered schedules give bitwise the same block;
+  * cfg5 (configs[4]): one dynamic step (dynamic.py:125-178): the reused
+    columns are the previous features' chosen columns bitwise, the fresh
+    columns equal the oracle's filter of the reference's raw draws
+    (<= 1e-10), the validation estimate's per-column terms agree, and the
+    cutoff decision is the one the oracle's estimate gives;
+  * cfg3 shape k-means (kmeans.py:64-117): k-means++ from the same seed then
+    3 Lloyd iterations, ARI >= 0.999 and cost <= 1e-9 relative vs the oracle.
+The graphs come from the O(m) generators (generators.py) with the seeds
+bench.py uses; the oracle reads the device-built Laplacian, whose values are
+checked bitwise separately (test_gpu_fullsize.py, test_gpu_parity.py).
+"""
+import numpy as np
+import pytest
+
+from oracle import csc_oracle as O
+from oracle import native as ON
+
+pytestmark = pytest.mark.gpu
+
+COLS = np.array([0, 1, 2, 3, 37, 64, 100, 127])
+
+
+def _ix(a, t):
+    import torch
+    return torch.as_tensor(np.asarray(a), dtype=torch.int64, device=t.device)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def cfg3(cuda_ok):
+    import paper_1706_03591_b200 as P
+    from paper_1706_03591_b200 import generators as G
+    n, k = 1_000_000, 100
+    q1, q2 = G.sbm_probabilities(n, k, 32.0, 0.02)
+    g = G.graph_from_codes(n, G.planted_partition_codes(n, k, q1, q2, 3))
+    return P, g, P.laplacian(g)
+
+
+def test_cfg3_filter_order100_vs_oracle(cfg3):
+    import torch
+    from paper_1706_03591_b200.filters import filter_block
+    from paper_1706_03591_b200.signals import device_signals
+    P, g, lap = cfg3
+    n, d = g.n, 128
+    x = device_signals(n, d, 3)
+    poly = P.cheb_coeffs(0.05, lap.lambda_max_bound, 100)
+    out, s = filter_block(lap, poly, x, d, want_sumsq=True)
+    m = lap.matrix
+    xh = x[:, _ix(COLS, x)].cpu().numpy()
+    assert np.array_equal(xh, O.random_signals(n, d, 3)[:, COLS])  # the reference's draws
+    ref = ON.cheb_filter(m.indptr, m.indices, m.data, 2.0, poly.coeffs, xh)
+    got = out[:, _ix(COLS, out)].cpu().numpy()
+    e64 = _rel(got, ref)
+    assert e64 <= 1e-10, e64
+    # the fused eigencount of the whole block vs the device block's own sum
+    assert abs(float(s.item()) - float((out[:, :d] ** 2).sum().item())) <= 1e-12 * float(s.item())
+    # fp32 variant, stated separately
+    x32 = torch.zeros((n, d), dtype=torch.float32, device=x.device)
+    x32.copy_(x[:, :d])
+    o32, _ = filter_block(lap, poly, x32, d)
+    e32 = _rel(o32[:, _ix(COLS, o32)].double().cpu().numpy(), ref)
+    print(f"cfg3 order-100 rel. Frobenius vs oracle: fp64 {e64:.3e}, fp32 {e32:.3e}")
+    assert e32 <= 1e-4
+
+
+@pytest.fixture(scope="module")
+def cfg4(cuda_ok):
+    import paper_1706_03591_b200 as P
+    from paper_1706_03591_b200 import generators as G
+    g, _ = G.chung_lu_sbm(4_000_000, 50, 16.0, 2.3, 20000.0, 0.05, seed=4)
+    return P, g, P.laplacian(g)
+
+
+def test_cfg4_skewed_filter_vs_oracle(cfg4):
+    import torch
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200.filters import filter_block
+    from paper_1706_03591_b200.signals import device_signals
+    P, g, lap = cfg4
+    n, d, order = g.n, 64, 80
+    plan = lap.plan(1.0, torch.float64)
+    assert plan.binned and plan.n_long > 1000  # length-ordered schedule + long-row segments
+    x = device_signals(n, d, 4)
+    poly = P.cheb_coeffs(0.05, lap.lambda_max_bound, order)
+    out, _ = filter_block(lap, poly, x, d)
+    cols = COLS[COLS < d]
+    m = lap.matrix
+    assert np.diff(m.indptr).max() > 10_000  # hub rows
+    xh = x[:, _ix(cols, x)].cpu().numpy()
+    ref = ON.cheb_filter(m.indptr, m.indices, m.data, 2.0, poly.coeffs, xh)
+    e64 = _rel(out[:, _ix(cols, out)].cpu().numpy(), ref)
+    assert e64 <= 1e-10, e64
+    x32 = torch.zeros((n, d), dtype=torch.float32, device=x.device)
+    x32.copy_(x[:, :d])
+    o32, _ = filter_block(lap, poly, x32, d)
+    assert lap.plan(1.0, torch.float32).binned
+    e32 = _rel(o32[:, _ix(cols, o32)].double().cpu().numpy(), ref)
+    print(f"cfg4 order-80 rel. Frobenius vs oracle: fp64 {e64:.3e}, fp32 {e32:.3e}")
+    assert e32 <= 1e-4
+    # the row schedule changes the order rows are visited, never a row's sum
+    lap2 = P.laplacian(g)
+    _native.call("csc_set_tuning", b"row_binning", 0)
+    try:
+        plan2 = lap2.plan(1.0, torch.float64)
+    finally:
+        _native.call("csc_set_tuning", b"row_binning", -1)
+    assert not plan2.binned
+    out2, _ = filter_block(lap2, poly, x, d)
+    assert torch.equal(out[:, :d], out2[:, :d])
+
+
+def test_cfg5_dynamic_step_vs_oracle(cuda_ok):
+    import paper_1706_03591_b200 as P
+    from paper_1706_03591_b200 import generators as G
+    n, k, d = 2_000_000, 64, 96
+    q1, q2 = G.sbm_probabilities(n, k, 20.0, 0.05)
+    codes = G.planted_partition_codes(n, k, q1, q2, 5)
+    labels = np.repeat(np.arange(k), G.block_sizes(n, k))
+    g1 = G.graph_from_codes(n, codes)
+    dl, il = G.edge_churn(codes, n, labels, q1, q2, 0.01, seed=105)
+    g2 = g1.apply_delta(dl, il)
+    cfg = P.DynamicConfig(k=k, d=d, p=0.5, filter=P.FilterConfig(order=80),
+                          kmeans=P.KmeansConfig(restarts=2, max_iters=20))
+    _, state, _ = P.dynamic_init(g1, cfg, seed=5)
+    prev_feats = state.features
+    prev_poly = state.filter
+    # the reference's step draws (dynamic.py:128-137): sel, sig, km = rng.spawn(3)
+    ss = state.rng
+    twin = np.random.SeedSequence(ss.entropy, spawn_key=ss.spawn_key, pool_size=ss.pool_size,
+                                  n_children_spawned=ss.n_children_spawned)
+    sel_ss, sig_ss, _ = twin.spawn(3)
+    _, state2, diag = P.dynamic_step(state, g2, cfg)
+    n_reuse, n_fresh = cfg.reuse_count, d - cfg.reuse_count
+    eligible = np.flatnonzero(prev_feats.step_tags == 1)
+    chosen = np.sort(np.random.default_rng(sel_ss).choice(eligible, size=n_reuse, replace=False))
+    theta = state2.features.device_block()
+    # reused columns: bitwise the previous features' chosen columns
+    sub = chosen[:4]
+    pb = prev_feats.device_block()
+    assert np.array_equal(theta[:, :4].cpu().numpy(), pb[:, _ix(sub, pb)].cpu().numpy())
+    # fresh columns: the oracle's filter of the reference's raw draws
+    fcols = np.array([0, 1, 17, n_fresh - 1])
+    raw = O.random_signals(n, n_fresh, sig_ss, scale_dim=d)[:, fcols]
+    lap2 = P.laplacian(g2)
+    m = lap2.matrix
+    poly = prev_poly if not diag.refined else state2.filter
+    ref = ON.cheb_filter(m.indptr, m.indices, m.data, lap2.lambda_max_bound, poly.coeffs, raw)
+    got = theta[:, _ix(n_reuse + fcols, theta)].cpu().numpy()
+    assert _rel(got, ref) <= 1e-10, _rel(got, ref)
+    # validation estimate: per-column energy terms, and the decision they give
+    fresh_all = theta[:, n_reuse:d]
+    col_e = (fresh_all ** 2).sum(0).cpu().numpy()
+    ref_e = (ref ** 2).sum(0)
+    np.testing.assert_allclose(col_e[fcols], ref_e, rtol=1e-10)
+    if not diag.refined:
+        est = float(col_e.sum() * d / n_fresh)
+        margin = abs(abs(est - k) - cfg.filter.count_tol * k)
+        assert abs(est - k) <= cfg.filter.count_tol * k
+        assert margin > 1e-8 * k  # no estimate within rounding of the acceptance edge
+        assert state2.lambda_k == state.lambda_k
+    print(f"cfg5 step: refined={diag.refined} lambda_k={state2.lambda_k:.6g} "
+          f"fresh rel {_rel(got, ref):.2e}")
+
+
+def test_cfg3_shape_kmeans_vs_oracle(cfg3):
+    import torch
+    from paper_1706_03591_b200.filters import filter_block
+    from paper_1706_03591_b200.signals import device_signals
+    P, g, lap = cfg3
+    n, d, k = g.n, 128, 100
+    x = device_signals(n, d, 30)
+    poly = P.cheb_coeffs(0.05, lap.lambda_max_bound, 40)
+    feats, _ = filter_block(lap, poly, x, d)
+    cfg = P.KmeansConfig(restarts=1, max_iters=3)
+    a = P.kmeans(feats[:, :d], k, cfg, seed=8)
+    fh = feats[:, :d].cpu().numpy()
+    labels, sizes, cost = O.kmeans(fh, k, restarts=1, max_iters=3, seed=8)
+    ari = O.adjusted_rand(a.labels, labels)
+    rel = abs(a.feature_cost - cost) / cost
+    print(f"cfg3-shape k-means (3 Lloyd iterations): ARI {ari:.6f}, cost rel {rel:.2e}")
+    assert ari >= 0.999
+    assert rel <= 1e-9
+    torch.cuda.synchronize()
+
+
+def test_high_order_eigencount_and_projector():
+    """m = 300 / 250 filters of the reference's tests (test_filters.py:178-184, 277-291)."""
+    import paper_1706_03591_b200 as P
+    from conftest import golden
+    g = golden("high_order")
+    gr = P.Graph(int(g["g300_n"]), g["g300_i"], g["g300_j"], g["g300_w"])
+    lap = P.laplacian(gr)
+    cut = float(g["g300_cut"])
+    ests = []
+    for s in range(5):
+        est, fm = P.eigencount(lap, cut, d=100, m=300, seed=s)
+        ests.append(est)
+        if s == 0:
+            assert _rel(fm.values, g["g300_feats0"]) <= 1e-10
+    np.testing.assert_allclose(ests, g["g300_ests"], rtol=1e-10)
+    gr = P.Graph(int(g["g120_n"]), g["g120_i"], g["g120_j"], g["g120_w"])
+    lap = P.laplacian(gr)
+    for tag in ("mid", "eig"):
+        poly = P.cheb_coeffs(float(g[f"g120_{tag}_cut"]), lap.lambda_max_bound, 250)
+        approx = P.apply_filter(lap, poly, g["g120_r"])
+        assert _rel(approx, g[f"g120_{tag}_approx"]) <= 1e-10
+        bound = float(g[f"g120_{tag}_worst"]) * np.linalg.norm(g["g120_r"]) + 1e-6
+        assert np.linalg.norm(approx - g[f"g120_{tag}_ideal"]) <= bound

@@ -164,3 +164,27 @@ def test_adjusted_rand_identity():
     a = np.array([0, 0, 1, 1, 2, 2])
     assert O.adjusted_rand(a, a) == 1.0
     assert O.adjusted_rand(a, np.array([1, 1, 0, 0, 2, 2])) == 1.0
+
+
+def test_row_sqdist_chunked_is_bitwise():
+    """The oracle's threaded row-chunked D^2 equals the reference's one-shot expression."""
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal((300_000, 37))
+    c = f[11]
+    assert np.array_equal(O.row_sqdist(f, c), ((f - c) ** 2).sum(axis=1))
+
+
+def test_high_order_filters_bitwise():
+    """m = 300 / m = 250 cases of the reference's own tests (test_filters.py:178-184, 277-291)."""
+    g = golden("high_order")
+    ip, ix, dv = g["l300_indptr"], g["l300_indices"], g["l300_data"]
+    n = len(ip) - 1
+    assert np.array_equal(O.step_coeffs(float(g["g300_cut"]), 2.0, 300), g["g300_coeffs"])
+    r = O.random_signals(n, 100, 0)
+    out = native.cheb_filter(ip, ix, dv, 2.0, g["g300_coeffs"], r)
+    assert np.array_equal(out, g["g300_feats0"])
+    assert O.count_from_block(out, 1.0) == float(g["g300_ests"][0])
+    ip, ix, dv = g["l120_indptr"], g["l120_indices"], g["l120_data"]
+    for tag in ("mid", "eig"):
+        c = O.step_coeffs(float(g[f"g120_{tag}_cut"]), 2.0, 250)
+        assert np.array_equal(O.apply_filter(ip, ix, dv, 2.0, c, g["g120_r"]), g[f"g120_{tag}_approx"])
