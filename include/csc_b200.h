@@ -264,6 +264,13 @@ int csc_kmeans_fused_trace(unsigned long long *trace_dev, int64_t iters_cap);
  * whenever f changes. set_screen(): the plan uses these buffers from now on
  * (NULL f32 disables); they must stay valid while the plan runs. */
 int csc_kmeans_screen_supported(int64_t d, int64_t k);
+/* Test hook of the tensor-core (tcgen05 kind::tf32, 3xTF32) screen: e_out
+ * (n x roundup(k, 16) fp32, row-major) = |f32_i|^2 - 2 f_i.c_j + |c_j|^2 as
+ * the screen computes it, from fp32 features (ld32 % 4 == 0, padding zero),
+ * their fp32 norms fn32 and fp64 centroids / norms. */
+int csc_kmeans_tc_distances(const void *f32_dev, int64_t n, int64_t d, int64_t ld32,
+                            const float *fn32_dev, const double *c_dev, int64_t k, int64_t ldc,
+                            const double *cnorm_dev, float *e_out_dev, void *stream);
 int csc_kmeans_screen_prepare(const double *f_dev, int64_t n, int64_t d, int64_t ld,
                               float *f32_dev, int64_t ld32, float *fn32_dev, void *stream);
 int csc_kmeans_plan_set_screen(csc_kmeans_plan *plan, const float *f32_dev, int64_t ld32,

@@ -30,4 +30,17 @@ int screen_assign(const float *f32, int64_t ld32, const float *fn32, const doubl
                   int32_t *labels, double *ub, double *lb, int32_t *counts, int32_t *amb,
                   int32_t *namb, cudaStream_t st);
 
+// Tensor-core variant (kmeans_screen_tc.cu, tcgen05 kind::tf32, 3xTF32 split):
+// same contract as screen_assign with centroids in hi / lo K-major tiles
+// (tc_convert_centroids); raw_out (tests) receives E instead of decisions.
+bool tc_screen_supported(int64_t d, int64_t k);
+int64_t tc_centroid_floats(int64_t d, int64_t k);
+int tc_convert_centroids(const double *c, int64_t k, int64_t d, int64_t ldc, const double *cnorm,
+                         float *chi, float *clo, float *cn32, double *cmax, cudaStream_t st);
+int tc_screen_assign(const float *f32, int64_t ld32, const float *fn32, int64_t n, int64_t d,
+                     const float *chi, const float *clo, const float *cn32, int64_t k,
+                     const double *cmax, const int32_t *rows, const int32_t *nrows_dev,
+                     int32_t *labels, double *ub, double *lb, int32_t *counts, int32_t *amb,
+                     int32_t *namb, float *raw_out, cudaStream_t st);
+
 }  // namespace csc

@@ -1,0 +1,444 @@
+// Tensor-core (tcgen05, kind::tf32) screen of the k-means assignment
+// (kmeans.py:54-61, 96-97), with the exact FP64 fallback of kmeans_screen.cu:
+// labels stay bit-identical to the pure FP64 path.
+//
+// The inner products f.c_j of a 128-row tile against all centroids are one
+// UMMA D[128 x N] (fp32 accumulators in tensor memory) per 8-column K step,
+// in the 3xTF32 split: with f = f_hi + f_lo and c = c_hi + c_lo (hi = the
+// fp32 value with its 13 low mantissa bits cleared, exactly a tf32; lo = the
+// exact fp32 remainder, rounded to tf32 by the tensor core),
+//     f.c ~ f_hi.c_hi + f_lo.c_hi + f_hi.c_lo,
+// three MMAs per K step accumulating in the same TMEM columns. Error bound
+// (per row, all j), conservative for an accumulator that truncates:
+//   split:  |f.c - (three products)| <= (2^-20 + 2 * 2^-21) |f| |c|
+//   sum:    3d products of tf32 operands are exact in fp32; each of the 3d
+//           accumulations loses < 2^-23 of the running |sum| <= sum |f_t c_t|
+//   norms / inputs: as the FP32 screen ((d + 5) 2^-24 (|f| + |c|)^2)
+// so |E_ij - T_ij| <= delta_i = (3d + 8) 2^-23 (|f_i| + max_j |c_j|)^2, and a
+// row whose best/second gap exceeds 2 delta_i is decided exactly as in the
+// FP32 screen (same Hamerly widening); the others go to the FP64 list.
+//
+// Layout. Operands are K-major, no swizzle: element (r, c) of a ROWS x K tile
+// sits at byte (c / 4) * ROWS * 16 + r * 16 + (c % 4) * 4 (16-byte K chunks,
+// the ROWS rows of a chunk contiguous), i.e. core matrices of 8 rows x 16 B
+// at SBO = 128 B along rows and LBO = ROWS * 16 B along K; one MMA (K = 8)
+// reads chunks 2s, 2s+1. Rows are gathered by index (Hamerly candidates) with
+// cp.async (one warp covers whole rows: coalesced), split into hi/lo in
+// shared memory, then one elected thread issues the 3 x K/8 MMAs and commits
+// them to an mbarrier; each of the 4 warps reads its 32 TMEM lanes (rows)
+// with tcgen05.ld and settles them.
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "kmeans_screen.cuh"
+
+namespace {
+
+constexpr int kTM = 128;       // rows per tile = UMMA M
+constexpr int kTThreads = 128; // warp w reads TMEM lanes 32w .. 32w + 31
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); base offset 0, SWIZZLE_NONE
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D fp32, A/B tf32, both K-major, M = 128
+__host__ __device__ constexpr uint32_t tf32_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+// centroids -> hi / lo K-major canonical tiles [Q][N][4] (zero past k / d),
+// cn (+inf past k), cmax = max_j |c_j| (from the fp64 norms)
+__global__ void tc_centroids_kernel(const double *__restrict__ c, int64_t k, int64_t d,
+                                    int64_t ldc, const double *__restrict__ cnorm, int n_pad,
+                                    int kp, float *__restrict__ chi, float *__restrict__ clo,
+                                    float *__restrict__ cn32, double *__restrict__ cmax) {
+  __shared__ double red[32];
+  for (int64_t e = threadIdx.x; e < (int64_t)n_pad * kp; e += blockDim.x) {
+    const int64_t j = e / kp, t = e - j * kp;
+    const float v = (j < k && t < d) ? (float)c[j * ldc + t] : 0.0f;
+    const float h = tf32_hi(v);
+    const int64_t off = (t / 4) * (int64_t)n_pad * 4 + j * 4 + (t % 4);
+    chi[off] = h;
+    clo[off] = v - h;
+  }
+  double m = 0.0;
+  for (int j = threadIdx.x; j < n_pad; j += blockDim.x) {
+    if (j < k) {
+      float s = 0.0f;
+      for (int64_t t = 0; t < d; ++t) {
+        const float v = (float)c[j * ldc + t];
+        s = fmaf(v, v, s);
+      }
+      cn32[j] = s;
+      m = fmax(m, cnorm[j]);
+    } else {
+      cn32[j] = INFINITY;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x / 32); ++w) m = fmax(m, red[w]);
+    cmax[0] = sqrt(fmax(m, red[0]));
+  }
+}
+
+struct TcArgs {
+  const float *f32;
+  int64_t ld32;
+  const float *fn32;
+  int64_t n;
+  int d, kp, k, n_pad;
+  const float *chi, *clo, *cn32;
+  const double *cmax;
+  const int32_t *rows;
+  const int32_t *nrows;
+  int32_t *labels;
+  double *ub, *lb;
+  int32_t *counts;
+  int32_t *amb, *namb;
+  float *raw_out;  // test hook: E (n x n_pad fp32) instead of the decision
+};
+
+template <int NP>  // padded centroid count = UMMA N (multiple of 16, <= 256)
+__global__ void __launch_bounds__(kTThreads, 1) tc_screen_kernel(TcArgs a) {
+  extern __shared__ __align__(128) uint8_t tsm[];
+  const int kp = a.kp, q4 = kp / 4;
+  float *Ahi = reinterpret_cast<float *>(tsm);
+  float *Alo = Ahi + (size_t)kTM * kp;
+  float *Bhi = Alo + (size_t)kTM * kp;
+  float *Blo = Bhi + (size_t)NP * kp;
+  float *Fn = Blo + (size_t)NP * kp;
+  float *Cn = Fn + kTM;
+  int32_t *Rid = reinterpret_cast<int32_t *>(Cn + NP);
+  int32_t *Hs = Rid + kTM;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(Hs + NP + (NP & 1));  // 8-byte aligned (NP even)
+  uint32_t *tmem_hold = reinterpret_cast<uint32_t *>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t nr = a.nrows ? (int64_t)*a.nrows : a.n;
+  const int64_t ntiles = (nr + kTM - 1) / kTM;
+  if ((int64_t)blockIdx.x >= ntiles) return;
+
+  constexpr uint32_t kCols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_hold)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(smem_u32(bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // centroid tiles (already in the canonical layout) and norms
+  {
+    const float4 *sh = reinterpret_cast<const float4 *>(a.chi);
+    const float4 *sl = reinterpret_cast<const float4 *>(a.clo);
+    float4 *dh = reinterpret_cast<float4 *>(Bhi);
+    float4 *dl = reinterpret_cast<float4 *>(Blo);
+    for (int e = tid; e < NP * q4; e += kTThreads) {
+      dh[e] = sh[e];
+      dl[e] = sl[e];
+    }
+    for (int j = tid; j < NP; j += kTThreads) {
+      Cn[j] = a.cn32[j];
+      Hs[j] = 0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_hold;
+  const double cmax = *a.cmax;
+  const double dscale = (double)(3 * a.d + 8) * 1.1920928955078125e-7;  // (3d + 8) 2^-23
+  const uint32_t idesc = tf32_idesc(NP);
+  const uint32_t sA = smem_u32(Ahi), sAl = smem_u32(Alo), sB = smem_u32(Bhi), sBl = smem_u32(Blo);
+  const uint32_t lboA = kTM * 16, lboB = NP * 16, sbo = 128;
+  uint32_t phase = 0;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    {
+      const int64_t lr = tile * kTM + tid;
+      const int64_t gr = lr < nr ? (a.rows ? (int64_t)a.rows[lr] : lr) : -1;
+      Rid[tid] = (int32_t)gr;
+      Fn[tid] = gr >= 0 ? a.fn32[gr] : 0.0f;
+    }
+    __syncthreads();
+    // gather the tile's rows: element e = (row, 16-byte chunk), chunks of a row
+    // on consecutive threads (coalesced 16-byte pieces of one row)
+    for (int e = tid; e < kTM * q4; e += kTThreads) {
+      const int r = e / q4, q = e - r * q4;
+      const int32_t gr = Rid[r];
+      const bool ok = gr >= 0 && 4 * q < a.d;
+      cp_async16(sA + (uint32_t)(q * kTM + r) * 16, ok ? a.f32 + (int64_t)gr * a.ld32 + 4 * q : a.f32,
+                 ok);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // hi / lo split in place
+    for (int e = tid; e < kTM * kp; e += kTThreads) {
+      const float v = Ahi[e];
+      const float h = tf32_hi(v);
+      Ahi[e] = h;
+      Alo[e] = v - h;
+    }
+    fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      for (int s = 0; s < kp / 8; ++s) {
+        const uint32_t oa = (uint32_t)s * 2 * lboA, ob = (uint32_t)s * 2 * lboB;
+        const uint64_t ahi = umma_desc(sA + oa, lboA, sbo), alo = umma_desc(sAl + oa, lboA, sbo);
+        const uint64_t bhi = umma_desc(sB + ob, lboB, sbo), blo = umma_desc(sBl + ob, lboB, sbo);
+        mma_tf32(tmem, ahi, bhi, idesc, s > 0 ? 1u : 0u);
+        mma_tf32(tmem, alo, bhi, idesc, 1u);
+        mma_tf32(tmem, ahi, blo, idesc, 1u);
+      }
+      mma_commit(smem_u32(bar));
+    }
+    mbar_wait(smem_u32(bar), phase);
+    phase ^= 1u;
+    tc_fence_after();
+    // epilogue: thread (warp w, lane l) owns row 32 w + l = TMEM lane
+    const int r = warp * 32 + lane;
+    const int32_t gr = Rid[r];
+    const float fni = Fn[r];
+    float bv = INFINITY, bv2 = INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int c0 = 0; c0 < NP; c0 += 16) {
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int cj = c0 + j;
+        const float e = fmaf(-2.0f, v[j], fni) + Cn[cj];
+        if (a.raw_out && gr >= 0) a.raw_out[(int64_t)gr * NP + cj] = e;
+        if (e < bv) {
+          bv2 = bv;
+          bv = e;
+          bi = cj;
+        } else {
+          bv2 = fminf(bv2, e);
+        }
+      }
+    }
+    if (gr >= 0 && !a.raw_out) {
+      const double fr = sqrt((double)fni * (1.0 + 2e-5)) + cmax;
+      const double delta = dscale * fr * fr * (1.0 + 1e-6);
+      const double e1 = (double)bv, e2 = (double)bv2;
+      if (e2 - e1 > 2.0 * delta) {
+        a.labels[gr] = bi;
+        a.ub[gr] = sqrt(fmax(e1 + delta, 0.0));
+        a.lb[gr] = sqrt(fmax(e2 - delta, 0.0));
+        if (a.counts) atomicAdd(Hs + bi, 1);
+      } else {
+        a.amb[atomicAdd(a.namb, 1)] = gr;
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // TMEM read and smem tiles consumed before the next tile
+    tc_fence_after();
+  }
+  if (a.counts) {
+    for (int j = tid; j < a.k; j += kTThreads)
+      if (Hs[j]) atomicAdd(a.counts + j, Hs[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+}
+
+int tc_npad(int64_t k) { return (int)((k + 15) / 16 * 16); }
+int tc_kp(int64_t d) { return (int)((d + 7) / 8 * 8); }
+
+size_t tc_smem(int64_t d, int64_t k) {
+  const int64_t kp = tc_kp(d), np = tc_npad(k);
+  return sizeof(float) * (2 * kTM * kp + 2 * np * kp + kTM + np) + sizeof(int32_t) * (kTM + np + 2) +
+         16 + 128;
+}
+
+template <int NP>
+int tc_launch(const TcArgs &a, cudaStream_t st) {
+  const size_t smem = tc_smem(a.d, a.k);
+  static std::mutex mu;
+  static size_t configured = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > configured) {
+      CSC_TRY_CUDA(cudaFuncSetAttribute(tc_screen_kernel<NP>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = smem;
+    }
+  }
+  const int64_t tiles = csc::ceil_div(a.n, kTM);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(csc::device_info().sm_count, tiles));
+  tc_screen_kernel<NP><<<(unsigned)grid, kTThreads, smem, st>>>(a);
+  CSC_CHECK_LAUNCH();
+  return CSC_OK;
+}
+
+int tc_dispatch(const TcArgs &a, cudaStream_t st) {
+  switch (a.n_pad) {
+    case 16: return tc_launch<16>(a, st);
+    case 32: return tc_launch<32>(a, st);
+    case 48: return tc_launch<48>(a, st);
+    case 64: return tc_launch<64>(a, st);
+    case 80: return tc_launch<80>(a, st);
+    case 96: return tc_launch<96>(a, st);
+    case 112: return tc_launch<112>(a, st);
+    case 128: return tc_launch<128>(a, st);
+    default: break;
+  }
+  csc::set_error("tc screen: unsupported centroid count (padded %d)", a.n_pad);
+  return CSC_ERR_ARG;
+}
+
+}  // namespace
+
+namespace csc {
+
+bool tc_screen_supported(int64_t d, int64_t k) {
+  const csc::DeviceInfo &info = csc::device_info();
+  return info.cc_major == 10 && d >= 1 && d <= 256 && k >= 2 && tc_npad(k) <= 128 &&
+         tc_smem(d, k) <= (size_t)info.max_smem_optin;
+}
+
+int64_t tc_centroid_floats(int64_t d, int64_t k) { return (int64_t)tc_npad(k) * tc_kp(d); }
+
+int tc_convert_centroids(const double *c, int64_t k, int64_t d, int64_t ldc, const double *cnorm,
+                         float *chi, float *clo, float *cn32, double *cmax, cudaStream_t st) {
+  tc_centroids_kernel<<<1, 256, 0, st>>>(c, k, d, ldc, cnorm, tc_npad(k), tc_kp(d), chi, clo, cn32,
+                                          cmax);
+  CSC_CHECK_LAUNCH();
+  return CSC_OK;
+}
+
+int tc_screen_assign(const float *f32, int64_t ld32, const float *fn32, int64_t n, int64_t d,
+                     const float *chi, const float *clo, const float *cn32, int64_t k,
+                     const double *cmax, const int32_t *rows, const int32_t *nrows_dev,
+                     int32_t *labels, double *ub, double *lb, int32_t *counts, int32_t *amb,
+                     int32_t *namb, float *raw_out, cudaStream_t st) {
+  TcArgs a{};
+  a.f32 = f32;
+  a.ld32 = ld32;
+  a.fn32 = fn32;
+  a.n = n;
+  a.d = (int)d;
+  a.kp = tc_kp(d);
+  a.k = (int)k;
+  a.n_pad = tc_npad(k);
+  a.chi = chi;
+  a.clo = clo;
+  a.cn32 = cn32;
+  a.cmax = cmax;
+  a.rows = rows;
+  a.nrows = nrows_dev;
+  a.labels = labels;
+  a.ub = ub;
+  a.lb = lb;
+  a.counts = counts;
+  a.amb = amb;
+  a.namb = namb;
+  a.raw_out = raw_out;
+  return tc_dispatch(a, st);
+}
+
+}  // namespace csc
+
+extern "C" int csc_kmeans_tc_distances(const void *f32, int64_t n, int64_t d, int64_t ld32,
+                                       const float *fn32, const double *c, int64_t k, int64_t ldc,
+                                       const double *cnorm, float *e_out, void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(csc::tc_screen_supported(d, k), "csc_kmeans_tc_distances: shape (d=%lld, k=%lld) "
+              "outside the tensor-core screen", (long long)d, (long long)k);
+  CSC_REQUIRE(ld32 % 4 == 0 && ld32 >= d, "csc_kmeans_tc_distances: ld32 must be a multiple of 4 >= d");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  csc::Scratch chi, clo, cn, cm;
+  const int64_t cf = csc::tc_centroid_floats(d, k);
+  CSC_TRY_CUDA(chi.alloc(sizeof(float) * cf, st));
+  CSC_TRY_CUDA(clo.alloc(sizeof(float) * cf, st));
+  CSC_TRY_CUDA(cn.alloc(sizeof(float) * tc_npad(k), st));
+  CSC_TRY_CUDA(cm.alloc(sizeof(double), st));
+  int rc = csc::tc_convert_centroids(c, k, d, ldc, cnorm, chi.as<float>(), clo.as<float>(),
+                                     cn.as<float>(), cm.as<double>(), st);
+  if (rc != CSC_OK) return rc;
+  return csc::tc_screen_assign(static_cast<const float *>(f32), ld32, fn32, n, d, chi.as<float>(),
+                               clo.as<float>(), cn.as<float>(), k, cm.as<double>(), nullptr,
+                               nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, e_out,
+                               st);
+}

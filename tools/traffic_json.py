@@ -19,14 +19,21 @@ per, dur, names = {}, {}, {}
 with open(prefix + ".csv") as fh:
     for r in csv.DictReader(ln for ln in fh if not ln.startswith("==")):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3}.get(r["Metric Unit"], 1.0)
+                 "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}.get(r["Metric Unit"], 1.0)
         v = float(r["Metric Value"].replace(",", "")) * scale
         names[r["ID"]] = r["Kernel Name"]
         if r["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             per[r["ID"]] = per.get(r["ID"], 0.0) + v
         elif r["Metric Name"] == "gpu__time_duration.sum":
             dur[r["ID"]] = v
-mid = [i for i in per if ", 1, " in names[i] or "1, (bool)" in names[i] or ", 1>" in names[i]]
+def mode_of(name):
+    """template arguments <T, G, VPL, MODE, PERM>: MODE 1 = a middle order"""
+    t = name[name.index("sweep_kernel<") + len("sweep_kernel<"):]
+    args = t[:t.index(">")].split(",")
+    return int(args[3].strip()) if len(args) >= 5 else -1
+
+
+mid = [i for i in per if mode_of(names[i]) == 1]
 ids = mid or list(per)
 commit = subprocess.run(["git", "-C", root, "rev-parse", "--short=12", "HEAD"], capture_output=True,
                         text=True).stdout.strip()
