@@ -726,6 +726,19 @@ int launch_assign_small(const double *f, const double *fnorm, int64_t n, int64_t
 
 int g_assign_tn = 8;
 int g_assign_ver = 3;
+// incremental centroid sums (update_sorted_kernel): tuning key "update_incremental"
+int g_update_incremental = 1;
+// assignment screen of the Lloyd plans: 2 = tensor cores (tcgen05 kind::tf32,
+// 3xTF32) when the shape fits, else 1 = FP32 SIMT; the env var CSC_KMEANS_TC=0
+// or the tuning key "screen_tc" = 0 keeps the SIMT screen (A/B)
+int g_screen_tc = -1;
+bool screen_tc_enabled() {
+  if (g_screen_tc < 0) {
+    const char *e = getenv("CSC_KMEANS_TC");
+    g_screen_tc = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_screen_tc != 0;
+}
 
 // 0 (auto): 8x8 per thread, 16x8 threads (fastest at k = 64 in
 // tools/ab_assign.py), 8x4 when k <= 32, 8x7 with 16x16 threads (one pass)
@@ -1534,50 +1547,79 @@ __global__ void gated_repair_kernel(int32_t *__restrict__ labels, double *__rest
 // is summed over its run in row order by the extra warp.
 constexpr int kSortedMaxChunk = 8192;
 
+// Incremental mode (prev != nullptr, one column block): only the clusters
+// whose membership changed in this chunk since the previous update ("dirty":
+// some row of the chunk left or joined them; prev holds the labels of that
+// update and is refreshed here) are re-summed, from scratch in row order, so
+// every psum / pq entry always equals the fresh fixed-order sum of its
+// current members (bit-identical to recomputing all of them). Late Lloyd
+// iterations move few rows, so most chunks re-read little or nothing. The
+// caller zeroes psum / pcnt / pq and sets prev = -1 before the first update
+// of a run (no members anywhere).
 __global__ void update_sorted_kernel(const double *__restrict__ f,
                                      const int32_t *__restrict__ labels, int64_t n, int64_t d,
                                      int64_t ld, int64_t k, int64_t chunk, int cw,
                                      double *__restrict__ psum, int32_t *__restrict__ pcnt,
-                                     const double *__restrict__ fnorm, double *__restrict__ pq) {
+                                     const double *__restrict__ fnorm, double *__restrict__ pq,
+                                     int32_t *__restrict__ prev) {
   extern __shared__ int32_t us[];
-  int32_t *lab_s = us;             // [chunk] labels in sorted order
+  int32_t *lab_s = us;             // [chunk] labels in sorted order (dirty clusters only)
   int32_t *perm_s = lab_s + chunk;  // [chunk] row offsets in sorted order
   int32_t *cnt_s = perm_s + chunk;  // [k] rows per label
   int32_t *run_s = cnt_s + k;       // [k] insert position, then end of each run
+  int32_t *dirty_s = run_s + k;     // [k] membership changed (always 1 without prev)
+  __shared__ int len_s;
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t b = blockIdx.x;
   const int64_t col0 = (int64_t)blockIdx.y * cw;
   const int64_t rbeg = b * chunk;
   const int len = (int)max((int64_t)0, min(n, rbeg + chunk) - rbeg);
-  for (int64_t j = tid; j < k; j += blockDim.x) cnt_s[j] = 0;
+  for (int64_t j = tid; j < k; j += blockDim.x) {
+    cnt_s[j] = 0;
+    dirty_s[j] = prev ? 0 : 1;
+  }
   __syncthreads();
-  for (int p = tid; p < len; p += blockDim.x) atomicAdd(cnt_s + labels[rbeg + p], 1);
-  __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int64_t j = 0; j < k; ++j) {
-      run_s[j] = acc;
-      acc += cnt_s[j];
+  for (int p = tid; p < len; p += blockDim.x) {
+    const int l = labels[rbeg + p];
+    atomicAdd(cnt_s + l, 1);
+    if (prev) {
+      const int pl = prev[rbeg + p];
+      if (pl != l) {
+        dirty_s[l] = 1;
+        if (pl >= 0) dirty_s[pl] = 1;
+        prev[rbeg + p] = l;
+      }
     }
   }
   __syncthreads();
-  if (tid < 32) {  // stable scatter, 32 rows at a time in order
+  if (tid == 0) {  // runs of the dirty clusters only, in label order
+    int acc = 0;
+    for (int64_t j = 0; j < k; ++j) {
+      run_s[j] = acc;
+      if (dirty_s[j]) acc += cnt_s[j];
+    }
+    len_s = acc;
+  }
+  __syncthreads();
+  if (tid < 32) {  // stable scatter of the dirty clusters' rows, 32 rows at a time in order
     for (int g = 0; g < len; g += 32) {
       const int p = g + lane;
-      const int l = p < len ? labels[rbeg + p] : -1;
+      int l = p < len ? labels[rbeg + p] : -1;
+      if (l >= 0 && !dirty_s[l]) l = -1;
       const unsigned m = __match_any_sync(0xffffffffu, l);
       const int rank = __popc(m & ((1u << lane) - 1u));
-      if (p < len) {
+      if (l >= 0) {
         const int pos = run_s[l] + rank;
         perm_s[pos] = p;
         lab_s[pos] = l;
       }
       __syncwarp();
-      if (p < len && rank == __popc(m) - 1) run_s[l] += __popc(m);
+      if (l >= 0 && rank == __popc(m) - 1) run_s[l] += __popc(m);
       __syncwarp();
     }
   }
   __syncthreads();
+  const int dlen = len_s;
   const int c = tid;
   if (c < cw && col0 + c < d) {
     const double *fc = f + col0 + c;
@@ -1606,20 +1648,20 @@ __global__ void update_sorted_kernel(const double *__restrict__ f,
         run += v[u];
       }
     };
-    if (p + U <= len) load(p, va, la);
-    while (p + U <= len) {
-      const bool more = p + 2 * U <= len;
+    if (p + U <= dlen) load(p, va, la);
+    while (p + U <= dlen) {
+      const bool more = p + 2 * U <= dlen;
       if (more) load(p + U, vb, lb2);
       add(va, la);
       p += U;
       if (!more) break;
-      const bool more2 = p + 2 * U <= len;
+      const bool more2 = p + 2 * U <= dlen;
       if (more2) load(p + U, va, la);
       add(vb, lb2);
       p += U;
       if (!more2) break;
     }
-    for (; p < len; ++p) {
+    for (; p < dlen; ++p) {
       const int l = lab_s[p];
       const double v = fc[(rbeg + perm_s[p]) * ld];
       if (l != cur) {
@@ -1631,12 +1673,12 @@ __global__ void update_sorted_kernel(const double *__restrict__ f,
     }
     if (cur >= 0) out[(int64_t)cur * d] = run;
     for (int64_t j = 0; j < k; ++j)
-      if (cnt_s[j] == 0) out[j * d] = 0.0;
+      if (cnt_s[j] == 0 && dirty_s[j]) out[j * d] = 0.0;
   }
   if (blockIdx.y == 0 && tid >= (int)blockDim.x - 32) {
     for (int64_t j = lane; j < k; j += 32) {
       pcnt[b * k + j] = cnt_s[j];
-      if (pq) {
+      if (pq && dirty_s[j]) {
         const int end = run_s[j], beg = end - cnt_s[j];
         double q = 0.0;
         for (int pp = beg; pp < end; ++pp) q += fnorm[rbeg + perm_s[pp]];
@@ -1903,7 +1945,7 @@ struct csc_kmeans_plan {
   int64_t nb = 0, chunk = 0, cw = 0, ny = 0;
   void *base = nullptr;
   double *ub, *lb, *own, *psum, *pq, *S, *Q, *cterm, *delta, *shalf, *scal;
-  int32_t *cand, *flags, *pcnt;
+  int32_t *cand, *flags, *pcnt, *prev;
   size_t smem = 0;
   cudaStream_t stream = nullptr;
   // graph-resident loop (built on first csc_kmeans_run for a buffer set)
@@ -1921,6 +1963,9 @@ struct csc_kmeans_plan {
   double *cmax = nullptr;
   int32_t *amb = nullptr, *namb = nullptr;
   void *screen_base = nullptr;
+  // tensor-core screen (kmeans_screen_tc.cu): hi / lo centroid tiles
+  bool tc = false;
+  float *chi = nullptr, *clo = nullptr;
 };
 
 extern "C" {
@@ -1983,6 +2028,15 @@ int csc_kmeans_tuning(const char *key, int64_t value) {
   if (std::string(key) == "assign_ver") {
     CSC_REQUIRE(value == 2 || value == 3, "assign_ver must be 2 or 3");
     g_assign_ver = (int)value;
+    return CSC_OK;
+  }
+  if (std::string(key) == "update_incremental") {
+    g_update_incremental = value ? 1 : 0;
+    return CSC_OK;
+  }
+  if (std::string(key) == "screen_tc") {
+    screen_tc_enabled();
+    g_screen_tc = value ? 1 : 0;
     return CSC_OK;
   }
   if (std::string(key) == "assign_tn") {
@@ -2069,7 +2123,7 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   p->smem = sizeof(double) * k * (p->cw + kSqLanes) + sizeof(int32_t) * k;
   const size_t nd = (size_t)n, kk = (size_t)k;
   const size_t doubles = 3 * nd + (size_t)p->nb * kk * d + (size_t)p->nb * kk + kk * d + 4 * kk + 8;
-  const size_t ints = nd + 4 + (size_t)p->nb * kk;
+  const size_t ints = 2 * nd + 4 + (size_t)p->nb * kk;
   if (cudaMallocAsync(&p->base, doubles * 8 + ints * 4 + 64, st) != cudaSuccess) {
     delete p;
     csc::set_error("csc_kmeans_plan_create: allocation failed");
@@ -2090,14 +2144,15 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   int32_t *ip = reinterpret_cast<int32_t *>(dp);
   p->cand = ip; ip += nd;
   p->flags = ip; ip += 4;
-  p->pcnt = ip;
+  p->pcnt = ip; ip += (size_t)p->nb * kk;
+  p->prev = ip;
   CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t) * 4, st));
   CSC_TRY_CUDA(cudaFuncSetAttribute(update_partial_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
   if (p->chunk <= kSortedMaxChunk)
     CSC_TRY_CUDA(cudaFuncSetAttribute(
         update_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        (int)(sizeof(int32_t) * (2 * (size_t)p->chunk + 2 * (size_t)k))));
+        (int)(sizeof(int32_t) * (2 * (size_t)p->chunk + 3 * (size_t)k))));
   *out = p;
   return CSC_OK;
 }
@@ -2132,19 +2187,25 @@ int csc_kmeans_plan_set_screen(csc_kmeans_plan *p, const float *f32, int64_t ld3
               (long long)p->d, (long long)p->k);
   if (!p->screen_base) {
     const int64_t kpad = csc::screen_kpad(p->k);
-    const size_t bytes = sizeof(float) * (p->d * kpad + kpad) + 16 + sizeof(double) +
+    const bool tc_ok = csc::tc_screen_supported(p->d, p->k);
+    const int64_t tcf = tc_ok ? csc::tc_centroid_floats(p->d, p->k) : 0;
+    const int64_t c32 = std::max<int64_t>(p->d * kpad, 2 * tcf);
+    const size_t bytes = sizeof(float) * (c32 + std::max<int64_t>(kpad, 256)) + 16 + sizeof(double) +
                          sizeof(int32_t) * (p->n + 4) + 64;
     CSC_TRY_CUDA(cudaMallocAsync(&p->screen_base, bytes, p->stream));
     char *b = static_cast<char *>(p->screen_base);
     p->cmax = reinterpret_cast<double *>(b);
     b += 16;
     p->c32t = reinterpret_cast<float *>(b);
-    b += sizeof(float) * p->d * kpad;
+    p->chi = p->c32t;  // the two screens share the centroid scratch
+    p->clo = p->c32t + tcf;
+    b += sizeof(float) * c32;
     p->cn32 = reinterpret_cast<float *>(b);
-    b += sizeof(float) * kpad;
+    b += sizeof(float) * std::max<int64_t>(kpad, 256);
     p->namb = reinterpret_cast<int32_t *>(b);
     p->amb = p->namb + 4;
   }
+  p->tc = screen_tc_enabled() && csc::tc_screen_supported(p->d, p->k);
   p->f32 = f32;
   p->fn32 = fn32;
   p->ld32 = ld32;
@@ -2202,10 +2263,19 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
   auto screened = [&](const int32_t *rows, const int32_t *nrows, int32_t *cnts) -> int {
     if (!p->f32) return assign(rows, nrows, cnts, nullptr);
     CSC_TRY_CUDA(cudaMemsetAsync(p->namb, 0, sizeof(int32_t), st));
-    int r2 = csc::screen_convert_centroids(cent, k, d, ldc, cnorm, p->c32t, p->cn32, p->cmax, st);
-    if (r2 != CSC_OK) return r2;
-    r2 = csc::screen_assign(p->f32, p->ld32, p->fn32, fnorm, n, d, p->c32t, p->cn32, k, p->cmax,
-                            rows, nrows, labels, p->ub, p->lb, cnts, p->amb, p->namb, st);
+    int r2;
+    if (p->tc) {
+      r2 = csc::tc_convert_centroids(cent, k, d, ldc, cnorm, p->chi, p->clo, p->cn32, p->cmax, st);
+      if (r2 != CSC_OK) return r2;
+      r2 = csc::tc_screen_assign(p->f32, p->ld32, p->fn32, n, d, p->chi, p->clo, p->cn32, k,
+                                 p->cmax, rows, nrows, labels, p->ub, p->lb, cnts, p->amb, p->namb,
+                                 nullptr, st);
+    } else {
+      r2 = csc::screen_convert_centroids(cent, k, d, ldc, cnorm, p->c32t, p->cn32, p->cmax, st);
+      if (r2 != CSC_OK) return r2;
+      r2 = csc::screen_assign(p->f32, p->ld32, p->fn32, fnorm, n, d, p->c32t, p->cn32, k, p->cmax,
+                              rows, nrows, labels, p->ub, p->lb, cnts, p->amb, p->namb, st);
+    }
     if (r2 != CSC_OK) return r2;
     return assign(p->amb, p->namb, cnts, nullptr);
   };
@@ -2236,9 +2306,15 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
   // means, counts, movement, cost terms
   const int threads = (int)(csc::ceil_div(p->cw, 32) * 32 + 32);
   if (p->chunk <= kSortedMaxChunk) {
-    const size_t ssmem = sizeof(int32_t) * (2 * (size_t)p->chunk + 2 * (size_t)k);
+    const size_t ssmem = sizeof(int32_t) * (2 * (size_t)p->chunk + 3 * (size_t)k);
+    int32_t *prev = (p->ny == 1 && g_update_incremental) ? p->prev : nullptr;
+    if (prev && full) {  // a new run: no members anywhere yet
+      CSC_TRY_CUDA(cudaMemsetAsync(prev, 0xff, sizeof(int32_t) * n, st));
+      CSC_TRY_CUDA(cudaMemsetAsync(p->psum, 0, sizeof(double) * p->nb * k * d, st));
+      CSC_TRY_CUDA(cudaMemsetAsync(p->pq, 0, sizeof(double) * p->nb * k, st));
+    }
     update_sorted_kernel<<<dim3((unsigned)p->nb, (unsigned)p->ny), threads, ssmem, st>>>(
-        f, labels, n, d, ld, k, p->chunk, (int)p->cw, p->psum, p->pcnt, fnorm, p->pq);
+        f, labels, n, d, ld, k, p->chunk, (int)p->cw, p->psum, p->pcnt, fnorm, p->pq, prev);
   } else {
     update_partial_kernel<<<dim3((unsigned)p->nb, (unsigned)p->ny), threads, p->smem, st>>>(
         f, labels, n, d, ld, k, p->chunk, (int)p->cw, p->psum, p->pcnt, fnorm, p->pq);

@@ -22,11 +22,17 @@
 // sits at byte (c / 4) * ROWS * 16 + r * 16 + (c % 4) * 4 (16-byte K chunks,
 // the ROWS rows of a chunk contiguous), i.e. core matrices of 8 rows x 16 B
 // at SBO = 128 B along rows and LBO = ROWS * 16 B along K; one MMA (K = 8)
-// reads chunks 2s, 2s+1. Rows are gathered by index (Hamerly candidates) with
-// cp.async (one warp covers whole rows: coalesced), split into hi/lo in
-// shared memory, then one elected thread issues the 3 x K/8 MMAs and commits
-// them to an mbarrier; each of the 4 warps reads its 32 TMEM lanes (rows)
-// with tcgen05.ld and settles them.
+// reads chunks 2s, 2s+1.
+//
+// Pipeline (warp-specialised, persistent, one CTA per SM): two producer warps
+// gather the candidate rows' fp32 features by index with cp.async into a
+// 3-unit shared-memory ring (a unit = 128 rows x 32 columns) and split them
+// into hi / lo there; one elected thread issues the 3 x 4 MMAs of a unit into
+// one of two TMEM accumulators and commits them to the ring's "empty"
+// mbarrier (and, after a tile's last unit, to the accumulator's "full" one);
+// four epilogue warps read their 32 TMEM lanes (rows) with tcgen05.ld, settle
+// the rows and release the accumulator. Loads of tile i+2, MMAs of tile i+1
+// and the epilogue of tile i overlap.
 #include <mutex>
 #include <vector>
 
@@ -36,7 +42,7 @@
 namespace {
 
 constexpr int kTM = 128;       // rows per tile = UMMA M
-constexpr int kTThreads = 128; // warp w reads TMEM lanes 32w .. 32w + 31
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -157,7 +163,7 @@ __global__ void tc_centroids_kernel(const double *__restrict__ c, int64_t k, int
 }
 
 struct TcArgs {
-  const float *f32;
+  const float *f32;  // fp32 features (ld32, zero padding); split into hi / lo per unit
   int64_t ld32;
   const float *fn32;
   int64_t n;
@@ -173,163 +179,239 @@ struct TcArgs {
   float *raw_out;  // test hook: E (n x n_pad fp32) instead of the decision
 };
 
-template <int NP>  // padded centroid count = UMMA N (multiple of 16, <= 256)
-__global__ void __launch_bounds__(kTThreads, 1) tc_screen_kernel(TcArgs a) {
-  extern __shared__ __align__(128) uint8_t tsm[];
-  const int kp = a.kp, q4 = kp / 4;
-  float *Ahi = reinterpret_cast<float *>(tsm);
-  float *Alo = Ahi + (size_t)kTM * kp;
-  float *Bhi = Alo + (size_t)kTM * kp;
+// Warp roles: 0-3 epilogue (warp w reads TMEM lanes 32w..32w+31 = tile rows),
+// 4 MMA issue (one elected lane), 5 row producer (cp.async gathers of the
+// candidate rows' fp32 features into the ring, never blocking on its own
+// copies: each unit's completion arrives on the unit's "raw" mbarrier via
+// cp.async.mbarrier.arrive.noinc), 6-7 splitters (alternate units: wait for
+// the raw unit, split it into hi / lo in place, fence to the async proxy,
+// arrive on "split"). A unit = 128 rows x kKU columns of one tile; `stages`
+// units in a shared-memory ring (as many as fit, 3..6); two TMEM
+// accumulators (2 x NP columns) so the epilogue of tile i overlaps the MMAs
+// of tile i+1 and the gathers of the following units.
+constexpr int kKU = 32;                // columns per unit (4 MMA K steps)
+constexpr int kMaxStages = 6;
+constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp = 5, kSplitWarp0 = 6, kSplitWarps = 2;
+constexpr int kTcThreads = 32 * (kEpiWarps + 2 + kSplitWarps);  // 256
+constexpr uint32_t kUnitBytes = kTM * kKU * 4;                  // one of hi / lo
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar)
+               : "memory");
+}
+
+template <int NP>  // padded centroid count = UMMA N (multiple of 16, <= 128)
+__global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int stages) {
+  extern __shared__ __align__(1024) uint8_t tsm[];
+  const int kp = a.kp;
+  const int units = kp / kKU;  // per tile
+  uint8_t *ring = tsm;                                         // [stage][hi|lo][kUnitBytes]
+  float *Bhi = reinterpret_cast<float *>(ring + (size_t)stages * 2 * kUnitBytes);
   float *Blo = Bhi + (size_t)NP * kp;
-  float *Fn = Blo + (size_t)NP * kp;
-  float *Cn = Fn + kTM;
-  int32_t *Rid = reinterpret_cast<int32_t *>(Cn + NP);
-  int32_t *Hs = Rid + kTM;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(Hs + NP + (NP & 1));  // 8-byte aligned (NP even)
-  uint32_t *tmem_hold = reinterpret_cast<uint32_t *>(bar + 1);
+  float *Cn = Blo + (size_t)NP * kp;
+  int32_t *Hs = reinterpret_cast<int32_t *>(Cn + NP);
+  uint64_t *rawf = reinterpret_cast<uint64_t *>(Hs + NP);  // NP even: 8-byte aligned
+  uint64_t *full = rawf + kMaxStages;
+  uint64_t *empty = full + kMaxStages;
+  uint64_t *tfull = empty + kMaxStages;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_hold = reinterpret_cast<uint32_t *>(tempty + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t nr = a.nrows ? (int64_t)*a.nrows : a.n;
   const int64_t ntiles = (nr + kTM - 1) / kTM;
   if ((int64_t)blockIdx.x >= ntiles) return;
+  const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
-  constexpr uint32_t kCols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+  constexpr uint32_t kCols = 2 * NP <= 32 ? 32 : 2 * NP <= 64 ? 64 : 2 * NP <= 128 ? 128 : 256;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_hold)),
                  "r"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
-    mbar_init(smem_u32(bar), 1);
+  if (tid == 32) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(smem_u32(rawf + s), 32);  // the producer warp's cp.async arrivals (noinc)
+      mbar_init(smem_u32(full + s), 32);  // the unit's splitter warp
+      mbar_init(smem_u32(empty + s), 1);  // MMA commit
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(tfull + s), 1);          // MMA commit
+      mbar_init(smem_u32(tempty + s), kEpiWarps);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // centroid tiles (already in the canonical layout) and norms
-  {
+  {  // centroid tiles (already in the canonical layout) and norms
     const float4 *sh = reinterpret_cast<const float4 *>(a.chi);
     const float4 *sl = reinterpret_cast<const float4 *>(a.clo);
     float4 *dh = reinterpret_cast<float4 *>(Bhi);
     float4 *dl = reinterpret_cast<float4 *>(Blo);
-    for (int e = tid; e < NP * q4; e += kTThreads) {
+    for (int e = tid; e < NP * kp / 4; e += kTcThreads) {
       dh[e] = sh[e];
       dl[e] = sl[e];
     }
-    for (int j = tid; j < NP; j += kTThreads) {
+    for (int j = tid; j < NP; j += kTcThreads) {
       Cn[j] = a.cn32[j];
       Hs[j] = 0;
     }
   }
+  fence_async_smem();  // B tiles written by the generic proxy, read by the tensor core
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_hold;
-  const double cmax = *a.cmax;
-  const double dscale = (double)(3 * a.d + 8) * 1.1920928955078125e-7;  // (3d + 8) 2^-23
-  const uint32_t idesc = tf32_idesc(NP);
-  const uint32_t sA = smem_u32(Ahi), sAl = smem_u32(Alo), sB = smem_u32(Bhi), sBl = smem_u32(Blo);
-  const uint32_t lboA = kTM * 16, lboB = NP * 16, sbo = 128;
-  uint32_t phase = 0;
+  const int64_t nunits = my_tiles * units;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    {
-      const int64_t lr = tile * kTM + tid;
-      const int64_t gr = lr < nr ? (a.rows ? (int64_t)a.rows[lr] : lr) : -1;
-      Rid[tid] = (int32_t)gr;
-      Fn[tid] = gr >= 0 ? a.fn32[gr] : 0.0f;
-    }
-    __syncthreads();
-    // gather the tile's rows: element e = (row, 16-byte chunk), chunks of a row
-    // on consecutive threads (coalesced 16-byte pieces of one row)
-    for (int e = tid; e < kTM * q4; e += kTThreads) {
-      const int r = e / q4, q = e - r * q4;
-      const int32_t gr = Rid[r];
-      const bool ok = gr >= 0 && 4 * q < a.d;
-      cp_async16(sA + (uint32_t)(q * kTM + r) * 16, ok ? a.f32 + (int64_t)gr * a.ld32 + 4 * q : a.f32,
-                 ok);
+  if (warp == kProdWarp) {
+    // ===== producer: gathers only; completion is tracked by the unit's raw barrier
+    for (int64_t u = 0; u < nunits; ++u) {
+      const int s = (int)(u % stages);
+      if (u >= stages) mbar_wait(smem_u32(empty + s), (uint32_t)((u / stages - 1) & 1));
+      const int64_t tile = blockIdx.x + (u / units) * gridDim.x;
+      const int h = (int)(u % units);
+      const uint32_t shi = smem_u32(ring + (size_t)s * 2 * kUnitBytes);
+      // 128 rows x 8 chunks: chunk q of row r at q * 2048 + r * 16 (canonical K-major);
+      // the 8 chunks of a row (128 contiguous bytes) on 8 consecutive lanes
+      for (int e = lane; e < kTM * (kKU / 4); e += 32) {
+        const int r = e >> 3, q = e & 7;
+        const int64_t lr = tile * kTM + r;
+        const int64_t gr = lr < nr ? (a.rows ? (int64_t)__ldg(a.rows + lr) : lr) : -1;
+        const int col = h * kKU + 4 * q;
+        const bool ok = gr >= 0 && col < a.d;
+        cp_async16(shi + (uint32_t)(q * kTM + r) * 16, ok ? a.f32 + gr * a.ld32 + col : a.f32, ok);
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(rawf + s))
+                   : "memory");
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    // hi / lo split in place
-    for (int e = tid; e < kTM * kp; e += kTThreads) {
-      const float v = Ahi[e];
-      const float h = tf32_hi(v);
-      Ahi[e] = h;
-      Alo[e] = v - h;
-    }
-    fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-    __syncthreads();
-    tc_fence_after();
-    if (tid == 0) {
-      for (int s = 0; s < kp / 8; ++s) {
-        const uint32_t oa = (uint32_t)s * 2 * lboA, ob = (uint32_t)s * 2 * lboB;
-        const uint64_t ahi = umma_desc(sA + oa, lboA, sbo), alo = umma_desc(sAl + oa, lboA, sbo);
-        const uint64_t bhi = umma_desc(sB + ob, lboB, sbo), blo = umma_desc(sBl + ob, lboB, sbo);
-        mma_tf32(tmem, ahi, bhi, idesc, s > 0 ? 1u : 0u);
-        mma_tf32(tmem, alo, bhi, idesc, 1u);
-        mma_tf32(tmem, ahi, blo, idesc, 1u);
+  } else if (warp >= kSplitWarp0) {
+    // ===== splitters: unit u is split by warp 6 + (u & 1)
+    for (int64_t u = warp - kSplitWarp0; u < nunits; u += kSplitWarps) {
+      const int s = (int)(u % stages);
+      mbar_wait(smem_u32(rawf + s), (uint32_t)((u / stages) & 1));
+      float4 *ph = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes);
+      float4 *pl = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes + kUnitBytes);
+#pragma unroll 4
+      for (int e = lane; e < (int)(kUnitBytes / 16); e += 32) {
+        const float4 v = ph[e];
+        const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        ph[e] = hv;
+        pl[e] = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
       }
-      mma_commit(smem_u32(bar));
+      fence_async_smem();  // this thread's smem writes -> visible to the tensor core
+      mbar_arrive(smem_u32(full + s));
     }
-    mbar_wait(smem_u32(bar), phase);
-    phase ^= 1u;
-    tc_fence_after();
-    // epilogue: thread (warp w, lane l) owns row 32 w + l = TMEM lane
-    const int r = warp * 32 + lane;
-    const int32_t gr = Rid[r];
-    const float fni = Fn[r];
-    float bv = INFINITY, bv2 = INFINITY;
-    int bi = 0x7fffffff;
+  } else if (warp == kMmaWarp) {
+    // ===== MMA issue
+    const uint32_t idesc = tf32_idesc(NP);
+    const uint32_t sB = smem_u32(Bhi), sBl = smem_u32(Blo);
+    const uint32_t lboA = kTM * 16, lboB = NP * 16, sbo = 128;
+    int64_t u = 0;
+    for (int64_t i = 0; i < my_tiles; ++i) {
+      const int slot = (int)(i & 1);
+      if (i >= 2) mbar_wait(smem_u32(tempty + slot), (uint32_t)((i / 2 - 1) & 1));
+      tc_fence_after();
+      const uint32_t acc = tmem + (uint32_t)(slot * NP);
+      for (int h = 0; h < units; ++h, ++u) {
+        const int s = (int)(u % stages);
+        mbar_wait(smem_u32(full + s), (uint32_t)((u / stages) & 1));
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t shi = smem_u32(ring + (size_t)s * 2 * kUnitBytes), slo = shi + kUnitBytes;
 #pragma unroll
-    for (int c0 = 0; c0 < NP; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+          for (int ks = 0; ks < kKU / 8; ++ks) {
+            const uint32_t oa = (uint32_t)ks * 2 * lboA;
+            const uint32_t ob = (uint32_t)(h * (kKU / 8) + ks) * 2 * lboB;
+            const uint64_t ahi = umma_desc(shi + oa, lboA, sbo), alo = umma_desc(slo + oa, lboA, sbo);
+            const uint64_t bhi = umma_desc(sB + ob, lboB, sbo), blo = umma_desc(sBl + ob, lboB, sbo);
+            mma_tf32(acc, ahi, bhi, idesc, (h > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32(acc, alo, bhi, idesc, 1u);
+            mma_tf32(acc, ahi, blo, idesc, 1u);
+          }
+          mma_commit(smem_u32(empty + s));  // the ring slot is free once these MMAs ran
+          if (h == units - 1) mma_commit(smem_u32(tfull + slot));
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===== epilogue: thread (warp w, lane l) settles row 32 w + l of each tile
+    const double cmax = *a.cmax;
+    const double dscale = (double)(3 * a.d + 8) * 1.1920928955078125e-7;  // (3d + 8) 2^-23
+    for (int64_t i = 0; i < my_tiles; ++i) {
+      const int slot = (int)(i & 1);
+      const int64_t tile = blockIdx.x + i * gridDim.x;
+      const int64_t lr = tile * kTM + warp * 32 + lane;
+      const int64_t gr = lr < nr ? (a.rows ? (int64_t)__ldg(a.rows + lr) : lr) : -1;
+      const float fni = gr >= 0 ? __ldg(a.fn32 + gr) : 0.0f;
+      mbar_wait(smem_u32(tfull + slot), (uint32_t)((i / 2) & 1));
+      tc_fence_after();
+      float bv = INFINITY, bv2 = INFINITY;
+      int bi = 0x7fffffff;
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(slot * NP);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int cj = c0 + j;
-        const float e = fmaf(-2.0f, v[j], fni) + Cn[cj];
-        if (a.raw_out && gr >= 0) a.raw_out[(int64_t)gr * NP + cj] = e;
-        if (e < bv) {
-          bv2 = bv;
-          bv = e;
-          bi = cj;
+      for (int c0 = 0; c0 < NP; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int cj = c0 + j;
+          const float e = fmaf(-2.0f, v[j], fni) + Cn[cj];
+          if (a.raw_out && gr >= 0) a.raw_out[gr * NP + cj] = e;
+          if (e < bv) {
+            bv2 = bv;
+            bv = e;
+            bi = cj;
+          } else {
+            bv2 = fminf(bv2, e);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(tempty + slot));
+      if (gr >= 0 && !a.raw_out) {
+        const double fr = sqrt((double)fni * (1.0 + 2e-5)) + cmax;
+        const double delta = dscale * fr * fr * (1.0 + 1e-6);
+        const double e1 = (double)bv, e2 = (double)bv2;
+        if (e2 - e1 > 2.0 * delta) {
+          a.labels[gr] = bi;
+          a.ub[gr] = sqrt(fmax(e1 + delta, 0.0));
+          a.lb[gr] = sqrt(fmax(e2 - delta, 0.0));
+          if (a.counts) atomicAdd(Hs + bi, 1);
         } else {
-          bv2 = fminf(bv2, e);
+          a.amb[atomicAdd(a.namb, 1)] = (int32_t)gr;
         }
       }
     }
-    if (gr >= 0 && !a.raw_out) {
-      const double fr = sqrt((double)fni * (1.0 + 2e-5)) + cmax;
-      const double delta = dscale * fr * fr * (1.0 + 1e-6);
-      const double e1 = (double)bv, e2 = (double)bv2;
-      if (e2 - e1 > 2.0 * delta) {
-        a.labels[gr] = bi;
-        a.ub[gr] = sqrt(fmax(e1 + delta, 0.0));
-        a.lb[gr] = sqrt(fmax(e2 - delta, 0.0));
-        if (a.counts) atomicAdd(Hs + bi, 1);
-      } else {
-        a.amb[atomicAdd(a.namb, 1)] = gr;
-      }
-    }
-    tc_fence_before();
-    __syncthreads();  // TMEM read and smem tiles consumed before the next tile
-    tc_fence_after();
-  }
-  if (a.counts) {
-    for (int j = tid; j < a.k; j += kTThreads)
-      if (Hs[j]) atomicAdd(a.counts + j, Hs[j]);
   }
   tc_fence_before();
   __syncthreads();
+  if (a.counts)
+    for (int j = tid; j < a.k; j += kTcThreads)
+      if (Hs[j]) atomicAdd(a.counts + j, Hs[j]);
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
 int tc_npad(int64_t k) { return (int)((k + 15) / 16 * 16); }
-int tc_kp(int64_t d) { return (int)((d + 7) / 8 * 8); }
+int tc_kp(int64_t d) { return (int)((d + kKU - 1) / kKU * kKU); }
+
+size_t tc_smem_fixed(int64_t d, int64_t k) {
+  const int64_t kp = tc_kp(d), np = tc_npad(k);
+  return sizeof(float) * (2 * np * kp + np) + sizeof(int32_t) * np +
+         sizeof(uint64_t) * (3 * kMaxStages + 4) + 16 + 1024;
+}
+
+// ring units that fit next to the centroid tiles (>= 3 required)
+int tc_stages(int64_t d, int64_t k) {
+  const int64_t cap = (int64_t)csc::device_info().max_smem_optin;
+  const int64_t left = cap - (int64_t)tc_smem_fixed(d, k);
+  return (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(0, left / (2 * kUnitBytes)));
+}
 
 size_t tc_smem(int64_t d, int64_t k) {
-  const int64_t kp = tc_kp(d), np = tc_npad(k);
-  return sizeof(float) * (2 * kTM * kp + 2 * np * kp + kTM + np) + sizeof(int32_t) * (kTM + np + 2) +
-         16 + 128;
+  return (size_t)std::max(tc_stages(d, k), 3) * 2 * kUnitBytes + tc_smem_fixed(d, k);
 }
 
 template <int NP>
@@ -347,7 +429,7 @@ int tc_launch(const TcArgs &a, cudaStream_t st) {
   }
   const int64_t tiles = csc::ceil_div(a.n, kTM);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(csc::device_info().sm_count, tiles));
-  tc_screen_kernel<NP><<<(unsigned)grid, kTThreads, smem, st>>>(a);
+  tc_screen_kernel<NP><<<(unsigned)grid, kTcThreads, smem, st>>>(a, tc_stages(a.d, a.k));
   CSC_CHECK_LAUNCH();
   return CSC_OK;
 }
@@ -375,7 +457,7 @@ namespace csc {
 bool tc_screen_supported(int64_t d, int64_t k) {
   const csc::DeviceInfo &info = csc::device_info();
   return info.cc_major == 10 && d >= 1 && d <= 256 && k >= 2 && tc_npad(k) <= 128 &&
-         tc_smem(d, k) <= (size_t)info.max_smem_optin;
+         tc_stages(d, k) >= 3;
 }
 
 int64_t tc_centroid_floats(int64_t d, int64_t k) { return (int64_t)tc_npad(k) * tc_kp(d); }

@@ -18,6 +18,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -246,16 +247,22 @@ class _LloydPool:
                          self.ld32, ptr(self.fn32), stream_handle)
 
 
-_LLOYD_POOL: _LloydPool | None = None
+_LLOYD_POOL: _LloydPool | None = None  # the most recently used pool (tests / tools read it)
+_LLOYD_POOLS: "OrderedDict[tuple, _LloydPool]" = OrderedDict()
+POOL_SHAPES = 2  # per-shape pools kept (LRU): alternating shapes reuse their lanes and graphs
 
 
 def _lloyd_pool(n, d, ld, k, dev) -> _LloydPool:
     global _LLOYD_POOL
     key = (dev.index, n, d, ld, k)
-    if _LLOYD_POOL is None or _LLOYD_POOL.key != key:
-        _LLOYD_POOL = None
-        _LLOYD_POOL = _LloydPool(n, d, ld, k, dev)
-    return _LLOYD_POOL
+    pool = _LLOYD_POOLS.pop(key, None)
+    if pool is None:
+        while len(_LLOYD_POOLS) >= POOL_SHAPES:
+            _LLOYD_POOLS.popitem(last=False)
+        pool = _LloydPool(n, d, ld, k, dev)
+    _LLOYD_POOLS[key] = pool
+    _LLOYD_POOL = pool
+    return pool
 
 
 _POOL_LOCK = threading.Lock()  # the lanes / streams / buffers of the pool are shared state
@@ -310,7 +317,8 @@ class _FusedState:
         return self.out[R]
 
 
-_FUSED: _FusedState | None = None
+_FUSED: _FusedState | None = None  # the most recently used output buffers
+_FUSED_STATES: "OrderedDict[tuple, _FusedState]" = OrderedDict()
 LAST_FUSED_ITERS: list[int] = []  # diagnostics: Lloyd iterations per restart of the last fused call
 
 
@@ -326,9 +334,13 @@ def _run_fused(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children, d
     dev = blk.device
     n, ld = blk.shape
     key = (dev.index, n, d, ld, k)
-    if _FUSED is None or _FUSED.key != key:
-        _FUSED = None
-        _FUSED = _FusedState(n, d, ld, k, dev)
+    st = _FUSED_STATES.pop(key, None)
+    if st is None:
+        while len(_FUSED_STATES) >= 4:
+            _FUSED_STATES.popitem(last=False)
+        st = _FusedState(n, d, ld, k, dev)
+    _FUSED_STATES[key] = st
+    _FUSED = st
     R = len(children)
     labels, packed, cost, iters, seeds, flags = _FUSED.outputs(R)
     ldc = _FUSED.ldc

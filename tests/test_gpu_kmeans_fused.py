@@ -223,3 +223,41 @@ def test_fp32_screen_same_labels_as_fp64(P, n, d, k):
     ref_labels, _, ref_cost = O.kmeans(f, k, restarts=3, max_iters=40, tol=1e-6, seed=k)
     assert O.adjusted_rand(la, ref_labels) >= 0.999
     assert abs(np.sqrt(ca) - ref_cost) <= COST_TOL * ref_cost
+
+
+@pytest.mark.parametrize("n,d,k,spread", [(60000, 64, 48, 1.2), (50000, 96, 64, 3.0), (20000, 24, 40, 2.0),
+                                          (8000, 37, 50, 1.5), (40000, 96, 64, 6.0)])
+def test_tensor_core_screen_same_labels(P, n, d, k, spread):
+    """The tcgen05 (kind::tf32, 3xTF32) screen, the FP32 SIMT screen and the
+    FP64-only plan give bit-identical labels and cost (the screens decide only
+    rows their error bound proves); wide spreads put many rows near ties."""
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import upload_block
+    import importlib
+    KM = importlib.import_module("paper_1706_03591_b200.kmeans")
+    assert _native.lib().csc_kmeans_screen_supported(d, k)
+    f = blobs(n, d, k, spread, seed=d + k)
+    blk = upload_block(f)
+    kids = np.random.SeedSequence(d).spawn(2)
+    cfg = P.KmeansConfig(restarts=2, max_iters=30)
+    out = {}
+    try:
+        for mode in ("tc", "simt", "fp64"):
+            _native.call("csc_kmeans_tuning", b"screen_tc", 1 if mode == "tc" else 0)
+            KM.run_restarts(blk, d, k, cfg, kids, fused=False)  # builds the pool for this shape
+            pool = KM._LLOYD_POOL
+            for lane in pool.lanes:
+                if mode == "fp64":
+                    _native.call("csc_kmeans_plan_set_screen", lane.plan, None, 0, None)
+                else:
+                    _native.call("csc_kmeans_plan_set_screen", lane.plan, KM.ptr(pool.F32), pool.ld32,
+                                 KM.ptr(pool.fn32))
+            out[mode] = KM.run_restarts(blk, d, k, cfg, kids, fused=False)
+    finally:
+        _native.call("csc_kmeans_tuning", b"screen_tc", 1)
+        pool = KM._LLOYD_POOL
+        for lane in pool.lanes:
+            _native.call("csc_kmeans_plan_set_screen", lane.plan, KM.ptr(pool.F32), pool.ld32, KM.ptr(pool.fn32))
+    for mode in ("tc", "simt"):
+        assert np.array_equal(out[mode][0], out["fp64"][0]), mode
+        assert out[mode][1] == out["fp64"][1], mode

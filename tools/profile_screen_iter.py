@@ -32,20 +32,26 @@ ld32 = (d + 3) // 4 * 4
 F32 = torch.zeros((n, ld32), dtype=torch.float32, device=F.device)
 fn32 = torch.empty(n, dtype=torch.float32, device=F.device)
 _native.call("csc_kmeans_screen_prepare", ptr(F), n, d, F.shape[1], ptr(F32), ld32, ptr(fn32), stream())
-for on in (False, True):
-    if on:
+import sys as _sys  # noqa: E402
+ITERS = int(_sys.argv[1]) if len(_sys.argv) > 1 else 40
+for mode in ("fp64", "simt", "tc", "tc_full_update"):
+    _native.call("csc_kmeans_tuning", b"screen_tc", 1 if mode.startswith("tc") else 0)
+    _native.call("csc_kmeans_tuning", b"update_incremental", 0 if mode == "tc_full_update" else 1)
+    if mode == "fp64":
+        _native.call("csc_kmeans_plan_set_screen", plan, None, 0, None)
+    else:
         _native.call("csc_kmeans_plan_set_screen", plan, ptr(F32), ld32, ptr(fn32))
     ws.cent.copy_(seeds[0])
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        c2 = ws.lloyd(12, 1e-6)
+        c2 = ws.lloyd(ITERS, 1e-6)
         torch.cuda.synchronize()
     tot = collections.defaultdict(lambda: [0, 0.0])
     for e in prof.events():
         if e.device_type == torch.autograd.DeviceType.CUDA:
             tot[e.name[:60]][0] += 1
             tot[e.name[:60]][1] += e.time_range.elapsed_us()
-    print(f"screen={on}: cost2 {c2!r}")
-    for name, (c, us) in sorted(tot.items(), key=lambda x: -x[1][1])[:12]:
+    total = sum(v[1] for v in tot.values())
+    print(f"mode={mode}: cost2 {c2!r}  GPU total {total / 1e3:.2f} ms over {ITERS} iterations")
+    for name, (c, us) in sorted(tot.items(), key=lambda x: -x[1][1])[:10]:
         print(f"   {us:9.1f} us x{c:4d}  {name}")
-    cand = ctypes_c = None
