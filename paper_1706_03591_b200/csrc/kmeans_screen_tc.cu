@@ -180,10 +180,11 @@ struct TcArgs {
 };
 
 // Warp roles: 0-3 epilogue (warp w reads TMEM lanes 32w..32w+31 = tile rows),
-// 4 MMA issue (one elected lane), 5 row producer (cp.async gathers of the
-// candidate rows' fp32 features into the ring, never blocking on its own
-// copies: each unit's completion arrives on the unit's "raw" mbarrier via
-// cp.async.mbarrier.arrive.noinc), 6-7 splitters (alternate units: wait for
+// 4 MMA issue (one elected lane), 5-6 row producers (alternate tiles:
+// cp.async gathers of the candidate rows' fp32 features into the ring, the
+// tile's 128 row ids staged in shared memory, the next tile's prefetched;
+// never blocking on their own copies: each unit's completion arrives on the
+// unit's "raw" mbarrier via cp.async.mbarrier.arrive.noinc), 7-8 splitters (alternate units: wait for
 // the raw unit, split it into hi / lo in place, fence to the async proxy,
 // arrive on "split"). A unit = 128 rows x kKU columns of one tile; `stages`
 // units in a shared-memory ring (as many as fit, 3..6); two TMEM
@@ -191,8 +192,9 @@ struct TcArgs {
 // of tile i+1 and the gathers of the following units.
 constexpr int kKU = 32;                // columns per unit (4 MMA K steps)
 constexpr int kMaxStages = 6;
-constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp = 5, kSplitWarp0 = 6, kSplitWarps = 2;
-constexpr int kTcThreads = 32 * (kEpiWarps + 2 + kSplitWarps);  // 256
+constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2, kSplitWarp0 = 7,
+              kSplitWarps = 2;
+constexpr int kTcThreads = 32 * (kEpiWarps + 1 + kProdWarps + kSplitWarps);  // 288
 constexpr uint32_t kUnitBytes = kTM * kKU * 4;                  // one of hi / lo
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -210,7 +212,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   float *Blo = Bhi + (size_t)NP * kp;
   float *Cn = Blo + (size_t)NP * kp;
   int32_t *Hs = reinterpret_cast<int32_t *>(Cn + NP);
-  uint64_t *rawf = reinterpret_cast<uint64_t *>(Hs + NP);  // NP even: 8-byte aligned
+  int32_t *Rs = Hs + NP;                                  // [kProdWarps][kTM] row ids
+  uint64_t *rawf = reinterpret_cast<uint64_t *>(Rs + kProdWarps * kTM);  // 8-byte aligned
   uint64_t *full = rawf + kMaxStages;
   uint64_t *empty = full + kMaxStages;
   uint64_t *tfull = empty + kMaxStages;
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   }
   if (tid == 32) {
     for (int s = 0; s < stages; ++s) {
-      mbar_init(smem_u32(rawf + s), 32);  // the producer warp's cp.async arrivals (noinc)
+      mbar_init(smem_u32(rawf + s), 32);  // the unit's producer warp: cp.async arrivals (noinc)
       mbar_init(smem_u32(full + s), 32);  // the unit's splitter warp
       mbar_init(smem_u32(empty + s), 1);  // MMA commit
     }
@@ -262,26 +265,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   const uint32_t tmem = *tmem_hold;
   const int64_t nunits = my_tiles * units;
 
-  if (warp == kProdWarp) {
-    // ===== producer: gathers only; completion is tracked by the unit's raw barrier
-    for (int64_t u = 0; u < nunits; ++u) {
-      const int s = (int)(u % stages);
-      if (u >= stages) mbar_wait(smem_u32(empty + s), (uint32_t)((u / stages - 1) & 1));
-      const int64_t tile = blockIdx.x + (u / units) * gridDim.x;
-      const int h = (int)(u % units);
-      const uint32_t shi = smem_u32(ring + (size_t)s * 2 * kUnitBytes);
-      // 128 rows x 8 chunks: chunk q of row r at q * 2048 + r * 16 (canonical K-major);
-      // the 8 chunks of a row (128 contiguous bytes) on 8 consecutive lanes
-      for (int e = lane; e < kTM * (kKU / 4); e += 32) {
-        const int r = e >> 3, q = e & 7;
-        const int64_t lr = tile * kTM + r;
-        const int64_t gr = lr < nr ? (a.rows ? (int64_t)__ldg(a.rows + lr) : lr) : -1;
-        const int col = h * kKU + 4 * q;
-        const bool ok = gr >= 0 && col < a.d;
-        cp_async16(shi + (uint32_t)(q * kTM + r) * 16, ok ? a.f32 + gr * a.ld32 + col : a.f32, ok);
+  if (warp >= kProdWarp0 && warp < kProdWarp0 + kProdWarps) {
+    // ===== producers: tile i (all its units) by warp 5 + (i & 1); gathers only,
+    // completion is tracked by each unit's raw barrier. The next tile's 128 row
+    // ids are loaded into registers while this tile's copies are issued.
+    const int pw = warp - kProdWarp0;
+    int32_t *rid = Rs + pw * kTM;
+    int32_t rn[kTM / 32];
+    auto load_ids = [&](int64_t i) {
+      const int64_t tile = blockIdx.x + i * gridDim.x;
+#pragma unroll
+      for (int j = 0; j < kTM / 32; ++j) {
+        const int64_t lr = tile * kTM + lane + 32 * j;
+        rn[j] = lr < nr ? (a.rows ? __ldg(a.rows + lr) : (int32_t)lr) : -1;
       }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(rawf + s))
-                   : "memory");
+    };
+    if (pw < my_tiles) load_ids(pw);
+    for (int64_t i = pw; i < my_tiles; i += kProdWarps) {
+      __syncwarp();  // the previous tile's reads of rid are done
+#pragma unroll
+      for (int j = 0; j < kTM / 32; ++j) rid[lane + 32 * j] = rn[j];
+      __syncwarp();
+      if (i + kProdWarps < my_tiles) load_ids(i + kProdWarps);
+      for (int h = 0; h < units; ++h) {
+        const int64_t u = i * units + h;
+        const int s = (int)(u % stages);
+        if (u >= stages) mbar_wait(smem_u32(empty + s), (uint32_t)((u / stages - 1) & 1));
+        const uint32_t shi = smem_u32(ring + (size_t)s * 2 * kUnitBytes);
+        // 128 rows x 8 chunks: chunk q of row r at q * 2048 + r * 16 (canonical
+        // K-major); the 8 chunks of a row (128 contiguous bytes) on 8 consecutive lanes
+#pragma unroll 8
+        for (int e = lane; e < kTM * (kKU / 4); e += 32) {
+          const int r = e >> 3, q = e & 7;
+          const int32_t gr = rid[r];
+          const int col = h * kKU + 4 * q;
+          const bool ok = gr >= 0 && col < a.d;
+          cp_async16(shi + (uint32_t)(q * kTM + r) * 16, ok ? a.f32 + (int64_t)gr * a.ld32 + col : a.f32,
+                     ok);
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(rawf + s))
+                     : "memory");
+      }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= kSplitWarp0) {
@@ -399,7 +423,7 @@ int tc_kp(int64_t d) { return (int)((d + kKU - 1) / kKU * kKU); }
 
 size_t tc_smem_fixed(int64_t d, int64_t k) {
   const int64_t kp = tc_kp(d), np = tc_npad(k);
-  return sizeof(float) * (2 * np * kp + np) + sizeof(int32_t) * np +
+  return sizeof(float) * (2 * np * kp + np) + sizeof(int32_t) * (np + kProdWarps * kTM) +
          sizeof(uint64_t) * (3 * kMaxStages + 4) + 16 + 1024;
 }
 

@@ -34,7 +34,8 @@ fn32 = torch.empty(n, dtype=torch.float32, device=F.device)
 _native.call("csc_kmeans_screen_prepare", ptr(F), n, d, F.shape[1], ptr(F32), ld32, ptr(fn32), stream())
 import sys as _sys  # noqa: E402
 ITERS = int(_sys.argv[1]) if len(_sys.argv) > 1 else 40
-for mode in ("fp64", "simt", "tc", "tc_full_update"):
+MODES = _sys.argv[2].split(",") if len(_sys.argv) > 2 else ["fp64", "simt", "tc", "tc_full_update"]
+for mode in MODES:
     _native.call("csc_kmeans_tuning", b"screen_tc", 1 if mode.startswith("tc") else 0)
     _native.call("csc_kmeans_tuning", b"update_incremental", 0 if mode == "tc_full_update" else 1)
     if mode == "fp64":
@@ -55,3 +56,11 @@ for mode in ("fp64", "simt", "tc", "tc_full_update"):
     print(f"mode={mode}: cost2 {c2!r}  GPU total {total / 1e3:.2f} ms over {ITERS} iterations")
     for name, (c, us) in sorted(tot.items(), key=lambda x: -x[1][1])[:10]:
         print(f"   {us:9.1f} us x{c:4d}  {name}")
+    seq = collections.defaultdict(list)
+    for e in sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
+                    key=lambda e: e.time_range.start):
+        for key in ("update_sorted", "screen_kernel", "tc_screen"):
+            if key in e.name:
+                seq[key].append(round(e.time_range.elapsed_us()))
+    for key, v in seq.items():
+        print(f"   per-iteration {key}: {v[:6]} ... {v[-6:]}")
