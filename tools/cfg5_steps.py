@@ -1,0 +1,68 @@
+"""Per-phase times of configs[4] dynamic steps (tools only): like bench.py's
+dynamic_cfg5 but with a device synchronisation at every phase mark, so the
+phase split is exact; also the k-means restarts' iteration counts.
+
+    python tools/cfg5_steps.py [--steps 4] [--p 0.5] [--churn 0.01]
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1706_03591_b200 as P  # noqa: E402
+from paper_1706_03591_b200 import generators as G  # noqa: E402
+import importlib  # noqa: E402
+
+K = importlib.import_module("paper_1706_03591_b200.kmeans")
+D = importlib.import_module("paper_1706_03591_b200.dynamic")
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=4)
+ap.add_argument("--p", type=float, default=0.5)
+ap.add_argument("--churn", type=float, default=0.01)
+a = ap.parse_args()
+w = bench.WORKLOADS["cfg5"]
+n, k, d = w["n"], w["k"], w["d"]
+q1, q2 = G.sbm_probabilities(n, k, w["deg"], w["ratio"])
+codes = G.planted_partition_codes(n, k, q1, q2, w["seed"])
+labels = np.repeat(np.arange(k), G.block_sizes(n, k))
+g = G.graph_from_codes(n, codes)
+deltas, cur = [], codes
+for s in range(a.steps):
+    dl, il = G.edge_churn(cur, n, labels, q1, q2, a.churn, seed=50 + s)
+    deltas.append((dl, il))
+    cur = np.union1d(np.setdiff1d(cur, dl, assume_unique=True), il)
+cfg = P.DynamicConfig(k=k, d=d, p=a.p, filter=P.FilterConfig(order=w["order"]))
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+_, state, diag0 = P.dynamic_init(g, cfg, seed=0)
+torch.cuda.synchronize()
+print(f"init {(time.perf_counter() - t0) * 1e3:.1f} ms, search iters {diag0.search_iters}", flush=True)
+orig_time = D.time.perf_counter
+
+
+def synced():
+    torch.cuda.synchronize()
+    return orig_time()
+
+
+D.time.perf_counter = synced  # phase marks after a device sync (tools only)
+for dl, il in deltas:
+    ph = {}
+    torch.cuda.synchronize()
+    t0 = orig_time()
+    g = g.apply_delta(dl, il)
+    torch.cuda.synchronize()
+    t1 = orig_time()
+    asg, state, diag = P.dynamic_step(state, g, cfg, timings=ph)
+    torch.cuda.synchronize()
+    t2 = orig_time()
+    pool = K._LLOYD_POOL
+    its = [int(pool.lanes[i].out[1].item()) for i in range(cfg.kmeans.restarts)] if pool else []
+    print(f"step {(t2 - t0) * 1e3:.1f} ms: delta {(t1 - t0) * 1e3:.1f} "
+          + " ".join(f"{kk} {v:.1f}" for kk, v in ph.items())
+          + f" | refined {diag.refined} | kmeans iters {its}", flush=True)

@@ -32,6 +32,8 @@ ld32 = (d + 3) // 4 * 4
 F32 = torch.zeros((n, ld32), dtype=torch.float32, device=F.device)
 fn32 = torch.empty(n, dtype=torch.float32, device=F.device)
 _native.call("csc_kmeans_screen_prepare", ptr(F), n, d, F.shape[1], ptr(F32), ld32, ptr(fn32), stream())
+Fsplit = torch.empty((n, int(_native.lib().csc_kmeans_split_stride(d))), dtype=torch.float32, device=F.device)
+_native.call("csc_kmeans_screen_split", ptr(F), n, d, F.shape[1], ptr(Fsplit), stream())
 import sys as _sys  # noqa: E402
 ITERS = int(_sys.argv[1]) if len(_sys.argv) > 1 else 40
 MODES = _sys.argv[2].split(",") if len(_sys.argv) > 2 else ["fp64", "simt", "tc", "tc_full_update"]
@@ -42,6 +44,7 @@ for mode in MODES:
         _native.call("csc_kmeans_plan_set_screen", plan, None, 0, None)
     else:
         _native.call("csc_kmeans_plan_set_screen", plan, ptr(F32), ld32, ptr(fn32))
+        _native.call("csc_kmeans_plan_set_split", plan, ptr(Fsplit) if mode.startswith("tc") else None)
     ws.cent.copy_(seeds[0])
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
@@ -59,8 +62,35 @@ for mode in MODES:
     seq = collections.defaultdict(list)
     for e in sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
                     key=lambda e: e.time_range.start):
-        for key in ("update_sorted", "screen_kernel", "tc_screen"):
+        for key in ("update_sorted", "screen_kernel", "assign3"):
             if key in e.name:
                 seq[key].append(round(e.time_range.elapsed_us()))
+                break
     for key, v in seq.items():
         print(f"   per-iteration {key}: {v[:6]} ... {v[-6:]}")
+
+# label changes per iteration (host diff of the labels after each iteration) and
+# the fraction of (chunk, cluster) partial sums they dirty (chunk = the plan's)
+if "changes" in MODES:
+    _native.call("csc_kmeans_tuning", b"screen_tc", 1)
+    _native.call("csc_kmeans_plan_set_screen", plan, ptr(F32), ld32, ptr(fn32))
+    _native.call("csc_kmeans_plan_set_split", plan, ptr(Fsplit))
+    ws.cent.copy_(seeds[0])
+    _native.call("csc_kmeans_rownorms", ptr(ws.cent), k, d, ws.ldc, ptr(ws.cnorm), stream())
+    ws.labels.zero_()
+    nb = max(1, min(148 * 8, -(-n // 64)))
+    chunk = -(-n // nb)
+    prev = None
+    out = []
+    for it in range(ITERS):
+        _native.call("csc_kmeans_iterate", plan, ptr(ws.blk), ptr(ws.fnorm), ptr(ws.cent), ws.ldc, ptr(ws.cnorm),
+                     ptr(ws.labels), ptr(ws.counts), int(it == 0), ptr(ws.scalars[1:]), stream())
+        lab = ws.labels.cpu().numpy().astype(np.int64)
+        if prev is not None:
+            ch = np.flatnonzero(lab != prev)
+            blocks = ch // chunk
+            pairs = np.unique(np.concatenate([blocks * k + lab[ch], blocks * k + prev[ch]]))
+            out.append((it, ch.size, pairs.size / (nb * k)))
+        prev = lab
+    for it, c, frac in out[::max(1, len(out) // 12)]:
+        print(f"   iter {it}: {c} rows changed, dirty (chunk, cluster) fraction {frac:.3f}")
