@@ -264,17 +264,6 @@ int csc_kmeans_fused_trace(unsigned long long *trace_dev, int64_t iters_cap);
  * whenever f changes. set_screen(): the plan uses these buffers from now on
  * (NULL f32 disables); they must stay valid while the plan runs. */
 int csc_kmeans_screen_supported(int64_t d, int64_t k);
-/* Tensor-core screen (tcgen05 kind::tf32, 3xTF32) of the Lloyd plans: used
- * when csc_kmeans_tc_supported(d, k) and the plan has pre-split features
- * (csc_kmeans_plan_set_split) and an FP32 screen (csc_kmeans_plan_set_screen:
- * its fp32 norms); labels stay bit-identical to the FP64 assignment.
- * csc_kmeans_screen_split writes f (fp64, n x d, ld) as per-row [hi 32 | lo 32]
- * float blocks per 32-column unit, row stride csc_kmeans_split_stride(d). */
-int csc_kmeans_tc_supported(int64_t d, int64_t k);
-int64_t csc_kmeans_split_stride(int64_t d);
-int csc_kmeans_screen_split(const double *f_dev, int64_t n, int64_t d, int64_t ld, float *fsplit_dev,
-                            void *stream);
-int csc_kmeans_plan_set_split(csc_kmeans_plan *plan, const float *fsplit_dev);
 /* Test hook of the tensor-core (tcgen05 kind::tf32, 3xTF32) screen: e_out
  * (n x roundup(k, 16) fp32, row-major) = |f32_i|^2 - 2 f_i.c_j + |c_j|^2 as
  * the screen computes it, from fp32 features (ld32 % 4 == 0, padding zero),

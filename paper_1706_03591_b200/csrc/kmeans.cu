@@ -1966,7 +1966,6 @@ struct csc_kmeans_plan {
   // tensor-core screen (kmeans_screen_tc.cu): hi / lo centroid tiles
   bool tc = false;
   float *chi = nullptr, *clo = nullptr;
-  const float *fsplit = nullptr;  // caller's pre-split features (csc_kmeans_screen_split)
 };
 
 extern "C" {
@@ -2213,29 +2212,6 @@ int csc_kmeans_plan_set_screen(csc_kmeans_plan *p, const float *f32, int64_t ld3
   return CSC_OK;
 }
 
-int csc_kmeans_tc_supported(int64_t d, int64_t k) {
-  return csc::tc_screen_supported(d, k) ? 1 : 0;
-}
-
-int64_t csc_kmeans_split_stride(int64_t d) { return csc::tc_split_stride(d); }
-
-int csc_kmeans_screen_split(const double *f, int64_t n, int64_t d, int64_t ld, float *fsplit,
-                            void *stream) {
-  csc::clear_error();
-  CSC_REQUIRE(f && fsplit && n >= 1 && d >= 1 && ld >= d &&
-                  (reinterpret_cast<uintptr_t>(fsplit) & 15u) == 0,
-              "csc_kmeans_screen_split: bad arguments");
-  return csc::tc_split_features(f, true, n, d, ld, fsplit, static_cast<cudaStream_t>(stream));
-}
-
-int csc_kmeans_plan_set_split(csc_kmeans_plan *p, const float *fsplit) {
-  CSC_REQUIRE(p != nullptr, "csc_kmeans_plan_set_split: NULL plan");
-  CSC_REQUIRE(fsplit == nullptr || (reinterpret_cast<uintptr_t>(fsplit) & 15u) == 0,
-              "csc_kmeans_plan_set_split: buffer must be 16-byte aligned");
-  p->fsplit = fsplit;
-  return CSC_OK;
-}
-
 int csc_kmeans_plan_stats(const csc_kmeans_plan *p, int64_t *candidates, int32_t *gated) {
   CSC_REQUIRE(p != nullptr, "csc_kmeans_plan_stats: NULL plan");
   int32_t h[4] = {0, 0, 0, 0};
@@ -2288,10 +2264,10 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
     if (!p->f32) return assign(rows, nrows, cnts, nullptr);
     CSC_TRY_CUDA(cudaMemsetAsync(p->namb, 0, sizeof(int32_t), st));
     int r2;
-    if (p->tc && p->fsplit) {
+    if (p->tc) {
       r2 = csc::tc_convert_centroids(cent, k, d, ldc, cnorm, p->chi, p->clo, p->cn32, p->cmax, st);
       if (r2 != CSC_OK) return r2;
-      r2 = csc::tc_screen_assign(p->fsplit, csc::tc_split_stride(d), p->fn32, n, d, p->chi, p->clo, p->cn32, k,
+      r2 = csc::tc_screen_assign(p->f32, p->ld32, p->fn32, n, d, p->chi, p->clo, p->cn32, k,
                                  p->cmax, rows, nrows, labels, p->ub, p->lb, cnts, p->amb, p->namb,
                                  nullptr, st);
     } else {

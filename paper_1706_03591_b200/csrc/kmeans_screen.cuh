@@ -37,11 +37,7 @@ bool tc_screen_supported(int64_t d, int64_t k);
 int64_t tc_centroid_floats(int64_t d, int64_t k);
 int tc_convert_centroids(const double *c, int64_t k, int64_t d, int64_t ldc, const double *cnorm,
                          float *chi, float *clo, float *cn32, double *cmax, cudaStream_t st);
-// features split once per call into [hi 32 | lo 32] per 32-column unit
-int64_t tc_split_stride(int64_t d);
-int tc_split_features(const void *f, bool fp64, int64_t n, int64_t d, int64_t ld, float *fs,
-                      cudaStream_t st);
-int tc_screen_assign(const float *fs, int64_t lds, const float *fn32, int64_t n, int64_t d,
+int tc_screen_assign(const float *f32, int64_t ld32, const float *fn32, int64_t n, int64_t d,
                      const float *chi, const float *clo, const float *cn32, int64_t k,
                      const double *cmax, const int32_t *rows, const int32_t *nrows_dev,
                      int32_t *labels, double *ub, double *lb, int32_t *counts, int32_t *amb,

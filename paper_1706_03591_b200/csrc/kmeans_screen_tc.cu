@@ -24,15 +24,15 @@
 // at SBO = 128 B along rows and LBO = ROWS * 16 B along K; one MMA (K = 8)
 // reads chunks 2s, 2s+1.
 //
-// Pipeline (warp-specialised, persistent, one CTA per SM): two producer
-// warps gather the candidate rows' pre-split hi / lo features by index with
-// cp.async into a shared-memory ring of units (a unit = 128 rows x 32
-// columns, hi and lo); one elected thread issues the 3 x 4 MMAs of a unit
-// into one of two TMEM accumulators and commits them to the ring's "empty"
+// Pipeline (warp-specialised, persistent, one CTA per SM): two producer warps
+// gather the candidate rows' fp32 features by index with cp.async into a
+// 3-unit shared-memory ring (a unit = 128 rows x 32 columns) and split them
+// into hi / lo there; one elected thread issues the 3 x 4 MMAs of a unit into
+// one of two TMEM accumulators and commits them to the ring's "empty"
 // mbarrier (and, after a tile's last unit, to the accumulator's "full" one);
 // four epilogue warps read their 32 TMEM lanes (rows) with tcgen05.ld, settle
-// the rows and release the accumulator. Loads of later units, MMAs of tile
-// i+1 and the epilogue of tile i overlap.
+// the rows and release the accumulator. Loads of tile i+2, MMAs of tile i+1
+// and the epilogue of tile i overlap.
 #include <mutex>
 #include <vector>
 
@@ -41,8 +41,7 @@
 
 namespace {
 
-constexpr int kTM = 128;  // rows per tile = UMMA M
-constexpr int kKU = 32;   // columns per ring unit (4 MMA K steps)
+constexpr int kTM = 128;       // rows per tile = UMMA M
 
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -163,27 +162,9 @@ __global__ void tc_centroids_kernel(const double *__restrict__ c, int64_t k, int
   }
 }
 
-// F (fp64 or fp32 rows, ld) -> per-row [hi 32 | lo 32] per 32-column unit
-// (row stride 2 kp floats, zero past d): hi = fp32(f) with the 13 low
-// mantissa bits cleared (a tf32), lo = fp32(f) - hi (exact)
-template <typename T>
-__global__ void tc_split_kernel(const T *__restrict__ f, int64_t n, int64_t d, int64_t ld, int kp,
-                                float *__restrict__ fs) {
-  const int64_t per_row = kp;  // (unit, column) pairs
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * per_row;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / per_row, c = e - r * per_row;
-    const float v = c < d ? (float)f[r * ld + c] : 0.0f;
-    const float h = tf32_hi(v);
-    float *row = fs + r * 2 * (int64_t)kp + (c / kKU) * 2 * kKU;
-    row[c % kKU] = h;
-    row[kKU + c % kKU] = v - h;
-  }
-}
-
 struct TcArgs {
-  const float *fs;  // features pre-split per 32-column unit: [hi 32 | lo 32] ..., row stride 2 kp
-  int64_t lds;
+  const float *f32;  // fp32 features (ld32, zero padding); split into hi / lo per unit
+  int64_t ld32;
   const float *fn32;
   int64_t n;
   int d, kp, k, n_pad;
@@ -200,19 +181,20 @@ struct TcArgs {
 
 // Warp roles: 0-3 epilogue (warp w reads TMEM lanes 32w..32w+31 = tile rows),
 // 4 MMA issue (one elected lane), 5-6 row producers (alternate tiles:
-// cp.async gathers of the candidate rows' pre-split hi / lo features into the
-// ring, the tile's 128 row ids staged in shared memory, the next tile's
-// prefetched; never blocking on their own copies: each unit's completion
-// arrives on the unit's mbarrier via cp.async.mbarrier.arrive.noinc). The
-// features are split into hi / lo once per k-means call
-// (csc_kmeans_screen_split), so a unit goes from HBM straight to the tensor
-// core. A unit = 128 rows x kKU columns of one tile (hi and lo); `stages`
+// cp.async gathers of the candidate rows' fp32 features into the ring, the
+// tile's 128 row ids staged in shared memory, the next tile's prefetched;
+// never blocking on their own copies: each unit's completion arrives on the
+// unit's "raw" mbarrier via cp.async.mbarrier.arrive.noinc), 7-8 splitters (alternate units: wait for
+// the raw unit, split it into hi / lo in place, fence to the async proxy,
+// arrive on "split"). A unit = 128 rows x kKU columns of one tile; `stages`
 // units in a shared-memory ring (as many as fit, 3..6); two TMEM
 // accumulators (2 x NP columns) so the epilogue of tile i overlaps the MMAs
 // of tile i+1 and the gathers of the following units.
+constexpr int kKU = 32;                // columns per unit (4 MMA K steps)
 constexpr int kMaxStages = 6;
-constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2;
-constexpr int kTcThreads = 32 * (kEpiWarps + 1 + kProdWarps);  // 224
+constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2, kSplitWarp0 = 7,
+              kSplitWarps = 2;
+constexpr int kTcThreads = 32 * (kEpiWarps + 1 + kProdWarps + kSplitWarps);  // 288
 constexpr uint32_t kUnitBytes = kTM * kKU * 4;                  // one of hi / lo
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -232,7 +214,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   int32_t *Hs = reinterpret_cast<int32_t *>(Cn + NP);
   int32_t *Rs = Hs + NP;                                  // [kProdWarps][kTM] row ids
   uint64_t *rawf = reinterpret_cast<uint64_t *>(Rs + kProdWarps * kTM);  // 8-byte aligned
-  uint64_t *empty = rawf + kMaxStages;
+  uint64_t *full = rawf + kMaxStages;
+  uint64_t *empty = full + kMaxStages;
   uint64_t *tfull = empty + kMaxStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_hold = reinterpret_cast<uint32_t *>(tempty + 2);
@@ -252,6 +235,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   if (tid == 32) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(smem_u32(rawf + s), 32);  // the unit's producer warp: cp.async arrivals (noinc)
+      mbar_init(smem_u32(full + s), 32);  // the unit's splitter warp
       mbar_init(smem_u32(empty + s), 1);  // MMA commit
     }
     for (int s = 0; s < 2; ++s) {
@@ -314,17 +298,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
         for (int e = lane; e < kTM * (kKU / 4); e += 32) {
           const int r = e >> 3, q = e & 7;
           const int32_t gr = rid[r];
-          const bool ok = gr >= 0;
-          const float *src = ok ? a.fs + (int64_t)gr * a.lds + h * 2 * kKU + 4 * q : a.fs;
-          const uint32_t so = (uint32_t)(q * kTM + r) * 16;
-          cp_async16(shi + so, src, ok);
-          cp_async16(shi + kUnitBytes + so, ok ? src + kKU : a.fs, ok);
+          const int col = h * kKU + 4 * q;
+          const bool ok = gr >= 0 && col < a.d;
+          cp_async16(shi + (uint32_t)(q * kTM + r) * 16, ok ? a.f32 + (int64_t)gr * a.ld32 + col : a.f32,
+                     ok);
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(rawf + s))
                      : "memory");
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp >= kSplitWarp0) {
+    // ===== splitters: unit u is split by warp 6 + (u & 1)
+    for (int64_t u = warp - kSplitWarp0; u < nunits; u += kSplitWarps) {
+      const int s = (int)(u % stages);
+      mbar_wait(smem_u32(rawf + s), (uint32_t)((u / stages) & 1));
+      float4 *ph = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes);
+      float4 *pl = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes + kUnitBytes);
+#pragma unroll 4
+      for (int e = lane; e < (int)(kUnitBytes / 16); e += 32) {
+        const float4 v = ph[e];
+        const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        ph[e] = hv;
+        pl[e] = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
+      }
+      fence_async_smem();  // this thread's smem writes -> visible to the tensor core
+      mbar_arrive(smem_u32(full + s));
+    }
   } else if (warp == kMmaWarp) {
     // ===== MMA issue
     const uint32_t idesc = tf32_idesc(NP);
@@ -338,8 +338,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
       const uint32_t acc = tmem + (uint32_t)(slot * NP);
       for (int h = 0; h < units; ++h, ++u) {
         const int s = (int)(u % stages);
-        mbar_wait(smem_u32(rawf + s), (uint32_t)((u / stages) & 1));
-        fence_async_smem();  // the producers' cp.async writes -> the tensor core's proxy
+        mbar_wait(smem_u32(full + s), (uint32_t)((u / stages) & 1));
         tc_fence_after();
         if (lane == 0) {
           const uint32_t shi = smem_u32(ring + (size_t)s * 2 * kUnitBytes), slo = shi + kUnitBytes;
@@ -425,7 +424,7 @@ int tc_kp(int64_t d) { return (int)((d + kKU - 1) / kKU * kKU); }
 size_t tc_smem_fixed(int64_t d, int64_t k) {
   const int64_t kp = tc_kp(d), np = tc_npad(k);
   return sizeof(float) * (2 * np * kp + np) + sizeof(int32_t) * (np + kProdWarps * kTM) +
-         sizeof(uint64_t) * (2 * kMaxStages + 4) + 16 + 1024;
+         sizeof(uint64_t) * (3 * kMaxStages + 4) + 16 + 1024;
 }
 
 // ring units that fit next to the centroid tiles (>= 3 required)
@@ -487,21 +486,6 @@ bool tc_screen_supported(int64_t d, int64_t k) {
 
 int64_t tc_centroid_floats(int64_t d, int64_t k) { return (int64_t)tc_npad(k) * tc_kp(d); }
 
-int64_t tc_split_stride(int64_t d) { return 2 * (int64_t)tc_kp(d); }
-
-int tc_split_features(const void *f, bool fp64, int64_t n, int64_t d, int64_t ld, float *fs,
-                      cudaStream_t st) {
-  const int64_t total = n * tc_kp(d);
-  const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>(csc::device_info().sm_count * 16, csc::ceil_div(total, 256)));
-  if (fp64)
-    tc_split_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double *>(f), n, d, ld, tc_kp(d), fs);
-  else
-    tc_split_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float *>(f), n, d, ld, tc_kp(d), fs);
-  CSC_CHECK_LAUNCH();
-  return CSC_OK;
-}
-
 int tc_convert_centroids(const double *c, int64_t k, int64_t d, int64_t ldc, const double *cnorm,
                          float *chi, float *clo, float *cn32, double *cmax, cudaStream_t st) {
   tc_centroids_kernel<<<1, 256, 0, st>>>(c, k, d, ldc, cnorm, tc_npad(k), tc_kp(d), chi, clo, cn32,
@@ -510,14 +494,14 @@ int tc_convert_centroids(const double *c, int64_t k, int64_t d, int64_t ldc, con
   return CSC_OK;
 }
 
-int tc_screen_assign(const float *fs, int64_t lds, const float *fn32, int64_t n, int64_t d,
+int tc_screen_assign(const float *f32, int64_t ld32, const float *fn32, int64_t n, int64_t d,
                      const float *chi, const float *clo, const float *cn32, int64_t k,
                      const double *cmax, const int32_t *rows, const int32_t *nrows_dev,
                      int32_t *labels, double *ub, double *lb, int32_t *counts, int32_t *amb,
                      int32_t *namb, float *raw_out, cudaStream_t st) {
   TcArgs a{};
-  a.fs = fs;
-  a.lds = lds;
+  a.f32 = f32;
+  a.ld32 = ld32;
   a.fn32 = fn32;
   a.n = n;
   a.d = (int)d;
@@ -550,20 +534,17 @@ extern "C" int csc_kmeans_tc_distances(const void *f32, int64_t n, int64_t d, in
               "outside the tensor-core screen", (long long)d, (long long)k);
   CSC_REQUIRE(ld32 % 4 == 0 && ld32 >= d, "csc_kmeans_tc_distances: ld32 must be a multiple of 4 >= d");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  csc::Scratch chi, clo, cn, cm, fsp;
+  csc::Scratch chi, clo, cn, cm;
   const int64_t cf = csc::tc_centroid_floats(d, k);
   CSC_TRY_CUDA(chi.alloc(sizeof(float) * cf, st));
   CSC_TRY_CUDA(clo.alloc(sizeof(float) * cf, st));
   CSC_TRY_CUDA(cn.alloc(sizeof(float) * tc_npad(k), st));
   CSC_TRY_CUDA(cm.alloc(sizeof(double), st));
-  CSC_TRY_CUDA(fsp.alloc(sizeof(float) * n * csc::tc_split_stride(d), st));
-  int rc = csc::tc_split_features(f32, false, n, d, ld32, fsp.as<float>(), st);
+  int rc = csc::tc_convert_centroids(c, k, d, ldc, cnorm, chi.as<float>(), clo.as<float>(),
+                                     cn.as<float>(), cm.as<double>(), st);
   if (rc != CSC_OK) return rc;
-  rc = csc::tc_convert_centroids(c, k, d, ldc, cnorm, chi.as<float>(), clo.as<float>(),
-                                 cn.as<float>(), cm.as<double>(), st);
-  if (rc != CSC_OK) return rc;
-  return csc::tc_screen_assign(fsp.as<float>(), csc::tc_split_stride(d), fn32, n, d,
-                               chi.as<float>(), clo.as<float>(), cn.as<float>(), k,
-                               cm.as<double>(), nullptr, nullptr, nullptr, nullptr, nullptr,
-                               nullptr, nullptr, nullptr, e_out, st);
+  return csc::tc_screen_assign(static_cast<const float *>(f32), ld32, fn32, n, d, chi.as<float>(),
+                               clo.as<float>(), cn.as<float>(), k, cm.as<double>(), nullptr,
+                               nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, e_out,
+                               st);
 }

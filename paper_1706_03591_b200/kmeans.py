@@ -237,23 +237,14 @@ class _LloydPool:
             self.ld32 = (d + 3) // 4 * 4
             self.F32 = torch.zeros((n, self.ld32), dtype=torch.float32, device=dev)
             self.fn32 = torch.empty(n, dtype=torch.float32, device=dev)
-            # tensor-core screen (tcgen05): features split into tf32 hi / lo once per call
-            self.Fsplit = None
-            if bool(_native.lib().csc_kmeans_tc_supported(d, k)):
-                lds = int(_native.lib().csc_kmeans_split_stride(d))
-                self.Fsplit = torch.empty((n, lds), dtype=torch.float32, device=dev)
             for lane in self.lanes:
                 _native.call("csc_kmeans_plan_set_screen", lane.plan, ptr(self.F32), self.ld32, ptr(self.fn32))
-                _native.call("csc_kmeans_plan_set_split", lane.plan, ptr(self.Fsplit))
 
     def prepare(self, stream_handle):
-        """Refresh the FP32 copy of F (and its tf32 hi / lo split) after F changed."""
+        """Refresh the FP32 copy of F (after F changed)."""
         if self.screen:
             _native.call("csc_kmeans_screen_prepare", ptr(self.F), self.n, self.d, self.ld, ptr(self.F32),
                          self.ld32, ptr(self.fn32), stream_handle)
-            if self.Fsplit is not None:
-                _native.call("csc_kmeans_screen_split", ptr(self.F), self.n, self.d, self.ld, ptr(self.Fsplit),
-                             stream_handle)
 
 
 _LLOYD_POOL: _LloydPool | None = None  # the most recently used pool (tests / tools read it)

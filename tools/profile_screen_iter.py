@@ -32,8 +32,6 @@ ld32 = (d + 3) // 4 * 4
 F32 = torch.zeros((n, ld32), dtype=torch.float32, device=F.device)
 fn32 = torch.empty(n, dtype=torch.float32, device=F.device)
 _native.call("csc_kmeans_screen_prepare", ptr(F), n, d, F.shape[1], ptr(F32), ld32, ptr(fn32), stream())
-Fsplit = torch.empty((n, int(_native.lib().csc_kmeans_split_stride(d))), dtype=torch.float32, device=F.device)
-_native.call("csc_kmeans_screen_split", ptr(F), n, d, F.shape[1], ptr(Fsplit), stream())
 import sys as _sys  # noqa: E402
 ITERS = int(_sys.argv[1]) if len(_sys.argv) > 1 else 40
 MODES = _sys.argv[2].split(",") if len(_sys.argv) > 2 else ["fp64", "simt", "tc", "tc_full_update"]
@@ -44,7 +42,6 @@ for mode in MODES:
         _native.call("csc_kmeans_plan_set_screen", plan, None, 0, None)
     else:
         _native.call("csc_kmeans_plan_set_screen", plan, ptr(F32), ld32, ptr(fn32))
-        _native.call("csc_kmeans_plan_set_split", plan, ptr(Fsplit) if mode.startswith("tc") else None)
     ws.cent.copy_(seeds[0])
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
@@ -74,7 +71,6 @@ for mode in MODES:
 if "changes" in MODES:
     _native.call("csc_kmeans_tuning", b"screen_tc", 1)
     _native.call("csc_kmeans_plan_set_screen", plan, ptr(F32), ld32, ptr(fn32))
-    _native.call("csc_kmeans_plan_set_split", plan, ptr(Fsplit))
     ws.cent.copy_(seeds[0])
     _native.call("csc_kmeans_rownorms", ptr(ws.cent), k, d, ws.ldc, ptr(ws.cnorm), stream())
     ws.labels.zero_()
