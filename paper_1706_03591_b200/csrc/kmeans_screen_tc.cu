@@ -25,14 +25,17 @@
 // reads chunks 2s, 2s+1.
 //
 // Pipeline (warp-specialised, persistent, one CTA per SM): two producer warps
-// gather the candidate rows' fp32 features by index with cp.async into a
-// 3-unit shared-memory ring (a unit = 128 rows x 32 columns) and split them
-// into hi / lo there; one elected thread issues the 3 x 4 MMAs of a unit into
-// one of two TMEM accumulators and commits them to the ring's "empty"
+// gather the candidate rows' fp32 features by index with cp.async into a ring
+// of shared-memory units (a unit = 128 rows x 32 columns; each producer warp
+// copies 64 of the rows), two splitter warps split every unit into hi / lo in
+// place (half of it each); one elected thread issues the 3 x 4 MMAs of a unit
+// into one of two TMEM accumulators and commits them to the ring's "empty"
 // mbarrier (and, after a tile's last unit, to the accumulator's "full" one);
 // four epilogue warps read their 32 TMEM lanes (rows) with tcgen05.ld, settle
-// the rows and release the accumulator. Loads of tile i+2, MMAs of tile i+1
-// and the epilogue of tile i overlap.
+// the rows and release the accumulator. Every role walks the units in order,
+// so each mbarrier wait is at most one phase ahead of the barrier (a parity
+// wait cannot tell phase p from phase p + 2: warps that took alternate units
+// of a slot could pass on a stale phase).
 #include <mutex>
 #include <vector>
 
@@ -180,16 +183,16 @@ struct TcArgs {
 };
 
 // Warp roles: 0-3 epilogue (warp w reads TMEM lanes 32w..32w+31 = tile rows),
-// 4 MMA issue (one elected lane), 5-6 row producers (alternate tiles:
-// cp.async gathers of the candidate rows' fp32 features into the ring, the
-// tile's 128 row ids staged in shared memory, the next tile's prefetched;
-// never blocking on their own copies: each unit's completion arrives on the
-// unit's "raw" mbarrier via cp.async.mbarrier.arrive.noinc), 7-8 splitters (alternate units: wait for
-// the raw unit, split it into hi / lo in place, fence to the async proxy,
-// arrive on "split"). A unit = 128 rows x kKU columns of one tile; `stages`
-// units in a shared-memory ring (as many as fit, 3..6); two TMEM
-// accumulators (2 x NP columns) so the epilogue of tile i overlaps the MMAs
-// of tile i+1 and the gathers of the following units.
+// 4 MMA issue (one elected lane), 5-6 row producers (warp 5 + h copies rows
+// 64h..64h+63 of every unit: cp.async gathers of the candidate rows' fp32
+// features, the tile's row ids staged in shared memory, the next tile's
+// prefetched; never blocking on their own copies: each unit's completion
+// arrives on the unit's "raw" mbarrier via cp.async.mbarrier.arrive.noinc),
+// 7-8 splitters (each splits half of every unit in place into hi / lo, fences
+// to the async proxy and arrives on "full"). `stages` units in a
+// shared-memory ring (as many as fit, 3..6); two TMEM accumulators (2 x NP
+// columns) so the epilogue of tile i overlaps the MMAs of tile i+1 and the
+// gathers of the following units.
 constexpr int kKU = 32;                // columns per unit (4 MMA K steps)
 constexpr int kMaxStages = 6;
 constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2, kSplitWarp0 = 7,
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   float *Blo = Bhi + (size_t)NP * kp;
   float *Cn = Blo + (size_t)NP * kp;
   int32_t *Hs = reinterpret_cast<int32_t *>(Cn + NP);
-  int32_t *Rs = Hs + NP;                                  // [kProdWarps][kTM] row ids
-  uint64_t *rawf = reinterpret_cast<uint64_t *>(Rs + kProdWarps * kTM);  // 8-byte aligned
+  int32_t *Rs = Hs + NP;                                  // [kTM] row ids (half per producer)
+  uint64_t *rawf = reinterpret_cast<uint64_t *>(Rs + kTM);  // 8-byte aligned
   uint64_t *full = rawf + kMaxStages;
   uint64_t *empty = full + kMaxStages;
   uint64_t *tfull = empty + kMaxStages;
@@ -234,8 +237,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   }
   if (tid == 32) {
     for (int s = 0; s < stages; ++s) {
-      mbar_init(smem_u32(rawf + s), 32);  // the unit's producer warp: cp.async arrivals (noinc)
-      mbar_init(smem_u32(full + s), 32);  // the unit's splitter warp
+      mbar_init(smem_u32(rawf + s), 32 * kProdWarps);  // cp.async arrivals (noinc) of both producers
+      mbar_init(smem_u32(full + s), 32 * kSplitWarps);  // both splitters
       mbar_init(smem_u32(empty + s), 1);  // MMA commit
     }
     for (int s = 0; s < 2; ++s) {
@@ -266,38 +269,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   const int64_t nunits = my_tiles * units;
 
   if (warp >= kProdWarp0 && warp < kProdWarp0 + kProdWarps) {
-    // ===== producers: tile i (all its units) by warp 5 + (i & 1); gathers only,
-    // completion is tracked by each unit's raw barrier. The next tile's 128 row
-    // ids are loaded into registers while this tile's copies are issued.
+    // ===== producers: warp 5 + h copies rows 64h..64h+63 of every unit, in unit
+    // order; completion is tracked by each unit's raw barrier. The next tile's
+    // row ids are loaded into registers while this tile's copies are issued.
+    constexpr int kHalf = kTM / kProdWarps;  // 64 rows per producer
     const int pw = warp - kProdWarp0;
-    int32_t *rid = Rs + pw * kTM;
-    int32_t rn[kTM / 32];
+    int32_t *rid = Rs + pw * kHalf;
+    int32_t rn[kHalf / 32];
     auto load_ids = [&](int64_t i) {
       const int64_t tile = blockIdx.x + i * gridDim.x;
 #pragma unroll
-      for (int j = 0; j < kTM / 32; ++j) {
-        const int64_t lr = tile * kTM + lane + 32 * j;
+      for (int j = 0; j < kHalf / 32; ++j) {
+        const int64_t lr = tile * kTM + pw * kHalf + lane + 32 * j;
         rn[j] = lr < nr ? (a.rows ? __ldg(a.rows + lr) : (int32_t)lr) : -1;
       }
     };
-    if (pw < my_tiles) load_ids(pw);
-    for (int64_t i = pw; i < my_tiles; i += kProdWarps) {
+    load_ids(0);
+    for (int64_t i = 0; i < my_tiles; ++i) {
       __syncwarp();  // the previous tile's reads of rid are done
 #pragma unroll
-      for (int j = 0; j < kTM / 32; ++j) rid[lane + 32 * j] = rn[j];
+      for (int j = 0; j < kHalf / 32; ++j) rid[lane + 32 * j] = rn[j];
       __syncwarp();
-      if (i + kProdWarps < my_tiles) load_ids(i + kProdWarps);
+      if (i + 1 < my_tiles) load_ids(i + 1);
       for (int h = 0; h < units; ++h) {
         const int64_t u = i * units + h;
         const int s = (int)(u % stages);
         if (u >= stages) mbar_wait(smem_u32(empty + s), (uint32_t)((u / stages - 1) & 1));
         const uint32_t shi = smem_u32(ring + (size_t)s * 2 * kUnitBytes);
-        // 128 rows x 8 chunks: chunk q of row r at q * 2048 + r * 16 (canonical
+        // 64 rows x 8 chunks: chunk q of row r at q * 2048 + r * 16 (canonical
         // K-major); the 8 chunks of a row (128 contiguous bytes) on 8 consecutive lanes
 #pragma unroll 8
-        for (int e = lane; e < kTM * (kKU / 4); e += 32) {
-          const int r = e >> 3, q = e & 7;
-          const int32_t gr = rid[r];
+        for (int e = lane; e < kHalf * (kKU / 4); e += 32) {
+          const int rl = e >> 3, q = e & 7;
+          const int r = pw * kHalf + rl;
+          const int32_t gr = rid[rl];
           const int col = h * kKU + 4 * q;
           const bool ok = gr >= 0 && col < a.d;
           cp_async16(shi + (uint32_t)(q * kTM + r) * 16, ok ? a.f32 + (int64_t)gr * a.ld32 + col : a.f32,
@@ -309,14 +314,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= kSplitWarp0) {
-    // ===== splitters: unit u is split by warp 6 + (u & 1)
-    for (int64_t u = warp - kSplitWarp0; u < nunits; u += kSplitWarps) {
+    // ===== splitters: warp 7 + h splits half h of every unit, in unit order
+    const int sw = warp - kSplitWarp0;
+    constexpr int kQuads = (int)(kUnitBytes / 16) / kSplitWarps;
+    for (int64_t u = 0; u < nunits; ++u) {
       const int s = (int)(u % stages);
       mbar_wait(smem_u32(rawf + s), (uint32_t)((u / stages) & 1));
-      float4 *ph = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes);
-      float4 *pl = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes + kUnitBytes);
+      float4 *ph = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes) + sw * kQuads;
+      float4 *pl = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes + kUnitBytes) + sw * kQuads;
 #pragma unroll 4
-      for (int e = lane; e < (int)(kUnitBytes / 16); e += 32) {
+      for (int e = lane; e < kQuads; e += 32) {
         const float4 v = ph[e];
         const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
         ph[e] = hv;
@@ -423,7 +430,7 @@ int tc_kp(int64_t d) { return (int)((d + kKU - 1) / kKU * kKU); }
 
 size_t tc_smem_fixed(int64_t d, int64_t k) {
   const int64_t kp = tc_kp(d), np = tc_npad(k);
-  return sizeof(float) * (2 * np * kp + np) + sizeof(int32_t) * (np + kProdWarps * kTM) +
+  return sizeof(float) * (2 * np * kp + np) + sizeof(int32_t) * (np + kTM) +
          sizeof(uint64_t) * (3 * kMaxStages + 4) + 16 + 1024;
 }
 

@@ -261,3 +261,72 @@ def test_tensor_core_screen_same_labels(P, n, d, k, spread):
     for mode in ("tc", "simt"):
         assert np.array_equal(out[mode][0], out["fp64"][0]), mode
         assert out[mode][1] == out["fp64"][1], mode
+
+
+@pytest.mark.parametrize("n,d,k", [(600_000, 128, 100), (500_000, 96, 64), (300_000, 37, 50)])
+def test_tensor_core_distances_many_tiles(P, n, d, k):
+    """The tcgen05 screen's distances with tens of 128-row tiles per CTA (the
+    shared-memory ring wraps many times; d = 128, k = 100 has an odd ring depth):
+    every E within the stated bound of the exact fp64 distances, and five
+    repeated calls bitwise equal (a pipeline race would show as a difference)."""
+    import torch
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import ptr, stream
+    g = torch.Generator(device="cuda").manual_seed(n + d)
+    cent = torch.randn((k, d), dtype=torch.float64, device="cuda", generator=g) / np.sqrt(d)
+    lab = torch.randint(0, k, (n,), device="cuda", generator=g)
+    f64 = cent[lab] + 0.3 * torch.randn((n, d), dtype=torch.float64, device="cuda", generator=g) / np.sqrt(d)
+    c64 = cent + 0.05 * torch.randn((k, d), dtype=torch.float64, device="cuda", generator=g) / np.sqrt(d)
+    ld32 = (d + 3) // 4 * 4
+    f32 = torch.zeros((n, ld32), dtype=torch.float32, device="cuda")
+    f32[:, :d] = f64.float()
+    fn32 = (f32.double() ** 2).sum(1).float()
+    cnorm = (c64 ** 2).sum(1)
+    npad = (k + 15) // 16 * 16
+    outs = []
+    for _ in range(5):
+        E = torch.full((n, npad), float("nan"), dtype=torch.float32, device="cuda")
+        _native.call("csc_kmeans_tc_distances", ptr(f32), n, d, ld32, ptr(fn32), ptr(c64), k, d, ptr(cnorm),
+                     ptr(E), stream())
+        outs.append(E)
+    torch.cuda.synchronize()
+    for E in outs[1:]:
+        assert torch.equal(E, outs[0])
+    D = (f64 ** 2).sum(1, keepdim=True) - 2 * f64 @ c64.T + cnorm[None, :]
+    scale = (f64.norm(dim=1, keepdim=True) + cnorm.sqrt().max()) ** 2
+    err = ((outs[0][:, :k].double() - D).abs() / scale).max().item()
+    assert err <= (3 * d + 8) * 2.0 ** -23, err
+
+
+@pytest.mark.parametrize("n,d,k,spread", [(400_000, 128, 100, 1.5), (300_000, 96, 64, 3.0)])
+def test_tensor_core_screen_many_tiles_same_labels(P, n, d, k, spread):
+    """As test_tensor_core_screen_same_labels, at sizes where every CTA of the
+    persistent screen runs many tiles (the cfg3 / cfg5 regime)."""
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import upload_block
+    import importlib
+    KM = importlib.import_module("paper_1706_03591_b200.kmeans")
+    f = blobs(n, d, k, spread, seed=n + k)
+    blk = upload_block(f)
+    kids = np.random.SeedSequence(n).spawn(1)
+    cfg = P.KmeansConfig(restarts=1, max_iters=8)
+    out = {}
+    try:
+        for mode in ("tc", "fp64"):
+            _native.call("csc_kmeans_tuning", b"screen_tc", 1 if mode == "tc" else 0)
+            KM.run_restarts(blk, d, k, cfg, kids, fused=False)
+            pool = KM._LLOYD_POOL
+            for lane in pool.lanes:
+                if mode == "fp64":
+                    _native.call("csc_kmeans_plan_set_screen", lane.plan, None, 0, None)
+                else:
+                    _native.call("csc_kmeans_plan_set_screen", lane.plan, KM.ptr(pool.F32), pool.ld32,
+                                 KM.ptr(pool.fn32))
+            out[mode] = KM.run_restarts(blk, d, k, cfg, kids, fused=False)
+    finally:
+        _native.call("csc_kmeans_tuning", b"screen_tc", 1)
+        pool = KM._LLOYD_POOL
+        for lane in pool.lanes:
+            _native.call("csc_kmeans_plan_set_screen", lane.plan, KM.ptr(pool.F32), pool.ld32, KM.ptr(pool.fn32))
+    assert np.array_equal(out["tc"][0], out["fp64"][0])
+    assert out["tc"][1] == out["fp64"][1]
