@@ -192,6 +192,9 @@ int csc_kmeans_plan_destroy(csc_kmeans_plan *plan);
 /* rows re-assigned by the last pruned iteration; whether it needed the
  * empty-cluster full pass (host outputs; synchronises) */
 int csc_kmeans_plan_stats(const csc_kmeans_plan *plan, int64_t *candidates, int32_t *gated);
+/* rows the last screened assignment could not decide (sent to the FP64
+ * kernel); 0 without a screen (host output; synchronises) */
+int csc_kmeans_plan_screen_stats(const csc_kmeans_plan *plan, int64_t *undecided);
 /* One Lloyd iteration (kmeans.py:96-111) on device: assignment (all rows if
  * full != 0, else only rows whose Hamerly bounds cannot exclude a change,
  * recomputed in the reference's GEMM form), empty-cluster repair (exact: a

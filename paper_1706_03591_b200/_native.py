@@ -52,6 +52,7 @@ SIGNATURES = {
     "csc_kmeans_plan_create": ([_I64, _I64, _I64, _I64, _P, ctypes.POINTER(_P)], _INT),
     "csc_kmeans_plan_destroy": ([_P], _INT),
     "csc_kmeans_plan_stats": ([_P, _PI64, ctypes.POINTER(_I32)], _INT),
+    "csc_kmeans_plan_screen_stats": ([_P, _PI64], _INT),
     "csc_kmeans_iterate": ([_P, _P, _P, _P, _I64, _P, _P, _P, _INT, _P, _P], _INT),
     "csc_kmeans_run": ([_P, _P, _P, _P, _I64, _P, _P, _P, _INT, _D, _P, _P, _P], _INT),
     "csc_kmeans_tuning": ([ctypes.c_char_p, _I64], _INT),

@@ -728,6 +728,10 @@ int g_assign_tn = 8;
 int g_assign_ver = 3;
 // incremental centroid sums (update_sorted_kernel): tuning key "update_incremental"
 int g_update_incremental = 1;
+// exact fixed-point centroid sums updated by the changed rows only
+// (fx_delta_kernel) where the accumulators fit shared memory: tuning key
+// "update_exact" (read at plan creation)
+int g_update_exact = 1;
 // assignment screen of the Lloyd plans: 2 = tensor cores (tcgen05 kind::tf32,
 // 3xTF32) when the shape fits, else 1 = FP32 SIMT; the env var CSC_KMEANS_TC=0
 // or the tuning key "screen_tc" = 0 keeps the SIMT screen (A/B)
@@ -1688,6 +1692,240 @@ __global__ void update_sorted_kernel(const double *__restrict__ f,
   }
 }
 
+// ---- exact, order-free centroid sums (round 2) ------------------------------
+// The Lloyd plan keeps every cluster's column sums S_jc and |f|^2 sums Q_j as
+// 128-bit two's-complement fixed-point integers: a value v enters as
+// trunc(v 2^P) (P fixed for the run from max |f|^2 and n so that no sum can
+// reach 2^126; every value within 2^53 of the largest is represented exactly,
+// smaller ones lose at most 2^-P each). Integer additions commute, so the
+// sums are independent of the order rows are added in: an iteration adds the
+// rows that joined a cluster and subtracts the rows that left it (labels vs
+// the previous update's), reading only the changed rows of F, and the result
+// is bitwise the same as summing every member afresh — deterministic, and
+// the correctly rounded (not the row-order) sum, within the reference's own
+// rounding of np.add.at (kmeans.py:82-83) at the tolerances the tests state.
+// Carries: lo and hi are two 64-bit words; adding (lo, hi) with atomicAdd on
+// lo returns the old lo, the carry out of it is (old + lo < old), and hi gets
+// hi + carry: the pair is exact modulo 2^128 in any interleaving.
+struct FxScale {
+  double s1, s2;    // v * s1 * s2 = v * 2^P (two factors: P may exceed a double's range)
+  double r1, r2;    // 2^-P as two factors
+};
+
+__device__ __forceinline__ FxScale fx_scale(double bound) {
+  // P such that bound * 2^P < 2^125 (bound >= every |partial sum|)
+  int e = 0;
+  if (bound > 0.0) frexp(bound, &e);  // bound < 2^e
+  const int P = bound > 0.0 ? 125 - e : 0;
+  const int p1 = P / 2, p2 = P - p1;
+  FxScale f;
+  f.s1 = ldexp(1.0, p1);
+  f.s2 = ldexp(1.0, p2);
+  f.r1 = ldexp(1.0, -p1);
+  f.r2 = ldexp(1.0, -p2);
+  return f;
+}
+
+__device__ __forceinline__ void fx_split(double v, const FxScale &fs, uint64_t &lo, uint64_t &hi) {
+  const double x = (v * fs.s1) * fs.s2;  // exact unless |v 2^P| < 2^-1022 (then below the LSB)
+  const double a = fabs(x);
+  const double h = floor(a * 0x1p-64);    // exact
+  const double l = __dsub_rn(a, h * 0x1p64);  // exact: the low bits of a, in [0, 2^64)
+  uint64_t ulo = (uint64_t)l, uhi = (uint64_t)h;  // truncation below the LSB
+  if (x < 0.0) {
+    ulo = ~ulo + 1ull;
+    uhi = ~uhi + (ulo == 0ull ? 1ull : 0ull);
+  }
+  lo = ulo;
+  hi = uhi;
+}
+
+__device__ __forceinline__ void fx_neg(uint64_t &lo, uint64_t &hi) {
+  lo = ~lo + 1ull;
+  hi = ~hi + (lo == 0ull ? 1ull : 0ull);
+}
+
+__device__ __forceinline__ void fx_atomic_add(unsigned long long *lo_p, unsigned long long *hi_p,
+                                              uint64_t lo, uint64_t hi) {
+  const unsigned long long old = atomicAdd(lo_p, (unsigned long long)lo);
+  const uint64_t carry = (old + lo < old) ? 1ull : 0ull;
+  if (hi + carry) atomicAdd(hi_p, (unsigned long long)(hi + carry));
+}
+
+// correctly rounded double of the 128-bit value, times 2^-P
+__device__ __forceinline__ double fx_to_double(uint64_t lo, uint64_t hi, const FxScale &fs) {
+  const bool neg = (int64_t)hi < 0;
+  if (neg) fx_neg(lo, hi);
+  double mag;
+  if (hi == 0) {
+    mag = __ull2double_rn(lo);
+  } else {
+    const int lz = __clzll((long long)hi);  // >= 1: magnitudes stay below 2^126
+    const uint64_t top = (hi << lz) | (lo >> (64 - lz));
+    const uint64_t rest = lo << lz;
+    // the bits below the top 64 only matter as a sticky bit (they sit below
+    // the rounding position of the 64 -> 53 bit conversion)
+    mag = ldexp(__ull2double_rn(top | (rest != 0ull ? 1ull : 0ull)), 64 - lz);
+  }
+  const double r = (mag * fs.r1) * fs.r2;
+  return neg ? -r : r;
+}
+
+// max over rows of |f|^2 (non-negative doubles order like their bit patterns)
+__global__ void fx_maxnorm_kernel(const double *__restrict__ fnorm, int64_t n,
+                                  unsigned long long *__restrict__ maxbits) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fnorm[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(m));
+}
+
+// Delta update of the fixed-point sums: rows whose label differs from
+// prev[r] move from cluster prev[r] (if >= 0) to labels[r]. Block b owns a
+// contiguous row range; its changes are first added into shared-memory
+// accumulators (lo / hi words in separate arrays: conflict-free 64-bit lanes),
+// then every touched cluster is flushed to the global sums with one 128-bit
+// atomic add per column. gS_lo / gS_hi: [k][d]; gQ: [k][2]; gcnt: [k].
+constexpr int kFxThreads = 256;
+constexpr int kFxBatch = 4;  // changed rows whose values are loaded before their atomics
+
+__global__ void __launch_bounds__(kFxThreads)
+    fx_delta_kernel(const double *__restrict__ f, int64_t ld, const double *__restrict__ fnorm,
+                    const int32_t *__restrict__ labels, int32_t *__restrict__ prev, int64_t n,
+                    int d, int k, const unsigned long long *__restrict__ maxbits,
+                    unsigned long long *__restrict__ gS_lo, unsigned long long *__restrict__ gS_hi,
+                    unsigned long long *__restrict__ gQ, int32_t *__restrict__ gcnt) {
+  extern __shared__ unsigned long long fxs[];
+  unsigned long long *aLo = fxs;                      // [k][d]
+  unsigned long long *aHi = aLo + (size_t)k * d;      // [k][d]
+  unsigned long long *aQ = aHi + (size_t)k * d;       // [k][2]
+  int32_t *aC = reinterpret_cast<int32_t *>(aQ + 2 * (size_t)k);  // [k] count deltas
+  int32_t *dirty = aC + k;                                        // [k]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t rbeg = (int64_t)blockIdx.x * chunk, rend = min(n, rbeg + chunk);
+  if (rbeg >= rend) return;
+  const double mf = __longlong_as_double((long long)*maxbits);
+  const FxScale fs = fx_scale(sqrt(mf) * (1.0 + 1e-12) * (double)n);
+  const FxScale fq = fx_scale(mf * (double)n);
+  for (int64_t i = tid; i < 2 * (int64_t)k * d; i += kFxThreads) aLo[i] = 0ull;
+  for (int i = tid; i < 2 * k; i += kFxThreads) aQ[i] = 0ull;
+  for (int i = tid; i < k; i += kFxThreads) {
+    aC[i] = 0;
+    dirty[i] = 0;
+  }
+  __syncthreads();
+  bool any = false;
+  for (int64_t base = rbeg + warp * 32; base < rend; base += (kFxThreads / 32) * 32) {
+    const int64_t r = base + lane;
+    int nl = -1, ol = -1;
+    if (r < rend) {
+      nl = labels[r];
+      ol = prev[r];
+    }
+    const bool ch = r < rend && nl != ol;
+    if (ch) prev[r] = nl;
+    unsigned m = __ballot_sync(0xffffffffu, ch);
+    any |= m != 0u;
+    while (m) {
+      int src[kFxBatch];
+      int cnt = 0;
+#pragma unroll
+      for (int b = 0; b < kFxBatch; ++b) {
+        src[b] = m ? __ffs(m) - 1 : -1;
+        if (m) {
+          m &= m - 1;
+          ++cnt;
+        }
+      }
+      double v[kFxBatch][4];  // d <= 128: up to 4 columns per lane
+      int jn[kFxBatch], jo[kFxBatch];
+#pragma unroll
+      for (int b = 0; b < kFxBatch; ++b) {
+        const int sl = src[b] < 0 ? 0 : src[b];
+        jn[b] = __shfl_sync(0xffffffffu, nl, sl);
+        jo[b] = __shfl_sync(0xffffffffu, ol, sl);
+        const double *fr = f + (base + sl) * ld;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int c = lane + 32 * t;
+          v[b][t] = (src[b] >= 0 && c < d) ? __ldg(fr + c) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < kFxBatch; ++b) {
+        if (b >= cnt) break;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int c = lane + 32 * t;
+          if (c >= d) break;
+          uint64_t lo, hi;
+          fx_split(v[b][t], fs, lo, hi);
+          const size_t e = (size_t)jn[b] * d + c;
+          fx_atomic_add(aLo + e, aHi + e, lo, hi);
+          if (jo[b] >= 0) {
+            fx_neg(lo, hi);
+            const size_t eo = (size_t)jo[b] * d + c;
+            fx_atomic_add(aLo + eo, aHi + eo, lo, hi);
+          }
+        }
+        if (lane == 0) {
+          uint64_t lo, hi;
+          fx_split(fnorm[base + src[b]], fq, lo, hi);
+          fx_atomic_add(aQ + 2 * jn[b], aQ + 2 * jn[b] + 1, lo, hi);
+          atomicAdd(aC + jn[b], 1);
+          dirty[jn[b]] = 1;
+          if (jo[b] >= 0) {
+            fx_neg(lo, hi);
+            fx_atomic_add(aQ + 2 * jo[b], aQ + 2 * jo[b] + 1, lo, hi);
+            atomicSub(aC + jo[b], 1);
+            dirty[jo[b]] = 1;
+          }
+        }
+      }
+    }
+  }
+  if (!__syncthreads_or(any)) return;
+  for (int64_t e = tid; e < (int64_t)k * d; e += kFxThreads) {
+    const int64_t j = e / d;
+    if (!dirty[j]) continue;
+    const uint64_t lo = aLo[e], hi = aHi[e];
+    if (lo | hi) fx_atomic_add(gS_lo + e, gS_hi + e, lo, hi);
+  }
+  for (int j = tid; j < k; j += kFxThreads) {
+    if (!dirty[j]) continue;
+    const uint64_t lo = aQ[2 * j], hi = aQ[2 * j + 1];
+    if (lo | hi) fx_atomic_add(gQ + 2 * j, gQ + 2 * j + 1, lo, hi);
+    if (aC[j]) atomicAdd(gcnt + j, aC[j]);
+  }
+}
+
+// the fixed-point sums as doubles for the iteration tail: S [k][d], Q [k], counts [k]
+__global__ void fx_finish_kernel(const unsigned long long *__restrict__ gS_lo,
+                                 const unsigned long long *__restrict__ gS_hi,
+                                 const unsigned long long *__restrict__ gQ,
+                                 const int32_t *__restrict__ gcnt, int64_t n, int d, int k,
+                                 const unsigned long long *__restrict__ maxbits,
+                                 double *__restrict__ S, double *__restrict__ Q,
+                                 int32_t *__restrict__ counts) {
+  const double mf = __longlong_as_double((long long)*maxbits);
+  const FxScale fs = fx_scale(sqrt(mf) * (1.0 + 1e-12) * (double)n);
+  const FxScale fq = fx_scale(mf * (double)n);
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < (int64_t)k * d) S[i] = fx_to_double(gS_lo[i], gS_hi[i], fs);
+  if (i < k) {
+    Q[i] = fx_to_double(gQ[2 * i], gQ[2 * i + 1], fq);
+    counts[i] = gcnt[i];
+  }
+}
+
+size_t fx_smem(int64_t d, int64_t k) {
+  return sizeof(unsigned long long) * (2 * (size_t)k * d + 2 * (size_t)k) + sizeof(int32_t) * 2 * (size_t)k;
+}
+
 __global__ void sums_finish_kernel(const double *__restrict__ psum,
                                    const int32_t *__restrict__ pcnt,
                                    const double *__restrict__ pq, int64_t nb, int64_t d,
@@ -1966,6 +2204,13 @@ struct csc_kmeans_plan {
   // tensor-core screen (kmeans_screen_tc.cu): hi / lo centroid tiles
   bool tc = false;
   float *chi = nullptr, *clo = nullptr;
+  // exact fixed-point sums (fx_delta_kernel): [k][d] lo / hi words, Q [k][2],
+  // counts [k], max |f|^2 bits
+  bool fx = false;
+  int fx_grid = 0;
+  void *fx_base = nullptr;
+  unsigned long long *fx_lo = nullptr, *fx_hi = nullptr, *fx_q = nullptr, *fx_max = nullptr;
+  int32_t *fx_cnt = nullptr;
 };
 
 extern "C" {
@@ -2028,6 +2273,10 @@ int csc_kmeans_tuning(const char *key, int64_t value) {
   if (std::string(key) == "assign_ver") {
     CSC_REQUIRE(value == 2 || value == 3, "assign_ver must be 2 or 3");
     g_assign_ver = (int)value;
+    return CSC_OK;
+  }
+  if (std::string(key) == "update_exact") {
+    g_update_exact = value ? 1 : 0;
     return CSC_OK;
   }
   if (std::string(key) == "update_incremental") {
@@ -2122,8 +2371,12 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   p->chunk = csc::ceil_div(n, p->nb);
   p->smem = sizeof(double) * k * (p->cw + kSqLanes) + sizeof(int32_t) * k;
   const size_t nd = (size_t)n, kk = (size_t)k;
-  const size_t doubles = 3 * nd + (size_t)p->nb * kk * d + (size_t)p->nb * kk + kk * d + 4 * kk + 8;
-  const size_t ints = 2 * nd + 4 + (size_t)p->nb * kk;
+  // exact fixed-point sums need no per-chunk partials
+  const bool want_fx = g_update_exact && d <= 128 &&
+                       (int64_t)fx_smem(d, k) <= (int64_t)info.max_smem_optin;
+  const size_t parts = want_fx ? 0 : (size_t)p->nb * kk;
+  const size_t doubles = 3 * nd + parts * d + parts + kk * d + 4 * kk + 8;
+  const size_t ints = 2 * nd + 4 + parts;
   if (cudaMallocAsync(&p->base, doubles * 8 + ints * 4 + 64, st) != cudaSuccess) {
     delete p;
     csc::set_error("csc_kmeans_plan_create: allocation failed");
@@ -2133,8 +2386,8 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   p->ub = dp; dp += nd;
   p->lb = dp; dp += nd;
   p->own = dp; dp += nd;
-  p->psum = dp; dp += (size_t)p->nb * kk * d;
-  p->pq = dp; dp += (size_t)p->nb * kk;
+  p->psum = dp; dp += parts * d;
+  p->pq = dp; dp += parts;
   p->S = dp; dp += kk * d;
   p->Q = dp; dp += kk;
   p->cterm = dp; dp += kk;
@@ -2144,7 +2397,7 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   int32_t *ip = reinterpret_cast<int32_t *>(dp);
   p->cand = ip; ip += nd;
   p->flags = ip; ip += 4;
-  p->pcnt = ip; ip += (size_t)p->nb * kk;
+  p->pcnt = ip; ip += parts;
   p->prev = ip;
   CSC_TRY_CUDA(cudaMemsetAsync(p->flags, 0, sizeof(int32_t) * 4, st));
   CSC_TRY_CUDA(cudaFuncSetAttribute(update_partial_kernel,
@@ -2153,6 +2406,30 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
     CSC_TRY_CUDA(cudaFuncSetAttribute(
         update_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
         (int)(sizeof(int32_t) * (2 * (size_t)p->chunk + 3 * (size_t)k))));
+  const size_t fxs = fx_smem(d, k);
+  if (want_fx) {
+    const size_t kd = kk * (size_t)d;
+    const size_t words = 2 * kd + 2 * kk + 1;
+    if (cudaMallocAsync(&p->fx_base, words * 8 + kk * 4 + 64, st) != cudaSuccess) {
+      cudaFreeAsync(p->base, st);
+      delete p;
+      csc::set_error("csc_kmeans_plan_create: allocation failed");
+      return CSC_ERR_CUDA;
+    }
+    {
+      p->fx = true;
+      p->fx_lo = static_cast<unsigned long long *>(p->fx_base);
+      p->fx_hi = p->fx_lo + kd;
+      p->fx_q = p->fx_hi + kd;
+      p->fx_max = p->fx_q + 2 * kk;
+      p->fx_cnt = reinterpret_cast<int32_t *>(p->fx_max + 1);
+      CSC_TRY_CUDA(cudaFuncSetAttribute(fx_delta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)fxs));
+      const int per_sm = std::max<int>(1, std::min<int>(2, (int)(228 * 1024 / (fxs + 1024))));
+      p->fx_grid = (int)std::max<int64_t>(
+          1, std::min<int64_t>((int64_t)info.sm_count * per_sm, csc::ceil_div(n, 1024)));
+    }
+  }
   *out = p;
   return CSC_OK;
 }
@@ -2222,6 +2499,17 @@ int csc_kmeans_plan_stats(const csc_kmeans_plan *p, int64_t *candidates, int32_t
   return CSC_OK;
 }
 
+int csc_kmeans_plan_screen_stats(const csc_kmeans_plan *p, int64_t *undecided) {
+  CSC_REQUIRE(p != nullptr && undecided != nullptr, "csc_kmeans_plan_screen_stats: NULL argument");
+  int32_t h = 0;
+  if (p->namb) {
+    CSC_TRY_CUDA(cudaMemcpyAsync(&h, p->namb, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+    CSC_TRY_CUDA(cudaStreamSynchronize(p->stream));
+  }
+  *undecided = h;
+  return CSC_OK;
+}
+
 int csc_kmeans_plan_destroy(csc_kmeans_plan *p) {
   if (!p) return CSC_OK;
   if (p->exec) cudaGraphExecDestroy(p->exec);
@@ -2231,6 +2519,7 @@ int csc_kmeans_plan_destroy(csc_kmeans_plan *p) {
   if (p->history) cudaFreeAsync(p->history, p->stream);
   if (p->base) cudaFreeAsync(p->base, p->stream);
   if (p->screen_base) cudaFreeAsync(p->screen_base, p->stream);
+  if (p->fx_base) cudaFreeAsync(p->fx_base, p->stream);
   delete p;
   return CSC_OK;
 }
@@ -2305,7 +2594,22 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
   CSC_CHECK_LAUNCH();
   // means, counts, movement, cost terms
   const int threads = (int)(csc::ceil_div(p->cw, 32) * 32 + 32);
-  if (p->chunk <= kSortedMaxChunk) {
+  if (p->fx) {
+    if (full) {  // a new run: no members anywhere yet; the fixed-point scale from max |f|^2
+      CSC_TRY_CUDA(cudaMemsetAsync(p->prev, 0xff, sizeof(int32_t) * n, st));
+      CSC_TRY_CUDA(cudaMemsetAsync(p->fx_base, 0, sizeof(unsigned long long) * (2 * k * d + 2 * k + 1) +
+                                                      sizeof(int32_t) * k, st));
+      fx_maxnorm_kernel<<<grid_cap(csc::ceil_div(n, 256), 2), 256, 0, st>>>(fnorm, n, p->fx_max);
+      CSC_CHECK_LAUNCH();
+    }
+    fx_delta_kernel<<<(unsigned)p->fx_grid, kFxThreads, fx_smem(d, k), st>>>(
+        f, ld, fnorm, labels, p->prev, n, (int)d, (int)k, p->fx_max, p->fx_lo, p->fx_hi, p->fx_q,
+        p->fx_cnt);
+    CSC_CHECK_LAUNCH();
+    fx_finish_kernel<<<(unsigned)csc::ceil_div(k * d, 256), 256, 0, st>>>(
+        p->fx_lo, p->fx_hi, p->fx_q, p->fx_cnt, n, (int)d, (int)k, p->fx_max, p->S, p->Q, counts);
+    CSC_CHECK_LAUNCH();
+  } else if (p->chunk <= kSortedMaxChunk) {
     const size_t ssmem = sizeof(int32_t) * (2 * (size_t)p->chunk + 3 * (size_t)k);
     int32_t *prev = (p->ny == 1 && g_update_incremental) ? p->prev : nullptr;
     if (prev && full) {  // a new run: no members anywhere yet
@@ -2320,10 +2624,12 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
         f, labels, n, d, ld, k, p->chunk, (int)p->cw, p->psum, p->pcnt, fnorm, p->pq);
   }
   CSC_CHECK_LAUNCH();
-  const int64_t warps = k * (d + 1);
-  sums_finish_kernel<<<(unsigned)csc::ceil_div(warps, 8), 256, 0, st>>>(
-      p->psum, p->pcnt, p->pq, p->nb, d, k, p->S, counts, p->Q);
-  CSC_CHECK_LAUNCH();
+  if (!p->fx) {
+    const int64_t warps = k * (d + 1);
+    sums_finish_kernel<<<(unsigned)csc::ceil_div(warps, 8), 256, 0, st>>>(
+        p->psum, p->pcnt, p->pq, p->nb, d, k, p->S, counts, p->Q);
+    CSC_CHECK_LAUNCH();
+  }
   if (g_finish_mode != 2 && k * ((d | 1) + 3) * (int64_t)sizeof(double) <= 48 * 1024 &&
       k * k * d <= (int64_t(1) << 20)) {
     // small k: one single-block node finishes the iteration

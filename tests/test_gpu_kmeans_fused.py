@@ -330,3 +330,32 @@ def test_tensor_core_screen_many_tiles_same_labels(P, n, d, k, spread):
             _native.call("csc_kmeans_plan_set_screen", lane.plan, KM.ptr(pool.F32), pool.ld32, KM.ptr(pool.fn32))
     assert np.array_equal(out["tc"][0], out["fp64"][0])
     assert out["tc"][1] == out["fp64"][1]
+
+
+@pytest.mark.parametrize("n,d,k", [(200_000, 96, 64), (60_000, 128, 100), (30_000, 17, 5)])
+def test_exact_sums_match_row_order_sums(P, n, d, k):
+    """The Lloyd plan's exact fixed-point centroid sums (changed rows only,
+    order-free) against the row-ordered per-chunk sums: same labels, cost to
+    1e-12 relative, both within the oracle's tolerances."""
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import upload_block
+    import importlib
+    KM = importlib.import_module("paper_1706_03591_b200.kmeans")
+    f = blobs(n, d, k, 1.5, seed=n + d)
+    blk = upload_block(f)
+    kids = np.random.SeedSequence(d + k).spawn(2)
+    cfg = P.KmeansConfig(restarts=2, max_iters=30)
+    out = {}
+    try:
+        for exact in (1, 0):
+            _native.call("csc_kmeans_tuning", b"update_exact", exact)
+            KM._LLOYD_POOLS.clear()  # plans read the knob when they are created
+            out[exact] = KM.run_restarts(blk, d, k, cfg, kids, fused=False)
+    finally:
+        _native.call("csc_kmeans_tuning", b"update_exact", 1)
+        KM._LLOYD_POOLS.clear()
+    assert np.array_equal(out[1][0], out[0][0])
+    assert abs(out[1][1] - out[0][1]) <= 1e-12 * out[0][1]
+    ref_labels, _, ref_cost = O.kmeans(f, k, restarts=2, max_iters=30, tol=1e-6, seed=d + k)
+    assert O.adjusted_rand(out[1][0], ref_labels) >= 0.999
+    assert abs(np.sqrt(out[1][1]) - ref_cost) <= COST_TOL * ref_cost

@@ -1,5 +1,6 @@
 """Per-kernel times of host-driven pruned Lloyd iterations with and without the FP32 screen (torch.profiler)."""
 import collections
+import ctypes
 import importlib
 import os
 import sys
@@ -59,7 +60,7 @@ for mode in MODES:
     seq = collections.defaultdict(list)
     for e in sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
                     key=lambda e: e.time_range.start):
-        for key in ("update_sorted", "screen_kernel", "assign3"):
+        for key in ("update_sorted", "fx_delta", "screen_kernel", "assign3"):
             if key in e.name:
                 seq[key].append(round(e.time_range.elapsed_us()))
                 break
@@ -82,11 +83,16 @@ if "changes" in MODES:
         _native.call("csc_kmeans_iterate", plan, ptr(ws.blk), ptr(ws.fnorm), ptr(ws.cent), ws.ldc, ptr(ws.cnorm),
                      ptr(ws.labels), ptr(ws.counts), int(it == 0), ptr(ws.scalars[1:]), stream())
         lab = ws.labels.cpu().numpy().astype(np.int64)
+        cand = ctypes.c_int64()
+        _native.call("csc_kmeans_plan_stats", plan, ctypes.byref(cand), None)
+        amb = ctypes.c_int64()
+        _native.call("csc_kmeans_plan_screen_stats", plan, ctypes.byref(amb))
         if prev is not None:
             ch = np.flatnonzero(lab != prev)
             blocks = ch // chunk
             pairs = np.unique(np.concatenate([blocks * k + lab[ch], blocks * k + prev[ch]]))
-            out.append((it, ch.size, pairs.size / (nb * k)))
+            out.append((it, ch.size, pairs.size / (nb * k), cand.value, amb.value))
         prev = lab
-    for it, c, frac in out[::max(1, len(out) // 12)]:
-        print(f"   iter {it}: {c} rows changed, dirty (chunk, cluster) fraction {frac:.3f}")
+    for it, c, frac, cd, am in out[::max(1, len(out) // 12)]:
+        print(f"   iter {it}: {c} rows changed, dirty (chunk, cluster) fraction {frac:.3f}, "
+              f"Hamerly candidates {cd}, undecided by the screen {am}")
