@@ -25,17 +25,20 @@
 // reads chunks 2s, 2s+1.
 //
 // Pipeline (warp-specialised, persistent, one CTA per SM): two producer warps
-// gather the candidate rows' fp32 features by index with cp.async into a ring
-// of shared-memory units (a unit = 128 rows x 32 columns; each producer warp
-// copies 64 of the rows), two splitter warps split every unit into hi / lo in
-// place (half of it each); one elected thread issues the 3 x 4 MMAs of a unit
-// into one of two TMEM accumulators and commits them to the ring's "empty"
-// mbarrier (and, after a tile's last unit, to the accumulator's "full" one);
-// four epilogue warps read their 32 TMEM lanes (rows) with tcgen05.ld, settle
-// the rows and release the accumulator. Every role walks the units in order,
-// so each mbarrier wait is at most one phase ahead of the barrier (a parity
-// wait cannot tell phase p from phase p + 2: warps that took alternate units
-// of a slot could pass on a stale phase).
+// gather the candidate rows' fp32 features by index with cp.async into a raw
+// ring of shared-memory units (a unit = 128 rows x 32 columns; each producer
+// warp copies 64 of the rows); two splitter warps write the units' low parts
+// into a two-unit lo ring; one elected thread issues the 3 x 4 MMAs of a unit
+// (high parts read straight from the raw unit) into one of two TMEM
+// accumulators and commits them to both rings' "empty" mbarriers (and, after
+// a tile's last unit, to the accumulator's "full" one); four epilogue warps
+// read their 32 TMEM lanes (rows) with tcgen05.ld, settle the rows and
+// release the accumulator. Every role walks the units in order, so each
+// mbarrier wait is at most one phase ahead of the barrier (a parity wait
+// cannot tell phase p from phase p + 2).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <mutex>
 #include <vector>
 
@@ -58,6 +61,43 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); base offset 0, SWIZZLE_NONE
   return d;
+}
+
+// K-major, 128-byte swizzle (rows of 128 B = 32 fp32 in 1024-byte atoms of 8
+// rows, the 16-byte chunk index XORed with the row within the atom: the
+// layout TMA writes with CU_TENSOR_MAP_SWIZZLE_128B); SBO = 1024 B between
+// 8-row groups, LBO unused; a K step of 8 tf32 advances the start by 32 B
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;                  // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO
+  d |= (uint64_t)1 << 46;                  // version 1 (sm_100)
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_tile2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                           uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int c0, int r0,
+                                            int r1, int r2, int r3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], "
+      "[%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
 }
 
 // kind::tf32 instruction descriptor: D fp32, A/B tf32, both K-major, M = 128
@@ -185,20 +225,25 @@ struct TcArgs {
 // Warp roles: 0-3 epilogue (warp w reads TMEM lanes 32w..32w+31 = tile rows),
 // 4 MMA issue (one elected lane), 5-6 row producers (warp 5 + h copies rows
 // 64h..64h+63 of every unit: cp.async gathers of the candidate rows' fp32
-// features, the tile's row ids staged in shared memory, the next tile's
-// prefetched; never blocking on their own copies: each unit's completion
-// arrives on the unit's "raw" mbarrier via cp.async.mbarrier.arrive.noinc),
-// 7-8 splitters (each splits half of every unit in place into hi / lo, fences
-// to the async proxy and arrives on "full"). `stages` units in a
-// shared-memory ring (as many as fit, 3..6); two TMEM accumulators (2 x NP
-// columns) so the epilogue of tile i overlaps the MMAs of tile i+1 and the
-// gathers of the following units.
+// features into the "raw" ring, from 16 row pointers per lane formed once per
+// tile, the next tile's row ids prefetched; never blocking on their own copies: each unit's
+// completion arrives on its raw "full" mbarrier via
+// cp.async.mbarrier.arrive.noinc), 7-8 splitters (each writes half of every
+// unit's low parts lo = f - tf32(f) into the small "lo" ring, fences to the
+// async proxy and arrives on its "full" barrier). A unit = 128 rows x kKU
+// columns of one tile. The tensor core reads a raw unit directly as the high
+// parts: kind::tf32 takes the top 19 bits of each fp32 operand (truncation),
+// exactly tf32_hi(f) — so a raw slot is never rewritten and is free again as
+// soon as its MMAs ran, and the raw ring (as deep as shared memory allows: 9
+// units at cfg5) carries the gathers in flight. Two TMEM accumulators
+// (2 x NP columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
 constexpr int kKU = 32;                // columns per unit (4 MMA K steps)
-constexpr int kMaxStages = 6;
+constexpr int kMaxRaw = 12;            // raw ring units (as many as fit, >= 2)
+constexpr int kLoStages = 2;           // lo ring units
 constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2, kSplitWarp0 = 7,
-              kSplitWarps = 2;
-constexpr int kTcThreads = 32 * (kEpiWarps + 1 + kProdWarps + kSplitWarps);  // 288
-constexpr uint32_t kUnitBytes = kTM * kKU * 4;                  // one of hi / lo
+              kSplitWarps = 4;
+constexpr int kTcThreads = 32 * (kEpiWarps + 1 + kProdWarps + kSplitWarps);  // 352
+constexpr uint32_t kUnitBytes = kTM * kKU * 4;
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar)
@@ -206,20 +251,24 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 }
 
 template <int NP>  // padded centroid count = UMMA N (multiple of 16, <= 128)
-__global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int stages) {
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_screen_kernel(TcArgs a, int stages, const __grid_constant__ CUtensorMap tile_map,
+                     const __grid_constant__ CUtensorMap row_map) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   const int kp = a.kp;
   const int units = kp / kKU;  // per tile
-  uint8_t *ring = tsm;                                         // [stage][hi|lo][kUnitBytes]
-  float *Bhi = reinterpret_cast<float *>(ring + (size_t)stages * 2 * kUnitBytes);
+  uint8_t *raw = tsm;                                          // [stages][kUnitBytes]
+  uint8_t *lor = raw + (size_t)stages * kUnitBytes;            // [kLoStages][kUnitBytes]
+  float *Bhi = reinterpret_cast<float *>(lor + (size_t)kLoStages * kUnitBytes);
   float *Blo = Bhi + (size_t)NP * kp;
   float *Cn = Blo + (size_t)NP * kp;
   int32_t *Hs = reinterpret_cast<int32_t *>(Cn + NP);
   int32_t *Rs = Hs + NP;                                  // [kTM] row ids (half per producer)
-  uint64_t *rawf = reinterpret_cast<uint64_t *>(Rs + kTM);  // 8-byte aligned
-  uint64_t *full = rawf + kMaxStages;
-  uint64_t *empty = full + kMaxStages;
-  uint64_t *tfull = empty + kMaxStages;
+  uint64_t *rfull = reinterpret_cast<uint64_t *>(Rs + kTM);  // 8-byte aligned
+  uint64_t *rempty = rfull + kMaxRaw;
+  uint64_t *lfull = rempty + kMaxRaw;
+  uint64_t *lempty = lfull + kLoStages;
+  uint64_t *tfull = lempty + kLoStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_hold = reinterpret_cast<uint32_t *>(tempty + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -237,9 +286,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   }
   if (tid == 32) {
     for (int s = 0; s < stages; ++s) {
-      mbar_init(smem_u32(rawf + s), 32 * kProdWarps);  // cp.async arrivals (noinc) of both producers
-      mbar_init(smem_u32(full + s), 32 * kSplitWarps);  // both splitters
-      mbar_init(smem_u32(empty + s), 1);  // MMA commit
+      // TMA: the producer's expect_tx (the bytes complete it); gathers: the
+      // cp.async arrivals (noinc) of every producer lane
+      mbar_init(smem_u32(rfull + s), a.rows ? 32 * kProdWarps : 1);
+      mbar_init(smem_u32(rempty + s), 1);               // MMA commit
+    }
+    for (int s = 0; s < kLoStages; ++s) {
+      mbar_init(smem_u32(lfull + s), 32 * kSplitWarps);  // both splitters
+      mbar_init(smem_u32(lempty + s), 1);                // MMA commit
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(tfull + s), 1);          // MMA commit
@@ -269,74 +323,100 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
   const int64_t nunits = my_tiles * units;
 
   if (warp >= kProdWarp0 && warp < kProdWarp0 + kProdWarps) {
-    // ===== producers: warp 5 + h copies rows 64h..64h+63 of every unit, in unit
-    // order; completion is tracked by each unit's raw barrier. The next tile's
-    // row ids are loaded into registers while this tile's copies are issued.
-    constexpr int kHalf = kTM / kProdWarps;  // 64 rows per producer
-    const int pw = warp - kProdWarp0;
-    int32_t *rid = Rs + pw * kHalf;
-    int32_t rn[kHalf / 32];
-    auto load_ids = [&](int64_t i) {
-      const int64_t tile = blockIdx.x + i * gridDim.x;
-#pragma unroll
-      for (int j = 0; j < kHalf / 32; ++j) {
-        const int64_t lr = tile * kTM + pw * kHalf + lane + 32 * j;
-        rn[j] = lr < nr ? (a.rows ? __ldg(a.rows + lr) : (int32_t)lr) : -1;
-      }
-    };
-    load_ids(0);
-    for (int64_t i = 0; i < my_tiles; ++i) {
-      __syncwarp();  // the previous tile's reads of rid are done
-#pragma unroll
-      for (int j = 0; j < kHalf / 32; ++j) rid[lane + 32 * j] = rn[j];
-      __syncwarp();
-      if (i + 1 < my_tiles) load_ids(i + 1);
-      for (int h = 0; h < units; ++h) {
-        const int64_t u = i * units + h;
-        const int s = (int)(u % stages);
-        if (u >= stages) mbar_wait(smem_u32(empty + s), (uint32_t)((u / stages - 1) & 1));
-        const uint32_t shi = smem_u32(ring + (size_t)s * 2 * kUnitBytes);
-        // 64 rows x 8 chunks: chunk q of row r at q * 2048 + r * 16 (canonical
-        // K-major); the 8 chunks of a row (128 contiguous bytes) on 8 consecutive lanes
-#pragma unroll 8
-        for (int e = lane; e < kHalf * (kKU / 4); e += 32) {
-          const int rl = e >> 3, q = e & 7;
-          const int r = pw * kHalf + rl;
-          const int32_t gr = rid[rl];
-          const int col = h * kKU + 4 * q;
-          const bool ok = gr >= 0 && col < a.d;
-          cp_async16(shi + (uint32_t)(q * kTM + r) * 16, ok ? a.f32 + (int64_t)gr * a.ld32 + col : a.f32,
-                     ok);
+    // ===== producers, in unit order; every unit lands in the 128-byte-swizzled
+    // K-major layout (row r at r * 128 B, its 16-byte chunk q at (q ^ (r % 8)) * 16).
+    if (!a.rows) {
+      // full pass: each unit is one 128-row x 32-column TMA tile (warp 5, lane 0),
+      // armed with the unit's bytes
+      if (warp == kProdWarp0 && lane == 0) {
+        for (int64_t i = 0; i < my_tiles; ++i) {
+          const int64_t tile = blockIdx.x + i * gridDim.x;
+          for (int h = 0; h < units; ++h) {
+            const int64_t u = i * units + h;
+            const int s = (int)(u % stages);
+            if (u >= stages) mbar_wait(smem_u32(rempty + s), (uint32_t)((u / stages - 1) & 1));
+            const uint32_t bar = smem_u32(rfull + s);
+            mbar_expect_tx(bar, kUnitBytes);
+            tma_tile2d(smem_u32(raw + (size_t)s * kUnitBytes), &tile_map, h * kKU, (int)(tile * kTM), bar);
+          }
         }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(rawf + s))
-                     : "memory");
       }
+    } else {
+      // candidate rows: warp 5 + h gathers rows 64h..64h+63 of every unit with
+      // cp.async (TMA gather4 moves 512 B per instruction: too few for one warp
+      // to keep the memory busy). Lane l copies chunk q = l % 8 of the rows
+      // 64h + l / 8 + 4t (t = 0..15) from 16 row pointers formed once per tile;
+      // completion arrives on the unit's raw full barrier (noinc).
+      constexpr int kHalf = kTM / kProdWarps;       // 64 rows per producer
+      constexpr int kPer = kHalf * (kKU / 4) / 32;  // 16 chunks per lane per unit
+      const int pw = warp - kProdWarp0;
+      const int q = lane & 7, r0 = lane >> 3;
+      int32_t rn[kHalf / 32];
+      auto load_ids = [&](int64_t i) {
+        const int64_t tile = blockIdx.x + i * gridDim.x;
+#pragma unroll
+        for (int j = 0; j < kHalf / 32; ++j) {
+          const int64_t lr = tile * kTM + pw * kHalf + lane + 32 * j;
+          rn[j] = lr < nr ? __ldg(a.rows + lr) : -1;
+        }
+      };
+      load_ids(0);
+      for (int64_t i = 0; i < my_tiles; ++i) {
+        const float *src[kPer];
+        uint32_t valid = 0;
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+          const int32_t gr = __shfl_sync(0xffffffffu, rn[t >> 3], r0 + 4 * (t & 7));
+          src[t] = a.f32 + (int64_t)(gr < 0 ? 0 : gr) * a.ld32 + 4 * q;
+          valid |= (gr >= 0 ? 1u : 0u) << t;
+        }
+        if (i + 1 < my_tiles) load_ids(i + 1);
+        for (int h = 0; h < units; ++h) {
+          const int64_t u = i * units + h;
+          const int s = (int)(u % stages);
+          if (u >= stages) mbar_wait(smem_u32(rempty + s), (uint32_t)((u / stages - 1) & 1));
+          const uint32_t base = smem_u32(raw + (size_t)s * kUnitBytes);
+          const uint32_t vmask = (h * kKU + 4 * q < a.d) ? valid : 0u;
+#pragma unroll
+          for (int t = 0; t < kPer; ++t) {
+            const int r = pw * kHalf + r0 + 4 * t;
+            cp_async16(base + (uint32_t)r * 128 + (uint32_t)((q ^ (r & 7)) << 4), src[t] + h * kKU,
+                       (vmask >> t) & 1u);
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(rfull + s))
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= kSplitWarp0) {
-    // ===== splitters: warp 7 + h splits half h of every unit, in unit order
+    // ===== splitters: warp 7 + h writes the low parts of quarter h of every unit, in unit order
     const int sw = warp - kSplitWarp0;
     constexpr int kQuads = (int)(kUnitBytes / 16) / kSplitWarps;
     for (int64_t u = 0; u < nunits; ++u) {
       const int s = (int)(u % stages);
-      mbar_wait(smem_u32(rawf + s), (uint32_t)((u / stages) & 1));
-      float4 *ph = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes) + sw * kQuads;
-      float4 *pl = reinterpret_cast<float4 *>(ring + (size_t)s * 2 * kUnitBytes + kUnitBytes) + sw * kQuads;
-#pragma unroll 4
-      for (int e = lane; e < kQuads; e += 32) {
-        const float4 v = ph[e];
-        const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-        ph[e] = hv;
-        pl[e] = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
-      }
+      const int t = (int)(u % kLoStages);
+      mbar_wait(smem_u32(rfull + s), (uint32_t)((u / stages) & 1));
+      if (u >= kLoStages) mbar_wait(smem_u32(lempty + t), (uint32_t)((u / kLoStages - 1) & 1));
+      const float4 *pr = reinterpret_cast<const float4 *>(raw + (size_t)s * kUnitBytes) + sw * kQuads;
+      float4 *pl = reinterpret_cast<float4 *>(lor + (size_t)t * kUnitBytes) + sw * kQuads;
+      constexpr int kPerLane = kQuads / 32;  // every load issued before the first store
+      float4 v[kPerLane];
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) v[j] = pr[lane + 32 * j];
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j)
+        pl[lane + 32 * j] = make_float4(v[j].x - tf32_hi(v[j].x), v[j].y - tf32_hi(v[j].y),
+                                        v[j].z - tf32_hi(v[j].z), v[j].w - tf32_hi(v[j].w));
       fence_async_smem();  // this thread's smem writes -> visible to the tensor core
-      mbar_arrive(smem_u32(full + s));
+      mbar_arrive(smem_u32(lfull + t));
     }
   } else if (warp == kMmaWarp) {
-    // ===== MMA issue
+    // ===== MMA issue: A_hi = the raw unit (read as tf32 = its top 19 bits), A_lo
+    // from the lo ring; the lo full barrier implies the raw unit's arrival
     const uint32_t idesc = tf32_idesc(NP);
     const uint32_t sB = smem_u32(Bhi), sBl = smem_u32(Blo);
-    const uint32_t lboA = kTM * 16, lboB = NP * 16, sbo = 128;
+    const uint32_t lboB = NP * 16, sbo = 128;
     int64_t u = 0;
     for (int64_t i = 0; i < my_tiles; ++i) {
       const int slot = (int)(i & 1);
@@ -345,21 +425,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_screen_kernel(TcArgs a, int 
       const uint32_t acc = tmem + (uint32_t)(slot * NP);
       for (int h = 0; h < units; ++h, ++u) {
         const int s = (int)(u % stages);
-        mbar_wait(smem_u32(full + s), (uint32_t)((u / stages) & 1));
+        const int t = (int)(u % kLoStages);
+        mbar_wait(smem_u32(lfull + t), (uint32_t)((u / kLoStages) & 1));
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t shi = smem_u32(ring + (size_t)s * 2 * kUnitBytes), slo = shi + kUnitBytes;
+          const uint32_t shi = smem_u32(raw + (size_t)s * kUnitBytes);
+          const uint32_t slo = smem_u32(lor + (size_t)t * kUnitBytes);
 #pragma unroll
           for (int ks = 0; ks < kKU / 8; ++ks) {
-            const uint32_t oa = (uint32_t)ks * 2 * lboA;
+            const uint32_t oa = (uint32_t)ks * 32;  // 8 tf32 of the 128-byte swizzled rows
             const uint32_t ob = (uint32_t)(h * (kKU / 8) + ks) * 2 * lboB;
-            const uint64_t ahi = umma_desc(shi + oa, lboA, sbo), alo = umma_desc(slo + oa, lboA, sbo);
+            const uint64_t ahi = umma_desc_sw128(shi + oa), alo = umma_desc_sw128(slo + oa);
             const uint64_t bhi = umma_desc(sB + ob, lboB, sbo), blo = umma_desc(sBl + ob, lboB, sbo);
             mma_tf32(acc, ahi, bhi, idesc, (h > 0 || ks > 0) ? 1u : 0u);
             mma_tf32(acc, alo, bhi, idesc, 1u);
             mma_tf32(acc, ahi, blo, idesc, 1u);
           }
-          mma_commit(smem_u32(empty + s));  // the ring slot is free once these MMAs ran
+          mma_commit(smem_u32(rempty + s));  // the raw slot and the lo slot are free once these MMAs ran
+          mma_commit(smem_u32(lempty + t));
           if (h == units - 1) mma_commit(smem_u32(tfull + slot));
         }
         __syncwarp();
@@ -431,23 +514,64 @@ int tc_kp(int64_t d) { return (int)((d + kKU - 1) / kKU * kKU); }
 size_t tc_smem_fixed(int64_t d, int64_t k) {
   const int64_t kp = tc_kp(d), np = tc_npad(k);
   return sizeof(float) * (2 * np * kp + np) + sizeof(int32_t) * (np + kTM) +
-         sizeof(uint64_t) * (3 * kMaxStages + 4) + 16 + 1024;
+         sizeof(uint64_t) * (2 * kMaxRaw + 2 * kLoStages + 4) + 16 + 1024 +
+         (size_t)kLoStages * kUnitBytes;
 }
 
-// ring units that fit next to the centroid tiles (>= 3 required)
+// raw ring units that fit next to the centroid tiles and the lo ring (>= 2 required)
 int tc_stages(int64_t d, int64_t k) {
   const int64_t cap = (int64_t)csc::device_info().max_smem_optin;
   const int64_t left = cap - (int64_t)tc_smem_fixed(d, k);
-  return (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(0, left / (2 * kUnitBytes)));
+  return (int)std::min<int64_t>(kMaxRaw, std::max<int64_t>(0, left / kUnitBytes));
 }
 
 size_t tc_smem(int64_t d, int64_t k) {
-  return (size_t)std::max(tc_stages(d, k), 3) * 2 * kUnitBytes + tc_smem_fixed(d, k);
+  return (size_t)std::max(tc_stages(d, k), 2) * kUnitBytes + tc_smem_fixed(d, k);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 map over the n x ld32 features, box = 32 columns x box_rows rows,
+// 128-byte swizzle (the UMMA K-major SW128 layout), zero fill out of bounds
+int feature_map(CUtensorMap *m, const float *f32, int64_t n, int64_t ld32, uint32_t box_rows) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) {
+    csc::set_error("tc screen: cuTensorMapEncodeTiled unavailable");
+    return CSC_ERR_CUDA;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)ld32, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld32 * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)kKU, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(f32), dims, strides,
+                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    csc::set_error("tc screen: cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return CSC_ERR_CUDA;
+  }
+  return CSC_OK;
 }
 
 template <int NP>
 int tc_launch(const TcArgs &a, cudaStream_t st) {
   const size_t smem = tc_smem(a.d, a.k);
+  CUtensorMap tile_map, row_map;
+  int rc = feature_map(&tile_map, a.f32, a.n, a.ld32, kTM);
+  if (rc == CSC_OK) rc = feature_map(&row_map, a.f32, a.n, a.ld32, 1);
+  if (rc != CSC_OK) return rc;
   static std::mutex mu;
   static size_t configured = 0;
   {
@@ -460,7 +584,7 @@ int tc_launch(const TcArgs &a, cudaStream_t st) {
   }
   const int64_t tiles = csc::ceil_div(a.n, kTM);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(csc::device_info().sm_count, tiles));
-  tc_screen_kernel<NP><<<(unsigned)grid, kTcThreads, smem, st>>>(a, tc_stages(a.d, a.k));
+  tc_screen_kernel<NP><<<(unsigned)grid, kTcThreads, smem, st>>>(a, tc_stages(a.d, a.k), tile_map, row_map);
   CSC_CHECK_LAUNCH();
   return CSC_OK;
 }
@@ -488,7 +612,7 @@ namespace csc {
 bool tc_screen_supported(int64_t d, int64_t k) {
   const csc::DeviceInfo &info = csc::device_info();
   return info.cc_major == 10 && d >= 1 && d <= 256 && k >= 2 && tc_npad(k) <= 128 &&
-         tc_stages(d, k) >= 3;
+         tc_stages(d, k) >= 2;
 }
 
 int64_t tc_centroid_floats(int64_t d, int64_t k) { return (int64_t)tc_npad(k) * tc_kp(d); }
