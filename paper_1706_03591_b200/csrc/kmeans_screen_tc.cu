@@ -114,6 +114,26 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// issued by the whole warp with warp-uniform operands; one elected lane (the
+// same one every time: elect.sync picks the lowest active lane) executes it
+__device__ __forceinline__ void mma_tf32_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -428,24 +448,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int t = (int)(u % kLoStages);
         mbar_wait(smem_u32(lfull + t), (uint32_t)((u / kLoStages) & 1));
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t shi = smem_u32(raw + (size_t)s * kUnitBytes);
-          const uint32_t slo = smem_u32(lor + (size_t)t * kUnitBytes);
+        // warp-uniform descriptors (the address field is the low 14 bits of
+        // addr >> 4: offsets add without carries below 256 KB)
+        const uint64_t dhi = umma_desc_sw128(smem_u32(raw + (size_t)s * kUnitBytes));
+        const uint64_t dlo = umma_desc_sw128(smem_u32(lor + (size_t)t * kUnitBytes));
 #pragma unroll
-          for (int ks = 0; ks < kKU / 8; ++ks) {
-            const uint32_t oa = (uint32_t)ks * 32;  // 8 tf32 of the 128-byte swizzled rows
-            const uint32_t ob = (uint32_t)(h * (kKU / 8) + ks) * 2 * lboB;
-            const uint64_t ahi = umma_desc_sw128(shi + oa), alo = umma_desc_sw128(slo + oa);
-            const uint64_t bhi = umma_desc(sB + ob, lboB, sbo), blo = umma_desc(sBl + ob, lboB, sbo);
-            mma_tf32(acc, ahi, bhi, idesc, (h > 0 || ks > 0) ? 1u : 0u);
-            mma_tf32(acc, alo, bhi, idesc, 1u);
-            mma_tf32(acc, ahi, blo, idesc, 1u);
-          }
-          mma_commit(smem_u32(rempty + s));  // the raw slot and the lo slot are free once these MMAs ran
-          mma_commit(smem_u32(lempty + t));
-          if (h == units - 1) mma_commit(smem_u32(tfull + slot));
+        for (int ks = 0; ks < kKU / 8; ++ks) {
+          const uint64_t ahi = dhi + (uint64_t)(ks * 2), alo = dlo + (uint64_t)(ks * 2);  // + 32 B
+          const uint32_t ob = (uint32_t)(h * (kKU / 8) + ks) * 2 * lboB;
+          const uint64_t bhi = umma_desc(sB + ob, lboB, sbo), blo = umma_desc(sBl + ob, lboB, sbo);
+          mma_tf32_elect(acc, ahi, bhi, idesc, (h > 0 || ks > 0) ? 1u : 0u);
+          mma_tf32_elect(acc, alo, bhi, idesc, 1u);
+          mma_tf32_elect(acc, ahi, blo, idesc, 1u);
         }
-        __syncwarp();
+        mma_commit_elect(smem_u32(rempty + s));  // the raw slot and the lo slot are free once these MMAs ran
+        mma_commit_elect(smem_u32(lempty + t));
+        if (h == units - 1) mma_commit_elect(smem_u32(tfull + slot));
       }
     }
   } else {
