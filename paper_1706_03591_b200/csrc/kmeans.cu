@@ -2006,7 +2006,9 @@ __global__ void __launch_bounds__(1024)
                         double *__restrict__ cent, int64_t ldc, double *__restrict__ cnorm,
                         double *__restrict__ delta, double *__restrict__ cterm,
                         double *__restrict__ scal, double *__restrict__ shalf,
-                        int32_t *__restrict__ flags) {
+                        int32_t *__restrict__ flags, float *__restrict__ chi,
+                        float *__restrict__ clo, float *__restrict__ cn32,
+                        double *__restrict__ cmax, int npad, int kp) {
   extern __shared__ double cs[];  // [k][lds] centroids, then [3][k] delta, |c|^2, cost term
   const int64_t lds = d | 1;
   double *sdel = cs + k * lds, *snrm = sdel + k, *sct = snrm + k;
@@ -2060,8 +2062,30 @@ __global__ void __launch_bounds__(1024)
     scal[2] = d2;
     scal[3] = (double)j1;
     scal[4] = sqrt(cm);
+    if (cmax) cmax[0] = sqrt(cm);
     flags[3] = flags[0];  // last candidate count, for csc_kmeans_plan_stats
     flags[0] = 0;
+  }
+  if (chi) {  // the next iteration's tensor-core screen tiles (tc_centroids_kernel's values)
+    for (int64_t e = threadIdx.x; e < (int64_t)npad * kp; e += blockDim.x) {
+      const int64_t j = e / kp, t = e - j * kp;
+      const float v = (j < k && t < d) ? (float)cs[j * lds + t] : 0.0f;
+      const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      const int64_t off = (t / 4) * (int64_t)npad * 4 + j * 4 + (t % 4);
+      chi[off] = h;
+      clo[off] = v - h;
+    }
+    for (int64_t j = threadIdx.x; j < npad; j += blockDim.x) {
+      float sq = INFINITY;
+      if (j < k) {
+        sq = 0.0f;
+        for (int64_t t = 0; t < d; ++t) {
+          const float v = (float)cs[j * lds + t];
+          sq = fmaf(v, v, sq);
+        }
+      }
+      cn32[j] = sq;
+    }
   }
   // half-separations: lane o of warp j accumulates |c_j - c_o|^2 over c in order
   for (int64_t j = wid; j < k; j += nw) {
@@ -2207,6 +2231,7 @@ struct csc_kmeans_plan {
   // exact fixed-point sums (fx_delta_kernel): [k][d] lo / hi words, Q [k][2],
   // counts [k], max |f|^2 bits
   bool fx = false;
+  bool finish_small = false;  // one single-block node finishes an iteration
   int fx_grid = 0;
   void *fx_base = nullptr;
   unsigned long long *fx_lo = nullptr, *fx_hi = nullptr, *fx_q = nullptr, *fx_max = nullptr;
@@ -2406,6 +2431,13 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
     CSC_TRY_CUDA(cudaFuncSetAttribute(
         update_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
         (int)(sizeof(int32_t) * (2 * (size_t)p->chunk + 3 * (size_t)k))));
+  {
+    const size_t fsm = sizeof(double) * (size_t)k * ((d | 1) + 3);
+    p->finish_small = (int64_t)fsm <= (int64_t)info.max_smem_optin && k * k * d <= (int64_t(1) << 21);
+    if (p->finish_small && fsm > 48 * 1024)
+      CSC_TRY_CUDA(cudaFuncSetAttribute(finish_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)fsm));
+  }
   const size_t fxs = fx_smem(d, k);
   if (want_fx) {
     const size_t kd = kk * (size_t)d;
@@ -2547,6 +2579,8 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
                : launch_assign2<4>(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own, cnts,
                                    asmem, st, rows, nrows, p->ub, p->lb, gate);
   };
+  // the single-block finish converts the new centroids for the tensor-core screen
+  const bool tc_fused = p->f32 && p->tc && p->finish_small && g_finish_mode != 2;
   // FP32 screen first when enabled: provably decided rows there, the rest
   // (listed in p->amb) by the FP64 assignment — the same labels either way
   auto screened = [&](const int32_t *rows, const int32_t *nrows, int32_t *cnts) -> int {
@@ -2554,8 +2588,10 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
     CSC_TRY_CUDA(cudaMemsetAsync(p->namb, 0, sizeof(int32_t), st));
     int r2;
     if (p->tc) {
-      r2 = csc::tc_convert_centroids(cent, k, d, ldc, cnorm, p->chi, p->clo, p->cn32, p->cmax, st);
-      if (r2 != CSC_OK) return r2;
+      if (full || !tc_fused) {  // else the previous iteration's finish wrote the tiles
+        r2 = csc::tc_convert_centroids(cent, k, d, ldc, cnorm, p->chi, p->clo, p->cn32, p->cmax, st);
+        if (r2 != CSC_OK) return r2;
+      }
       r2 = csc::tc_screen_assign(p->f32, p->ld32, p->fn32, n, d, p->chi, p->clo, p->cn32, k,
                                  p->cmax, rows, nrows, labels, p->ub, p->lb, cnts, p->amb, p->namb,
                                  nullptr, st);
@@ -2566,6 +2602,14 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
                               rows, nrows, labels, p->ub, p->lb, cnts, p->amb, p->namb, st);
     }
     if (r2 != CSC_OK) return r2;
+    // the undecided rows are few (~0.5% at cfg5): the warp-per-4-rows kernel
+    // (same per-pair arithmetic and ties, same labels) has no tile pipeline to fill
+    if (k <= 64 && d <= 128 && g_assign_tile == 0) {
+      return k <= 32 ? launch_assign_small<1>(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own,
+                                              cnts, st, p->amb, p->namb, p->ub, p->lb, nullptr)
+                     : launch_assign_small<2>(f, fnorm, n, d, ld, cent, ldc, cnorm, k, labels, p->own,
+                                              cnts, st, p->amb, p->namb, p->ub, p->lb, nullptr);
+    }
     return assign(p->amb, p->namb, cnts, nullptr);
   };
   int rc;
@@ -2630,12 +2674,13 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
         p->psum, p->pcnt, p->pq, p->nb, d, k, p->S, counts, p->Q);
     CSC_CHECK_LAUNCH();
   }
-  if (g_finish_mode != 2 && k * ((d | 1) + 3) * (int64_t)sizeof(double) <= 48 * 1024 &&
-      k * k * d <= (int64_t(1) << 20)) {
+  if (g_finish_mode != 2 && p->finish_small) {
     // small k: one single-block node finishes the iteration
     finish_small_kernel<<<1, g_finish_mode == 1 ? 256 : 1024, sizeof(double) * k * ((d | 1) + 3),
                           st>>>(d, k, p->S, counts, p->Q, cent, ldc, cnorm,
-                                            p->delta, p->cterm, p->scal, p->shalf, p->flags);
+                                            p->delta, p->cterm, p->scal, p->shalf, p->flags,
+                                            tc_fused ? p->chi : nullptr, p->clo, p->cn32, p->cmax,
+                                            csc::tc_npad_of(k), csc::tc_kp_of(d));
     CSC_CHECK_LAUNCH();
   } else {
     centroid_finish_kernel<<<(unsigned)k, 128, 0, st>>>(p->S, counts, p->Q, d, k, cent, ldc,

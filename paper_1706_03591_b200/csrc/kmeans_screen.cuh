@@ -34,6 +34,11 @@ int screen_assign(const float *f32, int64_t ld32, const float *fn32, const doubl
 // same contract as screen_assign with centroids in hi / lo K-major tiles
 // (tc_convert_centroids); raw_out (tests) receives E instead of decisions.
 bool tc_screen_supported(int64_t d, int64_t k);
+// centroid tile shape of the tensor-core screen: k rounded to 16 (UMMA N),
+// d rounded to 32 (one ring unit); tile element (j, t) of hi / lo at
+// (t / 4) * npad * 4 + j * 4 + t % 4
+inline int tc_npad_of(int64_t k) { return (int)((k + 15) / 16 * 16); }
+inline int tc_kp_of(int64_t d) { return (int)((d + 31) / 32 * 32); }
 int64_t tc_centroid_floats(int64_t d, int64_t k);
 int tc_convert_centroids(const double *c, int64_t k, int64_t d, int64_t ldc, const double *cnorm,
                          float *chi, float *clo, float *cn32, double *cmax, cudaStream_t st);
