@@ -320,22 +320,18 @@ def run_dynamic(args, rank):
     from paper_1706_03591_b200 import generators as G
     n, k, d = 20000, 20, 80
     q1, q2 = G.sbm_probabilities(n, k, 24.0, 0.05)
-    codes = G.planted_partition_codes(n, k, q1, q2, 7)
-    labels = np.repeat(np.arange(k), G.block_sizes(n, k))
-    g0 = G.graph_from_codes(n, codes)
-    cur = codes
+    # the sequence from the device generators (8f-3); each step's lists are
+    # handed to the timed step as host arrays, as a caller's would be
+    g0, labels = G.planted_partition_device(n, k, 24.0, 0.05, seed=7)
+    cur = g0
     steps = 10
-
-    def applied(c, dl, il):
-        return np.union1d(np.setdiff1d(c, dl, assume_unique=True), il)
-
     deltas = []
     for t in range(1, steps):  # nodes first, then edges
-        dn, inn, labels = G.node_switch(cur, n, labels, k, q1, q2, 0.005, seed=200 + t)
-        cur = applied(cur, dn, inn)
-        de, ie = G.edge_churn(cur, n, labels, q1, q2, 0.01, seed=100 + t)
-        cur = applied(cur, de, ie)
-        deltas.append((dn, inn, de, ie))
+        dn, inn, labels = G.node_switch_device(cur, labels, k, q1, q2, 0.005, seed=200 + t)
+        cur = cur.apply_delta(dn, inn)
+        de, ie = G.edge_churn_device(cur, labels, q1, q2, 0.01, seed=100 + t)
+        cur = cur.apply_delta(de, ie)
+        deltas.append(tuple(x.cpu().numpy() for x in (dn, inn, de, ie)))
     cfg = P.DynamicConfig(k=k, d=d, p=0.5, filter=P.FilterConfig(order=60))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -357,9 +353,7 @@ def run_dynamic(args, rank):
         refined += diag.refined
     # one refined step: the communities split (k 20 -> 26 planted blocks), the
     # validation eigencount leaves the tolerance band and the cutoff is re-bisected
-    q1s, q2s = G.sbm_probabilities(n, 26, 24.0, 0.05)
-    g_split = G.graph_from_codes(n, G.planted_partition_codes(n, 26, q1s, q2s, 9))
-    g_split.device_codes()
+    g_split, _ = G.planted_partition_device(n, 26, 24.0, 0.05, seed=9)
     ph = {}
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -405,14 +399,14 @@ def run_dynamic_cfg5(args, rank, steps=4):
     w = WORKLOADS["cfg5"]
     n, k, d = w["n"], w["k"], w["d"]
     q1, q2 = G.sbm_probabilities(n, k, w["deg"], w["ratio"])
-    codes = G.planted_partition_codes(n, k, q1, q2, w["seed"])
-    labels = np.repeat(np.arange(k), G.block_sizes(n, k))
-    g = G.graph_from_codes(n, codes)
-    deltas, cur = [], codes
+    t_gen = time.perf_counter()
+    g, labels = G.planted_partition_device(n, k, w["deg"], w["ratio"], seed=w["seed"])  # device generators (8f-3)
+    deltas, cur = [], g
     for s in range(steps):
-        dl, il = G.edge_churn(cur, n, labels, q1, q2, 0.01, seed=50 + s)
-        deltas.append((dl, il))
-        cur = np.union1d(np.setdiff1d(cur, dl, assume_unique=True), il)
+        dl, il = G.edge_churn_device(cur, labels, q1, q2, 0.01, seed=50 + s)
+        cur = cur.apply_delta(dl, il)
+        deltas.append((dl.cpu().numpy(), il.cpu().numpy()))  # host lists for the timed merge
+    gen_s = time.perf_counter() - t_gen
     cfg = P.DynamicConfig(k=k, d=d, p=0.5, filter=P.FilterConfig(order=w["order"]))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -437,7 +431,8 @@ def run_dynamic_cfg5(args, rank, steps=4):
                          f"k-means k={k} x 10 restarts"),
             "ms_per_step": statistics.median(ms), "ms_all": [round(v, 1) for v in ms], "steps_timed": len(ms),
             "init_ms": init_ms, "init_search_iters": diag0.search_iters, "refined_steps": refined,
-            "phase_ms_mean": {k2: round(v / len(ms), 2) for k2, v in phases.items()}}
+            "phase_ms_mean": {k2: round(v / len(ms), 2) for k2, v in phases.items()},
+            "graph_and_churn_gen_s": round(gen_s, 2)}
 
 
 def e2e_calls(P, lap, poly, x_np, precision, calls):

@@ -358,6 +358,46 @@ int csc_gather_columns(const double *src_dev, int64_t n, int64_t ld_src, const i
                        int64_t ncols, double *dst_dev, int64_t ld_dst, int64_t dst_col0,
                        void *stream);
 
+/* ---- O(m) synthetic graph generators on device ------------
+ * Replace the reference's O(n^2) samplers for n in the millions:
+ * sbm_generate (graphs.py:194-221), perturb_edges (graphs.py:236-273, with
+ * _absent_pairs graphs.py:228-233) and perturb_nodes (graphs.py:276-319).
+ * Equal in distribution, not stream-identical: Philox-4x32-10 keyed by
+ * `seed`, deterministic for a seed. Blocks are nblocks near-equal contiguous
+ * node ranges (sizes[:n % nblocks] one larger), as SbmParams uses. Outputs
+ * are sorted, duplicate-free canonical codes lo*n+hi. All SYNCHRONISE. */
+/* planted partition: pair_counts (host, nblocks*(nblocks+1)/2, pairs (a, b)
+ * with a <= b in row-major order) edges per block pair — the caller's
+ * Binomial(pairs of (a, b), q) draws — each a uniform distinct subset of the
+ * pair's node pairs. codes_out capacity >= sum of the counts. */
+int csc_gen_planted_partition(int64_t n, int32_t nblocks, const int64_t *pair_counts, uint64_t seed,
+                              int64_t *codes_out_dev, int64_t capacity, int64_t *m_out,
+                              void *stream);
+/* Chung-Lu / degree-corrected SBM: m_draw edge draws, each a block pair
+ * from pair_cum_host (nblocks^2 doubles, inclusive cumulative weights, index
+ * a*nblocks+b) and endpoints from cum_theta_dev (n doubles, per-block
+ * inclusive cumulative theta); self-loops and repeats dropped. */
+int csc_gen_chung_lu(int64_t n, int32_t nblocks, const double *cum_theta_dev,
+                     const double *pair_cum_host, int64_t m_draw, uint64_t seed,
+                     int64_t *codes_out_dev, int64_t capacity, int64_t *m_out, void *stream);
+/* edge churn (perturb_edges semantics): `count` present edges deleted
+ * uniformly, `count` absent pairs inserted in proportion to q1 (same label)
+ * / q2 (different labels) without replacement; pairs in both lists dropped
+ * from both. labels_dev: n int32 in [0, nblocks). del/ins capacity >= count. */
+int csc_gen_edge_churn(int64_t n, const int64_t *codes_dev, int64_t m, const int32_t *labels_dev,
+                       int32_t nblocks, double q1, double q2, int64_t count, uint64_t seed,
+                       int64_t *del_out_dev, int64_t *n_del, int64_t *ins_out_dev, int64_t *n_ins,
+                       void *stream);
+/* node switch (perturb_nodes semantics): `count` distinct nodes move to a
+ * uniformly drawn other label (labels_dev updated in place), every edge at a
+ * moved node is deleted, every pair with a moved endpoint is drawn once with
+ * q1 / q2 under the new labels; pairs in both lists dropped from both.
+ * del capacity >= m; CSC_ERR_CAPACITY if insertions exceed ins_capacity. */
+int csc_gen_node_switch(int64_t n, const int64_t *codes_dev, int64_t m, int32_t *labels_dev,
+                        int32_t nblocks, double q1, double q2, int64_t count, uint64_t seed,
+                        int64_t *del_out_dev, int64_t *n_del, int64_t *ins_out_dev,
+                        int64_t ins_capacity, int64_t *n_ins, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,12 @@ SIGNATURES = {
     "csc_kmeans_plan_destroy": ([_P], _INT),
     "csc_kmeans_plan_stats": ([_P, _PI64, ctypes.POINTER(_I32)], _INT),
     "csc_kmeans_plan_screen_stats": ([_P, _PI64], _INT),
+    "csc_gen_planted_partition": ([_I64, _I32, _P, ctypes.c_uint64, _P, _I64, _PI64, _P], _INT),
+    "csc_gen_chung_lu": ([_I64, _I32, _P, _P, _I64, ctypes.c_uint64, _P, _I64, _PI64, _P], _INT),
+    "csc_gen_edge_churn": ([_I64, _P, _I64, _P, _I32, _D, _D, _I64, ctypes.c_uint64, _P, _PI64, _P, _PI64, _P],
+                           _INT),
+    "csc_gen_node_switch": ([_I64, _P, _I64, _P, _I32, _D, _D, _I64, ctypes.c_uint64, _P, _PI64, _P, _I64, _PI64,
+                             _P], _INT),
     "csc_kmeans_iterate": ([_P, _P, _P, _P, _I64, _P, _P, _P, _INT, _P, _P], _INT),
     "csc_kmeans_run": ([_P, _P, _P, _P, _I64, _P, _P, _P, _INT, _D, _P, _P, _P], _INT),
     "csc_kmeans_tuning": ([ctypes.c_char_p, _I64], _INT),

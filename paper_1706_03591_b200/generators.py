@@ -18,11 +18,24 @@ edge_churn         per-step delete/insert code lists with perturb_edges
                    semantics (graphs.py:236-273): delete uniformly among
                    present edges, insert among absent pairs with probability
                    proportional to the model probability of the pair.
+
+The same four models run on the GPU (csrc/generators.cu,
+csc_gen_*): planted_partition_device, chung_lu_sbm_device,
+edge_churn_device and node_switch_device keep the edge codes and the
+delete/insert lists on the device (Graph.apply_delta takes device lists), with
+O(k^2) host work only (the block-pair Binomial counts, the Chung-Lu pair
+weights). The host versions above stay as the reference-style restatement
+the device ones are tested against in distribution.
 """
 from __future__ import annotations
 
-import numpy as np
+import ctypes
 
+import numpy as np
+import torch
+
+from . import _native
+from ._device import ptr, require_cuda, stream
 from .graphs import Graph
 
 
@@ -275,3 +288,139 @@ def node_switch(codes: np.ndarray, n: int, labels: np.ndarray, k: int, q1: float
         dels = np.setdiff1d(dels, both, assume_unique=True)
         ins = np.setdiff1d(ins, both, assume_unique=True)
     return dels, ins, new_labels
+
+
+# ---------------------------------------------------------------------------
+# Device generators (csrc/generators.cu)
+# ---------------------------------------------------------------------------
+def _device_seed(rng: np.random.Generator) -> int:
+    return int(rng.integers(0, 2 ** 63, dtype=np.int64))
+
+
+def _graph_from_device_codes(n: int, codes: torch.Tensor, m: int) -> Graph:
+    g = Graph.__new__(Graph)
+    g._init(int(n), None, None, None, codes[:m], int(m))
+    object.__setattr__(g, "_unit", True)
+    return g
+
+
+def planted_pair_counts(n: int, k: int, q1: float, q2: float, rng: np.random.Generator) -> np.ndarray:
+    """Binomial edge count per block pair (a <= b, row-major): Binomial(s_a (s_a - 1) / 2, q1)
+    inside a block, Binomial(s_a s_b, q2) across — the planted partition's O(k^2) host part."""
+    sizes = block_sizes(n, k)
+    a, b = np.triu_indices(k)
+    npairs = np.where(a == b, sizes[a] * (sizes[a] - 1) // 2, sizes[a] * sizes[b])
+    return rng.binomial(npairs, np.where(a == b, q1, q2)).astype(np.int64)
+
+
+def planted_partition_codes_device(n: int, k: int, q1: float, q2: float, seed=0) -> tuple[torch.Tensor, int]:
+    """Sorted unique canonical codes of a planted-partition graph on the GPU (device tensor, m)."""
+    dev = require_cuda()
+    rng = np.random.default_rng(seed)
+    counts = planted_pair_counts(n, k, q1, q2, rng)
+    total = int(counts.sum())
+    codes = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+    m = ctypes.c_int64(0)
+    _native.call("csc_gen_planted_partition", n, k, counts.ctypes.data, _device_seed(rng), ptr(codes),
+                 codes.numel(), ctypes.byref(m), stream())
+    return codes, int(m.value)
+
+
+def planted_partition_device(n: int, k: int, mean_degree: float, ratio: float, seed=0) -> tuple[Graph, np.ndarray]:
+    """planted_partition on the GPU: the graph's edge set never visits the host."""
+    q1, q2 = sbm_probabilities(n, k, mean_degree, ratio)
+    codes, m = planted_partition_codes_device(n, k, q1, q2, seed)
+    return _graph_from_device_codes(n, codes, m), np.repeat(np.arange(k, dtype=np.int64), block_sizes(n, k))
+
+
+def chung_lu_sbm_device(n: int, k: int, mean_degree: float, exponent: float, max_degree: float,
+                        ratio: float, seed=0) -> tuple[Graph, np.ndarray]:
+    """chung_lu_sbm on the GPU (same model and parameters): theta, its
+    per-block cumulative sums and the edge draws on the device; the k x k
+    block-pair weights and the Poisson draw count on the host."""
+    dev = require_cuda()
+    rng = np.random.default_rng(seed)
+    gamma = 1.0 / (exponent - 1.0)
+    target = max_degree / mean_degree
+    idx = torch.arange(n, dtype=torch.float64, device=dev)
+    lo, hi = 1e-6, float(n)
+    for _ in range(60):  # i0 with theta_max / theta_mean = max_degree / mean_degree
+        i0 = float(np.sqrt(lo * hi))
+        th = (idx + i0) ** -gamma
+        if float(th[0] / th.mean()) > target:
+            lo = i0
+        else:
+            hi = i0
+    theta = (idx + i0) ** -gamma
+    theta = theta / theta.mean() * mean_degree
+    perm = torch.from_numpy(rng.permutation(n)).to(dev)
+    theta = theta[perm]
+    sizes = block_sizes(n, k)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    cum = torch.empty_like(theta)
+    bw = np.empty(k)
+    for b in range(k):
+        seg = torch.cumsum(theta[offs[b]:offs[b + 1]], 0)
+        cum[offs[b]:offs[b + 1]] = seg
+        bw[b] = float(seg[-1])
+    pair_w = np.outer(bw, bw) * ratio
+    pair_w[np.diag_indices(k)] = bw ** 2
+    pair_cum = np.cumsum((pair_w / pair_w.sum()).ravel())
+    m_draw = int(rng.poisson(n * mean_degree / 2.0))
+    codes = torch.empty(max(m_draw, 1), dtype=torch.int64, device=dev)
+    m = ctypes.c_int64(0)
+    _native.call("csc_gen_chung_lu", n, k, ptr(cum), pair_cum.ctypes.data, m_draw, _device_seed(rng), ptr(codes),
+                 codes.numel(), ctypes.byref(m), stream())
+    return _graph_from_device_codes(n, codes, int(m.value)), np.repeat(np.arange(k, dtype=np.int64), sizes)
+
+
+def _labels_dev(labels) -> torch.Tensor:
+    if isinstance(labels, torch.Tensor):
+        return labels.to(device=require_cuda(), dtype=torch.int32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(labels, dtype=np.int32)).to(require_cuda())
+
+
+def edge_churn_device(g: Graph, labels, q1: float, q2: float, fraction: float,
+                      seed=0) -> tuple[torch.Tensor, torch.Tensor]:
+    """edge_churn on the GPU: (deletes, inserts) as sorted device code tensors."""
+    dev = require_cuda()
+    codes = g.device_codes()
+    count = int(round(fraction * g.m))
+    lab = _labels_dev(labels)
+    k = int(lab.max().item()) + 1
+    dels = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+    ins = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+    nd, ni = ctypes.c_int64(0), ctypes.c_int64(0)
+    rng = np.random.default_rng(seed)
+    _native.call("csc_gen_edge_churn", g.n, ptr(codes), g.m, ptr(lab), k, float(q1), float(q2), count,
+                 _device_seed(rng), ptr(dels), ctypes.byref(nd), ptr(ins), ctypes.byref(ni), stream())
+    return dels[:nd.value], ins[:ni.value]
+
+
+def node_switch_device(g: Graph, labels, k: int, q1: float, q2: float, fraction: float,
+                       seed=0) -> tuple[torch.Tensor, torch.Tensor, np.ndarray]:
+    """node_switch on the GPU: (deletes, inserts) as sorted device code tensors, new labels (numpy)."""
+    if k < 2:
+        raise ValueError("node reassignment needs k >= 2")
+    dev = require_cuda()
+    codes = g.device_codes()
+    count = int(round(fraction * g.n))
+    lab = _labels_dev(labels).clone()
+    dels = torch.empty(max(g.m, 1), dtype=torch.int64, device=dev)
+    rng = np.random.default_rng(seed)
+    dseed = _device_seed(rng)
+    expected = count * g.n * max(q1, q2)
+    cap = int(expected * 1.5 + 6 * np.sqrt(expected + 1) + 4096)
+    nd, ni = ctypes.c_int64(0), ctypes.c_int64(0)
+    while True:
+        ins = torch.empty(cap, dtype=torch.int64, device=dev)
+        lab_try = lab.clone()
+        try:
+            _native.call("csc_gen_node_switch", g.n, ptr(codes), g.m, ptr(lab_try), k, float(q1), float(q2), count,
+                         dseed, ptr(dels), ctypes.byref(nd), ptr(ins), cap, ctypes.byref(ni), stream())
+            break
+        except ValueError as exc:  # CSC_ERR_CAPACITY: same draws with a larger buffer
+            if "capacity" not in str(exc):
+                raise
+            cap *= 2
+    return dels[:nd.value], ins[:ni.value], lab_try.cpu().numpy().astype(np.int64)

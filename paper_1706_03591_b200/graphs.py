@@ -182,25 +182,37 @@ class Graph:
 
         Unit-weight graphs only (the perturbation models insert unit edges,
         graphs.py:270-272). Deletions must be edges of this graph and
-        insertions must be absent from the result of the deletions; both lists
-        are sorted on the host. The merged edge set stays on the GPU.
+        insertions must be absent from the result of the deletions. Host lists
+        are sorted on the host; device tensors (the device generators' sorted
+        lists) are used in place. The merged edge set stays on the GPU.
         """
         if not self.unit_weights():
             raise ValueError("apply_delta supports unit-weight graphs only")
         dev = require_cuda()
-        dl = _sorted_codes(deletes)
-        il = _sorted_codes(inserts)
-        if il.size:
-            lo, hi = il // self.n, il % self.n
-            if il.min() < 0 or np.any(lo >= hi) or hi.max() >= self.n:
-                raise ValueError("inserted codes must be canonical pairs i*n+j with i < j < n")
+        if isinstance(deletes, torch.Tensor) or isinstance(inserts, torch.Tensor):
+            # device lists (generators.edge_churn_device / node_switch_device): sorted, unique
+            d_t = torch.as_tensor(deletes, dtype=torch.int64, device=dev).contiguous()
+            i_t = torch.as_tensor(inserts, dtype=torch.int64, device=dev).contiguous()
+            if i_t.numel():
+                lo, hi = i_t // self.n, i_t % self.n
+                if not bool(((i_t >= 0) & (lo < hi) & (hi < self.n)).all()):
+                    raise ValueError("inserted codes must be canonical pairs i*n+j with i < j < n")
+            nd, ni = d_t.numel(), i_t.numel()
+        else:
+            dl = _sorted_codes(deletes)
+            il = _sorted_codes(inserts)
+            if il.size:
+                lo, hi = il // self.n, il % self.n
+                if il.min() < 0 or np.any(lo >= hi) or hi.max() >= self.n:
+                    raise ValueError("inserted codes must be canonical pairs i*n+j with i < j < n")
+            d_t = torch.from_numpy(dl).to(dev)
+            i_t = torch.from_numpy(il).to(dev)
+            nd, ni = dl.size, il.size
         prev = self.device_codes()
-        m_new = self.m - dl.size + il.size
+        m_new = self.m - nd + ni
         out = torch.empty(max(m_new, 1), dtype=torch.int64, device=dev)
-        d_t = torch.from_numpy(dl).to(dev)
-        i_t = torch.from_numpy(il).to(dev)
         got = ctypes.c_int64(0)
-        _native.call("csc_edge_delta", self.n, ptr(prev), self.m, ptr(d_t), dl.size, ptr(i_t), il.size,
+        _native.call("csc_edge_delta", self.n, ptr(prev), self.m, ptr(d_t), nd, ptr(i_t), ni,
                      ptr(out), out.numel(), ctypes.byref(got), stream())
         g = Graph.__new__(Graph)
         g._init(self.n, None, None, None, out[:m_new], int(got.value))

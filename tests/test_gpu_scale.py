@@ -17,8 +17,9 @@ live reference's goldens by tests/test_oracle_golden.py):
     cutoff decision is the one the oracle's estimate gives;
   * cfg3 shape k-means (kmeans.py:64-117): k-means++ from the same seed then
     3 Lloyd iterations, ARI >= 0.999 and cost <= 1e-9 relative vs the oracle.
-The graphs come from the O(m) generators (generators.py) with the seeds
-bench.py uses; the oracle reads the device-built Laplacian, whose values are
+The graphs come from the O(m) generators (generators.py; the cfg4 and cfg5
+ones from the device generators, csrc/generators.cu) with the seeds bench.py
+uses; the oracle reads the device-built Laplacian, whose values are
 checked bitwise separately (test_gpu_fullsize.py, test_gpu_parity.py).
 """
 import numpy as np
@@ -82,7 +83,7 @@ def test_cfg3_filter_order100_vs_oracle(cfg3):
 def cfg4(cuda_ok):
     import paper_1706_03591_b200 as P
     from paper_1706_03591_b200 import generators as G
-    g, _ = G.chung_lu_sbm(4_000_000, 50, 16.0, 2.3, 20000.0, 0.05, seed=4)
+    g, _ = G.chung_lu_sbm_device(4_000_000, 50, 16.0, 2.3, 20000.0, 0.05, seed=4)
     return P, g, P.laplacian(g)
 
 
@@ -129,10 +130,8 @@ def test_cfg5_dynamic_step_vs_oracle(cuda_ok):
     from paper_1706_03591_b200 import generators as G
     n, k, d = 2_000_000, 64, 96
     q1, q2 = G.sbm_probabilities(n, k, 20.0, 0.05)
-    codes = G.planted_partition_codes(n, k, q1, q2, 5)
-    labels = np.repeat(np.arange(k), G.block_sizes(n, k))
-    g1 = G.graph_from_codes(n, codes)
-    dl, il = G.edge_churn(codes, n, labels, q1, q2, 0.01, seed=105)
+    g1, labels = G.planted_partition_device(n, k, 20.0, 0.05, seed=5)  # device generators (8f-3)
+    dl, il = G.edge_churn_device(g1, labels, q1, q2, 0.01, seed=105)
     g2 = g1.apply_delta(dl, il)
     cfg = P.DynamicConfig(k=k, d=d, p=0.5, filter=P.FilterConfig(order=80),
                           kmeans=P.KmeansConfig(restarts=2, max_iters=20))

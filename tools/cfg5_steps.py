@@ -28,14 +28,12 @@ a = ap.parse_args()
 w = bench.WORKLOADS["cfg5"]
 n, k, d = w["n"], w["k"], w["d"]
 q1, q2 = G.sbm_probabilities(n, k, w["deg"], w["ratio"])
-codes = G.planted_partition_codes(n, k, q1, q2, w["seed"])
-labels = np.repeat(np.arange(k), G.block_sizes(n, k))
-g = G.graph_from_codes(n, codes)
-deltas, cur = [], codes
+g, labels = G.planted_partition_device(n, k, w["deg"], w["ratio"], seed=w["seed"])
+deltas, cur = [], g
 for s in range(a.steps):
-    dl, il = G.edge_churn(cur, n, labels, q1, q2, a.churn, seed=50 + s)
-    deltas.append((dl, il))
-    cur = np.union1d(np.setdiff1d(cur, dl, assume_unique=True), il)
+    dl, il = G.edge_churn_device(cur, labels, q1, q2, a.churn, seed=50 + s)
+    cur = cur.apply_delta(dl, il)
+    deltas.append((dl.cpu().numpy(), il.cpu().numpy()))
 cfg = P.DynamicConfig(k=k, d=d, p=a.p, filter=P.FilterConfig(order=w["order"]))
 torch.cuda.synchronize()
 t0 = time.perf_counter()
