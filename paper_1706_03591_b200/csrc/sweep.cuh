@@ -363,12 +363,15 @@ __device__ __forceinline__ void segment_body(const SweepArgs &A, int64_t first_w
 // all 4 x VPL gathers of a batch before their FMAs; left to its own register
 // heuristic it chose 58 registers and interleaved loads with FMAs (cfg3 fp64
 // 4.60 vs 5.96 ms per order, B200 A/B of the same source).
+#ifndef SWEEP_NARROW_MIN
+#define SWEEP_NARROW_MIN 4
+#endif
 #ifndef SWEEP_WIDE_MIN
 #define SWEEP_WIDE_MIN 3
 #endif
 template <int G, int VPL>
 struct SweepMinBlocks {
-  static constexpr int value = (G < 32 && VPL <= 2) ? 4 : (VPL <= 2 ? SWEEP_WIDE_MIN : 0);
+  static constexpr int value = (G < 32 && VPL <= 2) ? SWEEP_NARROW_MIN : (VPL <= 2 ? SWEEP_WIDE_MIN : 0);
 };
 
 template <typename T, int G, int VPL, int MODE, bool PERM>

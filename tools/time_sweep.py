@@ -32,12 +32,7 @@ if a.workload in ("cfg3", "cfg5"):
     g = G.graph_from_codes(n, G.planted_partition_codes(n, k, q1, q2, 3))
 else:
     n = 4_000_000
-    cache = "/tmp/csc_cfg4_codes.npy"  # tool-side cache only (tests/bench never read it)
-    if os.path.exists(cache):
-        g = G.graph_from_codes(n, np.load(cache))
-    else:
-        g, _ = G.chung_lu_sbm(n, 50, 16.0, 2.3, 20000.0, 0.05, seed=4)
-        np.save(cache, g.edge_i * n + g.edge_j)
+    g, _ = G.chung_lu_sbm_device(n, 50, 16.0, 2.3, 20000.0, 0.05, seed=4)
 lap = P.laplacian(g)
 dt = torch.float64 if a.precision == "fp64" else torch.float32
 ld = row_stride(a.d, dt)
