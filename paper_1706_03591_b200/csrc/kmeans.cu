@@ -729,7 +729,7 @@ int g_assign_ver = 3;
 // incremental centroid sums (update_sorted_kernel): tuning key "update_incremental"
 int g_update_incremental = 1;
 // exact fixed-point centroid sums updated by the changed rows only
-// (fx_delta_kernel) where the accumulators fit shared memory: tuning key
+// (fx_changes / fx_scatter / fx_sum kernels) when d <= 128: tuning key
 // "update_exact" (read at plan creation)
 int g_update_exact = 1;
 // assignment screen of the Lloyd plans: 2 = tensor cores (tcgen05 kind::tf32,
@@ -1710,6 +1710,7 @@ __global__ void update_sorted_kernel(const double *__restrict__ f,
 struct FxScale {
   double s1, s2;    // v * s1 * s2 = v * 2^P (two factors: P may exceed a double's range)
   double r1, r2;    // 2^-P as two factors
+  int P;
 };
 
 __device__ __forceinline__ FxScale fx_scale(double bound) {
@@ -1719,6 +1720,7 @@ __device__ __forceinline__ FxScale fx_scale(double bound) {
   const int P = bound > 0.0 ? 125 - e : 0;
   const int p1 = P / 2, p2 = P - p1;
   FxScale f;
+  f.P = P;
   f.s1 = ldexp(1.0, p1);
   f.s2 = ldexp(1.0, p2);
   f.r1 = ldexp(1.0, -p1);
@@ -1783,123 +1785,233 @@ __global__ void fx_maxnorm_kernel(const double *__restrict__ fnorm, int64_t n,
   if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(m));
 }
 
-// Delta update of the fixed-point sums: rows whose label differs from
-// prev[r] move from cluster prev[r] (if >= 0) to labels[r]. Block b owns a
-// contiguous row range; its changes are first added into shared-memory
-// accumulators (lo / hi words in separate arrays: conflict-free 64-bit lanes),
-// then every touched cluster is flushed to the global sums with one 128-bit
-// atomic add per column. gS_lo / gS_hi: [k][d]; gQ: [k][2]; gcnt: [k].
-constexpr int kFxThreads = 256;
-constexpr int kFxBatch = 4;  // changed rows whose values are loaded before their atomics
+// Delta update of the fixed-point sums: a row whose label differs from
+// prev[r] leaves cluster prev[r] (if >= 0) and joins labels[r]. Because the
+// sums are integers, the order the changes are added in does not matter, so
+// the changes are bucketed by cluster without sorting:
+//  1. fx_changes_kernel: one entry (row | sign << 31) per (row, cluster) it
+//     leaves or joins, appended with one atomic per warp; per-cluster entry
+//     counts and net membership changes through per-block shared histograms;
+//  2. fx_offsets_kernel (one block): cluster offsets (exclusive scan) and the
+//     chunk size for step 4 from the entry total;
+//  3. fx_scatter_kernel: entries into their cluster's bucket (atomic cursor;
+//     the order inside a bucket is immaterial);
+//  4. fx_sum_kernel: persistent blocks take chunks of the bucketed list; a
+//     thread per column sums its chunk's rows in a 128-bit register pair
+//     (add with carry), reading only changed rows of F, and adds the total
+//     into the cluster's global sum with one 128-bit atomic per (chunk,
+//     cluster, column) — no per-element atomics.
+// Buffers (plan): entries [2n], bucketed [2n], cnt/off/cursor [k], scalars.
+constexpr int kFxThreads = 256;   // changes / scatter kernels
+constexpr int kFxSumThreads = 128;  // sum kernel: one thread per column (d <= 128)
+
+struct FxWork {
+  int32_t *entries;    // [2n] row | (leave << 31), cluster in ecl
+  int32_t *ecl;        // [2n] cluster of the entry
+  int32_t *bucketed;   // [2n] rows | sign, grouped by cluster
+  int32_t *ccount;     // [k] entries per cluster
+  int32_t *coff;       // [k + 1] bucket offsets
+  int32_t *cursor;     // [k] scatter cursors
+  int32_t *scal;       // [0] entry total, [1] chunk size
+};
 
 __global__ void __launch_bounds__(kFxThreads)
-    fx_delta_kernel(const double *__restrict__ f, int64_t ld, const double *__restrict__ fnorm,
-                    const int32_t *__restrict__ labels, int32_t *__restrict__ prev, int64_t n,
-                    int d, int k, const unsigned long long *__restrict__ maxbits,
-                    unsigned long long *__restrict__ gS_lo, unsigned long long *__restrict__ gS_hi,
-                    unsigned long long *__restrict__ gQ, int32_t *__restrict__ gcnt) {
-  extern __shared__ unsigned long long fxs[];
-  unsigned long long *aLo = fxs;                      // [k][d]
-  unsigned long long *aHi = aLo + (size_t)k * d;      // [k][d]
-  unsigned long long *aQ = aHi + (size_t)k * d;       // [k][2]
-  int32_t *aC = reinterpret_cast<int32_t *>(aQ + 2 * (size_t)k);  // [k] count deltas
-  int32_t *dirty = aC + k;                                        // [k]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t rbeg = (int64_t)blockIdx.x * chunk, rend = min(n, rbeg + chunk);
-  if (rbeg >= rend) return;
-  const double mf = __longlong_as_double((long long)*maxbits);
-  const FxScale fs = fx_scale(sqrt(mf) * (1.0 + 1e-12) * (double)n);
-  const FxScale fq = fx_scale(mf * (double)n);
-  for (int64_t i = tid; i < 2 * (int64_t)k * d; i += kFxThreads) aLo[i] = 0ull;
-  for (int i = tid; i < 2 * k; i += kFxThreads) aQ[i] = 0ull;
-  for (int i = tid; i < k; i += kFxThreads) {
-    aC[i] = 0;
-    dirty[i] = 0;
-  }
+    fx_changes_kernel(const int32_t *__restrict__ labels, int32_t *__restrict__ prev, int64_t n, int k,
+                      FxWork w, int32_t *__restrict__ gcnt) {
+  extern __shared__ int32_t fsh[];
+  int32_t *hc = fsh;       // [k] entries per cluster
+  int32_t *hn = fsh + k;   // [k] net membership change
+  for (int i = threadIdx.x; i < 2 * k; i += kFxThreads) fsh[i] = 0;
   __syncthreads();
+  const int lane = threadIdx.x & 31;
   bool any = false;
-  for (int64_t base = rbeg + warp * 32; base < rend; base += (kFxThreads / 32) * 32) {
+  for (int64_t base = (blockIdx.x * (int64_t)kFxThreads + threadIdx.x) & ~(int64_t)31; base < n;
+       base += (int64_t)gridDim.x * kFxThreads) {
     const int64_t r = base + lane;
     int nl = -1, ol = -1;
-    if (r < rend) {
+    if (r < n) {
       nl = labels[r];
       ol = prev[r];
     }
-    const bool ch = r < rend && nl != ol;
+    const bool ch = r < n && nl != ol;
     if (ch) prev[r] = nl;
-    unsigned m = __ballot_sync(0xffffffffu, ch);
-    any |= m != 0u;
-    while (m) {
-      int src[kFxBatch];
-      int cnt = 0;
+    const int ne = ch ? (ol >= 0 ? 2 : 1) : 0;
+    // warp-aggregated append of this warp's entries
+    int incl = ne;
 #pragma unroll
-      for (int b = 0; b < kFxBatch; ++b) {
-        src[b] = m ? __ffs(m) - 1 : -1;
-        if (m) {
-          m &= m - 1;
-          ++cnt;
-        }
-      }
-      double v[kFxBatch][4];  // d <= 128: up to 4 columns per lane
-      int jn[kFxBatch], jo[kFxBatch];
-#pragma unroll
-      for (int b = 0; b < kFxBatch; ++b) {
-        const int sl = src[b] < 0 ? 0 : src[b];
-        jn[b] = __shfl_sync(0xffffffffu, nl, sl);
-        jo[b] = __shfl_sync(0xffffffffu, ol, sl);
-        const double *fr = f + (base + sl) * ld;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int c = lane + 32 * t;
-          v[b][t] = (src[b] >= 0 && c < d) ? __ldg(fr + c) : 0.0;
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < kFxBatch; ++b) {
-        if (b >= cnt) break;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int c = lane + 32 * t;
-          if (c >= d) break;
-          uint64_t lo, hi;
-          fx_split(v[b][t], fs, lo, hi);
-          const size_t e = (size_t)jn[b] * d + c;
-          fx_atomic_add(aLo + e, aHi + e, lo, hi);
-          if (jo[b] >= 0) {
-            fx_neg(lo, hi);
-            const size_t eo = (size_t)jo[b] * d + c;
-            fx_atomic_add(aLo + eo, aHi + eo, lo, hi);
-          }
-        }
-        if (lane == 0) {
-          uint64_t lo, hi;
-          fx_split(fnorm[base + src[b]], fq, lo, hi);
-          fx_atomic_add(aQ + 2 * jn[b], aQ + 2 * jn[b] + 1, lo, hi);
-          atomicAdd(aC + jn[b], 1);
-          dirty[jn[b]] = 1;
-          if (jo[b] >= 0) {
-            fx_neg(lo, hi);
-            fx_atomic_add(aQ + 2 * jo[b], aQ + 2 * jo[b] + 1, lo, hi);
-            atomicSub(aC + jo[b], 1);
-            dirty[jo[b]] = 1;
-          }
-        }
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (tot == 0) continue;
+    any = true;
+    int b0 = 0;
+    if (lane == 31) b0 = atomicAdd(w.scal, tot);
+    b0 = __shfl_sync(0xffffffffu, b0, 31);
+    int pos = b0 + incl - ne;
+    if (ch) {
+      w.entries[pos] = (int32_t)r;
+      w.ecl[pos] = nl;
+      atomicAdd(hc + nl, 1);
+      atomicAdd(hn + nl, 1);
+      if (ol >= 0) {
+        w.entries[pos + 1] = (int32_t)r | (int32_t)0x80000000;
+        w.ecl[pos + 1] = ol;
+        atomicAdd(hc + ol, 1);
+        atomicSub(hn + ol, 1);
       }
     }
   }
   if (!__syncthreads_or(any)) return;
-  for (int64_t e = tid; e < (int64_t)k * d; e += kFxThreads) {
-    const int64_t j = e / d;
-    if (!dirty[j]) continue;
-    const uint64_t lo = aLo[e], hi = aHi[e];
-    if (lo | hi) fx_atomic_add(gS_lo + e, gS_hi + e, lo, hi);
+  for (int j = threadIdx.x; j < k; j += kFxThreads) {
+    if (hc[j]) atomicAdd(w.ccount + j, hc[j]);
+    if (hn[j]) atomicAdd(gcnt + j, hn[j]);
   }
-  for (int j = tid; j < k; j += kFxThreads) {
-    if (!dirty[j]) continue;
-    const uint64_t lo = aQ[2 * j], hi = aQ[2 * j + 1];
-    if (lo | hi) fx_atomic_add(gQ + 2 * j, gQ + 2 * j + 1, lo, hi);
-    if (aC[j]) atomicAdd(gcnt + j, aC[j]);
+}
+
+// one warp: exclusive scan of the k (<= 32 * 8) bucket counts
+__global__ void fx_offsets_kernel(int k, FxWork w, int target_chunks) {
+  const int lane = threadIdx.x & 31;
+  constexpr int PER = 8;
+  int32_t v[PER], s = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int j = lane * PER + i;
+    v[i] = j < k ? w.ccount[j] : 0;
+    s += v[i];
+  }
+  int incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  int32_t acc = incl - s;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int j = lane * PER + i;
+    if (j < k) {
+      w.coff[j] = acc;
+      w.cursor[j] = 0;
+      w.ccount[j] = 0;  // ready for the next update
+    }
+    acc += v[i];
+  }
+  const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (lane == 0) {
+    w.coff[k] = total;
+    // chunk size: enough chunks to fill the GPU, at least 32 rows each
+    const int32_t c = (total + target_chunks - 1) / target_chunks;
+    w.scal[1] = c < 32 ? 32 : c;
+  }
+}
+
+// per block: a shared histogram of its entries' clusters, one global cursor
+// atomic per (block, cluster) reserves the block's ranges, then shared
+// cursors place the entries (one contiguous slice of the list per block)
+__global__ void __launch_bounds__(kFxThreads) fx_scatter_kernel(FxWork w, int k) {
+  extern __shared__ int32_t ssh[];
+  int32_t *hist = ssh, *basep = ssh + k;
+  const int32_t total = w.scal[0];
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min((int64_t)total, e0 + per);
+  if (e0 >= e1) return;
+  for (int j = threadIdx.x; j < k; j += kFxThreads) hist[j] = 0;
+  __syncthreads();
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kFxThreads) atomicAdd(hist + w.ecl[e], 1);
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += kFxThreads) {
+    basep[j] = hist[j] ? w.coff[j] + atomicAdd(w.cursor + j, hist[j]) : 0;
+    hist[j] = 0;
+  }
+  __syncthreads();
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kFxThreads) {
+    const int32_t c = w.ecl[e];
+    w.bucketed[basep[c] + atomicAdd(hist + c, 1)] = w.entries[e];
+  }
+}
+
+__device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t xlo, uint64_t xhi) {
+  lo += xlo;
+  hi += xhi + (lo < xlo ? 1ull : 0ull);
+}
+
+constexpr int kFxRowGroups = 4;  // row groups of a sum block (each a full set of column threads)
+
+__global__ void __launch_bounds__(kFxSumThreads * kFxRowGroups)
+    fx_sum_kernel(const double *__restrict__ f, int64_t ld, const double *__restrict__ fnorm, int64_t n,
+                  int d, int k, const unsigned long long *__restrict__ maxbits, FxWork w,
+                  unsigned long long *__restrict__ gS_lo, unsigned long long *__restrict__ gS_hi,
+                  unsigned long long *__restrict__ gQ) {
+  __shared__ uint64_t red[kFxRowGroups][kFxSumThreads + 1][2];
+  const int32_t total = w.scal[0], chunk = w.scal[1];
+  if (total == 0) return;
+  const double mf = __longlong_as_double((long long)*maxbits);
+  const FxScale fs = fx_scale(sqrt(mf) * (1.0 + 1e-12) * (double)n);
+  const FxScale fq = fx_scale(mf * (double)n);
+  const int c = threadIdx.x % kFxSumThreads, rg = threadIdx.x / kFxSumThreads;
+  const int32_t nchunks = (total + chunk - 1) / chunk;
+  for (int32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int32_t e0 = ch * chunk, e1 = min(total, e0 + chunk);
+    // cluster of e0: last j with coff[j] <= e0 (then coff[j + 1] > e0)
+    int lo = 0, hi = k - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (w.coff[mid] <= e0) lo = mid;
+      else hi = mid - 1;
+    }
+    // the chunk's clusters are handled one segment at a time by all row groups
+    for (int cl = lo; cl < k && w.coff[cl] < e1; ++cl) {
+      const int32_t s0 = max(e0, w.coff[cl]), s1 = min(e1, w.coff[cl + 1]);
+      uint64_t slo = 0, shi = 0, qlo = 0, qhi = 0;
+      constexpr int U = 4;  // rows per group whose values are loaded before they are added
+      for (int32_t e = s0 + rg * U; e < s1; e += kFxRowGroups * U) {
+        int32_t ent[U];
+        double v[U], q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ent[u] = e + u < s1 ? __ldg(w.bucketed + e + u) : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t row = (int64_t)(ent[u] & 0x7fffffff);
+          v[u] = (e + u < s1 && c < d) ? __ldg(f + row * ld + c) : 0.0;
+          q[u] = (e + u < s1 && c == 0) ? __ldg(fnorm + row) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (e + u >= s1) break;
+          uint64_t xl, xh;
+          fx_split(v[u], fs, xl, xh);
+          if (ent[u] < 0) fx_neg(xl, xh);
+          add128(slo, shi, xl, xh);
+          if (c == 0) {
+            fx_split(q[u], fq, xl, xh);
+            if (ent[u] < 0) fx_neg(xl, xh);
+            add128(qlo, qhi, xl, xh);
+          }
+        }
+      }
+      // combine the row groups (integer adds: any order), one 128-bit atomic per column
+      red[rg][c][0] = slo;
+      red[rg][c][1] = shi;
+      if (c == 0) {
+        red[rg][kFxSumThreads][0] = qlo;
+        red[rg][kFxSumThreads][1] = qhi;
+      }
+      __syncthreads();
+      if (rg == 0) {
+#pragma unroll
+        for (int g = 1; g < kFxRowGroups; ++g) add128(slo, shi, red[g][c][0], red[g][c][1]);
+        if (c < d && (slo | shi)) fx_atomic_add(gS_lo + (size_t)cl * d + c, gS_hi + (size_t)cl * d + c, slo, shi);
+        if (c == 0) {
+#pragma unroll
+          for (int g = 1; g < kFxRowGroups; ++g)
+            add128(qlo, qhi, red[g][kFxSumThreads][0], red[g][kFxSumThreads][1]);
+          if (qlo | qhi) fx_atomic_add(gQ + 2 * cl, gQ + 2 * cl + 1, qlo, qhi);
+        }
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -1922,9 +2034,7 @@ __global__ void fx_finish_kernel(const unsigned long long *__restrict__ gS_lo,
   }
 }
 
-size_t fx_smem(int64_t d, int64_t k) {
-  return sizeof(unsigned long long) * (2 * (size_t)k * d + 2 * (size_t)k) + sizeof(int32_t) * 2 * (size_t)k;
-}
+size_t fx_smem(int64_t, int64_t k) { return sizeof(int32_t) * 2 * (size_t)k; }
 
 __global__ void sums_finish_kernel(const double *__restrict__ psum,
                                    const int32_t *__restrict__ pcnt,
@@ -2228,9 +2338,11 @@ struct csc_kmeans_plan {
   // tensor-core screen (kmeans_screen_tc.cu): hi / lo centroid tiles
   bool tc = false;
   float *chi = nullptr, *clo = nullptr;
-  // exact fixed-point sums (fx_delta_kernel): [k][d] lo / hi words, Q [k][2],
-  // counts [k], max |f|^2 bits
+  // exact fixed-point sums (fx_* kernels): [k][d] lo / hi words, Q [k][2],
+  // counts [k], max |f|^2 bits; the change lists and buckets in fxw
   bool fx = false;
+  FxWork fxw{};
+  void *fxw_base = nullptr;
   bool finish_small = false;  // one single-block node finishes an iteration
   int fx_grid = 0;
   void *fx_base = nullptr;
@@ -2397,8 +2509,7 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   p->smem = sizeof(double) * k * (p->cw + kSqLanes) + sizeof(int32_t) * k;
   const size_t nd = (size_t)n, kk = (size_t)k;
   // exact fixed-point sums need no per-chunk partials
-  const bool want_fx = g_update_exact && d <= 128 &&
-                       (int64_t)fx_smem(d, k) <= (int64_t)info.max_smem_optin;
+  const bool want_fx = g_update_exact && d <= kFxSumThreads && k <= 256;
   const size_t parts = want_fx ? 0 : (size_t)p->nb * kk;
   const size_t doubles = 3 * nd + parts * d + parts + kk * d + 4 * kk + 8;
   const size_t ints = 2 * nd + 4 + parts;
@@ -2442,7 +2553,10 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
   if (want_fx) {
     const size_t kd = kk * (size_t)d;
     const size_t words = 2 * kd + 2 * kk + 1;
-    if (cudaMallocAsync(&p->fx_base, words * 8 + kk * 4 + 64, st) != cudaSuccess) {
+    const size_t ents = 2 * nd;
+    if (cudaMallocAsync(&p->fx_base, words * 8 + kk * 4 + 64, st) != cudaSuccess ||
+        cudaMallocAsync(&p->fxw_base, sizeof(int32_t) * (3 * ents + 3 * kk + 1 + 2), st) != cudaSuccess) {
+      if (p->fx_base) cudaFreeAsync(p->fx_base, st);
       cudaFreeAsync(p->base, st);
       delete p;
       csc::set_error("csc_kmeans_plan_create: allocation failed");
@@ -2455,11 +2569,16 @@ int csc_kmeans_plan_create(int64_t n, int64_t d, int64_t ld, int64_t k, void *st
       p->fx_q = p->fx_hi + kd;
       p->fx_max = p->fx_q + 2 * kk;
       p->fx_cnt = reinterpret_cast<int32_t *>(p->fx_max + 1);
-      CSC_TRY_CUDA(cudaFuncSetAttribute(fx_delta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)fxs));
-      const int per_sm = std::max<int>(1, std::min<int>(2, (int)(228 * 1024 / (fxs + 1024))));
-      p->fx_grid = (int)std::max<int64_t>(
-          1, std::min<int64_t>((int64_t)info.sm_count * per_sm, csc::ceil_div(n, 1024)));
+      int32_t *wp = static_cast<int32_t *>(p->fxw_base);
+      p->fxw.entries = wp; wp += ents;
+      p->fxw.ecl = wp; wp += ents;
+      p->fxw.bucketed = wp; wp += ents;
+      p->fxw.ccount = wp; wp += kk;
+      p->fxw.cursor = wp; wp += kk;
+      p->fxw.coff = wp; wp += kk + 1;
+      p->fxw.scal = wp;
+      CSC_TRY_CUDA(cudaMemsetAsync(p->fxw.ccount, 0, sizeof(int32_t) * kk, st));
+      p->fx_grid = grid_cap(csc::ceil_div(n, kFxThreads));
     }
   }
   *out = p;
@@ -2552,6 +2671,7 @@ int csc_kmeans_plan_destroy(csc_kmeans_plan *p) {
   if (p->base) cudaFreeAsync(p->base, p->stream);
   if (p->screen_base) cudaFreeAsync(p->screen_base, p->stream);
   if (p->fx_base) cudaFreeAsync(p->fx_base, p->stream);
+  if (p->fxw_base) cudaFreeAsync(p->fxw_base, p->stream);
   delete p;
   return CSC_OK;
 }
@@ -2646,9 +2766,18 @@ int csc_kmeans_iterate(csc_kmeans_plan *p, const double *f, const double *fnorm,
       fx_maxnorm_kernel<<<grid_cap(csc::ceil_div(n, 256), 2), 256, 0, st>>>(fnorm, n, p->fx_max);
       CSC_CHECK_LAUNCH();
     }
-    fx_delta_kernel<<<(unsigned)p->fx_grid, kFxThreads, fx_smem(d, k), st>>>(
-        f, ld, fnorm, labels, p->prev, n, (int)d, (int)k, p->fx_max, p->fx_lo, p->fx_hi, p->fx_q,
-        p->fx_cnt);
+    CSC_TRY_CUDA(cudaMemsetAsync(p->fxw.scal, 0, sizeof(int32_t), st));
+    fx_changes_kernel<<<(unsigned)p->fx_grid, kFxThreads, fx_smem(d, k), st>>>(labels, p->prev, n, (int)k,
+                                                                             p->fxw, p->fx_cnt);
+    CSC_CHECK_LAUNCH();
+    const int sum_grid = csc::device_info().sm_count * 2;
+    fx_offsets_kernel<<<1, 32, 0, st>>>((int)k, p->fxw, 2 * sum_grid);  // k <= 256
+    CSC_CHECK_LAUNCH();
+    fx_scatter_kernel<<<(unsigned)(csc::device_info().sm_count * 4), kFxThreads, sizeof(int32_t) * 2 * k, st>>>(
+        p->fxw, (int)k);
+    CSC_CHECK_LAUNCH();
+    fx_sum_kernel<<<(unsigned)sum_grid, kFxSumThreads * kFxRowGroups, 0, st>>>(
+        f, ld, fnorm, n, (int)d, (int)k, p->fx_max, p->fxw, p->fx_lo, p->fx_hi, p->fx_q);
     CSC_CHECK_LAUNCH();
     fx_finish_kernel<<<(unsigned)csc::ceil_div(k * d, 256), 256, 0, st>>>(
         p->fx_lo, p->fx_hi, p->fx_q, p->fx_cnt, n, (int)d, (int)k, p->fx_max, p->S, p->Q, counts);

@@ -60,7 +60,8 @@ for mode in MODES:
     seq = collections.defaultdict(list)
     for e in sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
                     key=lambda e: e.time_range.start):
-        for key in ("update_sorted", "fx_delta", "screen_kernel", "assign3"):
+        for key in ("update_sorted", "fx_delta", "fx_sum", "fx_scatter", "fx_changes", "screen_kernel",
+                    "assign3", "assign_small", "finish_small"):
             if key in e.name:
                 seq[key].append(round(e.time_range.elapsed_us()))
                 break
