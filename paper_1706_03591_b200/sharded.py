@@ -8,7 +8,10 @@ the global moments, every rank then runs the same host bisection and reaches
 the same decisions, and each filters its own columns at the accepted cutoff.
 
 The compute is injected (defaults: the GPU moment sweep and fused filter),
-so the host protocol is tested on CPU with world_size 2 over gloo.
+so the host protocol is tested on CPU with world_size 2 over gloo; the public
+entry sharded_csc_features (csc_features, csc.py:72-84, over column shards)
+runs it with the product compute (tests/test_gpu_sharded.py: two gloo ranks
+on one GPU reach the single-process cutoff, iterations and features).
 """
 from __future__ import annotations
 
@@ -16,6 +19,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _native
+from ._device import ptr, require_cuda, row_stride, stream
 from .filters import (EigencountSearchError, FilterConfig, MOMENT_GUARD, cheb_coeffs,
                       moment_energy)
 
@@ -93,3 +98,47 @@ def gpu_shard_fns(L, blk, d: int, lambda_max: float):
         return out, float(s.item())
 
     return moments_fn, filter_fn
+
+
+def shard_signals(n: int, d: int, c0: int, c1: int, seed=0) -> torch.Tensor:
+    """Columns [c0, c1) of random_signals(n, d, seed) (signals.py:16-37) as a
+    padded (n, ld) float64 device block: the same per-column PCG64 streams the
+    single-process draw uses (numpy's SeedSequence children c0..c1-1), drawn
+    on the GPU; flagged columns are redrawn with the exact host generator."""
+    from .signals import as_seed_sequence, child_states
+    if not 0 <= c0 < c1 <= d:
+        raise ValueError("need 0 <= c0 < c1 <= d")
+    ss = as_seed_sequence(seed)
+    base = int(ss.n_children_spawned)
+    states = np.ascontiguousarray(child_states(ss, d)[c0:c1])
+    nc = c1 - c0
+    blk = torch.zeros((n, row_stride(nc)), dtype=torch.float64, device=require_cuda())
+    bad = np.zeros(nc, dtype=np.int32)
+    sigma = 1.0 / np.sqrt(d)
+    _native.call("csc_normal_columns", states.ctypes.data, nc, n, sigma, ptr(blk), blk.shape[1], 0,
+                 bad.ctypes.data, stream())
+    for c in np.flatnonzero(bad):
+        child = np.random.SeedSequence(ss.entropy, spawn_key=tuple(ss.spawn_key) + (base + c0 + int(c),),
+                                       pool_size=ss.pool_size)
+        blk[:, c].copy_(torch.from_numpy(np.random.default_rng(child).standard_normal(n) * sigma + 0.0))
+    return blk
+
+
+def sharded_csc_features(L, k: int, d: int, filter_cfg: FilterConfig | None = None, seed=0, group=None):
+    """csc_features (csc.py:72-84) over column shards: this rank draws and
+    filters columns shard_columns(d, world, rank) of the same signal block,
+    the ranks agree on the cutoff through one all-reduce of the 2m+1 moments
+    (and of the energy at guard-band probes), and each returns its slice of
+    the features. Returns (local features (n, ld) device block, (c0, c1),
+    cutoff, iterations, global estimate)."""
+    cfg = filter_cfg or FilterConfig()
+    if not 1 <= k < L.n:
+        raise ValueError(f"need 1 <= k < n, got k={k}, n={L.n}")
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    c0, c1 = shard_columns(d, world, rank)
+    blk = shard_signals(L.n, d, c0, c1, seed)
+    moments_fn, filter_fn = gpu_shard_fns(L, blk, c1 - c0, L.lambda_max_bound)
+    cutoff, out, _, iters, est = sharded_search_cutoff(k, (0.0, L.lambda_max_bound), L.lambda_max_bound, cfg,
+                                                       moments_fn, filter_fn, 1.0, group)
+    return out, (c0, c1), cutoff, iters, est
