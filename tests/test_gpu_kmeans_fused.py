@@ -359,3 +359,42 @@ def test_exact_sums_match_row_order_sums(P, n, d, k):
     ref_labels, _, ref_cost = O.kmeans(f, k, restarts=2, max_iters=30, tol=1e-6, seed=d + k)
     assert O.adjusted_rand(out[1][0], ref_labels) >= 0.999
     assert abs(np.sqrt(out[1][1]) - ref_cost) <= COST_TOL * ref_cost
+
+
+@pytest.mark.parametrize("screen", ["tc", "fp64"])
+def test_plan_empty_cluster_repair_exact_sums(P, screen):
+    """The Lloyd plan (csc_kmeans_iterate: screened assignment, exact
+    fixed-point sums updated from the changed rows) through the empty-cluster
+    repair (kmeans.py:99-108): seeds far from every row leave clusters empty
+    on the first assignment and the reseeded rows move between clusters;
+    labels equal the oracle's Lloyd from the same seeds exactly, iterations
+    and cost agree."""
+    import importlib
+    import torch
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import ptr, upload_block
+    KM = importlib.import_module("paper_1706_03591_b200.kmeans")
+    rng = np.random.default_rng(11)
+    n, d, k = 6000, 64, 16  # inside the tensor-core screen's shapes
+    f = rng.normal(size=(n, d)) + 4.0 * rng.integers(0, 4, size=(n, 1))
+    c0 = f[rng.choice(n, k, replace=False)].copy()
+    for j in (2, 9, 13):
+        c0[j] = 1e3 + 10.0 * j
+    blk = upload_block(f)
+    ws = KM._Workspace(blk, d, k)
+    plan = ws._plan()
+    if screen == "tc":
+        ld32 = (d + 3) // 4 * 4
+        f32 = torch.zeros((n, ld32), dtype=torch.float32, device=blk.device)
+        fn32 = torch.empty(n, dtype=torch.float32, device=blk.device)
+        _native.call("csc_kmeans_screen_prepare", ptr(blk), n, d, blk.shape[1], ptr(f32), ld32, ptr(fn32),
+                     KM.stream())
+        _native.call("csc_kmeans_plan_set_screen", plan, ptr(f32), ld32, ptr(fn32))
+    ws.cent[:, :d].copy_(torch.from_numpy(c0))
+    hist = []
+    cost2 = ws.lloyd(100, 1e-6, history=hist)
+    labels = ws.labels.cpu().numpy().astype(np.int64)
+    ref_labels, ref_cost2, _, ref_it = O.lloyd(f, k, c0, 100, 1e-6)
+    assert len(hist) == ref_it
+    assert np.array_equal(labels, ref_labels)
+    assert abs(cost2 - ref_cost2) <= COST_TOL * ref_cost2
