@@ -279,6 +279,16 @@ __device__ __forceinline__ void epilogue(float4 acc, const float4 *prev, const f
 }
 
 
+// Entries per gather batch: narrow groups (G < 32) take SWEEP_NARROW_BATCH
+// (A/B knob), full-warp groups 4.
+#ifndef SWEEP_NARROW_BATCH
+#define SWEEP_NARROW_BATCH 4
+#endif
+template <int G>
+struct SweepBatch {
+  static constexpr int value = G < 32 ? SWEEP_NARROW_BATCH : 4;
+};
+
 // Gather-accumulate of entries [beg, end) of one row into acc[VPL] by a group
 // of G lanes (glane = lane within group, gmask = the group's lanes).
 template <typename T, int G, int VPL>
@@ -298,18 +308,19 @@ __device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
       my_val = ld_s(vals + nz, pol);
     }
     const int cnt = min(G, end - base);
+    constexpr int B = SweepBatch<G>::value;  // entries whose gathers are issued together
     int u = 0;
-    for (; u + 4 <= cnt; u += 4) {
-      int c[4];
-      T a[4];
+    for (; u + B <= cnt; u += B) {
+      int c[B];
+      T a[B];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < B; ++t) {
         c[t] = __shfl_sync(gmask, my_col, u + t, G);
         a[t] = __shfl_sync(gmask, my_val, u + t, G);
       }
-      VT x[4][VPL];
+      VT x[B][VPL];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < B; ++t) {
         const VT *src = gat + (int64_t)c[t] * ldv;
 #pragma unroll
         for (int q = 0; q < VPL; ++q) {
@@ -318,23 +329,23 @@ __device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
         }
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < B; ++t)
 #pragma unroll
         for (int q = 0; q < VPL; ++q) vfma(acc[q], a[t], x[t][q]);
     }
-    if (u < cnt) {  // 1..3 remaining entries: their gathers issued together
+    if (u < cnt) {  // 1..B-1 remaining entries: their gathers issued together
       const int rem = cnt - u;
-      int c[3];
-      T a[3];
+      int c[B - 1];
+      T a[B - 1];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
+      for (int t = 0; t < B - 1; ++t) {
         const int src_lane = min(u + t, cnt - 1);
         c[t] = __shfl_sync(gmask, my_col, src_lane, G);
         a[t] = __shfl_sync(gmask, my_val, src_lane, G);
       }
-      VT x[3][VPL];
+      VT x[B - 1][VPL];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
+      for (int t = 0; t < B - 1; ++t) {
         const VT *src = gat + (int64_t)c[t] * ldv;
 #pragma unroll
         for (int q = 0; q < VPL; ++q) {
@@ -343,7 +354,7 @@ __device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
         }
       }
 #pragma unroll
-      for (int t = 0; t < 3; ++t)
+      for (int t = 0; t < B - 1; ++t)
         if (t < rem)
 #pragma unroll
           for (int q = 0; q < VPL; ++q) vfma(acc[q], a[t], x[t][q]);
