@@ -270,7 +270,10 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
                : "memory");
 }
 
-template <int NP>  // padded centroid count = UMMA N (multiple of 16, <= 128)
+// NP: padded centroid count = UMMA N (multiple of 16, <= 128); RAW: the test
+// hook (E to raw_out instead of decisions) — a separate instantiation, so the
+// production epilogue carries no per-element store code
+template <int NP, bool RAW>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_screen_kernel(TcArgs a, int stages, const __grid_constant__ CUtensorMap tile_map,
                      const __grid_constant__ CUtensorMap row_map) {
@@ -478,6 +481,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const float fni = gr >= 0 ? __ldg(a.fn32 + gr) : 0.0f;
       mbar_wait(smem_u32(tfull + slot), (uint32_t)((i / 2) & 1));
       tc_fence_after();
+      // the row's norm is common to its k distances: rank g_j = |c_j|^2 - 2 f.c_j
+      // (one fp32 rounding per entry, as many as E had) and add |f|^2 to the best two
       float bv = INFINITY, bv2 = INFINITY;
       int bi = 0x7fffffff;
       const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(slot * NP);
@@ -485,27 +490,38 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int c0 = 0; c0 < NP; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + (uint32_t)c0, v);
+        float cn[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 t4 = reinterpret_cast<const float4 *>(Cn + c0)[q];
+          cn[4 * q] = t4.x;
+          cn[4 * q + 1] = t4.y;
+          cn[4 * q + 2] = t4.z;
+          cn[4 * q + 3] = t4.w;
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int cj = c0 + j;
-          const float e = fmaf(-2.0f, v[j], fni) + Cn[cj];
-          if (a.raw_out && gr >= 0) a.raw_out[gr * NP + cj] = e;
-          if (e < bv) {
+          const float g = fmaf(-2.0f, v[j], cn[j]);
+          if (RAW) {
+            if (gr >= 0) a.raw_out[gr * NP + cj] = fni + g;
+          }
+          if (g < bv) {
             bv2 = bv;
-            bv = e;
+            bv = g;
             bi = cj;
           } else {
-            bv2 = fminf(bv2, e);
+            bv2 = fminf(bv2, g);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(tempty + slot));
-      if (gr >= 0 && !a.raw_out) {
+      if (!RAW && gr >= 0) {
         const double fr = sqrt((double)fni * (1.0 + 2e-5)) + cmax;
         const double delta = dscale * fr * fr * (1.0 + 1e-6);
-        const double e1 = (double)bv, e2 = (double)bv2;
+        const double e1 = (double)fni + (double)bv, e2 = (double)fni + (double)bv2;  // exact in double
         if (e2 - e1 > 2.0 * delta) {
           a.labels[gr] = bi;
           a.ub[gr] = sqrt(fmax(e1 + delta, 0.0));
@@ -583,8 +599,8 @@ int feature_map(CUtensorMap *m, const float *f32, int64_t n, int64_t ld32, uint3
   return CSC_OK;
 }
 
-template <int NP>
-int tc_launch(const TcArgs &a, cudaStream_t st) {
+template <int NP, bool RAW>
+int tc_launch_t(const TcArgs &a, cudaStream_t st) {
   const size_t smem = tc_smem(a.d, a.k);
   CUtensorMap tile_map, row_map;
   int rc = feature_map(&tile_map, a.f32, a.n, a.ld32, kTM);
@@ -595,16 +611,21 @@ int tc_launch(const TcArgs &a, cudaStream_t st) {
   {
     std::lock_guard<std::mutex> lock(mu);
     if (smem > configured) {
-      CSC_TRY_CUDA(cudaFuncSetAttribute(tc_screen_kernel<NP>,
+      CSC_TRY_CUDA(cudaFuncSetAttribute(tc_screen_kernel<NP, RAW>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       configured = smem;
     }
   }
   const int64_t tiles = csc::ceil_div(a.n, kTM);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(csc::device_info().sm_count, tiles));
-  tc_screen_kernel<NP><<<(unsigned)grid, kTcThreads, smem, st>>>(a, tc_stages(a.d, a.k), tile_map, row_map);
+  tc_screen_kernel<NP, RAW><<<(unsigned)grid, kTcThreads, smem, st>>>(a, tc_stages(a.d, a.k), tile_map, row_map);
   CSC_CHECK_LAUNCH();
   return CSC_OK;
+}
+
+template <int NP>
+int tc_launch(const TcArgs &a, cudaStream_t st) {
+  return a.raw_out ? tc_launch_t<NP, true>(a, st) : tc_launch_t<NP, false>(a, st);
 }
 
 int tc_dispatch(const TcArgs &a, cudaStream_t st) {
