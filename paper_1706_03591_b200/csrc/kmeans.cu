@@ -228,10 +228,10 @@ __global__ void __launch_bounds__(16 * (kAN / TN), (TN == 8 ? 2 : 2))
   };
   for (int64_t c0 = 0; c0 < k; c0 += kAN) {
     __syncthreads();  // previous tile's readers of Cs / Fs are done
-    for (int64_t e = tid; e < dpad * kAN; e += NT) {
-      const int64_t cc = e / dpad, dd = e - cc * dpad;  // coalesced along a centroid row
-      Cs[dd * kANP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
-    }
+    // warp per centroid row, lanes along it (coalesced; no per-element division)
+    for (int64_t cc = tid / 32; cc < kAN; cc += NT / 32)
+      for (int64_t dd = tid % 32; dd < dpad; dd += 32)
+        Cs[dd * kANP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
     double acc[8][TN];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -387,10 +387,9 @@ __global__ void __launch_bounds__(RT * CT, (RT * CT <= 128 ? 2 : 1))
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const int64_t total = my_tiles * nst;
   if (!SC)
-    for (int64_t e = tid; e < dpad * BN; e += NT) {
-      const int64_t cc = e / dpad, dd = e - cc * dpad;
-      Cs[dd * BNP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
-    }
+    for (int64_t cc = tid / 32; cc < BN; cc += NT / 32)  // warp per centroid row
+      for (int64_t dd = tid % 32; dd < dpad; dd += 32)
+        Cs[dd * BNP + cc] = (c0 + cc < k && dd < d) ? cent[(c0 + cc) * ldc + dd] : 0.0;
   // padding columns get |c|^2 = +inf, so their distance is +inf without a select
   for (int cc = tid; cc < BN; cc += NT) Cn[cc] = c0 + cc < k ? cnorm[c0 + cc] : INFINITY;
   if (hist)
@@ -614,10 +613,8 @@ __global__ void __launch_bounds__(256)
   const int64_t ngroups = (nr + R - 1) / R;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if ((int64_t)blockIdx.x * 8 >= ngroups) return;
-  for (int64_t e = threadIdx.x; e < 32 * KPL * d; e += blockDim.x) {
-    const int64_t j = e / d, c = e - j * d;
-    Cs[j * lds + c] = j < k ? cent[j * ldc + c] : 0.0;
-  }
+  for (int64_t j = threadIdx.x / 32; j < 32 * KPL; j += blockDim.x / 32)  // warp per centroid row
+    for (int64_t c = threadIdx.x % 32; c < d; c += 32) Cs[j * lds + c] = j < k ? cent[j * ldc + c] : 0.0;
   double cn[KPL];
 #pragma unroll
   for (int q = 0; q < KPL; ++q) cn[q] = lane + 32 * q < k ? cnorm[lane + 32 * q] : 0.0;
@@ -1261,10 +1258,8 @@ __global__ void __launch_bounds__(128)
   double *cs = sh;
   double *wsum = sh + (size_t)R * d;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int64_t e = threadIdx.x; e < (int64_t)R * d; e += blockDim.x) {
-    const int64_t r = e / d, c = e - r * d;
-    cs[e] = crows[r * crow_stride + c];
-  }
+  for (int64_t r = threadIdx.x / 32; r < R; r += blockDim.x / 32)  // warp per centroid row
+    for (int64_t c = threadIdx.x % 32; c < d; c += 32) cs[r * d + c] = crows[r * crow_stride + c];
   __syncthreads();
   const int64_t rbeg = blockIdx.x * chunk, rend = min(n, rbeg + chunk);
   double part[R];
@@ -2177,14 +2172,14 @@ __global__ void __launch_bounds__(1024)
     flags[0] = 0;
   }
   if (chi) {  // the next iteration's tensor-core screen tiles (tc_centroids_kernel's values)
-    for (int64_t e = threadIdx.x; e < (int64_t)npad * kp; e += blockDim.x) {
-      const int64_t j = e / kp, t = e - j * kp;
-      const float v = (j < k && t < d) ? (float)cs[j * lds + t] : 0.0f;
-      const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-      const int64_t off = (t / 4) * (int64_t)npad * 4 + j * 4 + (t % 4);
-      chi[off] = h;
-      clo[off] = v - h;
-    }
+    for (int64_t j = threadIdx.x / 32; j < npad; j += blockDim.x / 32)  // warp per centroid
+      for (int64_t t = threadIdx.x % 32; t < kp; t += 32) {
+        const float v = (j < k && t < d) ? (float)cs[j * lds + t] : 0.0f;
+        const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        const int64_t off = (t / 4) * (int64_t)npad * 4 + j * 4 + (t % 4);
+        chi[off] = h;
+        clo[off] = v - h;
+      }
     for (int64_t j = threadIdx.x; j < npad; j += blockDim.x) {
       float sq = INFINITY;
       if (j < k) {

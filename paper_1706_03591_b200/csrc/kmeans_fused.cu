@@ -950,9 +950,9 @@ __global__ void __launch_bounds__(kFT, 1) lloyd_fused_kernel(const FusedArgs a) 
   // the block's rows into shared memory: features, |f|^2, |f|
   auto load_rows = [&](RowMap m, int cnt) {
     __syncthreads();
-    for (int64_t e = tid; e < (int64_t)cnt * d; e += kFT) {
-      const int64_t i = e / d, t = e - i * d;
-      s.Fs[i * ldf + t] = a.F[m(i) * a.ld + t];
+    for (int64_t i = tid / 32; i < cnt; i += kFT / 32) {  // warp per row
+      const int64_t src = m(i) * a.ld;
+      for (int64_t t = tid % 32; t < d; t += 32) s.Fs[i * ldf + t] = a.F[src + t];
     }
     if (a.fnorm) {
       for (int i = tid; i < cnt; i += kFT) s.fns[i] = a.fnorm[m(i)];

@@ -55,10 +55,8 @@ __global__ void c32_convert_kernel(const double *__restrict__ c, int64_t k, int6
                                    float *__restrict__ c32t, float *__restrict__ cn32,
                                    double *__restrict__ cmax) {
   __shared__ double red[32];
-  for (int64_t e = threadIdx.x; e < d * kpad; e += blockDim.x) {
-    const int64_t t = e / kpad, j = e - t * kpad;
-    c32t[e] = j < k ? (float)c[j * ldc + t] : 0.0f;
-  }
+  for (int64_t t = threadIdx.x / 32; t < d; t += blockDim.x / 32)  // warp per column of the transposed tile
+    for (int64_t j = threadIdx.x % 32; j < kpad; j += 32) c32t[t * kpad + j] = j < k ? (float)c[j * ldc + t] : 0.0f;
   double m = 0.0;
   for (int j = threadIdx.x; j < kpad; j += blockDim.x) {
     if (j < k) {

@@ -193,14 +193,14 @@ __global__ void tc_centroids_kernel(const double *__restrict__ c, int64_t k, int
                                     int kp, float *__restrict__ chi, float *__restrict__ clo,
                                     float *__restrict__ cn32, double *__restrict__ cmax) {
   __shared__ double red[32];
-  for (int64_t e = threadIdx.x; e < (int64_t)n_pad * kp; e += blockDim.x) {
-    const int64_t j = e / kp, t = e - j * kp;
-    const float v = (j < k && t < d) ? (float)c[j * ldc + t] : 0.0f;
-    const float h = tf32_hi(v);
-    const int64_t off = (t / 4) * (int64_t)n_pad * 4 + j * 4 + (t % 4);
-    chi[off] = h;
-    clo[off] = v - h;
-  }
+  for (int64_t j = threadIdx.x / 32; j < n_pad; j += blockDim.x / 32)  // warp per centroid
+    for (int64_t t = threadIdx.x % 32; t < kp; t += 32) {
+      const float v = (j < k && t < d) ? (float)c[j * ldc + t] : 0.0f;
+      const float h = tf32_hi(v);
+      const int64_t off = (t / 4) * (int64_t)n_pad * 4 + j * 4 + (t % 4);
+      chi[off] = h;
+      clo[off] = v - h;
+    }
   double m = 0.0;
   for (int j = threadIdx.x; j < n_pad; j += blockDim.x) {
     if (j < k) {
