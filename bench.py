@@ -258,6 +258,32 @@ def timed_filter(lap, poly, blk, d, out, work, reps, lib):
     return e0.elapsed_time(e1) / reps, sweep_times(lib)
 
 
+def run_cfg3_pipeline(lap, w, calls=3):
+    """BASELINE configs[2] end to end through the public API: csc_assign
+    (csc.py:87-108) on the cfg3 Laplacian — random signals d=128, eigencount
+    bisection for lambda_100 (order 100), k-means k=100 (10 restarts) — ms per
+    call (the first call warms plans and pools; the next `calls` are timed)."""
+    import torch
+    import paper_1706_03591_b200 as P
+    k, d = w["k"], w["d"]
+    fcfg = P.FilterConfig(order=w["order"])
+    P.csc_assign(lap, k, d, fcfg, P.KmeansConfig(), seed=0)
+    torch.cuda.synchronize()
+    ms, diags = [], []
+    for c in range(calls):
+        t0 = time.perf_counter()
+        a, diag = P.csc_assign(lap, k, d, fcfg, P.KmeansConfig(), seed=1 + c)
+        torch.cuda.synchronize()
+        ms.append((time.perf_counter() - t0) * 1e3)
+        diags.append(diag)
+    return {"workload": (f"configs[2] end to end: csc_assign(L, k={k}, d={d}, FilterConfig(order={w['order']}), "
+                         f"KmeansConfig()) on the cfg3 graph (n={lap.n}): device signals, moment bisection "
+                         f"for lambda_k, k-means k={k} x 10 restarts"),
+            "ms_per_call": round(statistics.median(ms), 1), "ms_all": [round(v, 1) for v in ms],
+            "lambda_k": diags[-1].lambda_k, "search_iters": diags[-1].search_iters,
+            "matvecs_logical": diags[-1].matvecs}
+
+
 def run_cfg4(hbm, lib):
     """BASELINE configs[3]: skewed-degree Chung-Lu graph, fp32 primary with an fp64 check."""
     import torch
@@ -520,6 +546,7 @@ def main():
     ap.add_argument("--no-cfg4", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true")
     ap.add_argument("--no-cfg5-matrix", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.workload]
@@ -661,6 +688,8 @@ def main():
                           f"extrapolated per order; {dt_ref:.1f} s"}
     del blk, out, work
     torch.cuda.empty_cache()
+    if dtype == torch.float64 and not args.no_variants and not args.no_pipeline:
+        variants["cfg3_pipeline"] = run_cfg3_pipeline(lap, w)
     if dtype == torch.float64 and not args.no_variants and not args.no_cfg4:
         variants["cfg4"] = run_cfg4(hbm, lib)
 
