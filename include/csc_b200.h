@@ -267,6 +267,10 @@ int csc_kmeans_fused_trace(unsigned long long *trace_dev, int64_t iters_cap);
  * whenever f changes. set_screen(): the plan uses these buffers from now on
  * (NULL f32 disables); they must stay valid while the plan runs. */
 int csc_kmeans_screen_supported(int64_t d, int64_t k);
+/* 1 when plans screen (d, k) on the tensor cores (sm_100, k <= 128, d <= 256,
+ * the centroid tiles and two ring units within shared memory), else 0 (the
+ * FP32 SIMT screen, or FP64 only, then decides). No device work. */
+int csc_kmeans_tc_supported(int64_t d, int64_t k);
 /* Test hook of the tensor-core (tcgen05 kind::tf32, 3xTF32) screen: e_out
  * (n x roundup(k, 16) fp32, row-major) = |f32_i|^2 - 2 f_i.c_j + |c_j|^2 as
  * the screen computes it, from fp32 features (ld32 % 4 == 0, padding zero),

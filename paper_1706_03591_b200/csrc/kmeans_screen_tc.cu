@@ -696,6 +696,10 @@ int tc_screen_assign(const float *f32, int64_t ld32, const float *fn32, int64_t 
 
 }  // namespace csc
 
+extern "C" int csc_kmeans_tc_supported(int64_t d, int64_t k) {
+  return csc::tc_screen_supported(d, k) ? 1 : 0;
+}
+
 extern "C" int csc_kmeans_tc_distances(const void *f32, int64_t n, int64_t d, int64_t ld32,
                                        const float *fn32, const double *c, int64_t k, int64_t ldc,
                                        const double *cnorm, float *e_out, void *stream) {

@@ -263,7 +263,8 @@ def test_tensor_core_screen_same_labels(P, n, d, k, spread):
         assert out[mode][1] == out["fp64"][1], mode
 
 
-@pytest.mark.parametrize("n,d,k", [(600_000, 128, 100), (500_000, 96, 64), (300_000, 37, 50)])
+@pytest.mark.parametrize("n,d,k", [(600_000, 128, 100), (500_000, 96, 64), (300_000, 37, 50),
+                                   (200_000, 160, 16), (100_000, 64, 128), (50_000, 1, 7), (70_000, 200, 33)])
 def test_tensor_core_distances_many_tiles(P, n, d, k):
     """The tcgen05 screen's distances with tens of 128-row tiles per CTA (the
     shared-memory ring wraps many times; d = 128, k = 100 has an odd ring depth):
@@ -272,6 +273,8 @@ def test_tensor_core_distances_many_tiles(P, n, d, k):
     import torch
     from paper_1706_03591_b200 import _native
     from paper_1706_03591_b200._device import ptr, stream
+    if not _native.lib().csc_kmeans_tc_supported(d, k):
+        pytest.skip(f"(d={d}, k={k}) outside the tensor-core screen")
     g = torch.Generator(device="cuda").manual_seed(n + d)
     cent = torch.randn((k, d), dtype=torch.float64, device="cuda", generator=g) / np.sqrt(d)
     lab = torch.randint(0, k, (n,), device="cuda", generator=g)
