@@ -617,7 +617,14 @@ int tc_launch_t(const TcArgs &a, cudaStream_t st) {
     }
   }
   const int64_t tiles = csc::ceil_div(a.n, kTM);
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(csc::device_info().sm_count, tiles));
+  // CSC_TC_GRID (A/B knob): fewer CTAs than SMs leaves SMs to the other
+  // restarts' lanes while this screen runs
+  static const int env_grid = [] {
+    const char *e = getenv("CSC_TC_GRID");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t cap = env_grid > 0 ? env_grid : csc::device_info().sm_count;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cap, tiles));
   tc_screen_kernel<NP, RAW><<<(unsigned)grid, kTcThreads, smem, st>>>(a, tc_stages(a.d, a.k), tile_map, row_map);
   CSC_CHECK_LAUNCH();
   return CSC_OK;

@@ -393,18 +393,21 @@ def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children
     costs: dict[int, float] = {}
     held: dict[int, int] = {}  # restart -> lane whose labels are still current
 
+    serial = os.environ.get("CSC_KMEANS_SERIAL", "0") != "0"
+
     def run_wave(restarts):
         ready = torch.cuda.Event()
         ready.record(cur)
         for li, r in enumerate(restarts):
             lane = pool.lanes[li]
-            lane.stream.wait_event(ready)
-            with torch.cuda.stream(lane.stream):
+            st = pool.lanes[0].stream if serial else lane.stream  # serial: one stream, graphs back to back
+            st.wait_event(ready)
+            with torch.cuda.stream(st):
                 lane.cent.copy_(seeds[r])
                 _native.call("csc_kmeans_run", lane.plan, ptr(pool.F), ptr(ws.fnorm), ptr(lane.cent), lane.ldc,
                              ptr(lane.cnorm), ptr(lane.labels), ptr(lane.counts), int(cfg.max_iters),
-                             float(cfg.tol), ptr(lane.out), None, lane.stream.cuda_stream)
-                lane.done.record(lane.stream)
+                             float(cfg.tol), ptr(lane.out), None, st.cuda_stream)
+                lane.done.record(st)
         for li in range(len(restarts)):
             cur.wait_event(pool.lanes[li].done)
         outs = torch.stack([pool.lanes[li].out[0] for li in range(len(restarts))]).cpu().numpy()
@@ -424,6 +427,7 @@ def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children
             checked = True
             redo = bad_restarts()
             if redo:
+                KPP_REPLAYS[0] += len(redo)
                 replay(redo)  # corrected seeds for every wave
                 if any(r in wave for r in redo):
                     run_wave(wave)
@@ -438,6 +442,7 @@ def _run_restarts(blk: torch.Tensor, d: int, k: int, cfg: KmeansConfig, children
 
 
 KPP_BATCH = 16  # restarts per batched k-means++ launch series (libcscb200 limit)
+KPP_REPLAYS = [0]  # diagnostics: restarts re-seeded sequentially after a zero D^2 mass
 
 
 def kpp_group(d: int) -> int:

@@ -72,6 +72,7 @@ for dl, il in deltas:
     t2 = orig_time()
     pool = K._LLOYD_POOL
     its = [int(pool.lanes[i].out[1].item()) for i in range(cfg.kmeans.restarts)] if pool else []
+    print(f"[replays {K.KPP_REPLAYS[0]}] ", end="")
     print(f"step {(t2 - t0) * 1e3:.1f} ms: delta {(t1 - t0) * 1e3:.1f} "
           + " ".join(f"{kk} {v:.1f}" for kk, v in ph.items())
           + f" | refined {diag.refined} | kmeans iters {its}", flush=True)
