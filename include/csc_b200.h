@@ -122,6 +122,21 @@ int csc_cheb_filter(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t
                     const double *coeffs_host, int32_t ncoeffs, void *out_dev, void *work_dev,
                     double *sumsq_dev, void *stream);
 
+/* csc_cheb_filter (no fused norm) whose result is also copied to host memory:
+ * rows of d elements to host_dst, host_pitch bytes apart (pinned memory for an
+ * asynchronous copy), on copy_stream. The last order runs as nslices row-range
+ * launches on `stream` and each slice's rows are downloaded while the next one
+ * computes, so only 1/nslices of the device->host copy is exposed (index-ordered
+ * plans without long-row segments and with d within one column chunk; other
+ * plans copy once after the last order). Returns after enqueuing: the host rows
+ * are valid once copy_stream has completed. Replaces the host side of the
+ * reference's apply_filter contract (filters.py:155-187: NumPy in, a new NumPy
+ * array out), output bitwise equal to csc_cheb_filter's. */
+int csc_cheb_filter_download(const csc_chebop *op, const void *x_dev, int64_t ld, int64_t d,
+                             const double *coeffs_host, int32_t ncoeffs, void *out_dev,
+                             void *work_dev, void *host_dst, int64_t host_pitch, int32_t nslices,
+                             void *copy_stream, void *stream);
+
 /* Chebyshev moments of the block (single-pass eigencount bisection):
  * mu_dev[q] = sum over columns of <x, T_q(M) x>, q = 0 .. 2*m, from one
  * m-order sweep via <T_j,T_j> and <T_{j+1},T_j>. mu_dev: 2m+1 doubles.

@@ -38,6 +38,7 @@ SIGNATURES = {
     "csc_chebop_info": ([_P, _PI64, _PI64, _PI64, _PI64], _INT),
     "csc_chebop_schedule": ([_P, ctypes.POINTER(_I32), _PD], _INT),
     "csc_cheb_filter": ([_P, _P, _I64, _I64, _PD, _I32, _P, _P, _P, _P], _INT),
+    "csc_cheb_filter_download": ([_P, _P, _I64, _I64, _PD, _I32, _P, _P, _P, _I64, _I32, _P, _P], _INT),
     "csc_cheb_moments": ([_P, _P, _I64, _I64, _I32, _P, _P, _P], _INT),
     "csc_cheb_moments_keep": ([_P, _P, _I64, _I64, _I32, _P, _P, _P], _INT),
     "csc_cheb_combine": ([_P, _P, _I64, _I64, _I64, _PD, _I32, _P, _P, _P], _INT),

@@ -456,9 +456,40 @@ int stream_hint() {
   return g_hint;
 }
 
+// Download of the filtered block to host memory overlapped with the last order
+// (apply_filter's host pipeline): the final sweep runs as `nslices` row-range
+// launches, and each slice's rows are copied to the host on `copy` as soon as
+// its launch completes, so only the last slice's copy is exposed. Row ranges
+// are exact sub-launches of the index-ordered schedule (rows keep their own
+// stored-order sums, so the output is bitwise that of one launch); plans with
+// long-row segments, the length-ordered schedule, column chunks or a fused
+// ||out||^2 take one final launch followed by one copy.
+struct HostDownload {
+  void *dst = nullptr;     // host rows, pitch bytes apart
+  int64_t pitch = 0;
+  int64_t width = 0;       // bytes per row to copy (d * element size)
+  int nslices = 1;
+  cudaStream_t copy = nullptr;
+};
+
+int enqueue_download(const HostDownload &h, const void *dev, int64_t dev_pitch, int64_t r0,
+                     int64_t r1, cudaStream_t st) {
+  cudaEvent_t ev;
+  CSC_TRY_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CSC_TRY_CUDA(cudaEventRecord(ev, st));
+  CSC_TRY_CUDA(cudaStreamWaitEvent(h.copy, ev, 0));
+  CSC_TRY_CUDA(cudaEventDestroy(ev));  // released once the recorded work completes
+  CSC_TRY_CUDA(cudaMemcpy2DAsync(static_cast<char *>(h.dst) + r0 * h.pitch, (size_t)h.pitch,
+                                 static_cast<const char *>(dev) + r0 * dev_pitch,
+                                 (size_t)dev_pitch, (size_t)h.width, (size_t)(r1 - r0),
+                                 cudaMemcpyDeviceToHost, h.copy));
+  return CSC_OK;
+}
+
 template <typename T>
 int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *coeffs,
-                  int ncoeffs, T *out, T *work, double *sumsq_dev, cudaStream_t st) {
+                  int ncoeffs, T *out, T *work, double *sumsq_dev, cudaStream_t st,
+                  const HostDownload *host = nullptr) {
   using VT = typename V16<T>::V;
   constexpr int E = V16<T>::E;
   const int64_t ldv = ld / E;
@@ -503,7 +534,33 @@ int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *co
     A.sumsq = (fused_sumsq && ncoeffs == 2) ? 1 : 0;
     int64_t np = 0;
     double *cparts = fused_sumsq ? parts.as<double>() + ch * maxp : nullptr;
-    int rc = run_order_sched<T>(op, A, kFirst, A.sumsq ? cparts : nullptr, np, st, segs.ptr);
+    const bool sliced = host && host->nslices > 1 && nchunks == 1 && op.n_long == 0 &&
+                        op.perm == nullptr && !fused_sumsq;
+    // the last order as row-range launches, each slice's rows downloaded on
+    // host->copy while the next slice computes
+    auto final_order = [&](int mode) -> int {
+      if (!sliced) return run_order_sched<T>(op, A, mode, A.sumsq ? cparts : nullptr, np, st, segs.ptr);
+      const int64_t step = csc::ceil_div(n, (int64_t)host->nslices);
+      for (int64_t r0 = 0; r0 < n; r0 += step) {
+        const int64_t r1 = std::min(n, r0 + step);
+        SweepPlan p;
+        p.n = r1 - r0;
+        SweepArgs B = A;
+        B.indptr = A.indptr + r0;
+        B.n = r1 - r0;
+        B.prev = static_cast<const VT *>(A.prev) + r0 * ldv;
+        B.next = static_cast<VT *>(A.next) + r0 * ldv;
+        B.out = static_cast<VT *>(A.out) + r0 * ldv;
+        int64_t npp = 0;
+        int rc = run_order<T, false>(p, B, mode, nullptr, npp, st, nullptr);
+        if (rc != CSC_OK) return rc;
+        rc = enqueue_download(*host, out, ld * (int64_t)sizeof(T), r0, r1, st);
+        if (rc != CSC_OK) return rc;
+      }
+      return CSC_OK;
+    };
+    int rc = ncoeffs == 2 ? final_order(kFirst)
+                          : run_order_sched<T>(op, A, kFirst, A.sumsq ? cparts : nullptr, np, st, segs.ptr);
     if (rc != CSC_OK) return rc;
     const VT *t_prev = xv;
     VT *t_cur = ta, *t_next = tb;
@@ -514,7 +571,8 @@ int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *co
       A.ca = coeffs[j];
       A.cb = 0.0;
       A.sumsq = (fused_sumsq && j == ncoeffs - 1) ? 1 : 0;
-      rc = run_order_sched<T>(op, A, kMid, A.sumsq ? cparts : nullptr, np, st, segs.ptr);
+      rc = j == ncoeffs - 1 ? final_order(kMid)
+                            : run_order_sched<T>(op, A, kMid, A.sumsq ? cparts : nullptr, np, st, segs.ptr);
       if (rc != CSC_OK) return rc;
       t_prev = t_cur;
       t_cur = t_next;
@@ -525,6 +583,9 @@ int cheb_filter_t(const csc_chebop &op, const T *x, int64_t ld, const double *co
     reduce_partials_kernel<<<1, 1024, 0, st>>>(parts.as<double>(), maxp * nchunks, sumsq_dev);
     CSC_CHECK_LAUNCH();
   }
+  if (host && !(host->nslices > 1 && nchunks == 1 && op.n_long == 0 && op.perm == nullptr &&
+                !fused_sumsq))
+    return enqueue_download(*host, out, ld * (int64_t)sizeof(T), 0, n, st);
   return CSC_OK;
 }
 
@@ -854,6 +915,40 @@ int csc_cheb_filter(const csc_chebop *op, const void *x, int64_t ld, int64_t d,
   return cheb_filter_t<float>(*op, static_cast<const float *>(x), ld, coeffs, ncoeffs,
                               static_cast<float *>(out), static_cast<float *>(work), sumsq_dev,
                               st);
+}
+
+int csc_cheb_filter_download(const csc_chebop *op, const void *x, int64_t ld, int64_t d,
+                             const double *coeffs, int32_t ncoeffs, void *out, void *work,
+                             void *host_dst, int64_t host_pitch, int32_t nslices, void *copy_stream,
+                             void *stream) {
+  csc::clear_error();
+  CSC_REQUIRE(op != nullptr, "csc_cheb_filter_download: NULL plan");
+  CSC_REQUIRE(ncoeffs >= 2, "csc_cheb_filter_download: need at least 2 coefficients, got %d", ncoeffs);
+  CSC_REQUIRE(d >= 1 && ld >= d, "csc_cheb_filter_download: need 1 <= d <= ld");
+  const int64_t esz = op->dtype == CSC_F64 ? 8 : 4;
+  CSC_REQUIRE((ld * esz) % 16 == 0, "csc_cheb_filter_download: row stride must be a multiple of 16 bytes");
+  CSC_REQUIRE(aligned16(x) && aligned16(out) && aligned16(work),
+              "csc_cheb_filter_download: buffers must be 16-byte aligned");
+  CSC_REQUIRE(coeffs != nullptr, "csc_cheb_filter_download: NULL coefficients");
+  CSC_REQUIRE(host_dst != nullptr && host_pitch >= d * esz,
+              "csc_cheb_filter_download: need a host buffer with pitch >= d * element size");
+  CSC_REQUIRE(nslices >= 1, "csc_cheb_filter_download: need nslices >= 1");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const_cast<csc_chebop *>(op)->stream = st;
+  if (op->n == 0) return CSC_OK;
+  HostDownload h;
+  h.dst = host_dst;
+  h.pitch = host_pitch;
+  h.width = d * esz;
+  h.nslices = nslices;
+  h.copy = static_cast<cudaStream_t>(copy_stream);
+  if (op->dtype == CSC_F64)
+    return cheb_filter_t<double>(*op, static_cast<const double *>(x), ld, coeffs, ncoeffs,
+                                 static_cast<double *>(out), static_cast<double *>(work), nullptr,
+                                 st, &h);
+  return cheb_filter_t<float>(*op, static_cast<const float *>(x), ld, coeffs, ncoeffs,
+                              static_cast<float *>(out), static_cast<float *>(work), nullptr, st,
+                              &h);
 }
 
 }  // extern "C"

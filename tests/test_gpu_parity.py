@@ -761,12 +761,28 @@ def test_filter_host_pipeline(P, monkeypatch):
     x = torch.from_numpy(np.ascontiguousarray(g["R"], dtype=np.float64)).pin_memory().numpy()
     monkeypatch.setattr(PF, "PIPE_MIN_BYTES", 0)
     monkeypatch.setattr(PF, "PIPE_MIN_COLS", 4)
+    monkeypatch.setattr(PF, "PIPE_MODE", "columns")
     for chunks in (2, 3):
         monkeypatch.setattr(PF, "PIPE_CHUNKS", chunks)
         counter = P.MatvecCounter()
         out = P.apply_filter(lap, poly, x, counter)
         assert rel(out, g["filt_05"]) <= FEAT_TOL
         assert counter.count == 50 * x.shape[1]
+    # row-slice pipeline (the default): pinned and pageable input, any slice count
+    monkeypatch.setattr(PF, "PIPE_MODE", "slices")
+    dev = P.apply_filter(lap, poly, torch.from_numpy(x).cuda()).cpu().numpy()
+    for slices, up in ((1, 1), (3, 2), (8, 8), (999, 7)):
+        monkeypatch.setattr(PF, "PIPE_SLICES", slices)
+        monkeypatch.setattr(PF, "PIPE_UP_SLICES", up)
+        for xin in (x, np.array(x)):  # pinned pages, then an ordinary array
+            counter = P.MatvecCounter()
+            out = P.apply_filter(lap, poly, xin, counter)
+            assert np.array_equal(out, dev), (slices, up)
+            assert rel(out, g["filt_05"]) <= FEAT_TOL
+            assert counter.count == 50 * x.shape[1]
+    one = P.apply_filter(lap, P.cheb_coeffs(0.5, 2.0, 1), x)  # the last order is the first
+    assert np.array_equal(one, P.apply_filter(lap, P.cheb_coeffs(0.5, 2.0, 1), torch.from_numpy(x).cuda()).cpu().numpy())
+    monkeypatch.setattr(PF, "PIPE_MODE", "columns")
     # a larger block: pipelined host result equals the device-tensor path
     rng = np.random.default_rng(7)
     n, d = 60000, 96
@@ -779,3 +795,14 @@ def test_filter_host_pipeline(P, monkeypatch):
     host = P.apply_filter(big, poly, xb.numpy())
     dev = P.apply_filter(big, poly, xb.cuda()).cpu().numpy()
     assert rel(host, dev) <= 1e-13
+    monkeypatch.setattr(PF, "PIPE_MODE", "slices")
+    monkeypatch.setattr(PF, "PIPE_SLICES", 8)
+    assert np.array_equal(P.apply_filter(big, poly, xb.numpy()), dev)
+    assert np.array_equal(P.apply_filter(big, poly, np.array(xb.numpy()[:, :37])),
+                          P.apply_filter(big, poly, xb[:, :37].contiguous().cuda()).cpu().numpy())
+    # a hub row past the segment cut: one final launch, then one copy
+    hub = np.arange(1, 3000)
+    star = P.laplacian(P.Graph(3000, np.zeros(hub.size, dtype=np.int64), hub, np.ones(hub.size)))
+    xs = rng.normal(size=(3000, 16))
+    ps = P.cheb_coeffs(0.7, 2.0, 12)
+    assert np.array_equal(P.apply_filter(star, ps, xs), P.apply_filter(star, ps, torch.from_numpy(xs).cuda()).cpu().numpy())

@@ -37,20 +37,23 @@ for rep in range(3):
           f"download {(t3 - t2) * 1e3:.1f} ms")
     del res, h, out, blk
 
-# host pipeline chunk counts (PIPE_CHUNKS = 1: the unpipelined path)
+# host pipelines: column chunks (round 1) vs row slices (download overlapped
+# with the last order), pinned and pageable input
 from paper_1706_03591_b200 import filters as PF  # noqa: E402
 ref = P.apply_filter(lap, poly, torch.from_numpy(x_np).cuda()).cpu().numpy()
-for chunks in (1, 2, 3, 4):
-    PF.PIPE_CHUNKS = chunks
-    PF.PIPE_MIN_BYTES = 1 << 28 if chunks > 1 else 1 << 62
-    res = P.apply_filter(lap, poly, x_np)
-    torch.cuda.synchronize()
-    ts = []
-    for rep in range(3):
-        t0 = time.perf_counter()
-        res = P.apply_filter(lap, poly, x_np)
-        torch.cuda.synchronize()
-        ts.append((time.perf_counter() - t0) * 1e3)
-    err = float(np.abs(res - ref).max())
-    print(f"chunks {chunks}: apply_filter {min(ts):.1f} / {np.median(ts):.1f} ms (min / median), "
-          f"max |host - device| {err:.2e}")
+x_pg = np.array(x_np)
+variants = [("columns", 2, 0), ("slices", 1, 8), ("slices", 4, 8), ("slices", 8, 8), ("slices", 16, 16)]
+for rnd in range(2):
+    for mode, sl, up in variants:
+        PF.PIPE_MODE, PF.PIPE_CHUNKS, PF.PIPE_SLICES, PF.PIPE_UP_SLICES = mode, 2, sl, max(1, up)
+        for name, xin in (("pinned", x_np), ("pageable", x_pg)):
+            res = P.apply_filter(lap, poly, xin)
+            ts = []
+            for rep in range(4):
+                t0 = time.perf_counter()
+                res = P.apply_filter(lap, poly, xin)
+                torch.cuda.synchronize()
+                ts.append((time.perf_counter() - t0) * 1e3)
+            same = bool(np.array_equal(res, ref))
+            print(f"{mode:8s} slices {sl:2d} up {up:2d} {name:8s}: {min(ts):.1f} / {np.median(ts):.1f} ms "
+                  f"(min / median), bitwise equal to the device path: {same}", flush=True)
