@@ -300,7 +300,9 @@ int csc_kmeans_plan_set_screen(csc_kmeans_plan *plan, const float *f32_dev, int6
 /* k-means tuning knobs (performance only; results do not change):
  * "assign_ver" 2|3, "assign_tn" 4|8 (v2 kernel), "assign_tile" 0 (auto) |
  * 1 (small-k kernel) | 88 | 84 | 87 | 48 | 44 | 42 (v3 register tile),
- * "finish_mode" 0|1|2 (fused / fused-256 / split iteration tail) */
+ * "finish_mode" 0|1|2 (fused / fused-256 / split iteration tail),
+ * "kpp_staged" 0|1 (batched k-means++ distances: direct row loads / rows
+ * staged through shared memory, the default for 16-byte-aligned blocks) */
 int csc_kmeans_tuning(const char *key, int64_t value);
 /* empty-cluster repair (kmeans.py:99-108): for each empty j ascending, move the
  * row with the largest own_d2 (first max) to j and set its own_d2 to -1.

@@ -721,6 +721,7 @@ int launch_assign_small(const double *f, const double *fnorm, int64_t n, int64_t
   return CSC_OK;
 }
 
+int g_kpp_staged = -1;  // batched k-means++ distance pass staged through shared memory (-1: env)
 int g_assign_tn = 8;
 int g_assign_ver = 3;
 // incremental centroid sums (update_sorted_kernel): tuning key "update_incremental"
@@ -1289,20 +1290,29 @@ __global__ void __launch_bounds__(128)
         acc2[r] = fma(t2, t2, acc2[r]);
       }
     }
+    if (!first) {  // all loads before the first store (one memory round trip)
+      double old[R], old2[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        old[r] = closest[(int64_t)r * n + i];
+        old2[r] = two ? closest[(int64_t)r * n + i2] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r] = fmin(old[r], acc[r]);
+        acc2[r] = fmin(old2[r], acc2[r]);
+      }
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      double *slot = closest + (int64_t)r * n + i;
-      const double cl = first ? acc[r] : fmin(*slot, acc[r]);
-      *slot = cl;
-      part[r] += cl;
+      closest[(int64_t)r * n + i] = acc[r];
+      part[r] += acc[r];
     }
     if (two) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        double *slot = closest + (int64_t)r * n + i2;
-        const double cl = first ? acc2[r] : fmin(*slot, acc2[r]);
-        *slot = cl;
-        part[r] += cl;
+        closest[(int64_t)r * n + i2] = acc2[r];
+        part[r] += acc2[r];
       }
     }
   }
@@ -1319,6 +1329,159 @@ __global__ void __launch_bounds__(128)
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += wsum[w * R + threadIdx.x];
     chunk_sums[(int64_t)threadIdx.x * nchunks + blockIdx.x] = t;
+  }
+}
+
+// Staged variant of kppb_dist_kernel for 16-byte-aligned rows (f % 16 == 0, ld
+// even). The direct kernel's per-thread row loads touch 32 cache lines per
+// warp instruction (~64 L1 wavefront cycles each), which holds the FP64 pipe
+// at ~20%. Here a tile of 256 rows x 16 columns (128 B per row, coalesced
+// 16-byte cp.async, double-buffered) is staged in shared memory with the
+// 16-byte pieces of row t stored at piece ^ (t & 7), so a thread reads two
+// columns of its row with one conflict-free 128-bit load; the centroid values
+// come as one broadcast 128-bit load per restart and column pair. Same thread
+// -> rows mapping (t, t + 128 of every 256-row tile) and the same per-row FMA
+// chain over ascending columns as the direct kernel: identical bits.
+constexpr int kKsRows = 256;   // rows per tile (two per thread)
+constexpr int kKsCols = 16;    // columns per stage (one 128-byte line per row)
+template <int R>
+__global__ void __launch_bounds__(128)
+    kppb_dist_staged_kernel(const double *__restrict__ f, int64_t n, int64_t d, int64_t ld,
+                            const double *__restrict__ crows, int64_t crow_stride,
+                            double *__restrict__ closest, int first, int64_t chunk,
+                            double *__restrict__ chunk_sums, int64_t nchunks) {
+  extern __shared__ __align__(16) unsigned char kraw[];
+  const int npair = (int)((d + 1) / 2);
+  double2 *cs2 = reinterpret_cast<double2 *>(kraw);                  // [npair][R] (x = even column)
+  double *wsum = reinterpret_cast<double *>(cs2 + (size_t)npair * R);  // 4 warps x R
+  unsigned char *tiles =
+      kraw + (((size_t)npair * R * 16 + (size_t)4 * R * 8 + 127) / 128) * 128;  // 2 x 32 KB
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < npair * R; e += 128) {
+    const int p = e / R, r = e % R;
+    const double *cr = crows + (int64_t)r * crow_stride;
+    cs2[e] = make_double2(cr[2 * p], 2 * p + 1 < d ? cr[2 * p + 1] : 0.0);
+  }
+  const int64_t rbeg = blockIdx.x * chunk, rend = min(n, rbeg + chunk);
+  const int nstage = (int)((d + kKsCols - 1) / kKsCols);
+  const int ntile = rend > rbeg ? (int)((rend - rbeg + kKsRows - 1) / kKsRows) : 0;
+  const int nunit = ntile * nstage;
+  auto issue = [&](int u) {  // stage (u % nstage) of tile (u / nstage) into buffer u & 1
+    const int tile = u / nstage, stg = u % nstage;
+    const int64_t row0 = rbeg + (int64_t)tile * kKsRows;
+    const int64_t c0 = (int64_t)stg * kKsCols;
+    const int pieces = (int)min((int64_t)(kKsCols / 2), (d - c0 + 1) / 2);  // valid 16-byte pieces per row
+    unsigned char *buf = tiles + (size_t)(u & 1) * (kKsRows * 128);
+#pragma unroll 4
+    for (int q = 0; q < kKsRows * 8 / 128; ++q) {
+      const int pc = tid + 128 * q;
+      const int lr = pc >> 3, j = pc & 7;
+      const int64_t gr = row0 + lr;
+      if (gr < rend && j < pieces)
+        cp_async16(buf + lr * 128 + ((j ^ (lr & 7)) << 4), f + gr * ld + c0 + 2 * j, true);
+    }
+    cp_async_commit();
+  };
+  double part[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) part[r] = 0.0;
+  if (nunit > 0) issue(0);
+  double acc[R], acc2[R];
+  const int sw = tid & 7;
+  for (int u = 0; u < nunit; ++u) {
+    const int tile = u / nstage, stg = u % nstage;
+    if (u + 1 < nunit) {
+      issue(u + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // unit u landed (and, at u == 0, the centroid pairs are visible)
+    if (stg == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r] = 0.0;
+        acc2[r] = 0.0;
+      }
+    }
+    const unsigned char *buf = tiles + (size_t)(u & 1) * (kKsRows * 128);
+    const unsigned char *xa = buf + tid * 128, *xb = buf + (tid + 128) * 128;
+    const int c0 = stg * kKsCols;
+    const int full = (int)min((int64_t)(kKsCols / 2), (d - c0) / 2);  // pairs with both columns valid
+    const double2 *cp = cs2 + (size_t)(c0 / 2) * R;
+#pragma unroll 2
+    for (int p = 0; p < full; ++p) {
+      const double2 x = *reinterpret_cast<const double2 *>(xa + ((p ^ sw) << 4));
+      const double2 y = *reinterpret_cast<const double2 *>(xb + ((p ^ sw) << 4));
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double2 cv = cp[p * R + r];
+        double t = x.x - cv.x, t2 = y.x - cv.x;
+        acc[r] = fma(t, t, acc[r]);
+        acc2[r] = fma(t2, t2, acc2[r]);
+        t = x.y - cv.y;
+        t2 = y.y - cv.y;
+        acc[r] = fma(t, t, acc[r]);
+        acc2[r] = fma(t2, t2, acc2[r]);
+      }
+    }
+    if (full < kKsCols / 2 && c0 + 2 * full < d) {  // odd d: the last column alone
+      const double x = *reinterpret_cast<const double *>(xa + ((full ^ sw) << 4));
+      const double y = *reinterpret_cast<const double *>(xb + ((full ^ sw) << 4));
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double cv = cp[full * R + r].x;
+        const double t = x - cv, t2 = y - cv;
+        acc[r] = fma(t, t, acc[r]);
+        acc2[r] = fma(t2, t2, acc2[r]);
+      }
+    }
+    if (stg == nstage - 1) {
+      const int64_t i = rbeg + (int64_t)tile * kKsRows + tid, i2 = i + 128;
+      // all previous values loaded before the first store (the stores may
+      // alias the loads for the compiler: one memory round trip, not 2R)
+      if (!first) {
+        double old[R], old2[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          old[r] = i < rend ? closest[(int64_t)r * n + i] : 0.0;
+          old2[r] = i2 < rend ? closest[(int64_t)r * n + i2] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r] = fmin(old[r], acc[r]);
+          acc2[r] = fmin(old2[r], acc2[r]);
+        }
+      }
+      if (i < rend) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          closest[(int64_t)r * n + i] = acc[r];
+          part[r] += acc[r];
+        }
+      }
+      if (i2 < rend) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          closest[(int64_t)r * n + i2] = acc2[r];
+          part[r] += acc2[r];
+        }
+      }
+    }
+    __syncthreads();  // buffer u & 1 is free for unit u + 2
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double v = part[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) wsum[wid * R + r] = v;
+  }
+  __syncthreads();
+  if (tid < R) {
+    double t = 0.0;
+    for (int w = 0; w < 4; ++w) t += wsum[w * R + tid];
+    chunk_sums[(int64_t)tid * nchunks + blockIdx.x] = t;
   }
 }
 
@@ -2420,6 +2583,10 @@ int csc_kmeans_tuning(const char *key, int64_t value) {
     g_screen_tc = value ? 1 : 0;
     return CSC_OK;
   }
+  if (std::string(key) == "kpp_staged") {
+    g_kpp_staged = value ? 1 : 0;
+    return CSC_OK;
+  }
   if (std::string(key) == "assign_tn") {
     CSC_REQUIRE(value == 4 || value == 8, "assign_tn must be 4 or 8");
     g_assign_tn = (int)value;
@@ -3026,6 +3193,15 @@ int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_
   CSC_REQUIRE((int64_t)smem <= (int64_t)csc::device_info().max_smem_optin,
               "csc_kmeanspp_batch: R*d too large for shared memory (R=%lld, d=%lld)",
               (long long)R, (long long)d);
+  // staged distance pass: 16-byte-aligned rows, chunks long enough to fill tiles
+  const size_t smem_staged = (((size_t)((d + 1) / 2) * R * 16 + (size_t)4 * R * 8 + 127) / 128) * 128 +
+                             (size_t)2 * kKsRows * 128;
+  if (g_kpp_staged < 0) {
+    const char *e = getenv("CSC_KPP_STAGED");
+    g_kpp_staged = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool staged = g_kpp_staged && (reinterpret_cast<uintptr_t>(f) % 16 == 0) && ld % 2 == 0 &&
+                      chunk >= kKsRows && (int64_t)smem_staged <= (int64_t)csc::device_info().max_smem_optin;
   for (int64_t j = 0; j < k; ++j) {
     if (j > 0) {
       kppb_pick_kernel<<<(unsigned)R, 1024, 0, st>>>(f, n, d, ld, closest.as<double>(),
@@ -3035,6 +3211,29 @@ int csc_kmeanspp_batch(const double *f, int64_t n, int64_t d, int64_t ld, int64_
       CSC_CHECK_LAUNCH();
     }
     if (j < k - 1) {
+      if (staged) {
+        switch (R) {
+#define CSC_KPPS_CASE(RR)                                                                      \
+  case RR:                                                                                     \
+    CSC_TRY_CUDA(cudaFuncSetAttribute(kppb_dist_staged_kernel<RR>,                             \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                                      (int)smem_staged));                                      \
+    kppb_dist_staged_kernel<RR><<<(unsigned)nchunks, 128, smem_staged, st>>>(                  \
+        f, n, d, ld, cent + j * ldc, cent_stride, closest.as<double>(), j == 0 ? 1 : 0, chunk, \
+        sums.as<double>(), nchunks);                                                           \
+    break;
+          CSC_KPPS_CASE(1) CSC_KPPS_CASE(2) CSC_KPPS_CASE(3) CSC_KPPS_CASE(4)
+          CSC_KPPS_CASE(5) CSC_KPPS_CASE(6) CSC_KPPS_CASE(7) CSC_KPPS_CASE(8)
+          CSC_KPPS_CASE(9) CSC_KPPS_CASE(10) CSC_KPPS_CASE(11) CSC_KPPS_CASE(12)
+          CSC_KPPS_CASE(13) CSC_KPPS_CASE(14) CSC_KPPS_CASE(15) CSC_KPPS_CASE(16)
+#undef CSC_KPPS_CASE
+          default:
+            csc::set_error("csc_kmeanspp_batch: R=%lld out of range", (long long)R);
+            return CSC_ERR_ARG;
+        }
+        CSC_CHECK_LAUNCH();
+        continue;
+      }
       switch (R) {
 #define CSC_KPPB_CASE(RR)                                                                      \
   case RR:                                                                                     \

@@ -401,3 +401,28 @@ def test_plan_empty_cluster_repair_exact_sums(P, screen):
     assert len(hist) == ref_it
     assert np.array_equal(labels, ref_labels)
     assert abs(cost2 - ref_cost2) <= COST_TOL * ref_cost2
+
+
+@pytest.mark.parametrize("n,d,k,R", [(300_000, 37, 6, 3), (600_000, 96, 5, 10), (270_001, 16, 4, 2),
+                                     (263_000, 130, 3, 7)])
+def test_batched_kpp_staged_equals_direct_and_reference(P, n, d, k, R):
+    """csc_kmeanspp_batch's shared-memory-staged distance pass (rows >= 256 per
+    chunk, 16-byte-aligned block) gives bitwise the seeds of the direct pass,
+    and both pick the reference's rows (kmeans.py:64-77)."""
+    from paper_1706_03591_b200 import _native
+    from paper_1706_03591_b200._device import upload_block
+    from paper_1706_03591_b200.kmeans import _Workspace, batched_kmeanspp
+    f = blobs(n, d, max(k, 8), 1.5, 5)
+    ws = _Workspace(upload_block(f), d, k)
+    kids = np.random.SeedSequence(11).spawn(R)
+    try:
+        _native.call("csc_kmeans_tuning", b"kpp_staged", 1)
+        staged = batched_kmeanspp(ws, kids).cpu().numpy()
+        _native.call("csc_kmeans_tuning", b"kpp_staged", 0)
+        direct = batched_kmeanspp(ws, kids).cpu().numpy()
+    finally:
+        _native.call("csc_kmeans_tuning", b"kpp_staged", 1)
+    assert np.array_equal(staged, direct)
+    for r in range(min(R, 2)):
+        ref, _ = O.kmeanspp(f, k, np.random.default_rng(kids[r]))
+        assert np.array_equal(staged[r, :, :d], ref), r
