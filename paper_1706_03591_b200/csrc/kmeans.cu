@@ -1366,19 +1366,25 @@ __global__ void __launch_bounds__(128)
   const int nstage = (int)((d + kKsCols - 1) / kKsCols);
   const int ntile = rend > rbeg ? (int)((rend - rbeg + kKsRows - 1) / kKsRows) : 0;
   const int nunit = ntile * nstage;
+  // thread t copies 16-byte piece (t & 7) of rows (t >> 3) + 16 q, q = 0..15, of
+  // every tile: piece and swizzle are per-thread constants, rows step by 16
+  const int pj = tid & 7, pr = tid >> 3;
+  const unsigned pdst = (unsigned)(pr * 128 + ((pj ^ (pr & 7)) << 4));
   auto issue = [&](int u) {  // stage (u % nstage) of tile (u / nstage) into buffer u & 1
     const int tile = u / nstage, stg = u % nstage;
-    const int64_t row0 = rbeg + (int64_t)tile * kKsRows;
-    const int64_t c0 = (int64_t)stg * kKsCols;
+    const int64_t row0 = rbeg + (int64_t)tile * kKsRows + pr;
+    const int c0 = stg * kKsCols;
     const int pieces = (int)min((int64_t)(kKsCols / 2), (d - c0 + 1) / 2);  // valid 16-byte pieces per row
-    unsigned char *buf = tiles + (size_t)(u & 1) * (kKsRows * 128);
+    if (pj < pieces) {
+      unsigned char *dst = tiles + (size_t)(u & 1) * (kKsRows * 128) + pdst;
+      const double *src = f + row0 * ld + c0 + 2 * pj;
+      const int nq = (int)min((int64_t)(kKsRows / 16), (rend - row0 + 15) / 16);  // rows row0 + 16 q < rend
 #pragma unroll 4
-    for (int q = 0; q < kKsRows * 8 / 128; ++q) {
-      const int pc = tid + 128 * q;
-      const int lr = pc >> 3, j = pc & 7;
-      const int64_t gr = row0 + lr;
-      if (gr < rend && j < pieces)
-        cp_async16(buf + lr * 128 + ((j ^ (lr & 7)) << 4), f + gr * ld + c0 + 2 * j, true);
+      for (int q = 0; q < nq; ++q) {
+        cp_async16(dst, src, true);
+        dst += 16 * 128;
+        src += 16 * ld;
+      }
     }
     cp_async_commit();
   };
