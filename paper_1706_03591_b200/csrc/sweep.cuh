@@ -382,7 +382,7 @@ __device__ __forceinline__ void segment_body(const SweepArgs &A, int64_t first_w
 #endif
 template <int G, int VPL>
 struct SweepMinBlocks {
-  static constexpr int value = (G < 32 && VPL <= 2) ? SWEEP_NARROW_MIN : (VPL <= 2 ? SWEEP_WIDE_MIN : 0);
+  static constexpr int value = (G < 32 && VPL <= 2) ? SWEEP_NARROW_MIN : (VPL <= 3 ? SWEEP_WIDE_MIN : 0);
 };
 
 template <typename T, int G, int VPL, int MODE, bool PERM>
@@ -684,6 +684,9 @@ int run_order_g(const SweepPlan &op, const SweepArgs &A, int mode, double *parti
   const int need = (A.nvec + G - 1) / G;  // vectors per lane at this group width
   if (need <= 1) return run_order_gv<T, G, 1, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
   if (need <= 2) return run_order_gv<T, G, 2, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
+  if constexpr (G == 8 || G == 16) {  // 3 vectors per lane: 24 (d = 48 fp64) / 36-48 vectors without idle lane slots
+    if (need == 3) return run_order_gv<T, G, 3, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
+  }
   if (need <= 4) return run_order_gv<T, G, 4, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
   return run_order_gv<T, G, 8, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
 }
@@ -704,6 +707,18 @@ int run_order(const SweepPlan &op, const SweepArgs &A, int mode, double *partial
   }
   const int pref = vpl_pref() ? vpl_pref() : (A.nvec <= 32 ? 2 : 1);
   const int want = (A.nvec + pref - 1) / pref;
+  if (!vpl_pref()) {
+    // three vectors per lane when that leaves fewer idle lane slots than the
+    // power-of-two choice below (B200 A/B, ms per order: cfg5 d = 48 3.20 ->
+    // 3.07, d = 72 5.26 -> 4.90, cfg3 d = 40 1.98 -> 1.89)
+    const int g0 = want <= 4 ? 4 : want <= 8 ? 8 : want <= 16 ? 16 : 32;
+    const int slots0 = g0 * ((A.nvec + g0 - 1) / g0 <= 2 ? (A.nvec + g0 - 1) / g0
+                             : (A.nvec + g0 - 1) / g0 <= 4 ? 4 : 8);
+    if (A.nvec > 16 && A.nvec <= 24 && 24 < slots0)
+      return run_order_g<T, 8, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
+    if (A.nvec > 32 && A.nvec <= 48 && 48 < slots0)
+      return run_order_g<T, 16, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
+  }
   if (want <= 4) return run_order_g<T, 4, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
   if (want <= 8) return run_order_g<T, 8, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
   if (want <= 16) return run_order_g<T, 16, PERM>(op, A, mode, partials, nparts, st, seg_scratch);
