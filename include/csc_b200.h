@@ -178,6 +178,9 @@ int csc_sweep_timing(int enable);
 int csc_sweep_last_launch(char *name_out, int cap, int *grid_out);
 int csc_sweep_times(float *ms_host, int max_count, int *count_out);
 
+/* Stream-ordered scratch pool of the current device (diagnostics): bytes
+ * reserved now, in use now, and the high-water marks of both. */
+int csc_pool_stats(int64_t *out4);
 /* rows x width_bytes strided copy (cudaMemcpy2DAsync, direction from the
  * pointers): the column-chunk staging of apply_filter's host pipeline
  * (filters.py apply_filter; reference filters.py:155-178 takes a host matrix). */

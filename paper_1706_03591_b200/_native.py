@@ -63,6 +63,7 @@ SIGNATURES = {
     "csc_kmeans_iterate": ([_P, _P, _P, _P, _I64, _P, _P, _P, _INT, _P, _P], _INT),
     "csc_kmeans_run": ([_P, _P, _P, _P, _I64, _P, _P, _P, _INT, _D, _P, _P, _P], _INT),
     "csc_kmeans_tuning": ([ctypes.c_char_p, _I64], _INT),
+    "csc_pool_stats": ([_P], _INT),
     "csc_kmeans_screen_supported": ([_I64, _I64], _INT),
     "csc_kmeans_tc_supported": ([_I64, _I64], _INT),
     "csc_kmeans_tc_distances": ([_P, _I64, _I64, _I64, _P, _P, _I64, _I64, _P, _P, _P], _INT),

@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <chrono>
 #include <cstdlib>
 #include <string>
 
@@ -700,6 +701,12 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
   CSC_REQUIRE(scale > 0.0 && isfinite(scale), "csc_chebop_create: scale must be positive");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   csc::device_info();
+  static const bool dbg_t = getenv("CSC_DEBUG_TIMING") != nullptr;
+  double dbg[8] = {0};
+  auto now = [] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  dbg[0] = now();
   csc_chebop *op = new csc_chebop();
   op->n = n;
   op->dtype = dtype;
@@ -715,7 +722,7 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
                                           std::max<int64_t>(1, csc::ceil_div(n, threads)));
   // row counts of M
   csc::Scratch counts, scan_tmp;
-  if (cudaMallocAsync((void **)&op->indptr, sizeof(int32_t) * (n + 1), st) != cudaSuccess) {
+  if (csc::pool_alloc((void **)&op->indptr, sizeof(int32_t) * (n + 1), st) != cudaSuccess) {
     csc::set_error("csc_chebop_create: allocation failed");
     return fail(CSC_ERR_CUDA);
   }
@@ -727,6 +734,7 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
     op_count_warp_kernel<<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale,
                                                    counts.as<int32_t>());
   }
+  dbg[1] = now();
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts.as<int32_t>(), op->indptr, n + 1, st);
   if (scan_tmp.alloc(tmp_bytes, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
@@ -736,12 +744,13 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
   // (isolated nodes; exact zeros are dropped): allocate nnz + n now and read
   // M's count back together with the long-row count below (one
   // synchronisation instead of two)
-  if (cudaMallocAsync((void **)&op->indices, sizeof(int32_t) * std::max<int64_t>(nnz + n, 1), st) !=
+  if (csc::pool_alloc((void **)&op->indices, sizeof(int32_t) * std::max<int64_t>(nnz + n, 1), st) !=
           cudaSuccess ||
-      cudaMallocAsync(&op->vals, esz * std::max<int64_t>(nnz + n, 1), st) != cudaSuccess) {
+      csc::pool_alloc(&op->vals, esz * std::max<int64_t>(nnz + n, 1), st) != cudaSuccess) {
     csc::set_error("csc_chebop_create: allocation failed");
     return fail(CSC_ERR_CUDA);
   }
+  dbg[2] = now();
   if (n > 0) {
     if (dtype == CSC_F64) {
       op_fill_kernel<double><<<grid, threads, 0, st>>>(indptr, indices, vals, n, scale, op->indptr,
@@ -759,7 +768,7 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
   // long-row schedule
   csc::Scratch nsel, sel_tmp, segcnt;
   if (nsel.alloc(sizeof(int32_t) * 2, st) != cudaSuccess) return fail(CSC_ERR_CUDA);
-  if (cudaMallocAsync((void **)&op->long_rows, sizeof(int32_t) * std::max<int64_t>(n, 1), st) !=
+  if (csc::pool_alloc((void **)&op->long_rows, sizeof(int32_t) * std::max<int64_t>(n, 1), st) !=
       cudaSuccess)
     return fail(CSC_ERR_CUDA);
   thrust::counting_iterator<int32_t> rows_it(0);
@@ -776,6 +785,7 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
   if (n > 0)
     len_stats_kernel<<<grid, threads, 0, st>>>(counts.as<int32_t>(), n,
                                                stats.as<unsigned long long>());
+  dbg[3] = now();
   // nsel[1] <- nnz(M) = indptr[n]; one copy of both counts
   int32_t cnt[2] = {0, 0};
   unsigned long long lst[2] = {0, 0};
@@ -788,12 +798,16 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
     csc::set_error("csc_chebop_create: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(CSC_ERR_CUDA);
   }
+  dbg[4] = now();
+  if (dbg_t && dbg[4] - dbg[0] > 20.0)
+    fprintf(stderr, "csc_chebop_create slow: first allocs+count %.1f, scan+allocs %.1f, fill+select %.1f, sync %.1f ms\n",
+            dbg[1] - dbg[0], dbg[2] - dbg[1], dbg[3] - dbg[2], dbg[4] - dbg[3]);
   const int32_t n_long = cnt[0];
   op->nnz = cnt[1];
   op->n_long = n_long;
   if (n_long > 0) {
     if (segcnt.alloc(sizeof(int32_t) * (n_long + 1), st) != cudaSuccess ||
-        cudaMallocAsync((void **)&op->seg_off, sizeof(int32_t) * (n_long + 1), st) != cudaSuccess)
+        csc::pool_alloc((void **)&op->seg_off, sizeof(int32_t) * (n_long + 1), st) != cudaSuccess)
       return fail(CSC_ERR_CUDA);
     cudaMemsetAsync(segcnt.ptr, 0, sizeof(int32_t) * (n_long + 1), st);
     seg_count_kernel<<<(int)std::min<int64_t>(1024, csc::ceil_div(n_long, 256)), 256, 0, st>>>(
@@ -820,7 +834,7 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
     csc::Scratch keys_out, ids, sort_tmp;
     if (keys_out.alloc(sizeof(int32_t) * n, st) != cudaSuccess ||
         ids.alloc(sizeof(int32_t) * n, st) != cudaSuccess ||
-        cudaMallocAsync((void **)&op->perm, sizeof(int32_t) * n, st) != cudaSuccess)
+        csc::pool_alloc((void **)&op->perm, sizeof(int32_t) * n, st) != cudaSuccess)
       return fail(CSC_ERR_CUDA);
     iota_kernel<<<grid, threads, 0, st>>>(ids.as<int32_t>(), n);
     size_t sb = 0;
@@ -844,12 +858,12 @@ int csc_chebop_create(const int32_t *indptr, const int32_t *indices, const doubl
 int csc_chebop_destroy(csc_chebop *op) {
   if (!op) return CSC_OK;
   cudaStream_t st = op->stream;
-  if (op->indptr) cudaFreeAsync(op->indptr, st);
-  if (op->indices) cudaFreeAsync(op->indices, st);
-  if (op->vals) cudaFreeAsync(op->vals, st);
-  if (op->long_rows) cudaFreeAsync(op->long_rows, st);
-  if (op->seg_off) cudaFreeAsync(op->seg_off, st);
-  if (op->perm) cudaFreeAsync(op->perm, st);
+  csc::pool_free(op->indptr, st);
+  csc::pool_free(op->indices, st);
+  csc::pool_free(op->vals, st);
+  csc::pool_free(op->long_rows, st);
+  csc::pool_free(op->seg_off, st);
+  csc::pool_free(op->perm, st);
   delete op;
   return CSC_OK;
 }

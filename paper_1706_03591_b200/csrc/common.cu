@@ -1,5 +1,7 @@
 // Library-level entry points and shared helpers.
 #include <mutex>
+#include <unordered_map>
+#include <vector>
 #include <string>
 
 #include <cstdlib>
@@ -60,14 +62,101 @@ const DeviceInfo &device_info() {
   return info;
 }
 
+// Size classes for pool requests of 1 MiB and more: eight steps per power of
+// two (<= 12.5% slack), so that buffers whose size follows nnz (operator plans,
+// sort and Laplacian scratch: a fraction of a percent apart between the steps
+// of a dynamic sequence) ask for equal sizes.
+size_t pool_size_class(size_t bytes) {
+  if (bytes < (size_t(1) << 20)) return bytes ? bytes : 16;
+  size_t p = size_t(1) << 20;
+  while ((p << 1) <= bytes) p <<= 1;
+  const size_t step = p >> 3;
+  return (bytes + step - 1) / step * step;
+}
+
+// Block cache in front of the stream-ordered pool for large blocks on the
+// default stream. cudaMallocAsync stalls the host when its free list is
+// fragmented: with the pool's reserved size constant (3.5 GiB) the 176 / 352 MB
+// plan arrays of a configs[4] step sporadically took 23-2,200 ms to allocate
+// (the pool re-maps physical granules into a contiguous range), one step in
+// ten. Freed blocks of >= kCacheMin bytes are kept here by size class and
+// handed back to the next request of that class on the same stream (work on
+// one stream is ordered, so no synchronisation is needed); the oldest blocks
+// go back to the pool past kCacheCap.
+namespace {
+constexpr size_t kCacheMin = size_t(4) << 20;
+struct CachedBlock {
+  void *ptr;
+  size_t bytes;
+  int dev;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;                 // free blocks, oldest first
+std::unordered_map<void *, size_t> g_block_bytes;  // live large blocks -> class size
+size_t g_cache_bytes = 0;
+size_t cache_cap() {
+  static size_t cap = [] {
+    const char *e = getenv("CSC_BLOCK_CACHE_GB");  // 0 turns the cache off
+    return (size_t)(e ? atoll(e) : 6) << 30;
+  }();
+  return cap;
+}
+}  // namespace
+
+cudaError_t pool_alloc(void **ptr, size_t bytes, cudaStream_t s) {
+  const size_t cls = pool_size_class(bytes);
+  if (s == nullptr && cls >= kCacheMin && cache_cap() > 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    for (size_t i = g_cache.size(); i-- > 0;) {
+      if (g_cache[i].bytes == cls && g_cache[i].dev == dev) {
+        *ptr = g_cache[i].ptr;
+        g_cache.erase(g_cache.begin() + (ptrdiff_t)i);
+        g_cache_bytes -= cls;
+        g_block_bytes[*ptr] = cls;
+        return cudaSuccess;
+      }
+    }
+    const cudaError_t e = cudaMallocAsync(ptr, cls, s);
+    if (e == cudaSuccess) g_block_bytes[*ptr] = cls;
+    return e;
+  }
+  return cudaMallocAsync(ptr, cls, s);
+}
+
+void pool_free(void *ptr, cudaStream_t s) {
+  if (!ptr) return;
+  {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    auto it = g_block_bytes.find(ptr);
+    if (it != g_block_bytes.end()) {
+      const size_t cls = it->second;
+      g_block_bytes.erase(it);  // whatever happens next, the address is no longer tracked
+      if (s == nullptr && cache_cap() > 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        g_cache.push_back({ptr, cls, dev});
+        g_cache_bytes += cls;
+        while (g_cache_bytes > cache_cap() && !g_cache.empty()) {
+          cudaFreeAsync(g_cache.front().ptr, nullptr);
+          g_cache_bytes -= g_cache.front().bytes;
+          g_cache.erase(g_cache.begin());
+        }
+        return;
+      }
+    }
+  }
+  cudaFreeAsync(ptr, s);
+}
+
 cudaError_t Scratch::alloc(size_t bytes, cudaStream_t s) {
   stream = s;
-  if (bytes == 0) bytes = 16;
-  return cudaMallocAsync(&ptr, bytes, s);
+  return pool_alloc(&ptr, bytes, s);
 }
 
 Scratch::~Scratch() {
-  if (ptr) cudaFreeAsync(ptr, stream);
+  if (ptr) pool_free(ptr, stream);
 }
 
 }  // namespace csc
@@ -95,6 +184,21 @@ int csc_device_info(int *sm_count, int *cc_major, int *cc_minor) {
   if (sm_count) *sm_count = info.sm_count;
   if (cc_major) *cc_major = info.cc_major;
   if (cc_minor) *cc_minor = info.cc_minor;
+  return CSC_OK;
+}
+
+int csc_pool_stats(int64_t *out4) {
+  CSC_REQUIRE(out4 != nullptr, "csc_pool_stats: NULL output");
+  int dev = 0;
+  CSC_TRY_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  CSC_TRY_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t v[4] = {0, 0, 0, 0};
+  CSC_TRY_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v[0]));
+  CSC_TRY_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &v[1]));
+  CSC_TRY_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &v[2]));
+  CSC_TRY_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &v[3]));
+  for (int i = 0; i < 4; ++i) out4[i] = (int64_t)v[i];
   return CSC_OK;
 }
 

@@ -36,6 +36,12 @@ struct Scratch {
   T *as() const { return static_cast<T *>(ptr); }
 };
 
+// Stream-ordered allocation in size classes with a block cache for large
+// default-stream blocks (see common.cu); pool_free pairs with pool_alloc
+size_t pool_size_class(size_t bytes);
+cudaError_t pool_alloc(void **ptr, size_t bytes, cudaStream_t s);
+void pool_free(void *ptr, cudaStream_t s);
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace csc
