@@ -7,8 +7,6 @@ nothing to any norm or distance.
 """
 from __future__ import annotations
 
-import os
-
 import numpy as np
 import torch
 
@@ -37,13 +35,9 @@ def ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
-# row alignment in bytes (A/B knob: CSC_ROW_ALIGN=128 pads rows to whole cache lines)
-_ROW_ALIGN = int(os.environ.get("CSC_ROW_ALIGN", "32"))
-
-
 def row_stride(d: int, dtype: torch.dtype = torch.float64) -> int:
     """Elements per padded row: d rounded up to a 32-byte multiple."""
-    per = _ROW_ALIGN // torch.empty((), dtype=dtype).element_size()
+    per = 32 // torch.empty((), dtype=dtype).element_size()
     return ((d + per - 1) // per) * per
 
 
