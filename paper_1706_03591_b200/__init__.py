@@ -8,7 +8,8 @@ include/csc_b200.h). Import works without a GPU; every compute call needs one.
 from .graphs import Graph, LaplacianMatrix, graphs_equal, laplacian
 from .signals import FeatureMatrix, as_seed_sequence, random_signals
 from .filters import (EigencountSearchError, FilterConfig, FilterPoly, MatvecCounter, apply_filter,
-                      cheb_coeffs, eigencount, find_lambda_k, jackson_damping, warm_interval)
+                      cheb_coeffs, eigencount, find_lambda_k, jackson_damping, release_resident_orders,
+                      warm_interval)
 from .kmeans import Assignment, KmeansConfig, kmeans, kmeans_cost
 from .csc import CscDiagnostics, csc_assign, csc_features
 from .dynamic import (DynamicConfig, DynamicState, SequenceError, StepDiagnostics, dynamic_init,
