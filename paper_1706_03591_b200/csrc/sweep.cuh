@@ -284,9 +284,15 @@ __device__ __forceinline__ void epilogue(float4 acc, const float4 *prev, const f
 #ifndef SWEEP_NARROW_BATCH
 #define SWEEP_NARROW_BATCH 4
 #endif
-template <int G>
+// three-vector groups: 5 (B200 A/B at 3 blocks/SM, ms per order at cfg5 d = 48 /
+// 72 / 96: batch 3 3.14 / 5.20 / 5.70, 4 3.06 / 4.91 / 5.47, 5 2.96 / 4.80 / 5.41,
+// 6 3.01 / 5.01 / 5.63; 6 or 8 at 2 blocks/SM and 3 or 4 at 4 blocks/SM slower)
+#ifndef SWEEP_V3_BATCH
+#define SWEEP_V3_BATCH 5
+#endif
+template <int G, int VPL = 1>
 struct SweepBatch {
-  static constexpr int value = G < 32 ? SWEEP_NARROW_BATCH : 4;
+  static constexpr int value = VPL == 3 ? SWEEP_V3_BATCH : (G < 32 ? SWEEP_NARROW_BATCH : 4);
 };
 
 // Gather-accumulate of entries [beg, end) of one row into acc[VPL] by a group
@@ -308,7 +314,7 @@ __device__ __forceinline__ void gather_row(const int32_t *__restrict__ indices,
       my_val = ld_s(vals + nz, pol);
     }
     const int cnt = min(G, end - base);
-    constexpr int B = SweepBatch<G>::value;  // entries whose gathers are issued together
+    constexpr int B = SweepBatch<G, VPL>::value;  // entries whose gathers are issued together
     int u = 0;
     for (; u + B <= cnt; u += B) {
       int c[B];
@@ -377,12 +383,16 @@ __device__ __forceinline__ void segment_body(const SweepArgs &A, int64_t first_w
 #ifndef SWEEP_NARROW_MIN
 #define SWEEP_NARROW_MIN 4
 #endif
+#ifndef SWEEP_V3_MIN
+#define SWEEP_V3_MIN 3
+#endif
 #ifndef SWEEP_WIDE_MIN
 #define SWEEP_WIDE_MIN 3
 #endif
 template <int G, int VPL>
 struct SweepMinBlocks {
-  static constexpr int value = (G < 32 && VPL <= 2) ? SWEEP_NARROW_MIN : (VPL <= 3 ? SWEEP_WIDE_MIN : 0);
+  static constexpr int value =
+      (G < 32 && VPL <= 2) ? SWEEP_NARROW_MIN : (VPL == 3 ? SWEEP_V3_MIN : (VPL <= 2 ? SWEEP_WIDE_MIN : 0));
 };
 
 template <typename T, int G, int VPL, int MODE, bool PERM>
