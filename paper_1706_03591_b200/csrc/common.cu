@@ -138,10 +138,13 @@ void pool_free(void *ptr, cudaStream_t s) {
         cudaGetDevice(&dev);
         g_cache.push_back({ptr, cls, dev});
         g_cache_bytes += cls;
-        while (g_cache_bytes > cache_cap() && !g_cache.empty()) {
-          cudaFreeAsync(g_cache.front().ptr, nullptr);
-          g_cache_bytes -= g_cache.front().bytes;
-          g_cache.erase(g_cache.begin());
+        while (g_cache_bytes > cache_cap()) {  // oldest block of this device back to the pool
+          size_t i = 0;
+          while (i < g_cache.size() && g_cache[i].dev != dev) ++i;
+          if (i == g_cache.size()) break;
+          cudaFreeAsync(g_cache[i].ptr, nullptr);
+          g_cache_bytes -= g_cache[i].bytes;
+          g_cache.erase(g_cache.begin() + (ptrdiff_t)i);
         }
         return;
       }
