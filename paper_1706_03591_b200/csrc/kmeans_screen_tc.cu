@@ -259,10 +259,34 @@ struct TcArgs {
 // (2 x NP columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
 constexpr int kKU = 32;                // columns per unit (4 MMA K steps)
 constexpr int kMaxRaw = 12;            // raw ring units (as many as fit, >= 2)
-constexpr int kLoStages = 2;           // lo ring units
+#ifndef TC_LO_STAGES
+#define TC_LO_STAGES 2
+#endif
+constexpr int kLoStages = TC_LO_STAGES;  // lo ring units
 constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2, kSplitWarp0 = 7,
               kSplitWarps = 4;
-constexpr int kTcThreads = 32 * (kEpiWarps + 1 + kProdWarps + kSplitWarps);  // 352
+// Warps issue on sub-partition warp % 4. With 11 consecutive warps the MMA warp
+// (4) shares sub-partition 0 with an epilogue warp (0) and a splitter (8): ~2,000
+// warp instructions per tile there, the kernel's critical path. TC_IDLE_WARP
+// leaves warp 8 idle and moves its splitter to warp 11, so sub-partition 0
+// carries the MMA and one epilogue warp only.
+#ifndef TC_IDLE_WARP
+#define TC_IDLE_WARP 1
+#endif
+// TC_EPI_SETS = 2 (A/B knob, off): a second set of four epilogue warps (12-15;
+// warp % 4 selects the TMEM lane quarter) settles the odd tiles (accumulator 1)
+// while warps 0-3 settle the even ones. Measured on cfg5 features (60 host-
+// driven iterations, us per screen launch, full / late): one set 228 / 126, two
+// sets 228 / 126; lo ring of 3 or 4 units instead of 2: 229 / 124; the idle warp
+// above: 228 vs 233 without. None of the consumer roles is the limit: the MMA
+// warp itself is (36 UTCHMMA per tile, each behind an ELECT and ~6 R2UR
+// broadcasts of its descriptors: ~950 dependent warp instructions per tile).
+#ifndef TC_EPI_SETS
+#define TC_EPI_SETS 1
+#endif
+constexpr int kEpi2Warp0 = kEpiWarps + 1 + kProdWarps + kSplitWarps + (TC_IDLE_WARP ? 1 : 0);  // 12
+static_assert(TC_EPI_SETS == 1 || kEpi2Warp0 % 4 == 0, "second epilogue set must start a warp quad");
+constexpr int kTcThreads = 32 * (kEpi2Warp0 + (TC_EPI_SETS == 2 ? kEpiWarps : 0));  // 512
 constexpr uint32_t kUnitBytes = kTM * kKU * 4;
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -412,9 +436,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
-  } else if (warp >= kSplitWarp0) {
-    // ===== splitters: warp 7 + h writes the low parts of quarter h of every unit, in unit order
-    const int sw = warp - kSplitWarp0;
+  } else if (TC_IDLE_WARP && warp == kSplitWarp0 + 1) {
+    // idle: keeps the MMA warp's sub-partition free of a third role
+  } else if (warp >= kSplitWarp0 && warp < kEpi2Warp0) {
+    // ===== splitters: each writes the low parts of one quarter of every unit, in unit order
+    const int sw = (TC_IDLE_WARP && warp > kSplitWarp0) ? warp - kSplitWarp0 - 1 : warp - kSplitWarp0;
     constexpr int kQuads = (int)(kUnitBytes / 16) / kSplitWarps;
     for (int64_t u = 0; u < nunits; ++u) {
       const int s = (int)(u % stages);
@@ -473,10 +499,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ===== epilogue: thread (warp w, lane l) settles row 32 w + l of each tile
     const double cmax = *a.cmax;
     const double dscale = (double)(3 * a.d + 8) * 1.1920928955078125e-7;  // (3d + 8) 2^-23
-    for (int64_t i = 0; i < my_tiles; ++i) {
+    const int eset = (TC_EPI_SETS == 2 && warp >= kEpi2Warp0) ? 1 : 0;
+    const int qw = warp & 3;  // TMEM lane quarter = tile rows 32 qw .. 32 qw + 31
+    for (int64_t i = (TC_EPI_SETS == 2 ? eset : 0); i < my_tiles; i += TC_EPI_SETS) {
       const int slot = (int)(i & 1);
       const int64_t tile = blockIdx.x + i * gridDim.x;
-      const int64_t lr = tile * kTM + warp * 32 + lane;
+      const int64_t lr = tile * kTM + qw * 32 + lane;
       const int64_t gr = lr < nr ? (a.rows ? (int64_t)__ldg(a.rows + lr) : lr) : -1;
       const float fni = gr >= 0 ? __ldg(a.fn32 + gr) : 0.0f;
       mbar_wait(smem_u32(tfull + slot), (uint32_t)((i / 2) & 1));
@@ -485,7 +513,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // (one fp32 rounding per entry, as many as E had) and add |f|^2 to the best two
       float bv = INFINITY, bv2 = INFINITY;
       int bi = 0x7fffffff;
-      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(slot * NP);
+      const uint32_t taddr = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(slot * NP);
 #pragma unroll
       for (int c0 = 0; c0 < NP; c0 += 16) {
         float v[16];
