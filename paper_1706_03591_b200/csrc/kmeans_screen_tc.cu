@@ -281,6 +281,15 @@ constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2, kSpli
 // above: 228 vs 233 without. None of the consumer roles is the limit: the MMA
 // warp itself is (36 UTCHMMA per tile, each behind an ELECT and ~6 R2UR
 // broadcasts of its descriptors: ~950 dependent warp instructions per tile).
+// TC_MMA_WARPS = 2 (A/B knob, off; needs TC_IDLE_WARP): the idle warp issues the
+// odd tiles' MMAs. Correct (tests pass) and no faster (227 / 127 us, also with a
+// lo ring of 4 or 6 units): the MMA warp is not the limit either. What is left
+// is shared-memory bandwidth: per 128-row tile the splitters read and write 48 +
+// 48 KB, TMA writes 48 KB and the 36 MMAs read 36 x (4 KB of A + 2 KB of B) =
+// 216 KB, 360 KB in all = 2,880 cycles at 128 B/clk of the ~4,100 a tile takes.
+#ifndef TC_MMA_WARPS
+#define TC_MMA_WARPS 1
+#endif
 #ifndef TC_EPI_SETS
 #define TC_EPI_SETS 1
 #endif
@@ -340,7 +349,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     for (int s = 0; s < kLoStages; ++s) {
       mbar_init(smem_u32(lfull + s), 32 * kSplitWarps);  // both splitters
-      mbar_init(smem_u32(lempty + s), 1);                // MMA commit
+      mbar_init(smem_u32(lempty + s), TC_MMA_WARPS);     // MMA commit (+ the other MMA warp's pass)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(tfull + s), 1);          // MMA commit
@@ -436,10 +445,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
-  } else if (TC_IDLE_WARP && warp == kSplitWarp0 + 1) {
+  } else if (TC_IDLE_WARP && TC_MMA_WARPS == 1 && warp == kSplitWarp0 + 1) {
     // idle: keeps the MMA warp's sub-partition free of a third role
-  } else if (warp >= kSplitWarp0 && warp < kEpi2Warp0) {
-    // ===== splitters: each writes the low parts of one quarter of every unit, in unit order
+  } else if (warp >= kSplitWarp0 && warp < kEpi2Warp0 && !(TC_IDLE_WARP && warp == kSplitWarp0 + 1)) {
+    // ===== splitters (warps 7, 9, 10, 11; 8 is idle or the second MMA warp): each writes the low parts of one quarter of every unit, in unit order
     const int sw = (TC_IDLE_WARP && warp > kSplitWarp0) ? warp - kSplitWarp0 - 1 : warp - kSplitWarp0;
     constexpr int kQuads = (int)(kUnitBytes / 16) / kSplitWarps;
     for (int64_t u = 0; u < nunits; ++u) {
@@ -460,14 +469,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       fence_async_smem();  // this thread's smem writes -> visible to the tensor core
       mbar_arrive(smem_u32(lfull + t));
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaWarp || (TC_MMA_WARPS == 2 && TC_IDLE_WARP && warp == kSplitWarp0 + 1)) {
     // ===== MMA issue: A_hi = the raw unit (read as tf32 = its top 19 bits), A_lo
-    // from the lo ring; the lo full barrier implies the raw unit's arrival
+    // from the lo ring; the lo full barrier implies the raw unit's arrival.
+    // TC_MMA_WARPS = 2: warp 4 issues the even tiles (accumulator 0), warp 8 the
+    // odd ones (accumulator 1); each accumulator's MMAs stay in one thread's order.
     const uint32_t idesc = tf32_idesc(NP);
     const uint32_t sB = smem_u32(Bhi), sBl = smem_u32(Blo);
     const uint32_t lboB = NP * 16, sbo = 128;
+    const int mw = (TC_MMA_WARPS == 2 && warp != kMmaWarp) ? 1 : 0;
     int64_t u = 0;
     for (int64_t i = 0; i < my_tiles; ++i) {
+      if (TC_MMA_WARPS == 2 && (int)(i & 1) != mw) {
+        // the other warp's tile: follow its units' lo barriers in order (a
+        // parity wait is only valid one phase away) and release them for this
+        // warp (lempty counts both MMA warps), without touching the data
+        for (int h = 0; h < units; ++h, ++u) {
+          const int t = (int)(u % kLoStages);
+          mbar_wait(smem_u32(lfull + t), (uint32_t)((u / kLoStages) & 1));
+          if (lane == 0) mbar_arrive(smem_u32(lempty + t));
+        }
+        continue;
+      }
       const int slot = (int)(i & 1);
       if (i >= 2) mbar_wait(smem_u32(tempty + slot), (uint32_t)((i / 2 - 1) & 1));
       tc_fence_after();
