@@ -281,6 +281,18 @@ constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2, kSpli
 // above: 228 vs 233 without. None of the consumer roles is the limit: the MMA
 // warp itself is (36 UTCHMMA per tile, each behind an ELECT and ~6 R2UR
 // broadcasts of its descriptors: ~950 dependent warp instructions per tile).
+// TC_CAT = 1: the centroid tiles' high and low parts form one N = 2 NP operand
+// per K quad ([Q][2 NP][4]: rows 0..NP-1 high, NP..2NP-1 low), so a K step is
+// two MMAs — A_hi x [B_hi | B_lo] (N = 2 NP) and A_lo x B_hi (N = NP, the first
+// rows of the same tiles) — instead of three: A_hi is read from shared memory
+// once per K step instead of twice (14 instead of 18 KB per K step). The
+// accumulator holds f_hi.c_hi + f_lo.c_hi in columns 0..NP-1 and f_hi.c_lo in
+// NP..2NP-1; the epilogue adds them (one more fp32 rounding: inside the bound's
+// +8 slack).
+#ifndef TC_CAT
+#define TC_CAT 1
+#endif
+constexpr int kAccW = TC_CAT ? 2 : 1;  // accumulator columns per centroid
 // TC_MMA_WARPS = 2 (A/B knob, off; needs TC_IDLE_WARP): the idle warp issues the
 // odd tiles' MMAs. Correct (tests pass) and no faster (227 / 127 us, also with a
 // lo ring of 4 or 6 units): the MMA warp is not the limit either. What is left
@@ -333,7 +345,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if ((int64_t)blockIdx.x >= ntiles) return;
   const int64_t my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
-  constexpr uint32_t kCols = 2 * NP <= 32 ? 32 : 2 * NP <= 64 ? 64 : 2 * NP <= 128 ? 128 : 256;
+  constexpr int kAccCols = 2 * kAccW * NP;  // two accumulators
+  constexpr uint32_t kCols = kAccCols <= 32 ? 32 : kAccCols <= 64 ? 64 : kAccCols <= 128 ? 128 : kAccCols <= 256 ? 256 : 512;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_hold)),
@@ -363,8 +376,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     float4 *dh = reinterpret_cast<float4 *>(Bhi);
     float4 *dl = reinterpret_cast<float4 *>(Blo);
     for (int e = tid; e < NP * kp / 4; e += kTcThreads) {
-      dh[e] = sh[e];
-      dl[e] = sl[e];
+      if (TC_CAT) {  // [Q][2 NP][4]: quad q's high rows, then its low rows
+        const int q = e / NP, j = e - q * NP;
+        dh[q * 2 * NP + j] = sh[e];
+        dh[q * 2 * NP + NP + j] = sl[e];
+      } else {
+        dh[e] = sh[e];
+        dl[e] = sl[e];
+      }
     }
     for (int j = tid; j < NP; j += kTcThreads) {
       Cn[j] = a.cn32[j];
@@ -474,9 +493,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // from the lo ring; the lo full barrier implies the raw unit's arrival.
     // TC_MMA_WARPS = 2: warp 4 issues the even tiles (accumulator 0), warp 8 the
     // odd ones (accumulator 1); each accumulator's MMAs stay in one thread's order.
-    const uint32_t idesc = tf32_idesc(NP);
+    const uint32_t idesc = tf32_idesc(NP), idesc2 = tf32_idesc(2 * NP);
     const uint32_t sB = smem_u32(Bhi), sBl = smem_u32(Blo);
-    const uint32_t lboB = NP * 16, sbo = 128;
+    const uint32_t lboB = (TC_CAT ? 2 : 1) * NP * 16, sbo = 128;
     const int mw = (TC_MMA_WARPS == 2 && warp != kMmaWarp) ? 1 : 0;
     int64_t u = 0;
     for (int64_t i = 0; i < my_tiles; ++i) {
@@ -494,7 +513,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int slot = (int)(i & 1);
       if (i >= 2) mbar_wait(smem_u32(tempty + slot), (uint32_t)((i / 2 - 1) & 1));
       tc_fence_after();
-      const uint32_t acc = tmem + (uint32_t)(slot * NP);
+      const uint32_t acc = tmem + (uint32_t)(slot * kAccW * NP);
       for (int h = 0; h < units; ++h, ++u) {
         const int s = (int)(u % stages);
         const int t = (int)(u % kLoStages);
@@ -508,10 +527,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int ks = 0; ks < kKU / 8; ++ks) {
           const uint64_t ahi = dhi + (uint64_t)(ks * 2), alo = dlo + (uint64_t)(ks * 2);  // + 32 B
           const uint32_t ob = (uint32_t)(h * (kKU / 8) + ks) * 2 * lboB;
-          const uint64_t bhi = umma_desc(sB + ob, lboB, sbo), blo = umma_desc(sBl + ob, lboB, sbo);
-          mma_tf32_elect(acc, ahi, bhi, idesc, (h > 0 || ks > 0) ? 1u : 0u);
-          mma_tf32_elect(acc, alo, bhi, idesc, 1u);
-          mma_tf32_elect(acc, ahi, blo, idesc, 1u);
+          const uint64_t bhi = umma_desc(sB + ob, lboB, sbo);
+          if (TC_CAT) {
+            mma_tf32_elect(acc, ahi, bhi, idesc2, (h > 0 || ks > 0) ? 1u : 0u);  // [hi.hi | hi.lo]
+            mma_tf32_elect(acc, alo, bhi, idesc, 1u);                             // lo.hi into the first half
+          } else {
+            const uint64_t blo = umma_desc(sBl + ob, lboB, sbo);
+            mma_tf32_elect(acc, ahi, bhi, idesc, (h > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32_elect(acc, alo, bhi, idesc, 1u);
+            mma_tf32_elect(acc, ahi, blo, idesc, 1u);
+          }
         }
         mma_commit_elect(smem_u32(rempty + s));  // the raw slot and the lo slot are free once these MMAs ran
         mma_commit_elect(smem_u32(lempty + t));
@@ -536,11 +561,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // (one fp32 rounding per entry, as many as E had) and add |f|^2 to the best two
       float bv = INFINITY, bv2 = INFINITY;
       int bi = 0x7fffffff;
-      const uint32_t taddr = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(slot * NP);
+      const uint32_t taddr = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(slot * kAccW * NP);
 #pragma unroll
       for (int c0 = 0; c0 < NP; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + (uint32_t)c0, v);
+        if (TC_CAT) {
+          float w[16];
+          tmem_ld16(taddr + (uint32_t)(NP + c0), w);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += w[j];
+        }
         float cn[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
