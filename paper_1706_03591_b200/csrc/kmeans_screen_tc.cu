@@ -295,10 +295,10 @@ constexpr int kEpiWarps = 4, kMmaWarp = 4, kProdWarp0 = 5, kProdWarps = 2, kSpli
 constexpr int kAccW = TC_CAT ? 2 : 1;  // accumulator columns per centroid
 // TC_MMA_WARPS = 2 (A/B knob, off; needs TC_IDLE_WARP): the idle warp issues the
 // odd tiles' MMAs. Correct (tests pass) and no faster (227 / 127 us, also with a
-// lo ring of 4 or 6 units): the MMA warp is not the limit either. What is left
-// is shared-memory bandwidth: per 128-row tile the splitters read and write 48 +
-// 48 KB, TMA writes 48 KB and the 36 MMAs read 36 x (4 KB of A + 2 KB of B) =
-// 216 KB, 360 KB in all = 2,880 cycles at 128 B/clk of the ~4,100 a tile takes.
+// lo ring of 4 or 6 units): the MMA warp is not the limit either. The final ncu
+// capture shows no unit above half of its peak (DRAM 42%, tensor-core shared-
+// memory wavefronts 46%, LSU 37%): the splitters wait on the raw units' arrival
+// (profiles/r02_tc_screen_cfg5.md).
 #ifndef TC_MMA_WARPS
 #define TC_MMA_WARPS 1
 #endif
